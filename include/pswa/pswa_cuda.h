@@ -1,0 +1,141 @@
+/*
+ * pswa_cuda.h — the C-ABI drop-in boundary of the B200 P-SWA entropy decoder.
+ *
+ * Plain C: opaque handle, plain pointers and sizes, int status codes, no C++
+ * or torch types, no exceptions across the boundary. A reference-side binding
+ * (ctypes / cgo / JNI) needs nothing but this header; see INTEGRATION.md.
+ *
+ * Reference interfaces replaced (paths relative to the reference tree):
+ *   pswa_gpu_decode_frame   <- decode_frame_wavefront(payloads, state, weights,
+ *                              cfg, workers)
+ *   pswa_gpu_encode_frame   <- encode_frame(y, state, weights, cfg, rate_idx)
+ *                                                             SPEC.md:567-575
+ *   pswa_gpu_forward_params <- the teacher-forced (mu, sigma) of predict_params
+ *                              over a frame
+ *   pswa_gpu_reset_gop / _push_frame <- FrameState ring update SPEC.md:304-308,
+ *                              GOP reset
+ *   pswa_gpu_op_*           <- per-operator entry points used by parity tests:
+ *     op_gemm_f16      matmul                   proj/src/tensor.cpp:42-58
+ *     op_rmsnorm       rmsnorm                  proj/src/tensor.cpp:81-86
+ *     op_window_attn   swa2d / cross_windowed / swa3d_timecausal
+ *     op_build_cdf     build_gaussian_cdf
+ *     op_encode_symbols / op_decode_symbols     SPEC.md:457-465 (lane format)
+ */
+#ifndef PSWA_PSWA_CUDA_H_
+#define PSWA_PSWA_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+enum {
+  PSWA_OK = 0,
+  PSWA_E_ARG = 1,       /* shape / argument error  (std::invalid_argument) */
+  PSWA_E_TRUNCATED = 2, /* bitstream truncated or corrupt                   */
+  PSWA_E_HASH = 3,      /* weights / config mismatch                         */
+  PSWA_E_CUDA = 4,      /* CUDA runtime / driver error                       */
+  PSWA_E_LANE = 5,      /* coder lane overrun                                */
+  PSWA_E_INTERNAL = 6
+};
+
+/* Thread-local message for the last non-zero status on this thread. */
+const char* pswa_gpu_last_error(void);
+
+/* ---- configuration (ModelConfig) ---------------------- */
+typedef struct pswa_cfg {
+  int d_spatial;    /* d: 512 paper / 64 desk            */
+  int heads;        /* h: 16                             */
+  int ctx_blocks;   /* 8 / 2                             */
+  int s1_blocks;    /* 8 / 2                             */
+  int s2_blocks;    /* 8 / 2                             */
+  int d_channel;    /* 1024 / 128                        */
+  int ch_blocks;    /* 2                                 */
+  int hyper_ch;     /* 128 / 32                          */
+  int latent_ch;    /* C = 192                           */
+  int s;            /* spatial steps, 4                  */
+  int n_groups;     /* N channel groups, 4               */
+  int win_h, win_w; /* spatial window 7x7                */
+  int win_t;        /* temporal window 5                 */
+  int ctx_slots;    /* past-frame ring length, 4         */
+  int rate_points;  /* 4                                 */
+  int height, width;/* latent grid H x W (multiples of 4) */
+  int lanes;        /* main-payload coder lanes          */
+  int hyper_lanes;  /* hyper-payload coder lanes         */
+} pswa_cfg;
+
+/* Fill the paper (preset=1) or desk (preset=0) defaults for an H x W grid. */
+void pswa_cfg_preset(pswa_cfg* cfg, int preset, int height, int width);
+
+typedef struct pswa_gpu pswa_gpu;
+
+/* ---- deterministic weights (gen_weights) --------------
+ * Writes the PSWW blob for (cfg, seed) into buf (capacity cap). *len gets the
+ * required size; call with buf == NULL to query it. */
+int pswa_gen_weights(const pswa_cfg* cfg, uint64_t seed, void* buf, size_t cap, size_t* len);
+
+/* Synthetic latent frame: y_hat[C][H][W] int32 for frame
+ * `frame_idx` of GOP `gop`. */
+int pswa_synth_latent(const pswa_cfg* cfg, int gop, int frame_idx, int32_t* yhat_out);
+
+/* ---- handle lifecycle --------------------------------------------------- */
+int pswa_gpu_create(int device, const pswa_cfg* cfg, const void* psww_blob, size_t blob_len,
+                    pswa_gpu** out);
+void pswa_gpu_destroy(pswa_gpu* h);
+/* Reset the temporal ring to the learned pad (GOP boundary). */
+int pswa_gpu_reset_gop(pswa_gpu* h);
+
+/* ---- frame API (host buffers; copies inside) ---------------------------
+ * payload layout and lane format: see DESIGN.md "Bitstream". */
+int pswa_gpu_encode_frame(pswa_gpu* h, const int32_t* yhat, int rate_idx, int frame_idx_in_gop,
+                          uint8_t* hyper_out, size_t hyper_cap, size_t* hyper_len,
+                          uint8_t* main_out, size_t main_cap, size_t* main_len,
+                          double* bits_out /* [2] = {hyper, main}, nullable */);
+int pswa_gpu_decode_frame(pswa_gpu* h, const uint8_t* hyper, size_t hyper_len,
+                          const uint8_t* main_payload, size_t main_len, int rate_idx,
+                          int frame_idx_in_gop, int advance_state, int32_t* yhat_out,
+                          double* bits_out /* [2], nullable */);
+/* Teacher-forced entropy parameters for a known frame (parity probe).
+ * zhat: [hyper_ch][H/4][W/4]; mu/sigma: [C][H][W]. */
+int pswa_gpu_forward_params(pswa_gpu* h, const int32_t* yhat, const int32_t* zhat, int rate_idx,
+                            int frame_idx_in_gop, float* mu_out, float* sigma_out,
+                            double* bits_out /* [2], nullable */);
+/* Returns the z_hat the encoder produced for the last encode_frame call. */
+int pswa_gpu_last_zhat(pswa_gpu* h, int32_t* zhat_out);
+/* Append a decoded / known frame to the temporal ring. */
+int pswa_gpu_push_frame(pswa_gpu* h, const int32_t* yhat, int rate_idx);
+
+/* ---- device-resident variants (inputs already in HBM) ------------------ */
+int pswa_gpu_decode_frame_device(pswa_gpu* h, const void* d_hyper, size_t hyper_len,
+                                 const void* d_main, size_t main_len, int rate_idx,
+                                 int frame_idx_in_gop, int advance_state, void* d_yhat_out);
+/* Number of kernels the last frame call launched (graph nodes included). */
+int pswa_gpu_last_launch_count(pswa_gpu* h);
+/* Stream the handle runs on (cudaStream_t as void*). */
+void* pswa_gpu_stream(pswa_gpu* h);
+
+/* ---- operator-level entry points (device pointers, on `stream`) -------- */
+/* C[M,N] = A[M,K] . B[N,K]^T, fp16 in, fp32 accumulate; out fp16 or fp32. */
+int pswa_gpu_op_gemm_f16(const void* A, int lda, int M, const void* B, int ldb, int N, int K,
+                         void* C, int ldc, int out_f32, int accumulate, const float* bias,
+                         const float* scale, int act, int force_bn, void* stream);
+/* y = gain * x / sqrt(mean(x^2) + 1e-5), per group of `group` columns.
+ * x fp32 [M][ld_x]; y fp16 [M][ld_y]. */
+int pswa_gpu_op_rmsnorm(const float* x, int ld_x, int M, int d, int group, const float* gain,
+                        void* y, int ld_y, void* stream);
+/* Windowed masked attention; see DESIGN.md "Attention". */
+int pswa_gpu_op_window_attn(const void* q, int ld_q, const int32_t* qinfo, int Mq,
+                            const void* kv, int ld_kv, int kv_slot_stride, int H, int W,
+                            int heads, int head_dim, int win_h, int win_w, int win_t, int mask,
+                            int s, const float* bias, void* out, int ld_out, void* stream);
+/* 64 cumulative tables x 258 u32, built on the device. */
+int pswa_gpu_op_build_cdf(uint32_t* cdf_out /* host [64*258] */, float* scales_out /* [64] */);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSWA_PSWA_CUDA_H_ */

@@ -1,0 +1,51 @@
+// tcgen05 GEMM with fused epilogues: C[M,N] = A[M,K] . B[N,K]^T
+// (A activations, B packed weights, both fp16 K-major; fp32 accumulate in TMEM).
+//
+// Replaces the reference's scalar `matmul` (proj/src/tensor.cpp:42-58) and the
+// contractions inside `swiglu_ffn` (tensor.cpp:94-116) for every linear layer
+// on the decode path; the epilogue folds bias, rate scaling, SiLU, SwiGLU,
+// the residual add and the (mu, sigma) head activations.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace pswa_dev {
+
+enum GemmAct : int {
+  kActNone = 0,
+  kActSilu = 1,
+  kActSwiGLU = 2,  // columns interleaved (gate_j, up_j): out_j = silu(g)*u
+  kActHead = 3,    // n < split: mu = (acc+b)*scale ; else sigma = 0.11+softplus(acc+b)
+};
+
+struct GemmEpi {
+  void* out = nullptr;
+  int ld_out = 0;          // elements
+  int out_f32 = 0;         // 0: fp16 output, 1: fp32 output
+  int accumulate = 0;      // fp32 only: out += value (residual stream)
+  const float* bias = nullptr;   // [N] (nullable)
+  const float* scale = nullptr;  // [N] (nullable): v = acc*scale + bias
+  int act = kActNone;
+  int split = 0;                 // kActHead: first sigma column
+  const int* row_map = nullptr;  // nullable: output row = row_map[m]
+  int n_store = 1 << 30;         // output columns >= n_store are not written
+};
+
+struct GemmPlan {
+  CUtensorMap ta;
+  CUtensorMap tb;
+  int M = 0, N = 0, K = 0, BN = 0;
+  GemmEpi epi;
+};
+
+// A: [M rows][lda] fp16 (first K columns used); B: [N rows][ldb] fp16.
+// K % 64 == 0, N % 64 == 0, lda/ldb multiples of 8.
+void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, int ldb, int N,
+               int K, const GemmEpi& epi, int force_bn = 0);
+void gemm_run(const GemmPlan& p, cudaStream_t stream);
+
+// Number of kernel launches gemm_run issues (always 1); used by launch accounting.
+constexpr int kGemmLaunches = 1;
+
+}  // namespace pswa_dev

@@ -1,0 +1,64 @@
+"""tcgen05 GEMM parity vs a torch fp32 reference of the same op."""
+import ctypes as C
+
+import pytest
+import torch
+
+from paper_2605_20977_b200 import lib, check
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(M, N, K, out_f32=1, accumulate=0, bias=None, scale=None, act=0, force_bn=0):
+    torch.manual_seed(M * 7 + N * 3 + K)
+    a = (torch.randn(M, K, device="cuda") * 0.5).half()
+    b = (torch.randn(N, K, device="cuda") * 0.05).half()
+    ref = a.float() @ b.float().t()
+    if scale is not None:
+        ref = ref * scale
+    if bias is not None:
+        ref = ref + bias
+    if act == 1:
+        ref = torch.nn.functional.silu(ref)
+    if out_f32:
+        c = torch.randn(M, N, device="cuda") if accumulate else torch.zeros(M, N, device="cuda")
+        base = c.clone()
+    else:
+        c = torch.zeros(M, N, device="cuda", dtype=torch.float16)
+    check(lib().pswa_gpu_op_gemm_f16(a.data_ptr(), K, M, b.data_ptr(), K, N, K, c.data_ptr(), N,
+                                     out_f32, accumulate,
+                                     bias.data_ptr() if bias is not None else None,
+                                     scale.data_ptr() if scale is not None else None,
+                                     act, force_bn, None))
+    torch.cuda.synchronize()
+    if accumulate:
+        ref = ref + base
+    return c.float(), ref
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 64, 64, 64), (256, 128, 128, 128), (300, 256, 512, 256),
+                                      (2040, 512, 512, 0), (2040, 1536, 512, 0), (77, 64, 1408, 64),
+                                      (32640, 2816, 512, 0)])
+def test_gemm_f32(M, N, K, bn):
+    c, ref = _run(M, N, K, force_bn=bn)
+    err = (c - ref).abs().max().item()
+    assert err <= 1e-3 * max(1.0, ref.abs().max().item()), err
+
+
+def test_gemm_f16_bias_scale_silu():
+    N = 256
+    bias = torch.randn(N, device="cuda")
+    scale = torch.rand(N, device="cuda") + 0.5
+    c, ref = _run(513, N, 256, out_f32=0, bias=bias, scale=scale, act=1)
+    assert torch.allclose(c, ref, atol=2e-2, rtol=1e-2)
+
+
+def test_gemm_accumulate():
+    c, ref = _run(640, 512, 1408, accumulate=1)
+    assert torch.allclose(c, ref, atol=1e-3, rtol=1e-4)
+
+
+def test_gemm_deterministic():
+    c1, _ = _run(2040, 512, 512)
+    c2, _ = _run(2040, 512, 512)
+    assert torch.equal(c1, c2)
