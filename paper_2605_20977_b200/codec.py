@@ -1,0 +1,131 @@
+"""Python mirror of the reference's pipeline API over the C ABI.
+
+``GpuCodec`` exposes encode_frame / decode_frame_wavefront / forward_params
+ for one handle of ``libpswa_cuda.so``; every call
+goes straight to the sm_100a path — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import PswaCfg, check, lib
+
+_P = C.c_void_p
+
+
+def make_cfg(preset: str = "paper", height: int = 68, width: int = 120, **over) -> PswaCfg:
+    cfg = PswaCfg()
+    lib().pswa_cfg_preset(C.byref(cfg), 1 if preset == "paper" else 0, height, width)
+    for k, v in over.items():
+        setattr(cfg, k, int(v))
+    return cfg
+
+
+def cfg_from_dict(d: dict) -> PswaCfg:
+    cfg = PswaCfg()
+    for k, v in d.items():
+        setattr(cfg, k, int(v))
+    return cfg
+
+
+def gen_weights(cfg: PswaCfg, seed: int = 1) -> bytes:
+    n = C.c_size_t()
+    check(lib().pswa_gen_weights(C.byref(cfg), seed, None, 0, C.byref(n)))
+    buf = (C.c_uint8 * n.value)()
+    check(lib().pswa_gen_weights(C.byref(cfg), seed, buf, n.value, C.byref(n)))
+    return bytes(buf)
+
+
+def synth_latent(cfg: PswaCfg, gop: int, frame: int) -> np.ndarray:
+    y = np.zeros((cfg.latent_ch, cfg.height, cfg.width), np.int32)
+    check(lib().pswa_synth_latent(C.byref(cfg), gop, frame, y.ctypes.data_as(_P)))
+    return y
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_P)
+
+
+class GpuCodec:
+    """One device handle: weights, K/V caches, temporal ring, coder lanes."""
+
+    def __init__(self, cfg: PswaCfg, weights: bytes, device: int = 0):
+        self.cfg = cfg
+        self._w = (C.c_uint8 * len(weights)).from_buffer_copy(weights)
+        h = C.c_void_p()
+        check(lib().pswa_gpu_create(device, C.byref(cfg), self._w, len(weights), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().pswa_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def shape(self):
+        return (self.cfg.latent_ch, self.cfg.height, self.cfg.width)
+
+    @property
+    def zshape(self):
+        return (self.cfg.hyper_ch, (self.cfg.height + 3) // 4, (self.cfg.width + 3) // 4)
+
+    def reset_gop(self):
+        check(lib().pswa_gpu_reset_gop(self.h))
+
+    def push_frame(self, yhat: np.ndarray, rate: int = 0):
+        y = np.ascontiguousarray(yhat, np.int32)
+        check(lib().pswa_gpu_push_frame(self.h, _ptr(y), rate))
+
+    def encode_frame(self, yhat: np.ndarray, rate: int = 0, fidx: int = 0):
+        y = np.ascontiguousarray(yhat, np.int32)
+        cap = 20 * y.size + (1 << 20)
+        hb = np.zeros(cap, np.uint8)
+        mb = np.zeros(cap, np.uint8)
+        hl, ml = C.c_size_t(), C.c_size_t()
+        bits = np.zeros(2, np.float64)
+        check(lib().pswa_gpu_encode_frame(self.h, _ptr(y), rate, fidx, _ptr(hb), cap, C.byref(hl),
+                                          _ptr(mb), cap, C.byref(ml),
+                                          bits.ctypes.data_as(C.POINTER(C.c_double))))
+        return bytes(hb[:hl.value]), bytes(mb[:ml.value]), bits
+
+    def last_zhat(self) -> np.ndarray:
+        z = np.zeros(self.zshape, np.int32)
+        check(lib().pswa_gpu_last_zhat(self.h, _ptr(z)))
+        return z
+
+    def decode_frame(self, hyper: bytes, main: bytes, rate: int = 0, fidx: int = 0,
+                     advance: bool = True):
+        hb = np.frombuffer(hyper, np.uint8)
+        mb = np.frombuffer(main, np.uint8)
+        y = np.zeros(self.shape, np.int32)
+        bits = np.zeros(2, np.float64)
+        check(lib().pswa_gpu_decode_frame(self.h, _ptr(hb), len(hyper), _ptr(mb), len(main), rate,
+                                          fidx, int(advance), _ptr(y),
+                                          bits.ctypes.data_as(C.POINTER(C.c_double))))
+        return y, bits
+
+    def forward_params(self, yhat: np.ndarray, zhat: np.ndarray, rate: int = 0, fidx: int = 0):
+        y = np.ascontiguousarray(yhat, np.int32)
+        z = np.ascontiguousarray(zhat, np.int32)
+        mu = np.zeros(self.shape, np.float32)
+        sg = np.zeros(self.shape, np.float32)
+        bits = np.zeros(2, np.float64)
+        check(lib().pswa_gpu_forward_params(self.h, _ptr(y), _ptr(z), rate, fidx, _ptr(mu), _ptr(sg),
+                                            bits.ctypes.data_as(C.POINTER(C.c_double))))
+        return mu, sg, bits
+
+    def decode_device(self, d_hyper: int, hyper_len: int, d_main: int, main_len: int, rate: int,
+                      fidx: int, advance: bool, d_out: int):
+        check(lib().pswa_gpu_decode_frame_device(self.h, d_hyper, hyper_len, d_main, main_len,
+                                                 rate, fidx, int(advance), d_out))
+
+    def last_launch_count(self) -> int:
+        return lib().pswa_gpu_last_launch_count(self.h)
+
+    def stream(self) -> int:
+        return lib().pswa_gpu_stream(self.h)

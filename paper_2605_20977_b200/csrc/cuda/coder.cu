@@ -1,0 +1,542 @@
+// Entropy coding on the device: quantised discretised-
+// Gaussian CDF tables, and the multi-lane 64-bit-state range coder.
+//
+// Lane format: [u32 L][u32 count][u32 len_0..L-1]
+// [lane 0 bytes]...; symbol ordinal o (canonical order: step, group, raster
+// position, channel) lives in lane o % L. Each lane is an independent range
+// coder with a 48-bit window (range in [2^40, 2^48)), big-endian byte
+// renormalisation, carry into written bytes and a 4-byte flush; the decoder
+// finds a symbol by multiply-compare binary search (no integer division).
+// One thread drives one lane; lanes run concurrently, symbols within a lane
+// sequentially.
+//
+// This file is compiled with -fmad=false: the fp64 table builder must round
+// every add/mul exactly like the host restatement (det_math.cpp:49-130).
+#include <cfloat>
+
+#include "check.h"
+#include "kernels.h"
+
+namespace pswa_dev {
+
+namespace {
+
+constexpr uint64_t kWin = (uint64_t{1} << 48) - 1;
+constexpr uint64_t kBot = uint64_t{1} << 40;
+constexpr int kEscLo = 255, kEscHi = 256;
+__device__ const uint32_t kBitCum[3] = {0, 32768, 65536};
+
+// ------------------------------------------------- fp64 det math (device) --
+__device__ double d_pow2i(int k) {
+  if (k > 1023) return __longlong_as_double(0x7FF0000000000000LL);
+  if (k < -1074) return 0.0;
+  if (k >= -1022) return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
+  return __longlong_as_double(1LL << (k + 1074));
+}
+__device__ double d_exp(double x) {
+  if (x != x) return x;
+  if (x > 709.782712893384) return __longlong_as_double(0x7FF0000000000000LL);
+  if (x < -745.1332191019412) return 0.0;
+  const double t = x * 1.44269504088896338700e+00;
+  const int n = static_cast<int>(t >= 0.0 ? t + 0.5 : t - 0.5);
+  const double nd = n;
+  const double r = (x - nd * 6.93147180369123816490e-01) - nd * 1.90821492927058770002e-10;
+  const double c[11] = {1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0,
+                        1.0 / 3628800.0,    1.0 / 362880.0,    1.0 / 40320.0,
+                        1.0 / 5040.0,       1.0 / 720.0,       1.0 / 120.0,
+                        1.0 / 24.0,         1.0 / 6.0};
+  double p = c[0];
+#pragma unroll
+  for (int i = 1; i < 11; ++i) p = p * r + c[i];
+  const double rr = r * r;
+  return (1.0 + r + 0.5 * rr + rr * r * p) * d_pow2i(n);
+}
+__device__ double d_log(double x) {
+  long long b = __double_as_longlong(x);
+  int e = 0;
+  if (b < (1LL << 52)) {
+    x *= 18014398509481984.0;  // 2^54
+    e = -54;
+    b = __double_as_longlong(x);
+  }
+  e += static_cast<int>((b >> 52) & 0x7FF) - 1023;
+  double m = __longlong_as_double((b & ((1LL << 52) - 1)) | (1023LL << 52));
+  if (m > 1.4142135623730951) {
+    m *= 0.5;
+    e += 1;
+  }
+  const double f = m - 1.0, s = f / (2.0 + f), z = s * s, w = z * z;
+  const double t1 = w * (3.999999999940941908e-01 +
+                         w * (2.222219843214978396e-01 + w * 1.531383769920937332e-01));
+  const double t2 = z * (6.666666666666735130e-01 +
+                         w * (2.857142874366239149e-01 +
+                              w * (1.818357216161805012e-01 + w * 1.479819860511658591e-01)));
+  const double hf = 0.5 * f * f, R = t2 + t1, ed = e;
+  return ed * 6.93147180369123816490e-01 -
+         ((hf - (s * (hf + R) + ed * 1.90821492927058770002e-10)) - f);
+}
+__device__ double d_erf(double x) {
+  const double a = x < 0.0 ? -x : x;
+  const double t = 1.0 / (1.0 + 0.3275911 * a);
+  const double poly =
+      t * (0.254829592 +
+           t * (-0.284496736 + t * (1.421413741 + t * (-1.453152027 + t * 1.061405429))));
+  const double y = 1.0 - poly * d_exp(-a * a);
+  return x < 0.0 ? -y : y;
+}
+
+__global__ void build_cdf_kernel(float* scales, uint32_t* cdf) {
+  const int idx = threadIdx.x;
+  if (idx >= kScales) return;
+  const double ratio = d_log(64.0 / 0.11);
+  const float sf = static_cast<float>(0.11 * d_exp(ratio * idx / 63.0));
+  scales[idx] = sf;
+  const double sigma = sf;
+  const double inv = 1.0 / (sigma * 1.4142135623730951);
+  uint32_t freq[kSyms];
+  auto q = [](double p) -> uint32_t {
+    if (p < 0.0) p = 0.0;
+    return 1u + static_cast<uint32_t>(floor(p * 65279.0));
+  };
+  freq[127] = q(d_erf(0.5 * inv));
+  for (int v = 1; v <= 127; ++v) {
+    const double p = 0.5 * (d_erf((v + 0.5) * inv) - d_erf((v - 0.5) * inv));
+    freq[127 + v] = freq[127 - v] = q(p);
+  }
+  freq[kEscLo] = freq[kEscHi] = q(0.5 * (1.0 - d_erf(127.5 * inv)));
+  uint32_t sum = 0;
+  for (int k = 0; k < kSyms; ++k) sum += freq[k];
+  freq[127] += 65536u - sum;
+  uint32_t* c = cdf + idx * (kSyms + 1);
+  c[0] = 0;
+  for (int k = 0; k < kSyms; ++k) c[k + 1] = c[k] + freq[k];
+}
+
+// ------------------------------------------------------------ helpers -----
+__device__ __forceinline__ int scale_index(const float* scales, float sigma) {
+  int lo = 0, hi = kScales;  // first i with scales[i] >= sigma
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (scales[mid] >= sigma)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo < kScales ? lo : kScales - 1;
+}
+
+__device__ __forceinline__ uint32_t rd32(const uint8_t* p) {
+  return p[0] | (p[1] << 8) | (p[2] << 16) | (static_cast<uint32_t>(p[3]) << 24);
+}
+
+__device__ __forceinline__ uint32_t next_byte(const uint8_t* pl, LaneState& s, int& err) {
+  if (s.pos < s.end) return pl[s.pos++];
+  if (s.pos < s.end + 2) {
+    ++s.pos;
+    return 0;
+  }
+  err = 1;
+  return 0;
+}
+
+__device__ __forceinline__ int dec_sym(const uint8_t* pl, LaneState& s, const uint32_t* cum,
+                                       int nsym, int& err) {
+  const uint64_t r = s.range >> 16;
+  if (s.code >= (r << 16)) {
+    err = 1;
+    s.code = (r << 16) - 1;
+  }
+  int lo = 0, hi = nsym;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (r * __ldg(cum + mid) <= s.code)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const uint32_t c0 = __ldg(cum + lo), c1 = __ldg(cum + lo + 1);
+  s.code -= r * c0;
+  s.range = r * (c1 - c0);
+  while (s.range < kBot) {
+    s.code = (s.code << 8) | next_byte(pl, s, err);
+    s.range <<= 8;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ double sym_bits(uint32_t freq) {
+  return 16.0 - log2(static_cast<double>(freq));
+}
+
+// Decodes one value (escape + Exp-Golomb included); returns v.
+__device__ int32_t dec_value(const uint8_t* pl, LaneState& s, const uint32_t* cdf_row, int& err) {
+  const int k = dec_sym(pl, s, cdf_row, kSyms, err);
+  s.bits += sym_bits(__ldg(cdf_row + k + 1) - __ldg(cdf_row + k));
+  if (k < kEscLo) return k - 127;
+  int nb = 0;
+  while (dec_sym(pl, s, kBitCum, 2, err) == 0) {
+    if (++nb > 31 || err) {
+      err = 1;
+      return 0;
+    }
+  }
+  uint64_t x = 1;
+  for (int i = 0; i < nb; ++i) x = (x << 1) | static_cast<uint64_t>(dec_sym(pl, s, kBitCum, 2, err));
+  s.bits += 2 * nb + 1;
+  const long long m = static_cast<long long>(x) - 1 + 128;
+  return static_cast<int32_t>(k == kEscLo ? -m : m);
+}
+
+// ------------------------------------------------------------ kernels -----
+__global__ void lanes_init_kernel(const uint8_t* __restrict__ pl, const uint32_t* __restrict__ len_p,
+                                  int L, uint32_t expect, LaneState* __restrict__ lanes, int* status) {
+  const uint32_t len = *len_p;
+  __shared__ uint64_t part[1024];
+  __shared__ int bad;
+  const int t = threadIdx.x;
+  if (t == 0) bad = 0;
+  __syncthreads();
+  const uint32_t hdr = 8u + 4u * static_cast<uint32_t>(L);
+  if (len < hdr || rd32(pl) != static_cast<uint32_t>(L) || rd32(pl + 4) != expect) {
+    if (t == 0) atomicOr(status, 1);
+    return;
+  }
+  const int per = (L + blockDim.x - 1) / blockDim.x;
+  const int l0 = t * per, l1 = min(L, l0 + per);
+  uint64_t acc = 0;
+  for (int l = l0; l < l1; ++l) acc += rd32(pl + 8 + 4 * l);
+  part[t] = acc;
+  __syncthreads();
+  if (t == 0) {  // exclusive scan of the partials (fixed order)
+    uint64_t run = 0;
+    for (int i = 0; i < static_cast<int>(blockDim.x); ++i) {
+      const uint64_t v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    if (hdr + run > len) bad = 1;
+  }
+  __syncthreads();
+  if (bad) {
+    if (t == 0) atomicOr(status, 1);
+    return;
+  }
+  uint64_t off = hdr + part[t];
+  for (int l = l0; l < l1; ++l) {
+    const uint32_t ln = rd32(pl + 8 + 4 * l);
+    LaneState s;
+    s.pos = static_cast<uint32_t>(off);
+    s.end = static_cast<uint32_t>(off + ln);
+    s.range = kWin;
+    s.code = 0;
+    s.bits = 0.0;
+    int err = ln < 4 ? 1 : 0;
+    for (int b = 0; b < 6; ++b) s.code = (s.code << 8) | next_byte(pl, s, err);
+    if (err) atomicOr(status, 1);
+    lanes[l] = s;
+    off += ln;
+  }
+}
+
+__global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* __restrict__ lanes,
+                                    int L, uint64_t o0, int n, int per,
+                                    const float* __restrict__ musig, int ldms, int sig_off,
+                                    const float* __restrict__ scales, const uint32_t* __restrict__ cdf,
+                                    const int* __restrict__ rows, int32_t* __restrict__ yhat, int C,
+                                    int c0, __half* __restrict__ yhat16, int ld16, int* status) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  const uint64_t total = static_cast<uint64_t>(n) * per;
+  // first ordinal of lane l at or after o0
+  const uint64_t first = o0 + ((static_cast<uint64_t>(l) + L - (o0 % L)) % L);
+  if (first >= o0 + total) return;
+  LaneState s = lanes[l];
+  int err = 0;
+  for (uint64_t o = first; o < o0 + total; o += L) {
+    const int i = static_cast<int>(o - o0);
+    const int k = i / per, j = i - k * per;
+    const float mu = musig[static_cast<size_t>(k) * ldms + j];
+    const float sg = musig[static_cast<size_t>(k) * ldms + sig_off + j];
+    const int idx = scale_index(scales, sg);
+    const int32_t v = dec_value(pl, s, cdf + idx * (kSyms + 1), err);
+    const int32_t y = v + __float2int_rn(mu);
+    yhat[static_cast<size_t>(rows[k]) * C + c0 + j] = y;
+    if (yhat16) yhat16[static_cast<size_t>(k) * ld16 + c0 + j] = __int2half_rn(y);
+  }
+  lanes[l] = s;
+  if (err) atomicOr(status, 2);
+}
+
+__global__ void decode_hyper_kernel(const uint8_t* __restrict__ pl, LaneState* __restrict__ lanes,
+                                    int L, int n, int per_ch, const float* __restrict__ loc,
+                                    const float* __restrict__ scale, const float* __restrict__ scales,
+                                    const uint32_t* __restrict__ cdf, int32_t* __restrict__ zhat,
+                                    int* status) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  LaneState s = lanes[l];
+  int err = 0;
+  for (int i = l; i < n; i += L) {
+    const int ch = i / per_ch;
+    const int idx = scale_index(scales, scale[ch]);
+    const int32_t v = dec_value(pl, s, cdf + idx * (kSyms + 1), err);
+    zhat[i] = v + __float2int_rn(loc[ch]);
+  }
+  lanes[l] = s;
+  if (err) atomicOr(status, 2);
+}
+
+__global__ void quantize_phase_kernel(const float* __restrict__ musig, int ldms, int sig_off, int n,
+                                      int per, uint64_t o0, const int* __restrict__ rows,
+                                      const int32_t* __restrict__ yhat, int C, int c0,
+                                      const float* __restrict__ scales, int32_t* __restrict__ sym_v,
+                                      uint8_t* __restrict__ sym_idx, __half* __restrict__ yhat16,
+                                      int ld16, float* __restrict__ mu_out,
+                                      float* __restrict__ sigma_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * per) return;
+  const int k = i / per, j = i - k * per;
+  const float mu = musig[static_cast<size_t>(k) * ldms + j];
+  const float sg = musig[static_cast<size_t>(k) * ldms + sig_off + j];
+  const size_t e = static_cast<size_t>(rows[k]) * C + c0 + j;
+  const int32_t y = yhat[e];
+  sym_v[o0 + i] = y - __float2int_rn(mu);
+  sym_idx[o0 + i] = static_cast<uint8_t>(scale_index(scales, sg));
+  if (yhat16) yhat16[static_cast<size_t>(k) * ld16 + c0 + j] = __int2half_rn(y);
+  if (mu_out) {
+    mu_out[e] = mu;
+    sigma_out[e] = sg;
+  }
+}
+
+__global__ void quantize_hyper_kernel(const int32_t* __restrict__ zhat, int n, int per_ch,
+                                      const float* __restrict__ loc, const float* __restrict__ scale,
+                                      const float* __restrict__ scales, int32_t* __restrict__ sym_v,
+                                      uint8_t* __restrict__ sym_idx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int ch = i / per_ch;
+  sym_v[i] = zhat[i] - __float2int_rn(loc[ch]);
+  sym_idx[i] = static_cast<uint8_t>(scale_index(scales, scale[ch]));
+}
+
+struct Enc {
+  uint64_t low, range;
+  uint32_t n;
+  bool overflow;
+  uint8_t* out;
+  uint32_t cap;
+  __device__ void carry() {
+    for (uint32_t i = n; i-- > 0;)
+      if (++out[i] != 0) break;
+  }
+  __device__ void emit(uint8_t b) {
+    if (n < cap)
+      out[n++] = b;
+    else
+      overflow = true;
+  }
+  __device__ void put(uint32_t cum, uint32_t freq) {
+    const uint64_t r = range >> 16;
+    low += r * cum;
+    range = r * freq;
+    if (low > kWin) {
+      low &= kWin;
+      carry();
+    }
+    while (range < kBot) {
+      emit(static_cast<uint8_t>(low >> 40));
+      low = (low << 8) & kWin;
+      range <<= 8;
+    }
+  }
+};
+
+__global__ void encode_lanes_kernel(const int32_t* __restrict__ sym_v, const uint8_t* __restrict__ sym_idx,
+                                    uint64_t n, int L, const uint32_t* __restrict__ cdf,
+                                    uint8_t* __restrict__ out, uint32_t cap, uint32_t* __restrict__ lens,
+                                    double* __restrict__ bits, int* status) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  Enc e{0, kWin, 0, false, out + static_cast<size_t>(l) * cap, cap};
+  double b = 0.0;
+  for (uint64_t o = l; o < n; o += L) {
+    const int32_t v = sym_v[o];
+    const uint32_t* c = cdf + sym_idx[o] * (kSyms + 1);
+    const int k = v < -127 ? kEscLo : (v > 127 ? kEscHi : v + 127);
+    const uint32_t c0 = __ldg(c + k), c1 = __ldg(c + k + 1);
+    e.put(c0, c1 - c0);
+    b += sym_bits(c1 - c0);
+    if (k >= kEscLo) {
+      const uint64_t x = static_cast<uint64_t>(v < 0 ? -static_cast<int64_t>(v) : v) - 128 + 1;
+      int nb = 0;
+      while ((x >> (nb + 1)) != 0) ++nb;
+      for (int i = 0; i < nb; ++i) e.put(0u, 32768u);
+      for (int i = nb; i >= 0; --i) e.put(((x >> i) & 1) ? 32768u : 0u, 32768u);
+      b += 2 * nb + 1;
+    }
+  }
+  uint64_t v = (e.low + 0xFFFF) & ~uint64_t{0xFFFF};
+  if (v > kWin) {
+    v &= kWin;
+    e.carry();
+  }
+  for (int sh = 40; sh >= 16; sh -= 8) e.emit(static_cast<uint8_t>(v >> sh));
+  lens[l] = e.n;
+  bits[l] = b;
+  if (e.overflow) atomicOr(status, 4);
+}
+
+__global__ void sum_bits_kernel(const double* __restrict__ v, int stride, int L, double* out) {
+  __shared__ double part[256];
+  const int t = threadIdx.x;
+  const int per = (L + 255) / 256;
+  double acc = 0.0;
+  for (int l = t * per; l < min(L, (t + 1) * per); ++l) acc += v[static_cast<size_t>(l) * stride];
+  part[t] = acc;
+  __syncthreads();
+  if (t == 0) {
+    double s = 0.0;
+    for (int i = 0; i < 256; ++i) s += part[i];
+    *out = s;
+  }
+}
+
+inline int blocks(long n, int t = 128) { return static_cast<int>((n + t - 1) / t); }
+
+}  // namespace
+
+void build_cdf_tables(float* scales, uint32_t* cdf, cudaStream_t st) {
+  build_cdf_kernel<<<1, kScales, 0, st>>>(scales, cdf);
+  PSWA_LAUNCH_CHECK();
+}
+
+void lanes_init(const uint8_t* payload, const uint32_t* len, int lanes, uint32_t expect_count,
+                LaneState* st_lanes, int* status, cudaStream_t st) {
+  lanes_init_kernel<<<1, 1024, 0, st>>>(payload, len, lanes, expect_count, st_lanes, status);
+  PSWA_LAUNCH_CHECK();
+}
+
+void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_t o0, int n,
+                        int per, const float* musig, int ldms, int sig_off, const float* scales,
+                        const uint32_t* cdf, const int* rows, int32_t* yhat, int C, int c0,
+                        __half* yhat16, int ld16, int* status, cudaStream_t st) {
+  if (n <= 0) return;
+  decode_phase_kernel<<<blocks(L), 128, 0, st>>>(payload, lanes, L, o0, n, per, musig, ldms,
+                                                  sig_off, scales, cdf, rows, yhat, C, c0, yhat16,
+                                                  ld16, status);
+  PSWA_LAUNCH_CHECK();
+}
+
+void lanes_decode_hyper(const uint8_t* payload, LaneState* lanes, int L, int n, int per_ch,
+                        const float* loc, const float* scale, const float* scales,
+                        const uint32_t* cdf, int32_t* zhat, int* status, cudaStream_t st) {
+  decode_hyper_kernel<<<blocks(L), 128, 0, st>>>(payload, lanes, L, n, per_ch, loc, scale, scales,
+                                                  cdf, zhat, status);
+  PSWA_LAUNCH_CHECK();
+}
+
+void quantize_phase(const float* musig, int ldms, int sig_off, int n, int per, uint64_t o0,
+                    const int* rows, const int32_t* yhat, int C, int c0, const float* scales,
+                    int32_t* sym_v, uint8_t* sym_idx, __half* yhat16, int ld16, float* mu_out,
+                    float* sigma_out, cudaStream_t st) {
+  if (n <= 0) return;
+  quantize_phase_kernel<<<blocks(static_cast<long>(n) * per, 256), 256, 0, st>>>(
+      musig, ldms, sig_off, n, per, o0, rows, yhat, C, c0, scales, sym_v, sym_idx, yhat16, ld16,
+      mu_out, sigma_out);
+  PSWA_LAUNCH_CHECK();
+}
+
+void quantize_hyper(const int32_t* zhat, int n, int per_ch, const float* loc, const float* scale,
+                    const float* scales, int32_t* sym_v, uint8_t* sym_idx, cudaStream_t st) {
+  quantize_hyper_kernel<<<blocks(n, 256), 256, 0, st>>>(zhat, n, per_ch, loc, scale, scales, sym_v,
+                                                        sym_idx);
+  PSWA_LAUNCH_CHECK();
+}
+
+void lanes_encode(const int32_t* sym_v, const uint8_t* sym_idx, uint64_t n, int L,
+                  const uint32_t* cdf, uint8_t* out, uint32_t cap, uint32_t* lens, double* bits,
+                  int* status, cudaStream_t st) {
+  encode_lanes_kernel<<<blocks(L), 128, 0, st>>>(sym_v, sym_idx, n, L, cdf, out, cap, lens, bits,
+                                                  status);
+  PSWA_LAUNCH_CHECK();
+}
+
+void sum_lane_bits(const LaneState* lanes, int L, double* out, cudaStream_t st) {
+  sum_bits_kernel<<<1, 256, 0, st>>>(&lanes[0].bits, static_cast<int>(sizeof(LaneState) / 8), L,
+                                     out);
+  PSWA_LAUNCH_CHECK();
+}
+
+void sum_doubles(const double* v, int L, double* out, cudaStream_t st) {
+  sum_bits_kernel<<<1, 256, 0, st>>>(v, 1, L, out);
+  PSWA_LAUNCH_CHECK();
+}
+
+}  // namespace pswa_dev
+
+namespace pswa_dev {
+namespace {
+__global__ void pack_offsets_kernel(const uint32_t* __restrict__ lens, int L, uint32_t count,
+                                    uint8_t* __restrict__ payload, uint64_t cap,
+                                    unsigned long long* total, uint64_t* __restrict__ offs, int* status) {
+  __shared__ uint64_t part[1024];
+  const int t = threadIdx.x;
+  const int per = (L + blockDim.x - 1) / blockDim.x;
+  const int l0 = t * per, l1 = min(L, l0 + per);
+  uint64_t acc = 0;
+  for (int l = l0; l < l1; ++l) acc += lens[l];
+  part[t] = acc;
+  __syncthreads();
+  if (t == 0) {
+    uint64_t run = 0;
+    for (int i = 0; i < static_cast<int>(blockDim.x); ++i) {
+      const uint64_t v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    const uint64_t hdr = 8 + 4ull * L;
+    *total = hdr + run;
+    if (hdr + run > cap) atomicOr(status, 8);
+  }
+  __syncthreads();
+  const uint64_t hdr = 8 + 4ull * L;
+  uint64_t off = hdr + part[t];
+  for (int l = l0; l < l1; ++l) {
+    offs[l] = off;
+    off += lens[l];
+  }
+  auto wr32 = [&](uint64_t at, uint32_t v) {
+    if (at + 4 <= cap)
+      for (int b = 0; b < 4; ++b) payload[at + b] = static_cast<uint8_t>(v >> (8 * b));
+  };
+  if (t == 0) {
+    wr32(0, static_cast<uint32_t>(L));
+    wr32(4, count);
+  }
+  for (int l = l0; l < l1; ++l) wr32(8 + 4ull * l, lens[l]);
+}
+
+__global__ void pack_copy_kernel(const uint8_t* __restrict__ enc, uint32_t cap_lane,
+                                 const uint32_t* __restrict__ lens, const uint64_t* __restrict__ offs,
+                                 int L, uint8_t* __restrict__ payload, uint64_t cap) {
+  const int l = blockIdx.x;
+  if (l >= L) return;
+  const uint64_t off = offs[l];
+  const uint32_t n = lens[l];
+  if (off + n > cap) return;
+  const uint8_t* src = enc + static_cast<size_t>(l) * cap_lane;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) payload[off + i] = src[i];
+}
+}  // namespace
+
+void lanes_pack(const uint8_t* enc, uint32_t cap, const uint32_t* lens, int L, uint32_t count,
+                uint8_t* payload, uint64_t payload_cap, unsigned long long* total, uint64_t* offs,
+                int* status, cudaStream_t st) {
+  pack_offsets_kernel<<<1, 1024, 0, st>>>(lens, L, count, payload, payload_cap, total, offs, status);
+  PSWA_LAUNCH_CHECK();
+  pack_copy_kernel<<<L, 64, 0, st>>>(enc, cap, lens, offs, L, payload, payload_cap);
+  PSWA_LAUNCH_CHECK();
+}
+
+}  // namespace pswa_dev

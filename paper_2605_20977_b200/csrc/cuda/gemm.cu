@@ -50,6 +50,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, int m, int n0,
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
   const int orow = ep.row_map ? ep.row_map[m] : m;
+  if (orow < 0) return;
 
   if (ep.act == kActSwiGLU) {
     // pairs (gate, up) -> one output column each; output col = n0/2 + j
@@ -89,8 +90,13 @@ __device__ __forceinline__ void epilogue_chunk(const GemmEpi& ep, int m, int n0,
         x = 0.11f + softplus_f(x + b);
       }
     } else {
-      if (ep.scale) x *= ep.scale[n];
-      if (ep.bias) x += ep.bias[n];
+      if (ep.bias_first) {
+        if (ep.bias) x += ep.bias[n];
+        if (ep.scale) x *= ep.scale[n];
+      } else {
+        if (ep.scale) x *= ep.scale[n];
+        if (ep.bias) x += ep.bias[n];
+      }
       if (ep.act == kActSilu) x = silu_f(x);
     }
     v[j] = x;
@@ -286,23 +292,23 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   p->epi = epi;
   make_tmap(&p->ta, A, lda, M, K, kBM);
   make_tmap(&p->tb, B, ldb, N, K, bn);
+  if (bn == 64) set_smem_attr<64>();
+  if (bn == 128) set_smem_attr<128>();
+  if (bn == 256) set_smem_attr<256>();
 }
 
 void gemm_run(const GemmPlan& p, cudaStream_t stream) {
   dim3 grid((p.M + kBM - 1) / kBM, p.N / p.BN);
   switch (p.BN) {
     case 64:
-      set_smem_attr<64>();
       gemm_tc_kernel<64><<<grid, kThreads, GemmCfg<64>::kSmem, stream>>>(p.ta, p.tb, p.M, p.K,
                                                                          p.epi);
       break;
     case 128:
-      set_smem_attr<128>();
       gemm_tc_kernel<128><<<grid, kThreads, GemmCfg<128>::kSmem, stream>>>(p.ta, p.tb, p.M,
                                                                            p.K, p.epi);
       break;
     case 256:
-      set_smem_attr<256>();
       gemm_tc_kernel<256><<<grid, kThreads, GemmCfg<256>::kSmem, stream>>>(p.ta, p.tb, p.M,
                                                                            p.K, p.epi);
       break;

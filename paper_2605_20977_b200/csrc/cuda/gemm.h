@@ -26,9 +26,10 @@ struct GemmEpi {
   int accumulate = 0;      // fp32 only: out += value (residual stream)
   const float* bias = nullptr;   // [N] (nullable)
   const float* scale = nullptr;  // [N] (nullable): v = acc*scale + bias
+  int bias_first = 0;            // v = (acc + bias) * scale instead
   int act = kActNone;
   int split = 0;                 // kActHead: first sigma column
-  const int* row_map = nullptr;  // nullable: output row = row_map[m]
+  const int* row_map = nullptr;  // nullable: output row = row_map[m] (< 0: skip)
   int n_store = 1 << 30;         // output columns >= n_store are not written
 };
 

@@ -1,0 +1,111 @@
+// Launchers for the non-GEMM sm_100a kernels of the decode path.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pswa_dev {
+
+// ---- rows: norms, casts, gathers (norm.cu) -------------------------------
+// y[i] = rmsnorm(x[src ? src[i] : i]) per `group` columns, times gain, fp16.
+// Matches tensor.cpp:81-86 (eps 1e-5) up to reduction order.
+void rmsnorm_rows(const float* x, int ldx, const int* src_rows, int M, int d, int group,
+                  const float* gain, __half* y, int ldy, cudaStream_t st);
+// dst[i][0:n] = src[rows ? rows[i] : i][0:n] (fp32)
+void gather_rows_f32(const float* src, int lds, const int* rows, int M, int n, float* dst,
+                     int ldd, cudaStream_t st);
+// dst[i][0:ncols] = half(yhat[rows[i]][c0 : c0+nc]), zero in [nc, ncols)
+void yhat_rows_f16(const int32_t* yhat, int C, const int* rows, int M, int c0, int nc, __half* dst,
+                   int ldd, int ncols, cudaStream_t st);
+void f32_to_f16_rows(const float* src, int lds, int M, int n, __half* dst, int ldd, int ncols,
+                     cudaStream_t st);
+// Broadcast a vector into M rows (learned pad) or copy rows from a source.
+// slot_src[k] >= 0 selects ring buffer ring[slot_src[k]], -1 the pad vector.
+void fill_context_slots(const float* const* ring, const int* slot_src, const float* pad, int T,
+                        int HW, int d, float* x, cudaStream_t st);
+// frame [HW][C] int32 -> [C][HW] int32
+void yhat_to_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st);
+void yhat_from_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st);
+void scatter_rows_f16(const __half* src, int lds, const int* rows, int M, int n, __half* dst,
+                      int ldd, cudaStream_t st);
+
+// ---- windowed attention (attention.cu) -----------------------------------
+// Queries: rows of q (fp16, head h at columns h*hd), qinfo[i] = slot<<24 |
+// y<<12 | x. Keys/values: kv rows (slot*kv_slot_stride + y*W + x), K at
+// column h*hd, V at column d + h*hd. Window win_h x win_w (x win_t slots
+// back when win_t > 0), out-of-bounds keys masked, mask: 0 none, 1 step <=,
+// 2 step <. bias[h][taps]. Zero allowed keys
+// -> zero output.
+void window_attention(const __half* q, int ldq, const int32_t* qinfo, int Mq, const __half* kv,
+                      int ldkv, int kv_slot_stride, int H, int W, int heads, int hd, int win_h,
+                      int win_w, int win_t, int mask, int s, const float* bias, __half* out,
+                      int ldo, cudaStream_t st);
+
+// ---- convolutions for the hyperprior (conv.cu) ---------------------------
+// NHWC fp32 input [h][w][c] -> fp16 patches [oh*ow][kcols], K order
+// (ky, kx, c), zero padding 1 for 3x3. up2: input is read at (y/2, x/2) of a
+// half-resolution grid (nearest x2 folded into the addressing).
+void im2col3x3(const float* x, int h, int w, int c, int stride, int up2, __half* out, int kcols,
+               cudaStream_t st);
+// out[y][x][:] = x[y/2][x/2][:] (fp32, NHWC) or subsample x[2y][2x]
+void upsample2_nhwc(const float* x, int h, int w, int c, float* out, cudaStream_t st);
+void subsample2_nhwc(const float* x, int h, int w, int c, float* out, cudaStream_t st);
+// z_hat [c][h][w] int32 -> NHWC fp32
+void zhat_to_nhwc(const int32_t* z, int c, int hw, float* out, cudaStream_t st);
+// NHWC fp32 -> rounded int32 [c][h][w] (half-to-even)
+void round_to_zhat(const float* x, int c, int hw, int32_t* z, cudaStream_t st);
+
+// ---- entropy coding (coder.cu) -------------------------------------------
+constexpr int kScales = 64;
+constexpr int kSyms = 257;  // v in [-127,127] + 2 escapes
+// Builds the 64 scale entries and 64 x 258 cumulative tables on the device
+// in fp64 with IEEE round-to-nearest ops only (bit-exact with the host rule).
+void build_cdf_tables(float* scales, uint32_t* cdf, cudaStream_t st);
+
+struct LaneState {
+  uint64_t code, range;  // decoder: code; encoder: low
+  uint32_t pos, end;     // byte offsets into the payload
+  double bits;           // estimated bits of this lane's symbols
+};
+
+// Parses a lane payload header in device memory and initialises lane states.
+// status[0] |= 1 on malformed payload.
+void lanes_init(const uint8_t* payload, const uint32_t* len, int lanes, uint32_t expect_count,
+                LaneState* st_lanes, int* status, cudaStream_t st);
+// Decodes one phase of the main payload: symbols [o0, o0 + n*per) where
+// ordinal o0 + k*per + j is channel c0 + j of batch position k. mu/sigma are
+// read from musig[k][j] / musig[k][sig_off + j]; y_hat = v + rint(mu) is
+// written to yhat[rows[k]][c0 + j] and to yhat16[k][c0 + j] (nullable).
+void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_t o0, int n,
+                        int per, const float* musig, int ldms, int sig_off, const float* scales,
+                        const uint32_t* cdf, const int* rows, int32_t* yhat, int C, int c0,
+                        __half* yhat16, int ld16, int* status, cudaStream_t st);
+// Hyper payload: ordinal i -> channel i / per_ch; mean/scale from the prior
+// bank entry; writes z_hat [c][h][w].
+void lanes_decode_hyper(const uint8_t* payload, LaneState* lanes, int L, int n, int per_ch,
+                        const float* loc, const float* scale, const float* scales,
+                        const uint32_t* cdf, int32_t* zhat, int* status, cudaStream_t st);
+// Encoder side of one phase: v = y_hat - rint(mu), idx = scale_index(sigma)
+// into sym_v / sym_idx at ordinals [o0, ...); also fills yhat16 from y_hat.
+void quantize_phase(const float* musig, int ldms, int sig_off, int n, int per, uint64_t o0,
+                    const int* rows, const int32_t* yhat, int C, int c0, const float* scales,
+                    int32_t* sym_v, uint8_t* sym_idx, __half* yhat16, int ld16,
+                    float* mu_out, float* sigma_out, cudaStream_t st);
+void quantize_hyper(const int32_t* zhat, int n, int per_ch, const float* loc, const float* scale,
+                    const float* scales, int32_t* sym_v, uint8_t* sym_idx, cudaStream_t st);
+// Encodes n symbols into L lanes: lane l writes at out + l*cap; lens[l]
+// receives its length (or status |= 2 on overflow); bits[l] its estimate.
+void lanes_encode(const int32_t* sym_v, const uint8_t* sym_idx, uint64_t n, int L,
+                  const uint32_t* cdf, uint8_t* out, uint32_t cap, uint32_t* lens, double* bits,
+                  int* status, cudaStream_t st);
+// Sum of per-lane bit estimates in lane order (deterministic).
+void sum_lane_bits(const LaneState* lanes, int L, double* out, cudaStream_t st);
+void sum_doubles(const double* v, int L, double* out, cudaStream_t st);
+// Packs L encoded lanes (lane l at enc + l*cap, lens[l]) into the lane
+// payload format; *total receives the payload size (device int64).
+void lanes_pack(const uint8_t* enc, uint32_t cap, const uint32_t* lens, int L, uint32_t count,
+                uint8_t* payload, uint64_t payload_cap, unsigned long long* total, uint64_t* offs,
+                int* status, cudaStream_t st);
+
+}  // namespace pswa_dev

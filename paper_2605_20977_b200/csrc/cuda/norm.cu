@@ -1,0 +1,169 @@
+// Row kernels: RMSNorm (tensor.cpp:81-86 semantics, eps 1e-5, optional
+// per-group normalisation for the channel transformer), gathers, casts.
+// All HBM-bound: one warp per row, coalesced 128 B accesses.
+#include "check.h"
+#include "kernels.h"
+
+namespace pswa_dev {
+
+namespace {
+
+__global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ src,
+                               int M, int d, int group, const float* __restrict__ gain,
+                               __half* __restrict__ y, int ldy) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float* xr = x + static_cast<size_t>(src ? src[row] : row) * ldx;
+  __half* yr = y + static_cast<size_t>(row) * ldy;
+  for (int g0 = 0; g0 < d; g0 += group) {
+    float ss = 0.0f;
+    for (int i = lane; i < group; i += 32) {
+      const float v = xr[g0 + i];
+      ss += v * v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float inv = 1.0f / sqrtf(ss / static_cast<float>(group) + 1e-5f);
+    for (int i = lane; i < group; i += 32)
+      yr[g0 + i] = __float2half_rn(gain[g0 + i] * xr[g0 + i] * inv);
+  }
+}
+
+__global__ void gather_f32_kernel(const float* __restrict__ src, int lds, const int* __restrict__ rows,
+                                  int M, int n, float* __restrict__ dst, int ldd) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float* s = src + static_cast<size_t>(rows ? rows[row] : row) * lds;
+  float* o = dst + static_cast<size_t>(row) * ldd;
+  if ((n & 3) == 0 && (lds & 3) == 0 && (ldd & 3) == 0) {
+    const float4* s4 = reinterpret_cast<const float4*>(s);
+    float4* o4 = reinterpret_cast<float4*>(o);
+    for (int i = lane; i < n / 4; i += 32) o4[i] = s4[i];
+  } else {
+    for (int i = lane; i < n; i += 32) o[i] = s[i];
+  }
+}
+
+__global__ void yhat_f16_kernel(const int32_t* __restrict__ yhat, int C, const int* __restrict__ rows,
+                                int M, int c0, int nc, __half* __restrict__ dst, int ldd, int ncols) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const int32_t* s = yhat + static_cast<size_t>(rows ? rows[row] : row) * C + c0;
+  __half* o = dst + static_cast<size_t>(row) * ldd;
+  for (int i = lane; i < ncols; i += 32)
+    o[i] = i < nc ? __int2half_rn(s[i]) : __float2half_rn(0.0f);
+}
+
+__global__ void f32_to_f16_kernel(const float* __restrict__ src, int lds, int M, int n,
+                                  __half* __restrict__ dst, int ldd, int ncols) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float* s = src + static_cast<size_t>(row) * lds;
+  __half* o = dst + static_cast<size_t>(row) * ldd;
+  for (int i = lane; i < ncols; i += 32) o[i] = __float2half_rn(i < n ? s[i] : 0.0f);
+}
+
+__global__ void fill_slots_kernel(const float* const* __restrict__ ring, const int* __restrict__ slot_src,
+                                  const float* __restrict__ pad, int T, int HW, int d,
+                                  float* __restrict__ x) {
+  const size_t total = static_cast<size_t>(T) * HW * (d / 4);
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int c4 = static_cast<int>(i % (d / 4));
+    const size_t r = i / (d / 4);
+    const int t = static_cast<int>(r / HW);
+    const int p = static_cast<int>(r % HW);
+    const int k = slot_src[t];
+    const float4 v = k >= 0 ? reinterpret_cast<const float4*>(ring[k] + static_cast<size_t>(p) * d)[c4]
+                            : reinterpret_cast<const float4*>(pad)[c4];
+    reinterpret_cast<float4*>(x)[i] = v;
+  }
+}
+
+__global__ void transpose_i32_kernel(const int32_t* __restrict__ src, int rows, int cols,
+                                     int32_t* __restrict__ dst) {
+  __shared__ int32_t tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int r = by + j, c = bx + threadIdx.x;
+    if (r < rows && c < cols) tile[j][threadIdx.x] = src[static_cast<size_t>(r) * cols + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int c = bx + j, r = by + threadIdx.x;
+    if (r < rows && c < cols) dst[static_cast<size_t>(c) * rows + r] = tile[threadIdx.x][j];
+  }
+}
+
+__global__ void scatter_f16_kernel(const __half* __restrict__ src, int lds, const int* __restrict__ rows,
+                                   int M, int n, __half* __restrict__ dst, int ldd) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const __half* s = src + static_cast<size_t>(row) * lds;
+  __half* o = dst + static_cast<size_t>(rows[row]) * ldd;
+  for (int i = lane; i < n; i += 32) o[i] = s[i];
+}
+
+inline int warp_grid(int M) { return (M + 7) / 8; }
+
+}  // namespace
+
+void rmsnorm_rows(const float* x, int ldx, const int* src_rows, int M, int d, int group,
+                  const float* gain, __half* y, int ldy, cudaStream_t st) {
+  if (M <= 0) return;
+  rmsnorm_kernel<<<warp_grid(M), 256, 0, st>>>(x, ldx, src_rows, M, d, group, gain, y, ldy);
+  PSWA_LAUNCH_CHECK();
+}
+
+void gather_rows_f32(const float* src, int lds, const int* rows, int M, int n, float* dst, int ldd,
+                     cudaStream_t st) {
+  if (M <= 0) return;
+  gather_f32_kernel<<<warp_grid(M), 256, 0, st>>>(src, lds, rows, M, n, dst, ldd);
+  PSWA_LAUNCH_CHECK();
+}
+
+void yhat_rows_f16(const int32_t* yhat, int C, const int* rows, int M, int c0, int nc, __half* dst,
+                   int ldd, int ncols, cudaStream_t st) {
+  if (M <= 0) return;
+  yhat_f16_kernel<<<warp_grid(M), 256, 0, st>>>(yhat, C, rows, M, c0, nc, dst, ldd, ncols);
+  PSWA_LAUNCH_CHECK();
+}
+
+void f32_to_f16_rows(const float* src, int lds, int M, int n, __half* dst, int ldd, int ncols,
+                     cudaStream_t st) {
+  if (M <= 0) return;
+  f32_to_f16_kernel<<<warp_grid(M), 256, 0, st>>>(src, lds, M, n, dst, ldd, ncols);
+  PSWA_LAUNCH_CHECK();
+}
+
+void fill_context_slots(const float* const* ring, const int* slot_src, const float* pad, int T,
+                        int HW, int d, float* x, cudaStream_t st) {
+  fill_slots_kernel<<<148 * 8, 256, 0, st>>>(ring, slot_src, pad, T, HW, d, x);
+  PSWA_LAUNCH_CHECK();
+}
+
+void yhat_to_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st) {
+  dim3 grid((C + 31) / 32, (HW + 31) / 32);
+  transpose_i32_kernel<<<grid, dim3(32, 8), 0, st>>>(src, HW, C, dst);
+  PSWA_LAUNCH_CHECK();
+}
+
+void yhat_from_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st) {
+  dim3 grid((HW + 31) / 32, (C + 31) / 32);
+  transpose_i32_kernel<<<grid, dim3(32, 8), 0, st>>>(src, C, HW, dst);
+  PSWA_LAUNCH_CHECK();
+}
+
+void scatter_rows_f16(const __half* src, int lds, const int* rows, int M, int n, __half* dst,
+                      int ldd, cudaStream_t st) {
+  if (M <= 0) return;
+  scatter_f16_kernel<<<warp_grid(M), 256, 0, st>>>(src, lds, rows, M, n, dst, ldd);
+  PSWA_LAUNCH_CHECK();
+}
+
+}  // namespace pswa_dev

@@ -1,0 +1,177 @@
+// C ABI: frame-level entry points (include/pswa/pswa_cuda.h).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+
+#include "../cuda/check.h"
+#include "../cuda/kernels.h"
+#include "abi_util.h"
+#include "engine.h"
+#include "model_spec.h"
+#include "pswa/pswa_cuda.h"
+
+struct pswa_gpu {
+  std::unique_ptr<pswa_host::Engine> eng;
+};
+
+using pswa_abi::guard;
+
+extern "C" {
+
+void pswa_cfg_preset(pswa_cfg* c, int preset, int height, int width) {
+  std::memset(c, 0, sizeof(*c));
+  const bool paper = preset != 0;
+  c->d_spatial = paper ? 512 : 64;
+  c->heads = 16;
+  c->ctx_blocks = c->s1_blocks = c->s2_blocks = paper ? 8 : 2;
+  c->d_channel = paper ? 1024 : 128;
+  c->ch_blocks = 2;
+  c->hyper_ch = paper ? 128 : 32;
+  c->latent_ch = 192;
+  c->s = 4;
+  c->n_groups = 4;
+  c->win_h = c->win_w = 7;
+  c->win_t = 5;
+  c->ctx_slots = 4;
+  c->rate_points = 4;
+  c->height = height;
+  c->width = width;
+  c->lanes = 1;
+  c->hyper_lanes = 1;
+}
+
+int pswa_gen_weights(const pswa_cfg* cfg, uint64_t seed, void* buf, size_t cap, size_t* len) {
+  return guard([&] {
+    const auto blob = pswa_host::gen_weights_psww(*cfg, seed);
+    *len = blob.size();
+    if (buf) {
+      if (cap < blob.size()) throw std::invalid_argument("pswa_gen_weights: buffer too small");
+      std::memcpy(buf, blob.data(), blob.size());
+    }
+  });
+}
+
+int pswa_synth_latent(const pswa_cfg* cfg, int gop, int frame_idx, int32_t* out) {
+  return guard([&] {
+    pswa_host::validate_cfg(*cfg);
+    pswa_host::synth_latent(*cfg, gop, frame_idx, out);
+  });
+}
+
+int pswa_gpu_create(int device, const pswa_cfg* cfg, const void* blob, size_t len, pswa_gpu** out) {
+  *out = nullptr;
+  return guard([&] {
+    auto h = std::make_unique<pswa_gpu>();
+    h->eng = std::make_unique<pswa_host::Engine>(device, *cfg, blob, len);
+    *out = h.release();
+  });
+}
+
+void pswa_gpu_destroy(pswa_gpu* h) { delete h; }
+
+int pswa_gpu_reset_gop(pswa_gpu* h) {
+  return guard([&] { h->eng->reset_gop(); });
+}
+
+int pswa_gpu_push_frame(pswa_gpu* h, const int32_t* yhat, int rate_idx) {
+  return guard([&] { h->eng->push_frame(yhat, rate_idx); });
+}
+
+int pswa_gpu_encode_frame(pswa_gpu* h, const int32_t* yhat, int rate_idx, int frame_idx_in_gop,
+                          uint8_t* hyper_out, size_t hyper_cap, size_t* hyper_len,
+                          uint8_t* main_out, size_t main_cap, size_t* main_len, double* bits_out) {
+  return guard([&] {
+    const auto r = h->eng->encode(yhat, rate_idx, frame_idx_in_gop, nullptr, nullptr, nullptr,
+                                  hyper_out, hyper_cap, main_out, main_cap, /*advance=*/true);
+    *hyper_len = r.hyper_len;
+    *main_len = r.main_len;
+    if (bits_out) {
+      bits_out[0] = r.bits[0];
+      bits_out[1] = r.bits[1];
+    }
+  });
+}
+
+int pswa_gpu_decode_frame(pswa_gpu* h, const uint8_t* hyper, size_t hyper_len,
+                          const uint8_t* main_payload, size_t main_len, int rate_idx,
+                          int frame_idx_in_gop, int advance_state, int32_t* yhat_out,
+                          double* bits_out) {
+  return guard([&] {
+    const auto r = h->eng->decode(hyper, hyper_len, main_payload, main_len, rate_idx,
+                                  frame_idx_in_gop, advance_state != 0, yhat_out, false);
+    if (bits_out) {
+      bits_out[0] = r.bits[0];
+      bits_out[1] = r.bits[1];
+    }
+  });
+}
+
+int pswa_gpu_decode_frame_device(pswa_gpu* h, const void* d_hyper, size_t hyper_len,
+                                 const void* d_main, size_t main_len, int rate_idx,
+                                 int frame_idx_in_gop, int advance_state, void* d_yhat_out) {
+  return guard([&] {
+    h->eng->decode(d_hyper, hyper_len, d_main, main_len, rate_idx, frame_idx_in_gop,
+                   advance_state != 0, static_cast<int32_t*>(d_yhat_out), true);
+  });
+}
+
+int pswa_gpu_forward_params(pswa_gpu* h, const int32_t* yhat, const int32_t* zhat, int rate_idx,
+                            int frame_idx_in_gop, float* mu_out, float* sigma_out,
+                            double* bits_out) {
+  return guard([&] {
+    if (!mu_out || !sigma_out) throw std::invalid_argument("mu_out / sigma_out required");
+    const auto r = h->eng->encode(yhat, rate_idx, frame_idx_in_gop, zhat, mu_out, sigma_out,
+                                  nullptr, 0, nullptr, 0, /*advance=*/false);
+    if (bits_out) {
+      bits_out[0] = r.bits[0];
+      bits_out[1] = r.bits[1];
+    }
+  });
+}
+
+int pswa_gpu_last_zhat(pswa_gpu* h, int32_t* zhat_out) {
+  return guard([&] { h->eng->last_zhat(zhat_out); });
+}
+
+int pswa_gpu_last_launch_count(pswa_gpu* h) { return h->eng->last_launches(); }
+
+void* pswa_gpu_stream(pswa_gpu* h) { return h->eng->stream(); }
+
+// ---- operator-level -------------------------------------------------------
+int pswa_gpu_op_rmsnorm(const float* x, int ld_x, int M, int d, int group, const float* gain,
+                        void* y, int ld_y, void* stream) {
+  return guard([&] {
+    pswa_dev::rmsnorm_rows(x, ld_x, nullptr, M, d, group, gain, static_cast<__half*>(y), ld_y,
+                           static_cast<cudaStream_t>(stream));
+  });
+}
+
+int pswa_gpu_op_window_attn(const void* q, int ld_q, const int32_t* qinfo, int Mq, const void* kv,
+                            int ld_kv, int kv_slot_stride, int H, int W, int heads, int head_dim,
+                            int win_h, int win_w, int win_t, int mask, int s, const float* bias,
+                            void* out, int ld_out, void* stream) {
+  return guard([&] {
+    pswa_dev::window_attention(static_cast<const __half*>(q), ld_q, qinfo, Mq,
+                               static_cast<const __half*>(kv), ld_kv, kv_slot_stride, H, W, heads,
+                               head_dim, win_h, win_w, win_t, mask, s, bias,
+                               static_cast<__half*>(out), ld_out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int pswa_gpu_op_build_cdf(uint32_t* cdf_out, float* scales_out) {
+  return guard([&] {
+    float* ds = nullptr;
+    uint32_t* dc = nullptr;
+    PSWA_CUDA(cudaMalloc(&ds, sizeof(float) * pswa_dev::kScales));
+    PSWA_CUDA(cudaMalloc(&dc, sizeof(uint32_t) * pswa_dev::kScales * (pswa_dev::kSyms + 1)));
+    pswa_dev::build_cdf_tables(ds, dc, nullptr);
+    PSWA_CUDA(cudaMemcpy(scales_out, ds, sizeof(float) * pswa_dev::kScales, cudaMemcpyDeviceToHost));
+    PSWA_CUDA(cudaMemcpy(cdf_out, dc, sizeof(uint32_t) * pswa_dev::kScales * (pswa_dev::kSyms + 1),
+                         cudaMemcpyDeviceToHost));
+    cudaFree(ds);
+    cudaFree(dc);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,889 @@
+// Engine: weight packing, device buffers and the per-frame programs.
+// See engine.h for the frame schedule; DESIGN.md for layouts and rooflines.
+#include "engine.h"
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+
+#include "../cuda/check.h"
+#include "abi_util.h"
+
+namespace pswa_host {
+
+using pswa_dev::GemmEpi;
+using pswa_dev::kActHead;
+using pswa_dev::kActSilu;
+using pswa_dev::kActSwiGLU;
+
+namespace {
+
+const HostTensor& W(const WeightMap& w, const std::string& n) {
+  auto it = w.find(n);
+  if (it == w.end()) throw std::invalid_argument("missing weight " + n);
+  return it->second;
+}
+
+// Host-side fp16 packing: dst[(row_off + o) * ldk + col_off + i] = src[i][o]
+// for a linear layer stored [in][out] (reference matmul convention).
+void put_linear(std::vector<__half>& dst, int ldk, const float* src, int in, int out, int row_off,
+                int col_off) {
+  for (int o = 0; o < out; ++o)
+    for (int i = 0; i < in; ++i)
+      dst[static_cast<size_t>(row_off + o) * ldk + col_off + i] =
+          __float2half_rn(src[static_cast<size_t>(i) * out + o]);
+}
+
+std::vector<int> positions(int H, int W, int s, int t) {
+  std::vector<int> v;
+  for (int y = 0; y < H; ++y)
+    for (int x = 0; x < W; ++x)
+      if ((y + x) % s == t) v.push_back(y * W + x);
+  return v;
+}
+
+}  // namespace
+
+template <class T>
+T* Engine::dalloc(size_t n) {
+  void* p = nullptr;
+  const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+  PSWA_CUDA(cudaMalloc(&p, bytes));
+  PSWA_CUDA(cudaMemsetAsync(p, 0, bytes, st_));
+  allocs_.push_back(p);
+  return static_cast<T*>(p);
+}
+
+Engine::Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len)
+    : D_((validate_cfg(cfg), cfg)), device_(device) {
+  if (D_.c.ctx_blocks > 16 || D_.c.s1_blocks > 16 || D_.c.s2_blocks > 16 || D_.c.s > 16 ||
+      D_.N > 8 || D_.c.ch_blocks > 4)
+    throw std::invalid_argument("pswa_cfg: block / group counts exceed engine limits");
+  PSWA_CUDA(cudaSetDevice(device));
+  PSWA_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  const WeightMap w = parse_psww(cfg, blob, len);
+  build_tables();
+  alloc_all();
+  upload_weights(w);
+  pswa_dev::build_cdf_tables(scales_, cdf_, st_);
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+}
+
+Engine::~Engine() {
+  for (auto& kv : progs_)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  if (st_) cudaStreamSynchronize(st_);
+  for (void* p : allocs_) cudaFree(p);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+// ------------------------------------------------------------- tables ----
+void Engine::build_tables() {
+  const Dims& D = D_;
+  step_rows_h_.clear();
+  nmax_ = 0;
+  for (int t = 0; t < D.c.s; ++t) {
+    step_rows_h_.push_back(positions(D.H, D.W, D.c.s, t));
+    nmax_ = std::max<int>(nmax_, static_cast<int>(step_rows_h_.back().size()));
+  }
+}
+
+void Engine::alloc_all() {
+  const Dims& D = D_;
+  const int d = D.d, HW = D.HW, T = D.T, C = D.C;
+  const size_t HWp = static_cast<size_t>(D.Hp) * D.Wp;
+  const int L = D.c.lanes, Lz = D.c.hyper_lanes;
+  auto up = [&](const std::vector<int>& v) {
+    int* p = dalloc<int>(v.size());
+    PSWA_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
+    return p;
+  };
+  for (int t = 0; t < D.c.s; ++t) {
+    const auto& r = step_rows_h_[t];
+    std::vector<int> qi(r.size()), rp(r.size());
+    for (size_t k = 0; k < r.size(); ++k) {
+      const int y = r[k] / D.W, x = r[k] % D.W;
+      qi[k] = (y << 12) | x;
+      rp[k] = y * D.Wp + x;
+    }
+    step_rows_[t] = up(r);
+    step_qinfo_[t] = up(qi);
+    step_rows_pad_[t] = up(rp);
+  }
+  {
+    std::vector<int> qi(static_cast<size_t>(T) * HW);
+    for (int j = 0; j < T; ++j)
+      for (int p = 0; p < HW; ++p) qi[static_cast<size_t>(j) * HW + p] = (j << 24) | ((p / D.W) << 12) | (p % D.W);
+    ctx_qinfo_ = up(qi);
+    std::vector<int> crop(HWp);
+    for (int y = 0; y < D.Hp; ++y)
+      for (int x = 0; x < D.Wp; ++x) crop[static_cast<size_t>(y) * D.Wp + x] = (y < D.H && x < D.W) ? y * D.W + x : -1;
+    crop_rows_ = up(crop);
+  }
+  scales_ = dalloc<float>(pswa_dev::kScales);
+  cdf_ = dalloc<uint32_t>(pswa_dev::kScales * (pswa_dev::kSyms + 1));
+
+  cur_rsi_ = dalloc<float>(d);
+  cur_rsh_ = dalloc<float>(d);
+  cur_rso_ = dalloc<float>(C);
+  cur_loc_ = dalloc<float>(D.hc);
+  cur_scale_ = dalloc<float>(D.hc);
+  slot_src_ = dalloc<int>(T);
+  ring_.clear();
+  for (int j = 0; j < T; ++j) ring_.push_back(dalloc<float>(static_cast<size_t>(HW) * d));
+  ring_ptrs_ = dalloc<float*>(T);
+  PSWA_CUDA(cudaMemcpyAsync(ring_ptrs_, ring_.data(), sizeof(float*) * T, cudaMemcpyHostToDevice, st_));
+
+  yfr_ = dalloc<int32_t>(static_cast<size_t>(HW) * C);
+  ychw_ = dalloc<int32_t>(static_cast<size_t>(HW) * C);
+  zhat_ = dalloc<int32_t>(static_cast<size_t>(D.hc) * D.zh * D.zw);
+  emb_cur_ = dalloc<float>(static_cast<size_t>(HW) * d);
+  hq_ = dalloc<float>(static_cast<size_t>(HW) * d);
+  const size_t TH = static_cast<size_t>(T) * HW;
+  ctx_x_ = dalloc<float>(TH * d);
+  ctx_xn_ = dalloc<__half>(TH * d);
+  ctx_kv_ = dalloc<__half>(TH * 2 * d);
+  ctx_q_ = dalloc<__half>(TH * d);
+  ctx_att_ = dalloc<__half>(TH * d);
+  ctx_h_ = dalloc<__half>(TH * D.fp);
+  ctx16_ = dalloc<__half>(static_cast<size_t>(HW) * d);
+  acc_kv_ = dalloc<__half>(static_cast<size_t>(HW) * 2 * d);
+
+  hx_ = dalloc<float>(HWp * D.hc);
+  hu_ = dalloc<float>(HWp * D.hc);
+  hh_ = dalloc<float>(HWp * D.hc);
+  hcol_ = dalloc<__half>(HWp * D.kconv);
+  hcast_ = dalloc<__half>(HWp * D.hcp);
+  s1full_ = dalloc<__half>(HWp * d);
+
+  const size_t nb = static_cast<size_t>(nmax_);
+  bx_ = dalloc<float>(nb * d);
+  bxn_ = dalloc<__half>(nb * d);
+  bq_ = dalloc<__half>(nb * d);
+  batt_ = dalloc<__half>(nb * d);
+  bh_ = dalloc<__half>(nb * D.fp);
+  bs1n_ = dalloc<__half>(nb * d);
+  bs2n_ = dalloc<__half>(nb * d);
+  y16_ = dalloc<__half>(nb * C);
+  chx_ = dalloc<float>(nb * D.N * D.sp);
+  for (int b = 0; b < D.c.ch_blocks; ++b) chxn_[b] = dalloc<__half>(nb * D.N * D.sp);
+  chn2_ = dalloc<__half>(nb * D.sp);
+  chh_ = dalloc<__half>(nb * D.fgp);
+  chfo_ = dalloc<__half>(nb * D.sp);
+  hh16_ = dalloc<__half>(nb * 2 * D.sp);
+  const int ms = (2 * D.Cg + 63) / 64 * 64;
+  musig_ = dalloc<float>(nb * ms);
+
+  const size_t nsym = static_cast<size_t>(HW) * C, nz = static_cast<size_t>(D.hc) * D.zh * D.zw;
+  main_cap_ = 8 + 4ull * L + 6 * static_cast<size_t>(L) + 16 * nsym;
+  hyper_cap_ = 8 + 4ull * Lz + 6 * static_cast<size_t>(Lz) + 16 * nz;
+  d_main_ = dalloc<uint8_t>(main_cap_);
+  d_hyper_ = dalloc<uint8_t>(hyper_cap_);
+  d_lens_ = dalloc<uint32_t>(2);
+  lanes_ = dalloc<pswa_dev::LaneState>(L);
+  hlanes_ = dalloc<pswa_dev::LaneState>(Lz);
+  status_ = dalloc<int>(1);
+  bits_ = dalloc<double>(2);
+  sym_v_ = dalloc<int32_t>(nsym);
+  sym_idx_ = dalloc<uint8_t>(nsym);
+  hsym_v_ = dalloc<int32_t>(nz);
+  hsym_idx_ = dalloc<uint8_t>(nz);
+  enc_cap_ = static_cast<uint32_t>(16 * ((nsym + L - 1) / L) + 16);
+  enc_hcap_ = static_cast<uint32_t>(16 * ((nz + Lz - 1) / Lz) + 16);
+  enc_lanes_ = dalloc<uint8_t>(static_cast<size_t>(enc_cap_) * L);
+  enc_hlanes_ = dalloc<uint8_t>(static_cast<size_t>(enc_hcap_) * Lz);
+  enc_lens_ = dalloc<uint32_t>(L);
+  enc_hlens_ = dalloc<uint32_t>(Lz);
+  enc_bits_ = dalloc<double>(L);
+  enc_hbits_ = dalloc<double>(Lz);
+  pack_total_ = dalloc<unsigned long long>(2);
+  pack_offs_ = dalloc<uint64_t>(std::max(L, Lz));
+  mu_full_ = dalloc<float>(nsym);
+  sg_full_ = dalloc<float>(nsym);
+}
+
+// ------------------------------------------------------------ weights ----
+void Engine::upload_weights(const WeightMap& w) {
+  const Dims& D = D_;
+  const int d = D.d;
+  auto upload_h = [&](const std::vector<__half>& v) {
+    __half* p = dalloc<__half>(v.size());
+    PSWA_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(__half), cudaMemcpyHostToDevice, st_));
+    return p;
+  };
+  auto upload_f = [&](const float* v, size_t n, size_t pad_to = 0) {
+    float* p = dalloc<float>(std::max(n, pad_to));
+    PSWA_CUDA(cudaMemcpyAsync(p, v, n * sizeof(float), cudaMemcpyHostToDevice, st_));
+    return p;
+  };
+  auto fv = [&](const std::string& n) { return W(w, n).v.data(); };
+  auto fsize = [&](const std::string& n) { return W(w, n).v.size(); };
+  auto linear = [&](const std::string& n, int in, int out, int Np, int Kp) {
+    std::vector<__half> h(static_cast<size_t>(Np) * Kp, __float2half_rn(0.0f));
+    put_linear(h, Kp, fv(n), in, out, 0, 0);
+    return PW{upload_h(h), Np, Kp};
+  };
+  auto kv = [&](const std::string& k, const std::string& v) {
+    std::vector<__half> h(static_cast<size_t>(2 * d) * d, __float2half_rn(0.0f));
+    put_linear(h, d, fv(k), d, d, 0, 0);
+    put_linear(h, d, fv(v), d, d, d, 0);
+    return PW{upload_h(h), 2 * d, d};
+  };
+  // SwiGLU gate/up interleaved by output column: rows 2j (gate), 2j+1 (up).
+  auto gate_up = [&](const std::string& g, const std::string& u, int in, int f, int fp, int Kp) {
+    std::vector<__half> h(static_cast<size_t>(2 * fp) * Kp, __float2half_rn(0.0f));
+    const float* G = fv(g);
+    const float* U = fv(u);
+    for (int j = 0; j < f; ++j)
+      for (int i = 0; i < in; ++i) {
+        h[static_cast<size_t>(2 * j) * Kp + i] = __float2half_rn(G[static_cast<size_t>(i) * f + j]);
+        h[static_cast<size_t>(2 * j + 1) * Kp + i] = __float2half_rn(U[static_cast<size_t>(i) * f + j]);
+      }
+    return PW{upload_h(h), 2 * fp, Kp};
+  };
+  auto stack = [&](const char* tag, int blocks, Block* out, bool spatial) {
+    for (int b = 0; b < blocks; ++b) {
+      const std::string p = std::string(tag) + ".b" + std::to_string(b);
+      Block& B = out[b];
+      B.cross = spatial && (b % 2 == 1);
+      B.wq = linear(p + ".wq", d, d, d, d);
+      B.wkv = kv(p + ".wk", p + ".wv");
+      B.wo = linear(p + ".wo", d, d, d, d);
+      B.wgu = gate_up(p + ".ffn.wg", p + ".ffn.wu", d, D.f, D.fp, d);
+      B.wd = linear(p + ".ffn.wd", D.f, d, d, D.fp);
+      B.g1 = upload_f(fv(p + ".norm1.g"), d);
+      B.g2 = upload_f(fv(p + ".norm2.g"), d);
+      B.pos = upload_f(fv(p + ".pos"), fsize(p + ".pos"));
+      if (spatial) B.kv_cache = dalloc<__half>(static_cast<size_t>(D.HW) * 2 * d);
+    }
+  };
+  stack("ctx", D.c.ctx_blocks, ctx_, false);
+  stack("s1", D.c.s1_blocks, s1_, true);
+  stack("s2", D.c.s2_blocks, s2_, true);
+  ctx_gout_ = upload_f(fv("ctx.norm_out.g"), d);
+  s1_gout_ = upload_f(fv("s1.norm_out.g"), d);
+  s2_gout_ = upload_f(fv("s2.norm_out.g"), d);
+
+  emb_w_ = linear("embed.w", D.C, d, d, D.C);
+  emb_b_ = upload_f(fv("embed.b"), d);
+  rate_in_ = upload_f(fv("rate.in"), fsize("rate.in"));
+  rate_hyper_ = upload_f(fv("rate.hyper"), fsize("rate.hyper"));
+  rate_out_ = upload_f(fv("rate.out"), fsize("rate.out"));
+  pad_ = upload_f(fv("pad"), d);
+  prior_loc_ = upload_f(fv("hyper.loc"), fsize("hyper.loc"));
+  prior_scale_ = upload_f(fv("hyper.scale"), fsize("hyper.scale"));
+
+  // conv weights [o][c][3][3] -> [o][(ky*3+kx)*c + ci]
+  auto conv3 = [&](const std::string& n) {
+    std::vector<__half> h(static_cast<size_t>(D.hcp) * D.kconv, __float2half_rn(0.0f));
+    const float* k = fv(n);
+    for (int o = 0; o < D.hc; ++o)
+      for (int ci = 0; ci < D.hc; ++ci)
+        for (int t = 0; t < 9; ++t)
+          h[static_cast<size_t>(o) * D.kconv + t * D.hc + ci] =
+              __float2half_rn(k[(static_cast<size_t>(o) * D.hc + ci) * 9 + t]);
+    return PW{upload_h(h), D.hcp, D.kconv};
+  };
+  for (int j = 0; j < 2; ++j)
+    for (int k = 0; k < 2; ++k) {
+      const std::string hd = "hd.rb" + std::to_string(j) + ".c" + std::to_string(k + 1);
+      const std::string he = "he.rb" + std::to_string(j) + ".c" + std::to_string(k + 1);
+      hd_c_[j][k] = conv3(hd + ".w");
+      hd_b_[j][k] = upload_f(fv(hd + ".b"), D.hc, D.hcp);
+      he_c_[j][k] = conv3(he + ".w");
+      he_b_[j][k] = upload_f(fv(he + ".b"), D.hc, D.hcp);
+    }
+  {
+    std::vector<__half> h(static_cast<size_t>(d) * D.hcp, __float2half_rn(0.0f));
+    const float* k = fv("hd.out.w");  // [d][hc]
+    for (int o = 0; o < d; ++o)
+      for (int ci = 0; ci < D.hc; ++ci)
+        h[static_cast<size_t>(o) * D.hcp + ci] = __float2half_rn(k[static_cast<size_t>(o) * D.hc + ci]);
+    hd_out_ = PW{upload_h(h), d, D.hcp};
+    hd_out_b_ = upload_f(fv("hd.out.b"), d);
+    std::vector<__half> e(static_cast<size_t>(D.hcp) * d, __float2half_rn(0.0f));
+    const float* ki = fv("he.in.w");  // [hc][d]
+    for (int o = 0; o < D.hc; ++o)
+      for (int ci = 0; ci < d; ++ci)
+        e[static_cast<size_t>(o) * d + ci] = __float2half_rn(ki[static_cast<size_t>(o) * d + ci]);
+    he_in_ = PW{upload_h(e), D.hcp, d};
+    he_in_b_ = upload_f(fv("he.in.b"), D.hc, D.hcp);
+  }
+  // accumulator
+  acc_.wq = linear("acc.wq", d, d, d, d);
+  acc_.wkv = kv("acc.wk", "acc.wv");
+  acc_.wo = linear("acc.wo", d, d, d, d);
+  acc_.g1 = upload_f(fv("acc.normq.g"), d);
+  acc_.pos = upload_f(fv("acc.pos"), fsize("acc.pos"));
+
+  // channel transformer, slots padded to sp columns
+  const int N = D.N, sl = D.slot, sp = D.sp, dchp = N * sp;
+  {
+    std::vector<__half> h(static_cast<size_t>(dchp) * d, __float2half_rn(0.0f));
+    for (int g = 0; g < N; ++g) put_linear(h, d, fv("ch.proj" + std::to_string(g) + ".w"), d, sl, g * sp, 0);
+    ch_proj_ = PW{upload_h(h), dchp, d};
+  }
+  for (int g = 1; g < N; ++g) ch_emb_[g] = linear("ch.emb" + std::to_string(g) + ".w", D.Cg, sl, sp, D.Cgp);
+  for (int b = 0; b < D.c.ch_blocks; ++b) {
+    const std::string p = "ch.b" + std::to_string(b);
+    std::vector<__half> h(static_cast<size_t>(dchp) * dchp, __float2half_rn(0.0f));
+    const float* m = fv(p + ".mix.w");  // [in][out], masked block-lower-triangular
+    for (int go = 0; go < N; ++go)
+      for (int io = 0; io < sl; ++io)
+        for (int gi = 0; gi <= go; ++gi)
+          for (int ii = 0; ii < sl; ++ii)
+            h[static_cast<size_t>(go * sp + io) * dchp + gi * sp + ii] =
+                __float2half_rn(m[static_cast<size_t>(gi * sl + ii) * D.dch + go * sl + io]);
+    ch_mix_[b] = PW{upload_h(h), dchp, dchp};
+    ch_g1_[b] = upload_f(fv(p + ".norm1.g"), D.dch);
+    ch_g2_[b] = upload_f(fv(p + ".norm2.g"), D.dch);
+    for (int g = 0; g < N; ++g) {
+      const std::string q = p + ".ffn" + std::to_string(g);
+      ch_gu_[b][g] = gate_up(q + ".wg", q + ".wu", sl, D.fg, D.fgp, sp);
+      ch_d_[b][g] = linear(q + ".wd", D.fg, sl, sp, D.fgp);
+    }
+  }
+  ch_gout_ = upload_f(fv("ch.norm_out.g"), D.dch);
+  const int ms = (2 * D.Cg + 63) / 64 * 64;
+  for (int g = 0; g < N; ++g) {
+    const std::string mu = "head.mu" + std::to_string(g), sg = "head.sg" + std::to_string(g);
+    std::vector<__half> h1(static_cast<size_t>(2 * sp) * sp, __float2half_rn(0.0f));
+    put_linear(h1, sp, fv(mu + ".w1"), sl, sl, 0, 0);
+    put_linear(h1, sp, fv(sg + ".w1"), sl, sl, sp, 0);
+    head_w1_[g] = PW{upload_h(h1), 2 * sp, sp};
+    std::vector<float> b1(static_cast<size_t>(2 * sp), 0.0f);
+    std::memcpy(b1.data(), fv(mu + ".b1"), sizeof(float) * sl);
+    std::memcpy(b1.data() + sp, fv(sg + ".b1"), sizeof(float) * sl);
+    head_b1_[g] = upload_f(b1.data(), b1.size());
+    std::vector<__half> h2(static_cast<size_t>(ms) * 2 * sp, __float2half_rn(0.0f));
+    put_linear(h2, 2 * sp, fv(mu + ".w2"), sl, D.Cg, 0, 0);
+    put_linear(h2, 2 * sp, fv(sg + ".w2"), sl, D.Cg, D.Cg, sp);
+    head_w2_[g] = PW{upload_h(h2), ms, 2 * sp};
+    std::vector<float> b2(static_cast<size_t>(ms), 0.0f);
+    std::memcpy(b2.data(), fv(mu + ".b2"), sizeof(float) * D.Cg);
+    std::memcpy(b2.data() + D.Cg, fv(sg + ".b2"), sizeof(float) * D.Cg);
+    head_b2_[g] = upload_f(b2.data(), b2.size());
+  }
+}
+
+// ----------------------------------------------------- program builders ---
+void Engine::add(Program& P, std::function<void(cudaStream_t)> op, int launches) {
+  P.ops.push_back(std::move(op));
+  P.launches += launches;
+}
+
+void Engine::gemm(Program& P, const __half* A, int lda, int M, const PW& B, int K, const GemmEpi& ep) {
+  pswa_dev::GemmPlan plan;
+  pswa_dev::gemm_plan(&plan, A, lda, M, B.p, B.K, B.N, K, ep);
+  add(P, [plan](cudaStream_t s) { pswa_dev::gemm_run(plan, s); });
+}
+
+namespace {
+GemmEpi f16_out(void* out, int ld) {
+  GemmEpi e;
+  e.out = out;
+  e.ld_out = ld;
+  return e;
+}
+GemmEpi f32_acc(void* out, int ld, int n_store = 1 << 30) {
+  GemmEpi e;
+  e.out = out;
+  e.ld_out = ld;
+  e.out_f32 = 1;
+  e.accumulate = 1;
+  e.n_store = n_store;
+  return e;
+}
+GemmEpi swiglu_out(void* out, int ld) {
+  GemmEpi e;
+  e.out = out;
+  e.ld_out = ld;
+  e.act = kActSwiGLU;
+  return e;
+}
+}  // namespace
+
+// One S1/S2 block on the step-t batch held in bx_ (residual stream, fp32).
+void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
+  const Dims& D = D_;
+  const int d = D.d, M = static_cast<int>(step_rows_h_[t].size());
+  const int* rows = step_rows_[t];
+  const int32_t* qinfo = step_qinfo_[t];
+  const float* g1 = B.g1;
+  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, g1, bxn_, d, s); });
+  gemm(P, bxn_, d, M, B.wq, d, f16_out(bq_, d));
+  if (!B.cross) {
+    GemmEpi e = f16_out(B.kv_cache, 2 * d);
+    e.row_map = rows;  // K/V of this step's positions into the frame cache
+    gemm(P, bxn_, d, M, B.wkv, d, e);
+  }
+  const __half* kvc = B.kv_cache;
+  const int mask = B.cross ? 0 : 1;
+  const float* pos = B.pos;
+  add(P, [=, this](cudaStream_t s) {
+    pswa_dev::window_attention(bq_, d, qinfo, M, kvc, 2 * d, 0, D.H, D.W, D.heads, D.hd, D.c.win_h,
+                               D.c.win_w, 0, mask, D.c.s, pos, batt_, d, s);
+  });
+  gemm(P, batt_, d, M, B.wo, d, f32_acc(bx_, d));
+  const float* g2 = B.g2;
+  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, g2, bxn_, d, s); });
+  gemm(P, bxn_, d, M, B.wgu, d, swiglu_out(bh_, D.fp));
+  gemm(P, bh_, D.fp, M, B.wd, D.fp, f32_acc(bx_, d));
+}
+
+void Engine::build_ctx(Program& P) {
+  const Dims& D = D_;
+  const int d = D.d, HW = D.HW, T = D.T, n = T * HW;
+  add(P, [=, this](cudaStream_t s) {
+    pswa_dev::fill_context_slots(ring_ptrs_, slot_src_, pad_, T, HW, d, ctx_x_, s);
+  });
+  for (int b = 0; b < D.c.ctx_blocks; ++b) {
+    const Block& B = ctx_[b];
+    const bool last = b == D.c.ctx_blocks - 1;
+    const int q0 = last ? (T - 1) * HW : 0, nq = n - q0;
+    const float *g1 = B.g1, *g2 = B.g2, *pos = B.pos;
+    add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(ctx_x_, d, nullptr, n, d, d, g1, ctx_xn_, d, s); });
+    gemm(P, ctx_xn_, d, n, B.wkv, d, f16_out(ctx_kv_, 2 * d));
+    gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, f16_out(ctx_q_, d));
+    add(P, [=, this](cudaStream_t s) {
+      pswa_dev::window_attention(ctx_q_, d, ctx_qinfo_ + q0, nq, ctx_kv_, 2 * d, HW, D.H, D.W,
+                                 D.heads, D.hd, D.c.win_h, D.c.win_w, D.c.win_t, 0, D.c.s, pos,
+                                 ctx_att_, d, s);
+    });
+    float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
+    __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;
+    gemm(P, ctx_att_, d, nq, B.wo, d, f32_acc(xq, d));
+    add(P, [=](cudaStream_t s) { pswa_dev::rmsnorm_rows(xq, d, nullptr, nq, d, d, g2, xnq, d, s); });
+    gemm(P, xnq, d, nq, B.wgu, d, swiglu_out(ctx_h_, D.fp));
+    gemm(P, ctx_h_, D.fp, nq, B.wd, D.fp, f32_acc(xq, d));
+  }
+  const float* last = ctx_x_ + static_cast<size_t>(T - 1) * HW * d;
+  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(last, d, nullptr, HW, d, d, ctx_gout_, ctx16_, d, s); });
+  // cross-attention K/V of every cross block, once per frame (K7)
+  for (Block* stackp : {s1_, s2_}) {
+    const int nb = stackp == s1_ ? D.c.s1_blocks : D.c.s2_blocks;
+    for (int b = 0; b < nb; ++b)
+      if (stackp[b].cross) gemm(P, ctx16_, d, HW, stackp[b].wkv, d, f16_out(stackp[b].kv_cache, 2 * d));
+  }
+}
+
+void Engine::build_hyper_decode(Program& P) {
+  const Dims& D = D_;
+  const int hc = D.hc;
+  add(P, [=, this](cudaStream_t s) { pswa_dev::zhat_to_nhwc(zhat_, hc, D.zh * D.zw, hx_, s); });
+  float* src = hx_;
+  float* dst = hu_;
+  int h = D.zh, w = D.zw;
+  for (int j = 0; j < 2; ++j) {
+    const int ih = h, iw = w;
+    float* in = src;
+    float* out = dst;
+    add(P, [=](cudaStream_t s) { pswa_dev::upsample2_nhwc(in, ih, iw, hc, out, s); });
+    h *= 2;
+    w *= 2;
+    const int oh = h, ow = w;
+    add(P, [=, this](cudaStream_t s) { pswa_dev::im2col3x3(out, oh, ow, hc, 1, 0, hcol_, D.kconv, s); });
+    GemmEpi e1;
+    e1.out = hh_;
+    e1.ld_out = hc;
+    e1.out_f32 = 1;
+    e1.bias = hd_b_[j][0];
+    e1.act = kActSilu;
+    e1.n_store = hc;
+    gemm(P, hcol_, D.kconv, oh * ow, hd_c_[j][0], D.kconv, e1);
+    add(P, [=, this](cudaStream_t s) { pswa_dev::im2col3x3(hh_, oh, ow, hc, 1, 0, hcol_, D.kconv, s); });
+    GemmEpi e2 = f32_acc(out, hc, hc);  // RB-up: out = up2(x) + conv(silu(conv(up2(x))))
+    e2.bias = hd_b_[j][1];
+    gemm(P, hcol_, D.kconv, oh * ow, hd_c_[j][1], D.kconv, e2);
+    std::swap(src, dst);
+  }
+  const float* fin = src;
+  const int np = D.Hp * D.Wp;
+  add(P, [=, this](cudaStream_t s) { pswa_dev::f32_to_f16_rows(fin, hc, np, hc, hcast_, D.hcp, D.hcp, s); });
+  GemmEpi e;
+  e.out = hq_;
+  e.ld_out = D.d;
+  e.out_f32 = 1;
+  e.bias = hd_out_b_;
+  e.scale = cur_rsh_;
+  e.bias_first = 1;
+  e.row_map = crop_rows_;  // crop the padded hyper grid to the latent grid
+  gemm(P, hcast_, D.hcp, np, hd_out_, D.hcp, e);
+}
+
+void Engine::build_hyper_encode(Program& P) {
+  const Dims& D = D_;
+  const int hc = D.hc;
+  GemmEpi e0;
+  e0.out = hx_;
+  e0.ld_out = hc;
+  e0.out_f32 = 1;
+  e0.bias = he_in_b_;
+  e0.n_store = hc;
+  gemm(P, s1full_, D.d, D.Hp * D.Wp, he_in_, D.d, e0);
+  float* src = hx_;
+  float* other = hu_;
+  int h = D.Hp, w = D.Wp;
+  for (int j = 0; j < 2; ++j) {
+    const int ih = h, iw = w;
+    float* in = src;
+    float* skip = other;
+    add(P, [=, this](cudaStream_t s) { pswa_dev::im2col3x3(in, ih, iw, hc, 2, 0, hcol_, D.kconv, s); });
+    h /= 2;
+    w /= 2;
+    const int oh = h, ow = w;
+    GemmEpi e1;
+    e1.out = hh_;
+    e1.ld_out = hc;
+    e1.out_f32 = 1;
+    e1.bias = he_b_[j][0];
+    e1.act = kActSilu;
+    e1.n_store = hc;
+    gemm(P, hcol_, D.kconv, oh * ow, he_c_[j][0], D.kconv, e1);
+    add(P, [=](cudaStream_t s) { pswa_dev::subsample2_nhwc(in, ih, iw, hc, skip, s); });
+    add(P, [=, this](cudaStream_t s) { pswa_dev::im2col3x3(hh_, oh, ow, hc, 1, 0, hcol_, D.kconv, s); });
+    GemmEpi e2 = f32_acc(skip, hc, hc);  // RB-down: out = x[::2, ::2] + conv(silu(conv_s2(x)))
+    e2.bias = he_b_[j][1];
+    gemm(P, hcol_, D.kconv, oh * ow, he_c_[j][1], D.kconv, e2);
+    std::swap(src, other);
+  }
+  const float* fin = src;
+  add(P, [=, this](cudaStream_t s) { pswa_dev::round_to_zhat(fin, hc, D.zh * D.zw, zhat_, s); });
+}
+
+void Engine::build_embed(Program& P, int t) {
+  const Dims& D = D_;
+  const int M = static_cast<int>(step_rows_h_[t].size());
+  GemmEpi e;
+  e.out = emb_cur_;
+  e.ld_out = D.d;
+  e.out_f32 = 1;
+  e.scale = cur_rsi_;  // e = rate_scale_in * (W y_hat) + b
+  e.bias = emb_b_;
+  e.row_map = step_rows_[t];
+  gemm(P, y16_, D.C, M, emb_w_, D.C, e);
+}
+
+void Engine::build_s1(Program& P, int t, bool encoder) {
+  const Dims& D = D_;
+  const int d = D.d, M = static_cast<int>(step_rows_h_[t].size());
+  const int* rows = step_rows_[t];
+  add(P, [=, this](cudaStream_t s) { pswa_dev::gather_rows_f32(emb_cur_, d, rows, M, d, bx_, d, s); });
+  for (int b = 0; b < D.c.s1_blocks; ++b) block_step(P, s1_[b], t, "s1", true);
+  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, s1_gout_, bs1n_, d, s); });
+  GemmEpi e = f16_out(acc_kv_, 2 * d);
+  e.row_map = rows;
+  gemm(P, bs1n_, d, M, acc_.wkv, d, e);
+  if (encoder) {
+    const int* rp = step_rows_pad_[t];
+    add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f16(bs1n_, d, rp, M, d, s1full_, d, s); });
+  }
+}
+
+void Engine::build_step(Program& P, int t, int mode) {
+  const Dims& D = D_;
+  const int d = D.d, M = static_cast<int>(step_rows_h_[t].size());
+  const int* rows = step_rows_[t];
+  const int32_t* qinfo = step_qinfo_[t];
+  // accumulator: A = Hq + xattn(Q = Hq, KV = S1 of strictly earlier steps)
+  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(hq_, d, rows, M, d, d, acc_.g1, bxn_, d, s); });
+  gemm(P, bxn_, d, M, acc_.wq, d, f16_out(bq_, d));
+  add(P, [=, this](cudaStream_t s) {
+    pswa_dev::window_attention(bq_, d, qinfo, M, acc_kv_, 2 * d, 0, D.H, D.W, D.heads, D.hd,
+                               D.c.win_h, D.c.win_w, 0, 2, D.c.s, acc_.pos, batt_, d, s);
+  });
+  add(P, [=, this](cudaStream_t s) { pswa_dev::gather_rows_f32(hq_, d, rows, M, d, bx_, d, s); });
+  gemm(P, batt_, d, M, acc_.wo, d, f32_acc(bx_, d));
+  // spatial module 2
+  for (int b = 0; b < D.c.s2_blocks; ++b) block_step(P, s2_[b], t, "s2", true);
+  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, s2_gout_, bs2n_, d, s); });
+  // channel transformer (incremental over groups) + heads + coder
+  const int N = D.N, sl = D.slot, sp = D.sp, dchp = N * sp, Cg = D.Cg, C = D.C;
+  const int ms = (2 * Cg + 63) / 64 * 64;
+  GemmEpi ep;
+  ep.out = chx_;
+  ep.ld_out = dchp;
+  ep.out_f32 = 1;
+  gemm(P, bs2n_, d, M, ch_proj_, d, ep);
+  uint64_t o_step = 0;
+  for (int tt = 0; tt < t; ++tt) o_step += static_cast<uint64_t>(step_rows_h_[tt].size()) * C;
+  for (int g = 0; g < N; ++g) {
+    float* xg = chx_ + g * sp;
+    if (g >= 1)  // channel shift: slot g sees y_hat group g-1
+      gemm(P, y16_ + (g - 1) * Cg, C, M, ch_emb_[g], D.Cgp, f32_acc(xg, dchp, sl));
+    for (int b = 0; b < D.c.ch_blocks; ++b) {
+      const float* g1 = ch_g1_[b] + g * sl;
+      const float* g2 = ch_g2_[b] + g * sl;
+      __half* xn = chxn_[b];
+      add(P, [=](cudaStream_t s) { pswa_dev::rmsnorm_rows(xg, dchp, nullptr, M, sl, sl, g1, xn + g * sp, dchp, s); });
+      const PW mixg{ch_mix_[b].p + static_cast<size_t>(g) * sp * dchp, sp, dchp};
+      gemm(P, xn, dchp, M, mixg, (g + 1) * sp, f32_acc(xg, dchp, sl));
+      add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(xg, dchp, nullptr, M, sl, sl, g2, chn2_, sp, s); });
+      gemm(P, chn2_, sp, M, ch_gu_[b][g], sp, swiglu_out(chh_, D.fgp));
+      gemm(P, chh_, D.fgp, M, ch_d_[b][g], D.fgp, f32_acc(xg, dchp, sl));
+    }
+    const float* go = ch_gout_ + g * sl;
+    add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(xg, dchp, nullptr, M, sl, sl, go, chfo_, sp, s); });
+    GemmEpi e1 = f16_out(hh16_, 2 * sp);
+    e1.bias = head_b1_[g];
+    e1.act = kActSilu;
+    gemm(P, chfo_, sp, M, head_w1_[g], sp, e1);
+    GemmEpi e2;
+    e2.out = musig_;
+    e2.ld_out = ms;
+    e2.out_f32 = 1;
+    e2.act = kActHead;
+    e2.split = Cg;
+    e2.bias = head_b2_[g];
+    e2.scale = cur_rso_ + g * Cg;
+    e2.n_store = 2 * Cg;
+    gemm(P, hh16_, 2 * sp, M, head_w2_[g], 2 * sp, e2);
+    const uint64_t o0 = o_step + static_cast<uint64_t>(g) * M * Cg;
+    const int c0 = g * Cg;
+    if (mode == 0) {
+      const int L = D.c.lanes;
+      add(P, [=, this](cudaStream_t s) {
+        pswa_dev::lanes_decode_phase(d_main_, lanes_, L, o0, M, Cg, musig_, ms, Cg, scales_, cdf_,
+                                     rows, yfr_, C, c0, y16_, C, status_, s);
+      });
+    } else {
+      const bool ms_out = want_musig_;
+      add(P, [=, this](cudaStream_t s) {
+        pswa_dev::quantize_phase(musig_, ms, Cg, M, Cg, o0, rows, yfr_, C, c0, scales_, sym_v_,
+                                 sym_idx_, y16_, C, ms_out ? mu_full_ : nullptr,
+                                 ms_out ? sg_full_ : nullptr, s);
+      });
+    }
+  }
+  if (mode == 0) build_embed(P, t);
+}
+
+Program& Engine::program(const std::string& key) {
+  auto it = progs_.find(key);
+  if (it != progs_.end()) return it->second;
+  Program& P = progs_[key];
+  const Dims& D = D_;
+  const int HW = D.HW, C = D.C, L = D.c.lanes, Lz = D.c.hyper_lanes;
+  const int nz = D.hc * D.zh * D.zw;
+  const std::string base = key.substr(0, key.find('+'));  // "+ms": mu/sigma outputs
+  if (base == "decode") {
+    add(P, [=, this](cudaStream_t s) {
+      pswa_dev::lanes_init(d_hyper_, d_lens_, Lz, static_cast<uint32_t>(nz), hlanes_, status_, s);
+    });
+    add(P, [=, this](cudaStream_t s) {
+      pswa_dev::lanes_decode_hyper(d_hyper_, hlanes_, Lz, nz, D.zh * D.zw, cur_loc_, cur_scale_,
+                                   scales_, cdf_, zhat_, status_, s);
+    });
+    add(P, [=, this](cudaStream_t s) { pswa_dev::sum_lane_bits(hlanes_, Lz, bits_, s); });
+    add(P, [=, this](cudaStream_t s) {
+      pswa_dev::lanes_init(d_main_, d_lens_ + 1, L, static_cast<uint32_t>(HW) * C, lanes_, status_, s);
+    });
+    build_hyper_decode(P);
+    build_ctx(P);
+    for (int t = 0; t < D.c.s; ++t) {
+      if (t > 0) build_s1(P, t - 1, false);
+      build_step(P, t, 0);
+    }
+    add(P, [=, this](cudaStream_t s) { pswa_dev::sum_lane_bits(lanes_, L, bits_ + 1, s); });
+    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_to_chw(yfr_, HW, C, ychw_, s); });
+  } else if (base == "encode" || base == "encode_z") {
+    const bool zgiven = base == "encode_z";
+    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_from_chw(ychw_, HW, C, yfr_, s); });
+    build_ctx(P);
+    for (int t = 0; t < D.c.s; ++t) {
+      const int M = static_cast<int>(step_rows_h_[t].size());
+      const int* rows = step_rows_[t];
+      add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_rows_f16(yfr_, C, rows, M, 0, C, y16_, C, C, s); });
+      build_embed(P, t);
+      build_s1(P, t, true);
+    }
+    if (!zgiven) build_hyper_encode(P);
+    add(P, [=, this](cudaStream_t s) {
+      pswa_dev::quantize_hyper(zhat_, nz, D.zh * D.zw, cur_loc_, cur_scale_, scales_, hsym_v_,
+                               hsym_idx_, s);
+    });
+    build_hyper_decode(P);
+    for (int t = 0; t < D.c.s; ++t) build_step(P, t, 1);
+    add(P, [=, this](cudaStream_t s) {
+      pswa_dev::lanes_encode(hsym_v_, hsym_idx_, nz, Lz, cdf_, enc_hlanes_, enc_hcap_, enc_hlens_,
+                             enc_hbits_, status_, s);
+    });
+    add(P, [=, this](cudaStream_t s) {
+      pswa_dev::lanes_pack(enc_hlanes_, enc_hcap_, enc_hlens_, Lz, static_cast<uint32_t>(nz),
+                           d_hyper_, hyper_cap_, pack_total_, pack_offs_, status_, s);
+    }, 2);
+    add(P, [=, this](cudaStream_t s) {
+      pswa_dev::lanes_encode(sym_v_, sym_idx_, static_cast<uint64_t>(HW) * C, L, cdf_, enc_lanes_,
+                             enc_cap_, enc_lens_, enc_bits_, status_, s);
+    });
+    add(P, [=, this](cudaStream_t s) {
+      pswa_dev::lanes_pack(enc_lanes_, enc_cap_, enc_lens_, L, static_cast<uint32_t>(HW) * C,
+                           d_main_, main_cap_, pack_total_ + 1, pack_offs_, status_, s);
+    }, 2);
+    add(P, [=, this](cudaStream_t s) { pswa_dev::sum_doubles(enc_hbits_, Lz, bits_, s); });
+    add(P, [=, this](cudaStream_t s) { pswa_dev::sum_doubles(enc_bits_, L, bits_ + 1, s); });
+  } else if (base == "push") {
+    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_from_chw(ychw_, HW, C, yfr_, s); });
+    for (int t = 0; t < D.c.s; ++t) {
+      const int M = static_cast<int>(step_rows_h_[t].size());
+      const int* rows = step_rows_[t];
+      add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_rows_f16(yfr_, C, rows, M, 0, C, y16_, C, C, s); });
+      build_embed(P, t);
+    }
+  } else {
+    throw std::invalid_argument("unknown program " + key);
+  }
+  return P;
+}
+
+void Engine::run(Program& P) {
+  static const bool no_graph = std::getenv("PSWA_NO_GRAPH") != nullptr;
+  last_launches_ = P.launches;
+  if (no_graph) {
+    for (auto& op : P.ops) op(st_);
+    return;
+  }
+  if (!P.exec) {
+    cudaGraph_t g = nullptr;
+    PSWA_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    try {
+      for (auto& op : P.ops) op(st_);
+    } catch (...) {
+      cudaStreamEndCapture(st_, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    PSWA_CUDA(cudaStreamEndCapture(st_, &g));
+    PSWA_CUDA(cudaGraphInstantiate(&P.exec, g, 0));
+    PSWA_CUDA(cudaGraphDestroy(g));
+  }
+  PSWA_CUDA(cudaGraphLaunch(P.exec, st_));
+}
+
+// ---------------------------------------------------------- frame API ----
+void Engine::set_frame_params(int rate, int fidx) {
+  const Dims& D = D_;
+  if (rate < 0 || rate >= D.c.rate_points) throw std::invalid_argument("rate_idx out of range");
+  if (fidx < 0) throw std::invalid_argument("frame_idx_in_gop < 0");
+  const int slot = fidx < 4 ? fidx : 4;  // select_prior
+  auto d2d = [&](float* dst, const float* src, int n) {
+    PSWA_CUDA(cudaMemcpyAsync(dst, src, sizeof(float) * n, cudaMemcpyDeviceToDevice, st_));
+  };
+  d2d(cur_rsi_, rate_in_ + static_cast<size_t>(rate) * D.d, D.d);
+  d2d(cur_rsh_, rate_hyper_ + static_cast<size_t>(rate) * D.d, D.d);
+  d2d(cur_rso_, rate_out_ + static_cast<size_t>(rate) * D.C, D.C);
+  d2d(cur_loc_, prior_loc_ + (static_cast<size_t>(rate) * 5 + slot) * D.hc, D.hc);
+  d2d(cur_scale_, prior_scale_ + (static_cast<size_t>(rate) * 5 + slot) * D.hc, D.hc);
+  std::vector<int> src(static_cast<size_t>(D.T));
+  for (int i = 0; i < D.T; ++i) {
+    const int k = D.T - i;  // slot i holds the k-th most recent frame
+    src[i] = k <= npast_ ? ((head_ - k) % D.T + D.T) % D.T : -1;
+  }
+  PSWA_CUDA(cudaMemcpyAsync(slot_src_, src.data(), sizeof(int) * D.T, cudaMemcpyHostToDevice, st_));
+  PSWA_CUDA(cudaMemsetAsync(status_, 0, sizeof(int), st_));
+  PSWA_CUDA(cudaMemsetAsync(bits_, 0, 2 * sizeof(double), st_));
+}
+
+void Engine::advance_ring() {
+  PSWA_CUDA(cudaMemcpyAsync(ring_[head_], emb_cur_, sizeof(float) * D_.HW * D_.d,
+                            cudaMemcpyDeviceToDevice, st_));
+  head_ = (head_ + 1) % D_.T;
+  npast_ = std::min(npast_ + 1, D_.T);
+}
+
+void Engine::reset_gop() {
+  head_ = 0;
+  npast_ = 0;
+}
+
+void Engine::push_frame(const int32_t* yhat_chw, int rate) {
+  set_frame_params(rate, 0);
+  PSWA_CUDA(cudaMemcpyAsync(ychw_, yhat_chw, sizeof(int32_t) * D_.HW * D_.C, cudaMemcpyHostToDevice, st_));
+  run(program("push"));
+  advance_ring();
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+}
+
+FrameResult Engine::encode(const int32_t* yhat_chw, int rate, int fidx, const int32_t* zhat_in,
+                           float* mu_out, float* sigma_out, uint8_t* hyper_out, size_t hyper_cap,
+                           uint8_t* main_out, size_t main_cap, bool advance) {
+  const Dims& D = D_;
+  const size_t nsym = static_cast<size_t>(D.HW) * D.C;
+  const size_t nz = static_cast<size_t>(D.hc) * D.zh * D.zw;
+  set_frame_params(rate, fidx);
+  PSWA_CUDA(cudaMemcpyAsync(ychw_, yhat_chw, sizeof(int32_t) * nsym, cudaMemcpyHostToDevice, st_));
+  if (zhat_in)
+    PSWA_CUDA(cudaMemcpyAsync(zhat_, zhat_in, sizeof(int32_t) * nz, cudaMemcpyHostToDevice, st_));
+  want_musig_ = mu_out != nullptr;
+  // the mu/sigma output pointers are baked into the captured graph, so the
+  // two variants are separate programs
+  const std::string key = std::string(zhat_in ? "encode_z" : "encode") + (want_musig_ ? "+ms" : "");
+  run(program(key));
+  FrameResult r;
+  unsigned long long tot[2];
+  PSWA_CUDA(cudaMemcpyAsync(tot, pack_total_, sizeof(tot), cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaMemcpyAsync(r.bits, bits_, sizeof(r.bits), cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaMemcpyAsync(&r.status, status_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+  if (r.status) throw pswa_abi::LaneError("encoder status " + std::to_string(r.status));
+  r.hyper_len = tot[0];
+  r.main_len = tot[1];
+  if (hyper_out) {
+    if (hyper_cap < r.hyper_len) throw std::invalid_argument("hyper output buffer too small");
+    PSWA_CUDA(cudaMemcpyAsync(hyper_out, d_hyper_, r.hyper_len, cudaMemcpyDeviceToHost, st_));
+  }
+  if (main_out) {
+    if (main_cap < r.main_len) throw std::invalid_argument("main output buffer too small");
+    PSWA_CUDA(cudaMemcpyAsync(main_out, d_main_, r.main_len, cudaMemcpyDeviceToHost, st_));
+  }
+  if (mu_out) {
+    std::vector<float> a(nsym), b(nsym);
+    PSWA_CUDA(cudaMemcpyAsync(a.data(), mu_full_, sizeof(float) * nsym, cudaMemcpyDeviceToHost, st_));
+    PSWA_CUDA(cudaMemcpyAsync(b.data(), sg_full_, sizeof(float) * nsym, cudaMemcpyDeviceToHost, st_));
+    PSWA_CUDA(cudaStreamSynchronize(st_));
+    for (int p = 0; p < D.HW; ++p)
+      for (int c = 0; c < D.C; ++c) {
+        mu_out[static_cast<size_t>(c) * D.HW + p] = a[static_cast<size_t>(p) * D.C + c];
+        sigma_out[static_cast<size_t>(c) * D.HW + p] = b[static_cast<size_t>(p) * D.C + c];
+      }
+  }
+  if (advance) advance_ring();
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+  return r;
+}
+
+FrameResult Engine::decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
+                           int rate, int fidx, bool advance, int32_t* yhat_out, bool device) {
+  const Dims& D = D_;
+  if (hyper_len > hyper_cap_ || main_len > main_cap_)
+    throw pswa_abi::TruncatedError("payload larger than the decoder's capacity");
+  set_frame_params(rate, fidx);
+  const cudaMemcpyKind in_kind = device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  PSWA_CUDA(cudaMemcpyAsync(d_hyper_, hyper, hyper_len, in_kind, st_));
+  PSWA_CUDA(cudaMemcpyAsync(d_main_, main_pl, main_len, in_kind, st_));
+  uint32_t lens[2] = {static_cast<uint32_t>(hyper_len), static_cast<uint32_t>(main_len)};
+  PSWA_CUDA(cudaMemcpyAsync(d_lens_, lens, sizeof(lens), cudaMemcpyHostToDevice, st_));
+  run(program("decode"));
+  FrameResult r;
+  PSWA_CUDA(cudaMemcpyAsync(yhat_out, ychw_, sizeof(int32_t) * D.HW * D.C,
+                            device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaMemcpyAsync(r.bits, bits_, sizeof(r.bits), cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaMemcpyAsync(&r.status, status_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+  if (r.status) throw pswa_abi::TruncatedError("corrupt or truncated payload (status " +
+                                               std::to_string(r.status) + ")");
+  if (advance) {
+    advance_ring();
+    PSWA_CUDA(cudaStreamSynchronize(st_));
+  }
+  return r;
+}
+
+void Engine::last_zhat(int32_t* out) {
+  PSWA_CUDA(cudaMemcpyAsync(out, zhat_, sizeof(int32_t) * D_.hc * D_.zh * D_.zw,
+                            cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+}
+
+}  // namespace pswa_host

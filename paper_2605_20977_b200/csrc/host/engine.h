@@ -1,0 +1,175 @@
+// The device engine behind the C ABI: owns every device allocation of one
+// handle (packed fp16 weights, frame-indexed K/V caches, the temporal ring,
+// coder lanes) and replays the per-frame programs as CUDA graphs.
+//
+// Decode of one frame as launched here:
+//   hyper lanes -> z_hat -> hyper decoder (im2col + tcgen05 GEMMs) -> Hq
+//   context transformer over the ring (dense, once per frame) -> ctx, cross K/V
+//   for t in 0..s-1:
+//     S1 for the step t-1 batch (incremental: per-layer K/V caches), acc K/V
+//     accumulator + S2 for the step t batch
+//     for g in 0..N-1: channel slot g -> mu/sigma heads -> lane decode
+//     embed the decoded step t latents
+// The encoder runs the decoder's exact per-batch kernels (teacher forced), so
+// mu/sigma are bitwise identical on both sides.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../cuda/gemm.h"
+#include "../cuda/kernels.h"
+#include "model_spec.h"
+
+namespace pswa_host {
+
+struct PW {  // packed weight: fp16 [N][K] row-major (K-major operand)
+  __half* p = nullptr;
+  int N = 0, K = 0;
+};
+
+struct Block {  // one transformer block of ctx / s1 / s2
+  bool cross = false;
+  PW wq, wkv, wo, wgu, wd;
+  float *g1 = nullptr, *g2 = nullptr, *pos = nullptr;
+  __half* kv_cache = nullptr;  // self layers of s1/s2: [HW][2d]; cross: ctx K/V
+};
+
+struct Program {
+  std::vector<std::function<void(cudaStream_t)>> ops;
+  int launches = 0;
+  cudaGraphExec_t exec = nullptr;
+};
+
+struct FrameResult {
+  double bits[2] = {0, 0};
+  int status = 0;
+  size_t hyper_len = 0, main_len = 0;
+};
+
+class Engine {
+ public:
+  Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  const Dims& dims() const { return D_; }
+  cudaStream_t stream() const { return st_; }
+  int last_launches() const { return last_launches_; }
+
+  void reset_gop();
+  void push_frame(const int32_t* yhat_chw_host, int rate);
+  // Encoder (teacher forced). zhat_in: nullable host [hc][zh][zw]; mu/sigma
+  // nullable host [C][H][W]. Payloads are written to host buffers.
+  FrameResult encode(const int32_t* yhat_chw_host, int rate, int fidx, const int32_t* zhat_in,
+                     float* mu_out, float* sigma_out, uint8_t* hyper_out, size_t hyper_cap,
+                     uint8_t* main_out, size_t main_cap, bool advance);
+  // Decoder. Payloads and output either on the host (copies inside the call)
+  // or already in device memory (device == true).
+  FrameResult decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
+                     int rate, int fidx, bool advance, int32_t* yhat_out, bool device);
+  void last_zhat(int32_t* out_host);
+
+ private:
+  // ---- setup
+  void alloc_all();
+  void upload_weights(const WeightMap& w);
+  void build_tables();
+  template <class T>
+  T* dalloc(size_t n);
+  // ---- program building blocks
+  void add(Program& P, std::function<void(cudaStream_t)> op, int launches = 1);
+  void gemm(Program& P, const __half* A, int lda, int M, const PW& B, int K,
+            const pswa_dev::GemmEpi& ep);
+  void block_step(Program& P, const Block& b, int t, const char* tag, bool self_mask_le);
+  void build_ctx(Program& P);
+  void build_hyper_decode(Program& P);
+  void build_hyper_encode(Program& P);
+  void build_s1(Program& P, int t, bool encoder);
+  void build_step(Program& P, int t, int mode /*0 decode, 1 encode*/);
+  void build_embed(Program& P, int t);
+  void run(Program& P);
+  void set_frame_params(int rate, int fidx);
+  void advance_ring();
+  Program& program(const std::string& key);
+
+  Dims D_;
+  int device_ = 0;
+  cudaStream_t st_ = nullptr;
+  std::vector<void*> allocs_;
+  std::map<std::string, Program> progs_;
+  int last_launches_ = 0;
+
+  // weights
+  Block ctx_[16], s1_[16], s2_[16];
+  float *ctx_gout_ = nullptr, *s1_gout_ = nullptr, *s2_gout_ = nullptr;
+  PW emb_w_;
+  float *emb_b_ = nullptr, *rate_in_ = nullptr, *rate_hyper_ = nullptr, *rate_out_ = nullptr;
+  float* pad_ = nullptr;
+  PW hd_c_[2][2], hd_out_, he_in_, he_c_[2][2];
+  float *hd_b_[2][2] = {}, *hd_out_b_ = nullptr, *he_in_b_ = nullptr, *he_b_[2][2] = {};
+  float *prior_loc_ = nullptr, *prior_scale_ = nullptr;
+  Block acc_;
+  PW ch_proj_, ch_emb_[8], ch_mix_[4], ch_gu_[4][8], ch_d_[4][8], head_w1_[8], head_w2_[8];
+  float *ch_g1_[4] = {}, *ch_g2_[4] = {}, *ch_gout_ = nullptr;
+  float *head_b1_[8] = {}, *head_b2_[8] = {};
+
+  // per-frame parameters (device; set before each program launch)
+  float *cur_rsi_ = nullptr, *cur_rsh_ = nullptr, *cur_rso_ = nullptr;
+  float *cur_loc_ = nullptr, *cur_scale_ = nullptr;
+  int* slot_src_ = nullptr;
+  float** ring_ptrs_ = nullptr;
+  std::vector<float*> ring_;
+  int head_ = 0, npast_ = 0;
+
+  // tables
+  std::vector<std::vector<int>> step_rows_h_;
+  int* step_rows_[16] = {};
+  int* step_rows_pad_[16] = {};
+  int32_t* step_qinfo_[16] = {};
+  int32_t* ctx_qinfo_ = nullptr;
+  int* crop_rows_ = nullptr;  // padded hyper grid index -> raster index (-1: pad)
+  float* scales_ = nullptr;
+  uint32_t* cdf_ = nullptr;
+
+  // frame buffers
+  int32_t *yfr_ = nullptr, *ychw_ = nullptr, *zhat_ = nullptr;
+  float *emb_cur_ = nullptr, *hq_ = nullptr;
+  float *ctx_x_ = nullptr;
+  __half *ctx_xn_ = nullptr, *ctx_kv_ = nullptr, *ctx_q_ = nullptr, *ctx_att_ = nullptr,
+         *ctx_h_ = nullptr, *ctx16_ = nullptr;
+  __half* acc_kv_ = nullptr;
+  // hyper
+  float *hx_ = nullptr, *hu_ = nullptr, *hh_ = nullptr;
+  __half *hcol_ = nullptr, *hcast_ = nullptr, *s1full_ = nullptr;
+  // batch buffers
+  int nmax_ = 0;
+  float *bx_ = nullptr, *chx_ = nullptr, *musig_ = nullptr;
+  __half *bxn_ = nullptr, *bq_ = nullptr, *batt_ = nullptr, *bh_ = nullptr, *bs1n_ = nullptr,
+         *bs2n_ = nullptr, *y16_ = nullptr, *chxn_[4] = {}, *chn2_ = nullptr, *chh_ = nullptr,
+         *chfo_ = nullptr, *hh16_ = nullptr;
+  // coder
+  uint8_t *d_hyper_ = nullptr, *d_main_ = nullptr;
+  size_t hyper_cap_ = 0, main_cap_ = 0;
+  uint32_t* d_lens_ = nullptr;  // [2] payload lengths (hyper, main)
+  pswa_dev::LaneState *lanes_ = nullptr, *hlanes_ = nullptr;
+  int* status_ = nullptr;
+  double* bits_ = nullptr;  // [2]
+  int32_t *sym_v_ = nullptr, *hsym_v_ = nullptr;
+  uint8_t *sym_idx_ = nullptr, *hsym_idx_ = nullptr;
+  uint8_t *enc_lanes_ = nullptr, *enc_hlanes_ = nullptr;
+  uint32_t enc_cap_ = 0, enc_hcap_ = 0;
+  uint32_t *enc_lens_ = nullptr, *enc_hlens_ = nullptr;
+  double *enc_bits_ = nullptr, *enc_hbits_ = nullptr;
+  unsigned long long* pack_total_ = nullptr;  // [2]
+  uint64_t* pack_offs_ = nullptr;
+  float *mu_full_ = nullptr, *sg_full_ = nullptr;  // [HW][C] (forward_params)
+  bool want_musig_ = false;
+};
+
+}  // namespace pswa_host
