@@ -112,6 +112,10 @@ int pswa_gpu_push_frame(pswa_gpu* h, const int32_t* yhat, int rate_idx);
 int pswa_gpu_decode_frame_device(pswa_gpu* h, const void* d_hyper, size_t hyper_len,
                                  const void* d_main, size_t main_len, int rate_idx,
                                  int frame_idx_in_gop, int advance_state, void* d_yhat_out);
+/* Intermediate activations of the last forward_params call, for parity
+ * triage: "ctx", "emb", "hq", "a" (fp32 / fp16 [H*W][d]) and "s1" (fp16, padded
+ * hyper grid). *bytes gets the size; out may be NULL to query it. */
+int pswa_gpu_debug_fetch(pswa_gpu* h, const char* name, void* out, size_t cap, size_t* bytes);
 /* Number of kernels the last frame call launched (graph nodes included). */
 int pswa_gpu_last_launch_count(pswa_gpu* h);
 /* Stream the handle runs on (cudaStream_t as void*). */

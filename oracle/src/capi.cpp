@@ -198,6 +198,21 @@ int oracle_forward(void* h, const int32_t* yhat, const int32_t* zhat_or_null, in
   });
 }
 
+int oracle_forward_debug(void* h, const int32_t* yhat, const int32_t* zhat, int rate,
+                         const int32_t* const* past, int npast, float* ctx, float* s1, float* hq,
+                         float* a, float* s2) {
+  return guard([&] {
+    const Model& m = *static_cast<Model*>(h);
+    const Forward f = forward(m, yhat, zhat, rate, past_list(past, npast));
+    const size_t n = f.ctx.size() * sizeof(float);
+    std::memcpy(ctx, f.ctx.data(), n);
+    std::memcpy(s1, f.s1.data(), n);
+    std::memcpy(hq, f.hq.data(), n);
+    std::memcpy(a, f.a.data(), n);
+    std::memcpy(s2, f.s2.data(), n);
+  });
+}
+
 int oracle_encode(void* h, const int32_t* yhat, int rate, int fidx, const int32_t* const* past,
                   int npast, const int32_t* zhat_override, uint8_t* hyper, size_t hcap,
                   size_t* hlen, uint8_t* main, size_t mcap, size_t* mlen, double* bits,

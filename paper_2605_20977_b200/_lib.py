@@ -49,6 +49,7 @@ _SIGS = {
     "pswa_gpu_last_zhat": (_I, [_VP, _VP]),
     "pswa_gpu_push_frame": (_I, [_VP, _VP, _I]),
     "pswa_gpu_decode_frame_device": (_I, [_VP, _VP, _SZ, _VP, _SZ, _I, _I, _I, _VP]),
+    "pswa_gpu_debug_fetch": (_I, [_VP, C.c_char_p, _VP, _SZ, C.POINTER(_SZ)]),
     "pswa_gpu_last_launch_count": (_I, [_VP]),
     "pswa_gpu_stream": (_VP, [_VP]),
     "pswa_gpu_op_gemm_f16": (_I, [_VP, _I, _I, _VP, _I, _I, _I, _VP, _I, _I, _I, _VP, _VP, _I,

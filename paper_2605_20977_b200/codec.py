@@ -124,6 +124,14 @@ class GpuCodec:
         check(lib().pswa_gpu_decode_frame_device(self.h, d_hyper, hyper_len, d_main, main_len,
                                                  rate, fidx, int(advance), d_out))
 
+    def debug_fetch(self, name: str) -> np.ndarray:
+        n = C.c_size_t()
+        check(lib().pswa_gpu_debug_fetch(self.h, name.encode(), None, 0, C.byref(n)))
+        buf = np.zeros(n.value, np.uint8)
+        check(lib().pswa_gpu_debug_fetch(self.h, name.encode(), _ptr(buf), n.value, C.byref(n)))
+        dt = np.float16 if name in ("ctx", "s1", "s2") else np.float32
+        return buf.view(dt).astype(np.float32).reshape(-1, self.cfg.d_spatial)
+
     def last_launch_count(self) -> int:
         return lib().pswa_gpu_last_launch_count(self.h)
 

@@ -27,6 +27,8 @@ void fill_context_slots(const float* const* ring, const int* slot_src, const flo
 // frame [HW][C] int32 -> [C][HW] int32
 void yhat_to_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st);
 void yhat_from_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st);
+void scatter_rows_f32(const float* src, int lds, const int* rows, int M, int n, float* dst,
+                      int ldd, cudaStream_t st);
 void scatter_rows_f16(const __half* src, int lds, const int* rows, int M, int n, __half* dst,
                       int ldd, cudaStream_t st);
 

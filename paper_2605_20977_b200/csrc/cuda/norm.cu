@@ -109,6 +109,16 @@ __global__ void scatter_f16_kernel(const __half* __restrict__ src, int lds, cons
   for (int i = lane; i < n; i += 32) o[i] = s[i];
 }
 
+__global__ void scatter_f32_kernel(const float* __restrict__ src, int lds, const int* __restrict__ rows,
+                                   int M, int n, float* __restrict__ dst, int ldd) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float* s = src + static_cast<size_t>(row) * lds;
+  float* o = dst + static_cast<size_t>(rows[row]) * ldd;
+  for (int i = lane; i < n; i += 32) o[i] = s[i];
+}
+
 inline int warp_grid(int M) { return (M + 7) / 8; }
 
 }  // namespace
@@ -156,6 +166,13 @@ void yhat_to_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t s
 void yhat_from_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st) {
   dim3 grid((HW + 31) / 32, (C + 31) / 32);
   transpose_i32_kernel<<<grid, dim3(32, 8), 0, st>>>(src, C, HW, dst);
+  PSWA_LAUNCH_CHECK();
+}
+
+void scatter_rows_f32(const float* src, int lds, const int* rows, int M, int n, float* dst,
+                      int ldd, cudaStream_t st) {
+  if (M <= 0) return;
+  scatter_f32_kernel<<<warp_grid(M), 256, 0, st>>>(src, lds, rows, M, n, dst, ldd);
   PSWA_LAUNCH_CHECK();
 }
 

@@ -134,6 +134,10 @@ int pswa_gpu_last_zhat(pswa_gpu* h, int32_t* zhat_out) {
   return guard([&] { h->eng->last_zhat(zhat_out); });
 }
 
+int pswa_gpu_debug_fetch(pswa_gpu* h, const char* name, void* out, size_t cap, size_t* bytes) {
+  return guard([&] { *bytes = h->eng->debug_fetch(name, out, cap); });
+}
+
 int pswa_gpu_last_launch_count(pswa_gpu* h) { return h->eng->last_launches(); }
 
 void* pswa_gpu_stream(pswa_gpu* h) { return h->eng->stream(); }

@@ -201,6 +201,8 @@ void Engine::alloc_all() {
   pack_offs_ = dalloc<uint64_t>(std::max(L, Lz));
   mu_full_ = dalloc<float>(nsym);
   sg_full_ = dalloc<float>(nsym);
+  afull_ = dalloc<float>(static_cast<size_t>(HW) * d);
+  s2full_ = dalloc<__half>(static_cast<size_t>(HW) * d);
 }
 
 // ------------------------------------------------------------ weights ----
@@ -595,9 +597,14 @@ void Engine::build_step(Program& P, int t, int mode) {
   });
   add(P, [=, this](cudaStream_t s) { pswa_dev::gather_rows_f32(hq_, d, rows, M, d, bx_, d, s); });
   gemm(P, batt_, d, M, acc_.wo, d, f32_acc(bx_, d));
+  const bool taps = mode == 1 && want_musig_;  // debug taps in forward_params only
+  if (taps)
+    add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f32(bx_, d, rows, M, d, afull_, d, s); });
   // spatial module 2
   for (int b = 0; b < D.c.s2_blocks; ++b) block_step(P, s2_[b], t, "s2", true);
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, s2_gout_, bs2n_, d, s); });
+  if (taps)
+    add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f16(bs2n_, d, rows, M, d, s2full_, d, s); });
   // channel transformer (incremental over groups) + heads + coder
   const int N = D.N, sl = D.slot, sp = D.sp, dchp = N * sp, Cg = D.Cg, C = D.C;
   const int ms = (2 * Cg + 63) / 64 * 64;
@@ -878,6 +885,25 @@ FrameResult Engine::decode(const void* hyper, size_t hyper_len, const void* main
     PSWA_CUDA(cudaStreamSynchronize(st_));
   }
   return r;
+}
+
+size_t Engine::debug_fetch(const std::string& name, void* out, size_t cap) {
+  const size_t hwd = static_cast<size_t>(D_.HW) * D_.d;
+  const void* src = nullptr;
+  size_t bytes = 0;
+  if (name == "ctx") src = ctx16_, bytes = hwd * 2;
+  else if (name == "emb") src = emb_cur_, bytes = hwd * 4;
+  else if (name == "hq") src = hq_, bytes = hwd * 4;
+  else if (name == "s1") src = s1full_, bytes = static_cast<size_t>(D_.Hp) * D_.Wp * D_.d * 2;
+  else if (name == "a") src = afull_, bytes = hwd * 4;
+  else if (name == "s2") src = s2full_, bytes = hwd * 2;
+  else throw std::invalid_argument("debug_fetch: unknown buffer " + name);
+  if (out) {
+    if (cap < bytes) throw std::invalid_argument("debug_fetch: buffer too small");
+    PSWA_CUDA(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, st_));
+    PSWA_CUDA(cudaStreamSynchronize(st_));
+  }
+  return bytes;
 }
 
 void Engine::last_zhat(int32_t* out) {

@@ -74,6 +74,9 @@ class Engine {
   FrameResult decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
                      int rate, int fidx, bool advance, int32_t* yhat_out, bool device);
   void last_zhat(int32_t* out_host);
+  // Debug taps (filled by forward_params): ctx, emb, hq, s1 (padded grid),
+  // a, s2. Returns the byte size; copies when out != nullptr.
+  size_t debug_fetch(const std::string& name, void* out, size_t cap);
 
  private:
   // ---- setup
@@ -169,6 +172,8 @@ class Engine {
   unsigned long long* pack_total_ = nullptr;  // [2]
   uint64_t* pack_offs_ = nullptr;
   float *mu_full_ = nullptr, *sg_full_ = nullptr;  // [HW][C] (forward_params)
+  float* afull_ = nullptr;    // debug tap: accumulator output [HW][d]
+  __half* s2full_ = nullptr;  // debug tap: S2 output [HW][d]
   bool want_musig_ = false;
 };
 

@@ -70,6 +70,7 @@ def oracle():
         L.oracle_gen_weights.argtypes = [_P, C.c_uint64, _P, C.c_size_t, C.POINTER(C.c_size_t)]
         L.oracle_param_count.restype = C.c_int64
         L.oracle_forward.argtypes = [_P, _P, _P, C.c_int, _P, C.c_int, _P, _P, _P, _P]
+        L.oracle_forward_debug.argtypes = [_P, _P, _P, C.c_int, _P, C.c_int, _P, _P, _P, _P, _P]
         L.oracle_encode.argtypes = [_P, _P, C.c_int, C.c_int, _P, C.c_int, _P, _P, C.c_size_t,
                                     C.POINTER(C.c_size_t), _P, C.c_size_t, C.POINTER(C.c_size_t),
                                     _P, _P]
@@ -150,6 +151,18 @@ class OracleModel:
                                      len(past), ptr(mu), ptr(sg), ptr(zo), None)
         assert rc == 0, oracle().oracle_last_error()
         return mu, sg, zo
+
+    def forward_debug(self, yhat, zhat, rate=0, past=()):
+        """Stage outputs [H*W][d]: ctx, s1, hq, a, s2 (parity triage)."""
+        y = np.ascontiguousarray(yhat, dtype=np.int32)
+        z = np.ascontiguousarray(zhat, dtype=np.int32)
+        hw = self.cfg["height"] * self.cfg["width"]
+        outs = [np.zeros((hw, self.cfg["d_spatial"]), np.float32) for _ in range(5)]
+        pa, keep = _past_array(past)
+        rc = oracle().oracle_forward_debug(self.h, ptr(y), ptr(z), rate, pa, len(past),
+                                           *[ptr(o) for o in outs])
+        assert rc == 0, oracle().oracle_last_error()
+        return dict(zip(("ctx", "s1", "hq", "a", "s2"), outs))
 
     def encode(self, yhat, rate=0, fidx=0, past=(), zhat=None):
         y = np.ascontiguousarray(yhat, dtype=np.int32)

@@ -94,6 +94,7 @@ def test_roundtrip_and_params_iframe(paper, H, W):
     yd, bits_d = g.decode_frame(hyper, main, rate=1, fidx=0)
     assert np.array_equal(yd, y)                       # (1) bit-exact latents
     assert np.allclose(bits_d, bits_e, rtol=1e-12)
+    g.reset_gop()  # decode advanced the temporal ring; evaluate as an I-frame again
     mu_g, sg_g, bits_g = g.forward_params(y, z, rate=1, fidx=0)
     mu_o, sg_o, _ = om.forward(y, rate=1, zhat=z)
     bits_o = om.encode(y, rate=1, fidx=0, zhat=z)[2]
