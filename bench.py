@@ -1,0 +1,319 @@
+#!/usr/bin/env python3
+"""Benchmark: 1080p P-frame P-SWA entropy decode on B200 (BASELINE.json metric).
+
+Workload (config[2] of BASELINE.json, the metric's config): paper-scale model
+(d=512, h=16, 8/8/8 blocks, d_ch=1024, hyper 128), random-init
+weights (gen_weights seed 1), a 120x68 latent grid (1920x1088 / 16), frame 4
+of a GOP (4 real past frames in the temporal window), C=192, s=N=4, rate 0.
+Synthetic latents; each rank decodes its own GOP (rank r ->
+GOP r): weak scaling, no collective on the data path.
+
+One step = one full frame decode: z-hat lane decode, hyper decoder, context
+transformer, 16 (step, group) phases, lane range decoding of 1.57 M symbols.
+  value : latents/s over all ranks, payload already in HBM, y_hat left in HBM
+  e2e   : same metric through pswa_gpu_decode_frame with pinned host buffers
+          (payload H2D and y_hat D2H inside the timed region)
+The decoded latents are checked bit-exact against the encoder input once.
+
+`--impl reference` times the reference algorithm on the host CPU instead: the
+oracle port of decode_frame_wavefront (per-step recompute as
+specified) on a bounded band of the same frame.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, W = 68, 120          # 1080p / 16 (1920 x 1088 padded)
+GOP_INDEX = 4           # P-frame with 4 past frames
+LANES, HYPER_LANES = 4096, 1024
+FLOP_PER_LATENT = 296.0e6   # 148.0 MMAC minimal work per position (paper)
+METRIC = "1080p P-frame entropy decode ms/frame and latents/s at 1/2/4/8 B200 vs CPU"
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 7 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 7
+                          for k in range(4) if r[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- reference --
+def cpu_reference(band_rows=8, band_cols=W, seconds_budget=30.0):
+    """Oracle port of decode_frame_wavefront on a band of the 1080p frame
+    (paper scale, GOP index 4), all host threads. Returns latents/s."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_api import OracleModel, gen_weights as ogen, oracle, preset
+    from paper_2605_20977_b200.codec import cfg_from_dict, synth_latent
+    cores = os.cpu_count() or 1
+    oracle().oracle_set_threads(cores)
+    c = preset(True, band_rows, band_cols, lanes=64, hyper_lanes=16)
+    om = OracleModel(c, ogen(c, 1))
+    full = cfg_from_dict(preset(True, H, W))
+    frames = [synth_latent(full, 0, f)[:, :band_rows, :band_cols].copy() for f in range(GOP_INDEX + 1)]
+    past, y = frames[:GOP_INDEX], frames[GOP_INDEX]
+    hyper, main, bits, _ = om.encode(y, fidx=GOP_INDEX, past=past)
+    t0 = time.perf_counter()
+    res = om.decode(hyper, main, fidx=GOP_INDEX, past=past)
+    dt = time.perf_counter() - t0
+    assert res is not None and np.array_equal(res[0], y)
+    n = band_rows * band_cols
+    return {"latents_per_s": n / dt, "seconds": dt, "cores": cores, "phases": res[2],
+            "sample": f"paper-scale P-frame (GOP index 4) band {band_rows}x{band_cols} of the "
+                      f"120x68 latent grid, oracle decode_frame_wavefront (per-step recompute, "
+                      f"SPEC.md:620), {cores} threads"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    samples = [cpu_reference() for _ in range(max(1, args.steps))]
+    lps = statistics.median(s["latents_per_s"] for s in samples)
+    ms = H * W / lps * 1e3
+    cb = {"value": lps, "unit": "latents/s", "cores": samples[0]["cores"], "kind": "port",
+          "sample": samples[0]["sample"]}
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": lps, "unit": "latents/s",
+        "n_gpus": 0, "steps": args.steps, "warmup": 0, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": "1080p P-frame paper-scale entropy decode "
+                                                    "(CPU band sample, extrapolated per frame)",
+                                        "grid": [H, W], "gop_index": GOP_INDEX},
+        "cpu_baseline": cb,
+        "e2e": {"value": lps, "unit": "latents/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+# ---------------------------------------------------------------- ours ------
+def dominant_kernel_roofline(torch, lib, stream_ptr, pk):
+    """Context-transformer FFN gate/up GEMM (the largest single tcgen05 launch
+    of the frame: M = 4 x 8160 tokens, K = 512, N = 2 x 1408) timed alone with
+    CUDA events on its launch stream."""
+    M, K, N = 4 * H * W, 512, 2816
+    a = (torch.randn(M, K, device="cuda") * 0.5).half()
+    b = (torch.randn(N, K, device="cuda") * 0.05).half()
+    c = torch.empty(M, N // 2, device="cuda", dtype=torch.float16)
+    s = torch.cuda.ExternalStream(stream_ptr)
+    def launch():
+        rc = lib.pswa_gpu_op_gemm_f16(a.data_ptr(), K, M, b.data_ptr(), K, N, K, c.data_ptr(),
+                                      N // 2, 0, 0, None, None, 2, 0, stream_ptr)
+        assert rc == 0
+    for _ in range(5):
+        launch()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 50
+    e0.record(s)
+    for _ in range(reps):
+        launch()
+    e1.record(s)
+    e1.synchronize()
+    t = e0.elapsed_time(e1) / reps * 1e-3
+    flops = 2.0 * M * N * K
+    achieved = flops / t / 1e12
+    return {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": achieved / pk["bf16_tflops"], "traffic": None,
+            "kernel": "gemm_tc_kernel<256> ctx FFN gate|up (swiglu epilogue) M=32640 N=2816 K=512",
+            "us_per_launch": t * 1e6, "peak_kind": "measured burst (MEASURED_PEAKS.json bf16_tflops)"}
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2605_20977_b200 import lib
+    from paper_2605_20977_b200.codec import GpuCodec, gen_weights, make_cfg, synth_latent
+
+    cfg = make_cfg("paper", H, W, lanes=LANES, hyper_lanes=HYPER_LANES)
+    blob = gen_weights(cfg, 1)
+    gop = rank
+    frames = [synth_latent(cfg, gop, f) for f in range(GOP_INDEX + 1)]
+    enc = GpuCodec(cfg, blob, device=local)
+    for f in frames[:GOP_INDEX]:
+        enc.push_frame(f)
+    hyper, main, bits = enc.encode_frame(frames[GOP_INDEX], fidx=GOP_INDEX)
+    enc.close()
+    dec = GpuCodec(cfg, blob, device=local)
+    for f in frames[:GOP_INDEX]:
+        dec.push_frame(f)
+    # correctness gate: decoded latents bit-exact to the encoder input
+    y, dbits = dec.decode_frame(hyper, main, fidx=GOP_INDEX, advance=False)
+    exact = bool(np.array_equal(y, frames[GOP_INDEX]))
+    if not exact:
+        raise SystemExit("decoded latents differ from the encoded ones")
+
+    sp = dec.stream()
+    stream = torch.cuda.ExternalStream(sp)
+    d_hyper = torch.frombuffer(bytearray(hyper), dtype=torch.uint8).cuda()
+    d_main = torch.frombuffer(bytearray(main), dtype=torch.uint8).cuda()
+    d_out = torch.empty(192 * H * W, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+
+    def step_device():
+        dec.decode_device(d_hyper.data_ptr(), len(hyper), d_main.data_ptr(), len(main), 0,
+                          GOP_INDEX, False, d_out.data_ptr())
+
+    h_hyper = torch.frombuffer(bytearray(hyper), dtype=torch.uint8).pin_memory()
+    h_main = torch.frombuffer(bytearray(main), dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(192 * H * W, dtype=torch.int32).pin_memory()
+    hb = np.zeros(2, np.float64)
+    import ctypes as C
+
+    def step_host():
+        rc = lib().pswa_gpu_decode_frame(dec.h, h_hyper.data_ptr(), len(hyper), h_main.data_ptr(),
+                                         len(main), 0, GOP_INDEX, 0, h_out.data_ptr(),
+                                         hb.ctypes.data_as(C.POINTER(C.c_double)))
+        assert rc == 0
+
+    def timed(fn, steps):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms
+
+    with ClockSampler(local) as clk:
+        ms_dev = timed(step_device, args.steps)
+    launches = dec.last_launch_count()
+    ms_e2e = timed(step_host, args.steps)
+    assert np.array_equal(h_out.numpy().reshape(192, H, W), frames[GOP_INDEX])
+
+    pk = peaks()
+    roof = dominant_kernel_roofline(torch, lib(), sp, pk) if rank == 0 else None
+    per_frame_ms = ms_dev / args.steps
+    value = world * args.steps * H * W / (ms_dev * 1e-3)
+    e2e_value = world * args.steps * H * W / (ms_e2e * 1e-3)
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        r = cpu_reference()
+        cpu = {"value": r["latents_per_s"], "unit": "latents/s", "cores": r["cores"],
+               "kind": "port", "sample": r["sample"]}
+    frame_tflops = H * W * FLOP_PER_LATENT / (per_frame_ms * 1e-3) / 1e12
+    out = {
+        "metric": METRIC, "value": value, "unit": "latents/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_frame_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+        "data": "synthetic",
+        "config": {"workload": "1080p P-frame (GOP index 4) paper-scale P-SWA entropy decode, "
+                               "1 frame per rank per step", "grid": [H, W], "latent_ch": 192,
+                   "d_spatial": 512, "blocks": [8, 8, 8], "d_channel": 1024, "s": 4, "N": 4,
+                   "lanes": LANES, "hyper_lanes": HYPER_LANES, "parallelism": f"gop-replicas x{world}",
+                   "l2": "per-frame working set (171 MB fp16 weights + ~1 GB activations/caches) "
+                         "exceeds the 126 MB L2; no explicit flush"},
+        "ms_per_frame": per_frame_ms,
+        "symbols_per_s": value * 192,
+        "bits_per_frame": {"hyper": float(dbits[0]), "main": float(dbits[1])},
+        "payload_bytes": {"hyper": len(hyper), "main": len(main)},
+        "decoded_bit_exact": exact,
+        "gpu_launches": launches * args.steps,
+        "frame_roofline": {"bound": "tensor", "achieved": frame_tflops,
+                           "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                           "frac": frame_tflops / pk["bf16_tflops_sustained"],
+                           "algorithmic_flop_per_frame": H * W * FLOP_PER_LATENT},
+        "roofline": roof,
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_value, "unit": "latents/s",
+                "h2d_bytes_per_step": len(hyper) + len(main), "d2h_bytes_per_step": 192 * H * W * 4,
+                "ms_per_frame": ms_e2e / args.steps},
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -4,6 +4,9 @@
 #include <cstring>
 #include <sstream>
 #include <stdexcept>
+#include <algorithm>
+#include <atomic>
+#include <thread>
 
 #include "pswa/det_math.h"
 #include "pswa/rng.h"
@@ -183,7 +186,10 @@ std::vector<uint8_t> gen_weights_psww(const pswa_cfg& c, uint64_t seed) {
   w.u32(1);
   w.u64(pswa::fnv1a64(canonical_cfg(c)));
   w.u32(static_cast<uint32_t>(inv.size()));
-  for (const ParamDecl& p : inv) {
+  // layout pass: headers written now, data offsets recorded
+  std::vector<size_t> off(inv.size()), cnt(inv.size());
+  for (size_t k = 0; k < inv.size(); ++k) {
+    const ParamDecl& p = inv[k];
     w.u32(static_cast<uint32_t>(p.name.size()));
     w.b.insert(w.b.end(), p.name.begin(), p.name.end());
     w.u32(static_cast<uint32_t>(p.shape.size()));
@@ -192,9 +198,18 @@ std::vector<uint8_t> gen_weights_psww(const pswa_cfg& c, uint64_t seed) {
       w.u32(static_cast<uint32_t>(e));
       n *= static_cast<size_t>(e);
     }
+    off[k] = w.b.size();
+    cnt[k] = n;
+    w.b.resize(w.b.size() + 4 * n);
+  }
+  // value pass: one independent stream per parameter, so parameters can be
+  // generated concurrently without changing a single byte
+  auto fill = [&](size_t k) {
+    const ParamDecl& p = inv[k];
     pswa::Rng r = pswa::rng_for_parameter(seed, p.name);
     const float sd = 1.0f / std::sqrt(static_cast<float>(p.fan_in < 1 ? 1 : p.fan_in));
-    for (size_t i = 0; i < n; ++i) {
+    uint8_t* dst = w.b.data() + off[k];
+    for (size_t i = 0; i < cnt[k]; ++i) {
       float x = 0.0f;
       switch (p.init) {
         case Init::kScaledNormal: x = r.next_normal() * sd; break;
@@ -202,11 +217,17 @@ std::vector<uint8_t> gen_weights_psww(const pswa_cfg& c, uint64_t seed) {
         case Init::kOnes: x = 1.0f; break;
         case Init::kTwo: x = 1.0f * 2.0f; break;
       }
-      uint32_t bits;
-      std::memcpy(&bits, &x, 4);
-      w.u32(bits);
+      std::memcpy(dst + 4 * i, &x, 4);  // little-endian host
     }
-  }
+  };
+  const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  std::atomic<size_t> next{0};
+  for (unsigned t = 0; t < nt; ++t)
+    pool.emplace_back([&] {
+      for (size_t k; (k = next.fetch_add(1)) < inv.size();) fill(k);
+    });
+  for (auto& th : pool) th.join();
   return w.b;
 }
 

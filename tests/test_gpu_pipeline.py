@@ -24,7 +24,7 @@ OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
 # fp32 accumulation/softmax vs the fp32 no-FMA oracle): per element
 # |d mu| <= MU_ATOL + MU_RTOL*|mu|, |d sigma| <= SG_RTOL*sigma, on >= 99.9%
 # of elements, and a hard cap of 5x on the rest.
-MU_ATOL, MU_RTOL, SG_RTOL = 0.05, 0.02, 0.02
+MU_ATOL, MU_RTOL, SG_RTOL = 0.02, 0.01, 0.01
 RATE_RTOL = 1e-3
 
 
