@@ -44,6 +44,19 @@ void window_attention(const __half* q, int ldq, const int32_t* qinfo, int Mq, co
                       int win_w, int win_t, int mask, int s, const float* bias, __half* out,
                       int ldo, cudaStream_t st);
 
+// Tensor-core variant (attention_mma.cu) for head_dim 32 and 7x7 windows.
+// Work is a list of warp tiles, kAttnTileInts ints each: [0] halo top row,
+// [1] halo left col, [2] halo rows (<= 10), [3] halo cols (22), [4] query
+// slot, [5] query count, [8..23] query row indices (-1 = empty); the halo
+// must contain every query's window. Same contract as window_attention.
+constexpr int kAttnTileInts = 24;
+bool window_attention_tiles_supported(int hd, int win_h, int win_w);
+void window_attention_tiles_init();
+void window_attention_tiles(const __half* q, int ldq, const int32_t* qinfo, const int32_t* tiles,
+                            int ntiles, const __half* kv, int ldkv, int kv_slot_stride, int H,
+                            int W, int heads, int wt, int mask, int s, const float* bias,
+                            __half* out, int ldo, cudaStream_t st);
+
 // ---- convolutions for the hyperprior (conv.cu) ---------------------------
 // NHWC fp32 input [h][w][c] -> fp16 patches [oh*ow][kcols], K order
 // (ky, kx, c), zero padding 1 for 3x3. up2: input is read at (y/2, x/2) of a

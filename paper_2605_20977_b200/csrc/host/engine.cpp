@@ -116,6 +116,57 @@ void Engine::alloc_all() {
     for (int j = 0; j < T; ++j)
       for (int p = 0; p < HW; ++p) qi[static_cast<size_t>(j) * HW + p] = (j << 24) | ((p / D.W) << 12) | (p % D.W);
     ctx_qinfo_ = up(qi);
+    mma_attn_ = pswa_dev::window_attention_tiles_supported(D.hd, D.c.win_h, D.c.win_w);
+    if (mma_attn_) {
+      constexpr int TI = pswa_dev::kAttnTileInts;
+      auto strip_tiles = [&](int slot_from, int row_base) {
+        std::vector<int> v;
+        for (int j = slot_from; j < T; ++j)
+          for (int y = 0; y < D.H; ++y)
+            for (int x0 = 0; x0 < D.W; x0 += 16) {
+              std::vector<int> t(TI, -1);
+              t[0] = y - 3;
+              t[1] = x0 - 3;
+              t[2] = 7;
+              t[3] = 22;
+              t[4] = j;
+              int n = 0;
+              for (int x = x0; x < std::min(D.W, x0 + 16); ++x) t[8 + n++] = j * HW + y * D.W + x - row_base;
+              t[5] = n;
+              v.insert(v.end(), t.begin(), t.end());
+            }
+        return v;
+      };
+      const auto all = strip_tiles(0, 0), last = strip_tiles(T - 1, (T - 1) * HW);
+      n_ctx_tiles_ = static_cast<int>(all.size()) / TI;
+      n_ctx_tiles_last_ = static_cast<int>(last.size()) / TI;
+      ctx_tiles_ = up(all);
+      ctx_tiles_last_ = up(last);
+      for (int t = 0; t < D.c.s; ++t) {
+        std::vector<int> idx(static_cast<size_t>(HW), -1);
+        for (size_t k = 0; k < step_rows_h_[t].size(); ++k) idx[step_rows_h_[t][k]] = static_cast<int>(k);
+        std::vector<int> v;
+        for (int by = 0; by < D.H; by += 4)
+          for (int bx = 0; bx < D.W; bx += 16) {
+            std::vector<int> tt(TI, -1);
+            tt[0] = by - 3;
+            tt[1] = bx - 3;
+            tt[2] = 10;
+            tt[3] = 22;
+            tt[4] = 0;
+            int n = 0;
+            for (int y = by; y < std::min(D.H, by + 4); ++y)
+              for (int x = bx; x < std::min(D.W, bx + 16); ++x)
+                if (idx[y * D.W + x] >= 0) tt[8 + n++] = idx[y * D.W + x];
+            if (n == 0) continue;
+            tt[5] = n;
+            v.insert(v.end(), tt.begin(), tt.end());
+          }
+        n_step_tiles_[t] = static_cast<int>(v.size()) / TI;
+        step_tiles_[t] = up(v);
+      }
+      pswa_dev::window_attention_tiles_init();
+    }
     std::vector<int> crop(HWp);
     for (int y = 0; y < D.Hp; ++y)
       for (int x = 0; x < D.Wp; ++x) crop[static_cast<size_t>(y) * D.Wp + x] = (y < D.H && x < D.W) ? y * D.W + x : -1;
@@ -406,6 +457,26 @@ GemmEpi swiglu_out(void* out, int ld) {
 }
 }  // namespace
 
+// Windowed attention: tensor-core warp tiles when the shape allows
+// (head_dim 32, 7x7), the SIMT kernel otherwise (desk preset, head_dim 4).
+void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq,
+                       const int32_t* tiles, int ntiles, const __half* kv, int slot_stride, int wt,
+                       int mask, const float* bias, __half* out) {
+  const Dims& D = D_;
+  const int d = D.d;
+  if (mma_attn_) {
+    add(P, [=](cudaStream_t s) {
+      pswa_dev::window_attention_tiles(q, d, qinfo, tiles, ntiles, kv, 2 * d, slot_stride, D.H, D.W,
+                                       D.heads, wt, mask, D.c.s, bias, out, d, s);
+    });
+  } else {
+    add(P, [=](cudaStream_t s) {
+      pswa_dev::window_attention(q, d, qinfo, Mq, kv, 2 * d, slot_stride, D.H, D.W, D.heads, D.hd,
+                                 D.c.win_h, D.c.win_w, wt, mask, D.c.s, bias, out, d, s);
+    });
+  }
+}
+
 // One S1/S2 block on the step-t batch held in bx_ (residual stream, fp32).
 void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
   const Dims& D = D_;
@@ -420,13 +491,8 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
     e.row_map = rows;  // K/V of this step's positions into the frame cache
     gemm(P, bxn_, d, M, B.wkv, d, e);
   }
-  const __half* kvc = B.kv_cache;
-  const int mask = B.cross ? 0 : 1;
-  const float* pos = B.pos;
-  add(P, [=, this](cudaStream_t s) {
-    pswa_dev::window_attention(bq_, d, qinfo, M, kvc, 2 * d, 0, D.H, D.W, D.heads, D.hd, D.c.win_h,
-                               D.c.win_w, 0, mask, D.c.s, pos, batt_, d, s);
-  });
+  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], B.kv_cache, 0, 0, B.cross ? 0 : 1,
+            B.pos, batt_);
   gemm(P, batt_, d, M, B.wo, d, f32_acc(bx_, d));
   const float* g2 = B.g2;
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, g2, bxn_, d, s); });
@@ -448,11 +514,8 @@ void Engine::build_ctx(Program& P) {
     add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(ctx_x_, d, nullptr, n, d, d, g1, ctx_xn_, d, s); });
     gemm(P, ctx_xn_, d, n, B.wkv, d, f16_out(ctx_kv_, 2 * d));
     gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, f16_out(ctx_q_, d));
-    add(P, [=, this](cudaStream_t s) {
-      pswa_dev::window_attention(ctx_q_, d, ctx_qinfo_ + q0, nq, ctx_kv_, 2 * d, HW, D.H, D.W,
-                                 D.heads, D.hd, D.c.win_h, D.c.win_w, D.c.win_t, 0, D.c.s, pos,
-                                 ctx_att_, d, s);
-    });
+    attention(P, ctx_q_, ctx_qinfo_ + q0, nq, last ? ctx_tiles_last_ : ctx_tiles_,
+              last ? n_ctx_tiles_last_ : n_ctx_tiles_, ctx_kv_, HW, D.c.win_t, 0, pos, ctx_att_);
     float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
     __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;
     gemm(P, ctx_att_, d, nq, B.wo, d, f32_acc(xq, d));
@@ -591,10 +654,7 @@ void Engine::build_step(Program& P, int t, int mode) {
   // accumulator: A = Hq + xattn(Q = Hq, KV = S1 of strictly earlier steps)
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(hq_, d, rows, M, d, d, acc_.g1, bxn_, d, s); });
   gemm(P, bxn_, d, M, acc_.wq, d, f16_out(bq_, d));
-  add(P, [=, this](cudaStream_t s) {
-    pswa_dev::window_attention(bq_, d, qinfo, M, acc_kv_, 2 * d, 0, D.H, D.W, D.heads, D.hd,
-                               D.c.win_h, D.c.win_w, 0, 2, D.c.s, acc_.pos, batt_, d, s);
-  });
+  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], acc_kv_, 0, 0, 2, acc_.pos, batt_);
   add(P, [=, this](cudaStream_t s) { pswa_dev::gather_rows_f32(hq_, d, rows, M, d, bx_, d, s); });
   gemm(P, batt_, d, M, acc_.wo, d, f32_acc(bx_, d));
   const bool taps = mode == 1 && want_musig_;  // debug taps in forward_params only

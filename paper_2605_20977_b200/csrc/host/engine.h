@@ -136,6 +136,16 @@ class Engine {
   int* step_rows_pad_[16] = {};
   int32_t* step_qinfo_[16] = {};
   int32_t* ctx_qinfo_ = nullptr;
+  // tensor-core attention work lists (warp tiles); empty when unsupported
+  bool mma_attn_ = false;
+  int32_t* ctx_tiles_ = nullptr;        // all slots (rows relative to slot 0)
+  int32_t* ctx_tiles_last_ = nullptr;   // last slot only (rows relative to it)
+  int n_ctx_tiles_ = 0, n_ctx_tiles_last_ = 0;
+  int32_t* step_tiles_[16] = {};
+  int n_step_tiles_[16] = {};
+  void attention(struct Program& P, const __half* q, const int32_t* qinfo, int Mq, const int32_t* tiles,
+                 int ntiles, const __half* kv, int slot_stride, int wt, int mask, const float* bias,
+                 __half* out);
   int* crop_rows_ = nullptr;  // padded hyper grid index -> raster index (-1: pad)
   float* scales_ = nullptr;
   uint32_t* cdf_ = nullptr;
