@@ -45,17 +45,20 @@ void window_attention(const __half* q, int ldq, const int32_t* qinfo, int Mq, co
                       int ldo, cudaStream_t st);
 
 // Tensor-core variant (attention_mma.cu) for head_dim 32 and 7x7 windows.
-// Work is a list of warp tiles, kAttnTileInts ints each: [0] halo top row,
-// [1] halo left col, [2] halo rows (<= 10), [3] halo cols (22), [4] query
-// slot, [5] query count, [8..23] query row indices (-1 = empty); the halo
-// must contain every query's window. Same contract as window_attention.
-constexpr int kAttnTileInts = 24;
+// Work is a list of CTA tiles, kAttnTileInts ints each: [0] halo top row,
+// [1] halo left col (halo is 22 columns wide), [2] halo rows, [3] query rows
+// per warp (RPW; warp w's band is halo rows [w*RPW, w*RPW+RPW+6)), [4] query
+// slot, [5] warps with queries, [8 + 16*w + i] query row i of warp w (-1 =
+// none). Every query of warp w must lie in halo rows [w*RPW+3, w*RPW+RPW+3)
+// and halo columns [3, 19). Same contract as window_attention otherwise.
+constexpr int kAttnTileInts = 8 + 16 * 8;
 bool window_attention_tiles_supported(int hd, int win_h, int win_w);
-void window_attention_tiles_init();
+int window_attention_tiles_smem(int halo_rows, bool three_d);
+void window_attention_tiles_init(int max_smem_bytes);
 void window_attention_tiles(const __half* q, int ldq, const int32_t* qinfo, const int32_t* tiles,
-                            int ntiles, const __half* kv, int ldkv, int kv_slot_stride, int H,
-                            int W, int heads, int wt, int mask, int s, const float* bias,
-                            __half* out, int ldo, cudaStream_t st);
+                            int ntiles, int warps_per_tile, int halo_rows, const __half* kv,
+                            int ldkv, int kv_slot_stride, int H, int W, int heads, int wt, int mask,
+                            int s, const float* bias, __half* out, int ldo, cudaStream_t st);
 
 // ---- convolutions for the hyperprior (conv.cu) ---------------------------
 // NHWC fp32 input [h][w][c] -> fp16 patches [oh*ow][kcols], K order

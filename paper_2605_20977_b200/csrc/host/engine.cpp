@@ -35,6 +35,9 @@ void put_linear(std::vector<__half>& dst, int ldk, const float* src, int in, int
           __float2half_rn(src[static_cast<size_t>(i) * out + o]);
 }
 
+constexpr int kCtxWarps = 8;   // attention CTA shape for the 3D context window
+constexpr int kStepWarps = 4;  // ... and for the step-batched 2D windows
+
 std::vector<int> positions(int H, int W, int s, int t) {
   std::vector<int> v;
   for (int y = 0; y < H; ++y)
@@ -119,53 +122,63 @@ void Engine::alloc_all() {
     mma_attn_ = pswa_dev::window_attention_tiles_supported(D.hd, D.c.win_h, D.c.win_w);
     if (mma_attn_) {
       constexpr int TI = pswa_dev::kAttnTileInts;
-      auto strip_tiles = [&](int slot_from, int row_base) {
+      // context: CTA = 8 warps x (1 row x 16 cols) query strips of one slot
+      auto ctx_tiles = [&](int slot_from, int row_base) {
         std::vector<int> v;
         for (int j = slot_from; j < T; ++j)
-          for (int y = 0; y < D.H; ++y)
+          for (int y0 = 0; y0 < D.H; y0 += kCtxWarps)
             for (int x0 = 0; x0 < D.W; x0 += 16) {
               std::vector<int> t(TI, -1);
-              t[0] = y - 3;
+              t[0] = y0 - 3;
               t[1] = x0 - 3;
-              t[2] = 7;
-              t[3] = 22;
+              t[2] = kCtxWarps + 6;
+              t[3] = 1;
               t[4] = j;
-              int n = 0;
-              for (int x = x0; x < std::min(D.W, x0 + 16); ++x) t[8 + n++] = j * HW + y * D.W + x - row_base;
-              t[5] = n;
+              t[5] = std::min(kCtxWarps, D.H - y0);
+              for (int w = 0; w < t[5]; ++w)
+                for (int x = x0, i = 0; x < std::min(D.W, x0 + 16); ++x, ++i)
+                  t[8 + 16 * w + i] = j * HW + (y0 + w) * D.W + x - row_base;
               v.insert(v.end(), t.begin(), t.end());
             }
         return v;
       };
-      const auto all = strip_tiles(0, 0), last = strip_tiles(T - 1, (T - 1) * HW);
+      const auto all = ctx_tiles(0, 0), last = ctx_tiles(T - 1, (T - 1) * HW);
       n_ctx_tiles_ = static_cast<int>(all.size()) / TI;
       n_ctx_tiles_last_ = static_cast<int>(last.size()) / TI;
       ctx_tiles_ = up(all);
       ctx_tiles_last_ = up(last);
+      // step batches: CTA = 4 warps stacked vertically, warp = the step-t
+      // positions of a 4x16 block (16 when the block is inside the grid)
       for (int t = 0; t < D.c.s; ++t) {
         std::vector<int> idx(static_cast<size_t>(HW), -1);
         for (size_t k = 0; k < step_rows_h_[t].size(); ++k) idx[step_rows_h_[t][k]] = static_cast<int>(k);
         std::vector<int> v;
-        for (int by = 0; by < D.H; by += 4)
+        for (int by = 0; by < D.H; by += 4 * kStepWarps)
           for (int bx = 0; bx < D.W; bx += 16) {
             std::vector<int> tt(TI, -1);
             tt[0] = by - 3;
             tt[1] = bx - 3;
-            tt[2] = 10;
-            tt[3] = 22;
+            tt[2] = 4 * kStepWarps + 6;
+            tt[3] = 4;
             tt[4] = 0;
-            int n = 0;
-            for (int y = by; y < std::min(D.H, by + 4); ++y)
-              for (int x = bx; x < std::min(D.W, bx + 16); ++x)
-                if (idx[y * D.W + x] >= 0) tt[8 + n++] = idx[y * D.W + x];
-            if (n == 0) continue;
-            tt[5] = n;
+            tt[5] = kStepWarps;
+            int total = 0;
+            for (int w = 0; w < kStepWarps; ++w) {
+              int n = 0;
+              for (int y = by + 4 * w; y < std::min(D.H, by + 4 * w + 4); ++y)
+                for (int x = bx; x < std::min(D.W, bx + 16); ++x)
+                  if (idx[y * D.W + x] >= 0) tt[8 + 16 * w + n++] = idx[y * D.W + x];
+              total += n;
+            }
+            if (total == 0) continue;
             v.insert(v.end(), tt.begin(), tt.end());
           }
         n_step_tiles_[t] = static_cast<int>(v.size()) / TI;
         step_tiles_[t] = up(v);
       }
-      pswa_dev::window_attention_tiles_init();
+      pswa_dev::window_attention_tiles_init(
+          std::max(pswa_dev::window_attention_tiles_smem(kCtxWarps + 6, true),
+                   pswa_dev::window_attention_tiles_smem(4 * kStepWarps + 6, false)));
     }
     std::vector<int> crop(HWp);
     for (int y = 0; y < D.Hp; ++y)
@@ -465,9 +478,12 @@ void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq
   const Dims& D = D_;
   const int d = D.d;
   if (mma_attn_) {
+    const int warps = wt > 0 ? kCtxWarps : kStepWarps;
+    const int halo_rows = wt > 0 ? kCtxWarps + 6 : 4 * kStepWarps + 6;
     add(P, [=](cudaStream_t s) {
-      pswa_dev::window_attention_tiles(q, d, qinfo, tiles, ntiles, kv, 2 * d, slot_stride, D.H, D.W,
-                                       D.heads, wt, mask, D.c.s, bias, out, d, s);
+      pswa_dev::window_attention_tiles(q, d, qinfo, tiles, ntiles, warps, halo_rows, kv, 2 * d,
+                                       slot_stride, D.H, D.W, D.heads, wt, mask, D.c.s, bias, out,
+                                       d, s);
     });
   } else {
     add(P, [=](cudaStream_t s) {
