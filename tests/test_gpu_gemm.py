@@ -62,3 +62,33 @@ def test_gemm_deterministic():
     c1, _ = _run(2040, 512, 512)
     c2, _ = _run(2040, 512, 512)
     assert torch.equal(c1, c2)
+
+
+@pytest.mark.parametrize("M,N,K", [(2040, 1408, 256), (32640, 2816, 512), (100, 128, 64)])
+def test_gemm_swiglu(M, N, K):
+    torch.manual_seed(M + N)
+    a = (torch.randn(M, K, device="cuda") * 0.5).half()
+    b = (torch.randn(N, K, device="cuda") * 0.05).half()
+    c = torch.zeros(M, N // 2, device="cuda", dtype=torch.float16)
+    check(lib().pswa_gpu_op_gemm_f16(a.data_ptr(), K, M, b.data_ptr(), K, N, K, c.data_ptr(), N // 2,
+                                     0, 0, None, None, 2, 0, None))
+    torch.cuda.synchronize()
+    acc = a.float() @ b.float().t()
+    ref = torch.nn.functional.silu(acc[:, 0::2]) * acc[:, 1::2]
+    assert torch.allclose(c.float(), ref, atol=3e-2, rtol=2e-2)
+
+
+def test_gemm_head_epilogue():
+    torch.manual_seed(5)
+    M, N, K = 333, 128, 512
+    a = (torch.randn(M, K, device="cuda") * 0.5).half()
+    b = (torch.randn(N, K, device="cuda") * 0.05).half()
+    bias = torch.randn(N, device="cuda") * 0.1
+    scale = torch.rand(N, device="cuda") + 0.5
+    c = torch.zeros(M, N, device="cuda")
+    check(lib().pswa_gpu_op_gemm_f16(a.data_ptr(), K, M, b.data_ptr(), K, N, K, c.data_ptr(), N, 1, 0,
+                                     bias.data_ptr(), scale.data_ptr(), 3, 0, None))
+    torch.cuda.synchronize()
+    acc = a.float() @ b.float().t() + bias
+    ref = torch.cat([acc[:, :64] * scale[:64], 0.11 + torch.nn.functional.softplus(acc[:, 64:])], 1)
+    assert torch.allclose(c, ref, atol=1e-3, rtol=1e-3)
