@@ -13,6 +13,7 @@
 
 #include "check.h"
 #include "kernels.h"
+#include "launch.cuh"
 
 namespace pswa_dev {
 
@@ -26,6 +27,8 @@ __global__ void __launch_bounds__(256)
                        int Mq, const __half* __restrict__ kv, int ldkv, int kv_slot_stride, int H,
                        int W, int heads, int wh, int ww, int wt, int mask, int s,
                        const float* __restrict__ bias, __half* __restrict__ out, int ldo, int d) {
+  pdl_wait();
+  pdl_trigger();
   const int gw = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int i = gw / heads, h = gw % heads;
@@ -144,7 +147,7 @@ void window_attention(const __half* q, int ldq, const int32_t* qinfo, int Mq, co
   const long warps = static_cast<long>(Mq) * heads;
   const int grid = static_cast<int>((warps + 7) / 8);
 #define PSWA_ATTN(HD)                                                                         \
-  window_attn_kernel<HD><<<grid, 256, 0, st>>>(q, ldq, qinfo, Mq, kv, ldkv, kv_slot_stride, H, \
+  launch_k(window_attn_kernel<HD>, dim3(grid), dim3(256), 0, st, q, ldq, qinfo, Mq, kv, ldkv, kv_slot_stride, H, \
                                                W, heads, win_h, win_w, win_t, mask, s, bias,  \
                                                out, ldo, d)
   switch (hd) {

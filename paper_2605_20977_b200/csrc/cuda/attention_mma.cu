@@ -22,6 +22,7 @@
 
 #include "check.h"
 #include "kernels.h"
+#include "launch.cuh"
 
 namespace pswa_dev {
 
@@ -92,6 +93,8 @@ struct AttnArgs {
 };
 
 __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.y;
@@ -331,7 +334,7 @@ void window_attention_tiles(const __half* q, int ldq, const int32_t* qinfo, cons
   AttnArgs a{q, ldq, qinfo, tiles, ntiles, kv, ldkv, kv_slot_stride, H, W, wt, mask, s,
              heads * kHD, bias, out, ldo, window_attention_halo_keys(halo_rows)};
   dim3 grid(ntiles, heads);
-  window_attn_mma_kernel<<<grid, warps_per_tile * 32, smem_bytes(a.halo_keys, wt > 0), st>>>(a);
+  launch_k(window_attn_mma_kernel, grid, dim3(warps_per_tile * 32), smem_bytes(a.halo_keys, wt > 0), st, a);
   PSWA_LAUNCH_CHECK();
 }
 

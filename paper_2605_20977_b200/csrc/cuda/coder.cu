@@ -16,6 +16,7 @@
 
 #include "check.h"
 #include "kernels.h"
+#include "launch.cuh"
 
 namespace pswa_dev {
 
@@ -86,6 +87,8 @@ __device__ double d_erf(double x) {
 }
 
 __global__ void build_cdf_kernel(float* scales, uint32_t* cdf) {
+  pdl_wait();
+  pdl_trigger();
   const int idx = threadIdx.x;
   if (idx >= kScales) return;
   const double ratio = d_log(64.0 / 0.11);
@@ -190,6 +193,8 @@ __device__ int32_t dec_value(const uint8_t* pl, LaneState& s, const uint32_t* cd
 // ------------------------------------------------------------ kernels -----
 __global__ void lanes_init_kernel(const uint8_t* __restrict__ pl, const uint32_t* __restrict__ len_p,
                                   int L, uint32_t expect, LaneState* __restrict__ lanes, int* status) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t len = *len_p;
   __shared__ uint64_t part[1024];
   __shared__ int bad;
@@ -244,6 +249,8 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
                                     const float* __restrict__ scales, const uint32_t* __restrict__ cdf,
                                     const int* __restrict__ rows, int32_t* __restrict__ yhat, int C,
                                     int c0, __half* __restrict__ yhat16, int ld16, int* status) {
+  pdl_wait();
+  pdl_trigger();
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
   const uint64_t total = static_cast<uint64_t>(n) * per;
@@ -272,6 +279,8 @@ __global__ void decode_hyper_kernel(const uint8_t* __restrict__ pl, LaneState* _
                                     const float* __restrict__ scale, const float* __restrict__ scales,
                                     const uint32_t* __restrict__ cdf, int32_t* __restrict__ zhat,
                                     int* status) {
+  pdl_wait();
+  pdl_trigger();
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
   LaneState s = lanes[l];
@@ -293,6 +302,8 @@ __global__ void quantize_phase_kernel(const float* __restrict__ musig, int ldms,
                                       uint8_t* __restrict__ sym_idx, __half* __restrict__ yhat16,
                                       int ld16, float* __restrict__ mu_out,
                                       float* __restrict__ sigma_out) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n * per) return;
   const int k = i / per, j = i - k * per;
@@ -313,6 +324,8 @@ __global__ void quantize_hyper_kernel(const int32_t* __restrict__ zhat, int n, i
                                       const float* __restrict__ loc, const float* __restrict__ scale,
                                       const float* __restrict__ scales, int32_t* __restrict__ sym_v,
                                       uint8_t* __restrict__ sym_idx) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int ch = i / per_ch;
@@ -356,6 +369,8 @@ __global__ void encode_lanes_kernel(const int32_t* __restrict__ sym_v, const uin
                                     uint64_t n, int L, const uint32_t* __restrict__ cdf,
                                     uint8_t* __restrict__ out, uint32_t cap, uint32_t* __restrict__ lens,
                                     double* __restrict__ bits, int* status) {
+  pdl_wait();
+  pdl_trigger();
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
   Enc e{0, kWin, 0, false, out + static_cast<size_t>(l) * cap, cap};
@@ -388,6 +403,8 @@ __global__ void encode_lanes_kernel(const int32_t* __restrict__ sym_v, const uin
 }
 
 __global__ void sum_bits_kernel(const double* __restrict__ v, int stride, int L, double* out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double part[256];
   const int t = threadIdx.x;
   const int per = (L + 255) / 256;
@@ -407,13 +424,13 @@ inline int blocks(long n, int t = 128) { return static_cast<int>((n + t - 1) / t
 }  // namespace
 
 void build_cdf_tables(float* scales, uint32_t* cdf, cudaStream_t st) {
-  build_cdf_kernel<<<1, kScales, 0, st>>>(scales, cdf);
+  launch_k(build_cdf_kernel, dim3(1), dim3(kScales), 0, st, scales, cdf);
   PSWA_LAUNCH_CHECK();
 }
 
 void lanes_init(const uint8_t* payload, const uint32_t* len, int lanes, uint32_t expect_count,
                 LaneState* st_lanes, int* status, cudaStream_t st) {
-  lanes_init_kernel<<<1, 1024, 0, st>>>(payload, len, lanes, expect_count, st_lanes, status);
+  launch_k(lanes_init_kernel, dim3(1), dim3(1024), 0, st, payload, len, lanes, expect_count, st_lanes, status);
   PSWA_LAUNCH_CHECK();
 }
 
@@ -422,7 +439,7 @@ void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_
                         const uint32_t* cdf, const int* rows, int32_t* yhat, int C, int c0,
                         __half* yhat16, int ld16, int* status, cudaStream_t st) {
   if (n <= 0) return;
-  decode_phase_kernel<<<blocks(L), 128, 0, st>>>(payload, lanes, L, o0, n, per, musig, ldms,
+  launch_k(decode_phase_kernel, dim3(blocks(L)), dim3(128), 0, st, payload, lanes, L, o0, n, per, musig, ldms,
                                                   sig_off, scales, cdf, rows, yhat, C, c0, yhat16,
                                                   ld16, status);
   PSWA_LAUNCH_CHECK();
@@ -431,7 +448,7 @@ void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_
 void lanes_decode_hyper(const uint8_t* payload, LaneState* lanes, int L, int n, int per_ch,
                         const float* loc, const float* scale, const float* scales,
                         const uint32_t* cdf, int32_t* zhat, int* status, cudaStream_t st) {
-  decode_hyper_kernel<<<blocks(L), 128, 0, st>>>(payload, lanes, L, n, per_ch, loc, scale, scales,
+  launch_k(decode_hyper_kernel, dim3(blocks(L)), dim3(128), 0, st, payload, lanes, L, n, per_ch, loc, scale, scales,
                                                   cdf, zhat, status);
   PSWA_LAUNCH_CHECK();
 }
@@ -441,15 +458,14 @@ void quantize_phase(const float* musig, int ldms, int sig_off, int n, int per, u
                     int32_t* sym_v, uint8_t* sym_idx, __half* yhat16, int ld16, float* mu_out,
                     float* sigma_out, cudaStream_t st) {
   if (n <= 0) return;
-  quantize_phase_kernel<<<blocks(static_cast<long>(n) * per, 256), 256, 0, st>>>(
-      musig, ldms, sig_off, n, per, o0, rows, yhat, C, c0, scales, sym_v, sym_idx, yhat16, ld16,
+  launch_k(quantize_phase_kernel, dim3(blocks(static_cast<long>(n) * per, 256)), dim3(256), 0, st, musig, ldms, sig_off, n, per, o0, rows, yhat, C, c0, scales, sym_v, sym_idx, yhat16, ld16,
       mu_out, sigma_out);
   PSWA_LAUNCH_CHECK();
 }
 
 void quantize_hyper(const int32_t* zhat, int n, int per_ch, const float* loc, const float* scale,
                     const float* scales, int32_t* sym_v, uint8_t* sym_idx, cudaStream_t st) {
-  quantize_hyper_kernel<<<blocks(n, 256), 256, 0, st>>>(zhat, n, per_ch, loc, scale, scales, sym_v,
+  launch_k(quantize_hyper_kernel, dim3(blocks(n, 256)), dim3(256), 0, st, zhat, n, per_ch, loc, scale, scales, sym_v,
                                                         sym_idx);
   PSWA_LAUNCH_CHECK();
 }
@@ -457,19 +473,19 @@ void quantize_hyper(const int32_t* zhat, int n, int per_ch, const float* loc, co
 void lanes_encode(const int32_t* sym_v, const uint8_t* sym_idx, uint64_t n, int L,
                   const uint32_t* cdf, uint8_t* out, uint32_t cap, uint32_t* lens, double* bits,
                   int* status, cudaStream_t st) {
-  encode_lanes_kernel<<<blocks(L), 128, 0, st>>>(sym_v, sym_idx, n, L, cdf, out, cap, lens, bits,
+  launch_k(encode_lanes_kernel, dim3(blocks(L)), dim3(128), 0, st, sym_v, sym_idx, n, L, cdf, out, cap, lens, bits,
                                                   status);
   PSWA_LAUNCH_CHECK();
 }
 
 void sum_lane_bits(const LaneState* lanes, int L, double* out, cudaStream_t st) {
-  sum_bits_kernel<<<1, 256, 0, st>>>(&lanes[0].bits, static_cast<int>(sizeof(LaneState) / 8), L,
+  launch_k(sum_bits_kernel, dim3(1), dim3(256), 0, st, &lanes[0].bits, static_cast<int>(sizeof(LaneState) / 8), L,
                                      out);
   PSWA_LAUNCH_CHECK();
 }
 
 void sum_doubles(const double* v, int L, double* out, cudaStream_t st) {
-  sum_bits_kernel<<<1, 256, 0, st>>>(v, 1, L, out);
+  launch_k(sum_bits_kernel, dim3(1), dim3(256), 0, st, v, 1, L, out);
   PSWA_LAUNCH_CHECK();
 }
 
@@ -480,6 +496,8 @@ namespace {
 __global__ void pack_offsets_kernel(const uint32_t* __restrict__ lens, int L, uint32_t count,
                                     uint8_t* __restrict__ payload, uint64_t cap,
                                     unsigned long long* total, uint64_t* __restrict__ offs, int* status) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint64_t part[1024];
   const int t = threadIdx.x;
   const int per = (L + blockDim.x - 1) / blockDim.x;
@@ -520,6 +538,8 @@ __global__ void pack_offsets_kernel(const uint32_t* __restrict__ lens, int L, ui
 __global__ void pack_copy_kernel(const uint8_t* __restrict__ enc, uint32_t cap_lane,
                                  const uint32_t* __restrict__ lens, const uint64_t* __restrict__ offs,
                                  int L, uint8_t* __restrict__ payload, uint64_t cap) {
+  pdl_wait();
+  pdl_trigger();
   const int l = blockIdx.x;
   if (l >= L) return;
   const uint64_t off = offs[l];
@@ -533,9 +553,9 @@ __global__ void pack_copy_kernel(const uint8_t* __restrict__ enc, uint32_t cap_l
 void lanes_pack(const uint8_t* enc, uint32_t cap, const uint32_t* lens, int L, uint32_t count,
                 uint8_t* payload, uint64_t payload_cap, unsigned long long* total, uint64_t* offs,
                 int* status, cudaStream_t st) {
-  pack_offsets_kernel<<<1, 1024, 0, st>>>(lens, L, count, payload, payload_cap, total, offs, status);
+  launch_k(pack_offsets_kernel, dim3(1), dim3(1024), 0, st, lens, L, count, payload, payload_cap, total, offs, status);
   PSWA_LAUNCH_CHECK();
-  pack_copy_kernel<<<L, 64, 0, st>>>(enc, cap, lens, offs, L, payload, payload_cap);
+  launch_k(pack_copy_kernel, dim3(L), dim3(64), 0, st, enc, cap, lens, offs, L, payload, payload_cap);
   PSWA_LAUNCH_CHECK();
 }
 

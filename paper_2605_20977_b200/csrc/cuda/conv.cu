@@ -6,6 +6,7 @@
 // conv weights.
 #include "check.h"
 #include "kernels.h"
+#include "launch.cuh"
 
 namespace pswa_dev {
 
@@ -13,6 +14,8 @@ namespace {
 
 __global__ void im2col3x3_kernel(const float* __restrict__ x, int h, int w, int c, int stride,
                                  int up2, int oh, int ow, __half* __restrict__ out, int kcols) {
+  pdl_wait();
+  pdl_trigger();
   const size_t total = static_cast<size_t>(oh) * ow * kcols;
   const int ih = up2 ? 2 * h : h, iw = up2 ? 2 * w : w;  // logical input grid
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -35,6 +38,8 @@ __global__ void im2col3x3_kernel(const float* __restrict__ x, int h, int w, int 
 
 __global__ void resample_kernel(const float* __restrict__ x, int h, int w, int c, int up,
                                 float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int oh = up ? 2 * h : h / 2, ow = up ? 2 * w : w / 2;
   const size_t total = static_cast<size_t>(oh) * ow * c;
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -48,6 +53,8 @@ __global__ void resample_kernel(const float* __restrict__ x, int h, int w, int c
 }
 
 __global__ void zhat_nhwc_kernel(const int32_t* __restrict__ z, int c, int hw, float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const size_t total = static_cast<size_t>(c) * hw;
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -58,6 +65,8 @@ __global__ void zhat_nhwc_kernel(const int32_t* __restrict__ z, int c, int hw, f
 }
 
 __global__ void round_zhat_kernel(const float* __restrict__ x, int c, int hw, int32_t* __restrict__ z) {
+  pdl_wait();
+  pdl_trigger();
   const size_t total = static_cast<size_t>(c) * hw;
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -78,29 +87,28 @@ void im2col3x3(const float* x, int h, int w, int c, int stride, int up2, __half*
                cudaStream_t st) {
   const int ih = up2 ? 2 * h : h, iw = up2 ? 2 * w : w;
   const int oh = (ih + 2 - 3) / stride + 1, ow = (iw + 2 - 3) / stride + 1;
-  im2col3x3_kernel<<<grid_for(static_cast<size_t>(oh) * ow * kcols), 256, 0, st>>>(
-      x, h, w, c, stride, up2, oh, ow, out, kcols);
+  launch_k(im2col3x3_kernel, dim3(grid_for(static_cast<size_t>(oh) * ow * kcols)), dim3(256), 0, st, x, h, w, c, stride, up2, oh, ow, out, kcols);
   PSWA_LAUNCH_CHECK();
 }
 
 void upsample2_nhwc(const float* x, int h, int w, int c, float* out, cudaStream_t st) {
-  resample_kernel<<<grid_for(static_cast<size_t>(4) * h * w * c), 256, 0, st>>>(x, h, w, c, 1, out);
+  launch_k(resample_kernel, dim3(grid_for(static_cast<size_t>(4) * h * w * c)), dim3(256), 0, st, x, h, w, c, 1, out);
   PSWA_LAUNCH_CHECK();
 }
 
 void subsample2_nhwc(const float* x, int h, int w, int c, float* out, cudaStream_t st) {
-  resample_kernel<<<grid_for(static_cast<size_t>(h) * w * c / 4 + 1), 256, 0, st>>>(x, h, w, c, 0,
+  launch_k(resample_kernel, dim3(grid_for(static_cast<size_t>(h) * w * c / 4 + 1)), dim3(256), 0, st, x, h, w, c, 0,
                                                                                      out);
   PSWA_LAUNCH_CHECK();
 }
 
 void zhat_to_nhwc(const int32_t* z, int c, int hw, float* out, cudaStream_t st) {
-  zhat_nhwc_kernel<<<grid_for(static_cast<size_t>(c) * hw), 256, 0, st>>>(z, c, hw, out);
+  launch_k(zhat_nhwc_kernel, dim3(grid_for(static_cast<size_t>(c) * hw)), dim3(256), 0, st, z, c, hw, out);
   PSWA_LAUNCH_CHECK();
 }
 
 void round_to_zhat(const float* x, int c, int hw, int32_t* z, cudaStream_t st) {
-  round_zhat_kernel<<<grid_for(static_cast<size_t>(c) * hw), 256, 0, st>>>(x, c, hw, z);
+  launch_k(round_zhat_kernel, dim3(grid_for(static_cast<size_t>(c) * hw)), dim3(256), 0, st, x, c, hw, z);
   PSWA_LAUNCH_CHECK();
 }
 

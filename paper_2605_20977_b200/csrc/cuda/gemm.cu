@@ -21,6 +21,7 @@
 
 #include "check.h"
 #include "gemm.h"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace pswa_dev {
@@ -99,11 +100,30 @@ __device__ __forceinline__ void epi_values(const GemmEpi& ep, int n0, float (&v)
   }
 }
 
+// Residual rows of one 32x32 fp32 chunk in the coalesced store mapping,
+// loaded ahead of time (independent of the accumulator) so their latency
+// overlaps the MMA / TMEM wait instead of serialising the epilogue.
+__device__ __forceinline__ void prefetch_residual(const GemmEpi& ep, int M, int m0w, int oc0,
+                                                  int lane, float4 (&res)[8]) {
+#pragma unroll
+  for (int pass = 0; pass < 8; ++pass) {
+    const int r = pass * 4 + (lane >> 3), c = (lane & 7) * 4;
+    const int m = m0w + r;
+    res[pass] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (m >= M || oc0 + c + 4 > ep.n_store) continue;
+    const int orow = ep.row_map ? ep.row_map[m] : m;
+    if (orow < 0) continue;
+    res[pass] = *reinterpret_cast<const float4*>(static_cast<const float*>(ep.out) +
+                                                 static_cast<size_t>(orow) * ep.ld_out + oc0 + c);
+  }
+}
+
 // Drain one 32 x 32 accumulator chunk (rows m0w..m0w+31 of this warp,
 // accumulator columns n0..n0+31): values -> smem transpose -> coalesced rows.
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int M, int m0w, int n0, int lane,
-                                          float* stage, const uint32_t (&raw)[32]) {
+                                          float* stage, const uint32_t (&raw)[32],
+                                          const float4 (&res)[8]) {
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
@@ -118,7 +138,8 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int M, int m0w, int
   if (oc0 >= ep.n_store) return;
   const int nvalid = min(ncols, ep.n_store - oc0);
   if (EPI == kEpiF32) {
-    // 8 lanes per row (4 floats each), 4 rows per pass
+    // 8 lanes per row (4 floats each), 4 rows per pass; the residual (when
+    // accumulating) was prefetched into `res` before the accumulator wait
 #pragma unroll
     for (int pass = 0; pass < 8; ++pass) {
       const int r = pass * 4 + (lane >> 3), c = (lane & 7) * 4;
@@ -131,11 +152,10 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int M, int m0w, int
       if (c + 4 <= nvalid) {
         float4 o = make_float4(s[0], s[1], s[2], s[3]);
         if (ep.accumulate) {
-          const float4 a = *reinterpret_cast<const float4*>(dst);
-          o.x += a.x;
-          o.y += a.y;
-          o.z += a.z;
-          o.w += a.w;
+          o.x += res[pass].x;
+          o.y += res[pass].y;
+          o.z += res[pass].z;
+          o.w += res[pass].w;
         }
         *reinterpret_cast<float4*>(dst) = o;
       } else {
@@ -217,6 +237,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // everything above overlaps the previous kernel (PDL); inputs are read below
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -265,15 +288,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       const int buf = it & 1, use = it >> 1;
       const int m0 = (t % tiles_m) * kBM, n0 = (t / tiles_m) * BN;
+      const int c0 = half * (BN / 64), c1 = (half + 1) * (BN / 64);
+      float4 res[8];
+      const bool acc_res = EPI == kEpiF32 && ep.accumulate;
+      if (acc_res) prefetch_residual(ep, M, m0 + q * 32, n0 + c0 * 32, lane, res);
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const uint32_t acc = tmem + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
-      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+      for (int c = c0; c < c1; ++c) {
         uint32_t raw[32];
         tmem_ld_32x32(acc + c * 32, raw);
         tc_wait_ld();
-        epi_chunk<EPI>(ep, M, m0 + q * 32, n0 + c * 32, lane, stage, raw);
+        epi_chunk<EPI>(ep, M, m0 + q * 32, n0 + c * 32, lane, stage, raw, res);
+        if (acc_res && c + 1 < c1) prefetch_residual(ep, M, m0 + q * 32, n0 + (c + 1) * 32, lane, res);
       }
       tc_fence_before();
       __syncwarp();
@@ -363,16 +391,20 @@ void launch(const GemmPlan& p, int kind, cudaStream_t st) {
   const int smem = GemmCfg<BN>::kSmem;
   switch (kind) {
     case kEpiF16:
-      gemm_tc_kernel<BN, kEpiF16><<<grid, kThreads, smem, st>>>(p.ta, p.tb, p.M, p.K, tiles_m, tiles, p.epi);
+      launch_k(gemm_tc_kernel<BN, kEpiF16>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.M, p.K,
+               tiles_m, tiles, p.epi);
       break;
     case kEpiF32:
-      gemm_tc_kernel<BN, kEpiF32><<<grid, kThreads, smem, st>>>(p.ta, p.tb, p.M, p.K, tiles_m, tiles, p.epi);
+      launch_k(gemm_tc_kernel<BN, kEpiF32>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.M, p.K,
+               tiles_m, tiles, p.epi);
       break;
     case kEpiSwiGLU:
-      gemm_tc_kernel<BN, kEpiSwiGLU><<<grid, kThreads, smem, st>>>(p.ta, p.tb, p.M, p.K, tiles_m, tiles, p.epi);
+      launch_k(gemm_tc_kernel<BN, kEpiSwiGLU>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.M, p.K,
+               tiles_m, tiles, p.epi);
       break;
     default:
-      gemm_tc_kernel<BN, kEpiHead><<<grid, kThreads, smem, st>>>(p.ta, p.tb, p.M, p.K, tiles_m, tiles, p.epi);
+      launch_k(gemm_tc_kernel<BN, kEpiHead>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.M, p.K,
+               tiles_m, tiles, p.epi);
       break;
   }
 }

@@ -3,6 +3,7 @@
 // All HBM-bound: one warp per row, coalesced 128 B accesses.
 #include "check.h"
 #include "kernels.h"
+#include "launch.cuh"
 
 namespace pswa_dev {
 
@@ -11,6 +12,8 @@ namespace {
 __global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ src,
                                int M, int d, int group, const float* __restrict__ gain,
                                __half* __restrict__ y, int ldy) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -32,6 +35,8 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const int* 
 
 __global__ void gather_f32_kernel(const float* __restrict__ src, int lds, const int* __restrict__ rows,
                                   int M, int n, float* __restrict__ dst, int ldd) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -48,6 +53,8 @@ __global__ void gather_f32_kernel(const float* __restrict__ src, int lds, const 
 
 __global__ void yhat_f16_kernel(const int32_t* __restrict__ yhat, int C, const int* __restrict__ rows,
                                 int M, int c0, int nc, __half* __restrict__ dst, int ldd, int ncols) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -59,6 +66,8 @@ __global__ void yhat_f16_kernel(const int32_t* __restrict__ yhat, int C, const i
 
 __global__ void f32_to_f16_kernel(const float* __restrict__ src, int lds, int M, int n,
                                   __half* __restrict__ dst, int ldd, int ncols) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -70,6 +79,8 @@ __global__ void f32_to_f16_kernel(const float* __restrict__ src, int lds, int M,
 __global__ void fill_slots_kernel(const float* const* __restrict__ ring, const int* __restrict__ slot_src,
                                   const float* __restrict__ pad, int T, int HW, int d,
                                   float* __restrict__ x) {
+  pdl_wait();
+  pdl_trigger();
   const size_t total = static_cast<size_t>(T) * HW * (d / 4);
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -86,6 +97,8 @@ __global__ void fill_slots_kernel(const float* const* __restrict__ ring, const i
 
 __global__ void transpose_i32_kernel(const int32_t* __restrict__ src, int rows, int cols,
                                      int32_t* __restrict__ dst) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int32_t tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   for (int j = threadIdx.y; j < 32; j += 8) {
@@ -101,6 +114,8 @@ __global__ void transpose_i32_kernel(const int32_t* __restrict__ src, int rows, 
 
 __global__ void scatter_f16_kernel(const __half* __restrict__ src, int lds, const int* __restrict__ rows,
                                    int M, int n, __half* __restrict__ dst, int ldd) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -111,6 +126,8 @@ __global__ void scatter_f16_kernel(const __half* __restrict__ src, int lds, cons
 
 __global__ void scatter_f32_kernel(const float* __restrict__ src, int lds, const int* __restrict__ rows,
                                    int M, int n, float* __restrict__ dst, int ldd) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -126,60 +143,60 @@ inline int warp_grid(int M) { return (M + 7) / 8; }
 void rmsnorm_rows(const float* x, int ldx, const int* src_rows, int M, int d, int group,
                   const float* gain, __half* y, int ldy, cudaStream_t st) {
   if (M <= 0) return;
-  rmsnorm_kernel<<<warp_grid(M), 256, 0, st>>>(x, ldx, src_rows, M, d, group, gain, y, ldy);
+  launch_k(rmsnorm_kernel, dim3(warp_grid(M)), dim3(256), 0, st, x, ldx, src_rows, M, d, group, gain, y, ldy);
   PSWA_LAUNCH_CHECK();
 }
 
 void gather_rows_f32(const float* src, int lds, const int* rows, int M, int n, float* dst, int ldd,
                      cudaStream_t st) {
   if (M <= 0) return;
-  gather_f32_kernel<<<warp_grid(M), 256, 0, st>>>(src, lds, rows, M, n, dst, ldd);
+  launch_k(gather_f32_kernel, dim3(warp_grid(M)), dim3(256), 0, st, src, lds, rows, M, n, dst, ldd);
   PSWA_LAUNCH_CHECK();
 }
 
 void yhat_rows_f16(const int32_t* yhat, int C, const int* rows, int M, int c0, int nc, __half* dst,
                    int ldd, int ncols, cudaStream_t st) {
   if (M <= 0) return;
-  yhat_f16_kernel<<<warp_grid(M), 256, 0, st>>>(yhat, C, rows, M, c0, nc, dst, ldd, ncols);
+  launch_k(yhat_f16_kernel, dim3(warp_grid(M)), dim3(256), 0, st, yhat, C, rows, M, c0, nc, dst, ldd, ncols);
   PSWA_LAUNCH_CHECK();
 }
 
 void f32_to_f16_rows(const float* src, int lds, int M, int n, __half* dst, int ldd, int ncols,
                      cudaStream_t st) {
   if (M <= 0) return;
-  f32_to_f16_kernel<<<warp_grid(M), 256, 0, st>>>(src, lds, M, n, dst, ldd, ncols);
+  launch_k(f32_to_f16_kernel, dim3(warp_grid(M)), dim3(256), 0, st, src, lds, M, n, dst, ldd, ncols);
   PSWA_LAUNCH_CHECK();
 }
 
 void fill_context_slots(const float* const* ring, const int* slot_src, const float* pad, int T,
                         int HW, int d, float* x, cudaStream_t st) {
-  fill_slots_kernel<<<148 * 8, 256, 0, st>>>(ring, slot_src, pad, T, HW, d, x);
+  launch_k(fill_slots_kernel, dim3(148 * 8), dim3(256), 0, st, ring, slot_src, pad, T, HW, d, x);
   PSWA_LAUNCH_CHECK();
 }
 
 void yhat_to_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st) {
   dim3 grid((C + 31) / 32, (HW + 31) / 32);
-  transpose_i32_kernel<<<grid, dim3(32, 8), 0, st>>>(src, HW, C, dst);
+  launch_k(transpose_i32_kernel, dim3(grid), dim3(32, 8), 0, st, src, HW, C, dst);
   PSWA_LAUNCH_CHECK();
 }
 
 void yhat_from_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st) {
   dim3 grid((HW + 31) / 32, (C + 31) / 32);
-  transpose_i32_kernel<<<grid, dim3(32, 8), 0, st>>>(src, C, HW, dst);
+  launch_k(transpose_i32_kernel, dim3(grid), dim3(32, 8), 0, st, src, C, HW, dst);
   PSWA_LAUNCH_CHECK();
 }
 
 void scatter_rows_f32(const float* src, int lds, const int* rows, int M, int n, float* dst,
                       int ldd, cudaStream_t st) {
   if (M <= 0) return;
-  scatter_f32_kernel<<<warp_grid(M), 256, 0, st>>>(src, lds, rows, M, n, dst, ldd);
+  launch_k(scatter_f32_kernel, dim3(warp_grid(M)), dim3(256), 0, st, src, lds, rows, M, n, dst, ldd);
   PSWA_LAUNCH_CHECK();
 }
 
 void scatter_rows_f16(const __half* src, int lds, const int* rows, int M, int n, __half* dst,
                       int ldd, cudaStream_t st) {
   if (M <= 0) return;
-  scatter_f16_kernel<<<warp_grid(M), 256, 0, st>>>(src, lds, rows, M, n, dst, ldd);
+  launch_k(scatter_f16_kernel, dim3(warp_grid(M)), dim3(256), 0, st, src, lds, rows, M, n, dst, ldd);
   PSWA_LAUNCH_CHECK();
 }
 
