@@ -90,6 +90,7 @@ struct AttnArgs {
   __half* out;
   int ldo;
   int halo_keys;  // staged keys per slot buffer (>= halo rows * 22, multiple of 32, + slack)
+  const int8_t* taps;  // [band keys (chunk-padded)][16 queries]: tap index or -1 (masked)
 };
 
 __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) {
@@ -107,11 +108,23 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
   float* sbias = reinterpret_cast<float*>(smem + (a.wt > 0 ? 4 : 2) * kbuf);  // 2 slot buffers in 3D
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
 
-  // ---- stage the bias row of this head (pre-scaled by log2 e)
+  const int band_keys = (RPW + 6) * kHaloW;
+  const int nchunks = (band_keys + kChunk - 1) / kChunk;
+  int8_t* stt = reinterpret_cast<int8_t*>(sbias + 256);       // [nchunks*32][16]
+  uint8_t* skv = reinterpret_cast<uint8_t*>(stt + nchunks * kChunk * 16);  // [halo_keys]
+
+  // ---- stage the bias row of this head (pre-scaled by log2 e), the tap
+  // table of this tile shape and the per-key in-grid flags
   for (int i = threadIdx.x; i < taps_total; i += blockDim.x)
     sbias[i] = a.bias[h * taps_total + i] * kLog2e;
-
+  for (int i = threadIdx.x; i < nchunks * kChunk * 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(stt)[i] = reinterpret_cast<const uint32_t*>(a.taps)[i];
   const int hkeys = HR * kHaloW;
+  for (int key = threadIdx.x; key < a.halo_keys; key += blockDim.x) {
+    const int ky = hy0 + key / kHaloW, kx = hx0 + key % kHaloW;
+    skv[key] = key < hkeys && ky >= 0 && ky < a.H && kx >= 0 && kx < a.W;
+  }
+
   auto stage = [&](int j, int buf) {
     const uint32_t kb = sbase + buf * 2 * kbuf, vb = kb + kbuf;
     for (int idx = threadIdx.x; idx < a.halo_keys * 4; idx += blockDim.x) {
@@ -132,20 +145,6 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
   const int32_t* Q = T + 8 + warp * 16;
   const int r0 = lane >> 2;
   const int qr[2] = {warp < T[5] ? Q[r0] : -1, warp < T[5] ? Q[r0 + 8] : -1};
-  int qhr[2], qhc[2], qs[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    qhr[i] = -1000;
-    qhc[i] = -1000;
-    qs[i] = 0;
-    if (qr[i] >= 0) {
-      const int inf = a.qinfo[qr[i]];
-      const int y = (inf >> 12) & 0xFFF, x = inf & 0xFFF;
-      qhr[i] = y - hy0 - warp * RPW;  // relative to this warp's band
-      qhc[i] = x - hx0;
-      qs[i] = (y + x) % a.s;
-    }
-  }
   uint32_t qa[2][4];
   {
     const int kc = (lane & 3) * 2;
@@ -160,11 +159,7 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
   }
   const bool live = __any_sync(0xffffffffu, qr[0] >= 0 || qr[1] >= 0);
   const float qscale = 0.17677669529663687f * kLog2e;  // log2(e) / sqrt(32)
-  const int band_keys = (RPW + 6) * kHaloW;
-  const int nchunks = (band_keys + kChunk - 1) / kChunk;
   const int key0 = warp * RPW * kHaloW;  // first key of my band in the CTA halo
-  const int hy_band = hy0 + warp * RPW;
-  const int pow2 = (a.s & (a.s - 1)) == 0;
 
   float o[4][4];
 #pragma unroll
@@ -183,18 +178,8 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
     }
     __syncthreads();
     const uint32_t sK = sbase + buf * 2 * kbuf, sV = sK + kbuf;
-    const int tap_base = a.wt > 0 ? (j - sl + a.wt - 1) * 49 : 0;
+    const float* sb = sbias + (a.wt > 0 ? (j - sl + a.wt - 1) * 49 : 0);
     if (live) {
-      // band-relative (row, col) of my 8 key columns, advanced by 32 per chunk
-      int hr[4][2], hc[4][2];
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int off = nt * 8 + (lane & 3) * 2 + b;
-          hr[nt][b] = off / kHaloW;
-          hc[nt][b] = off % kHaloW;
-        }
       for (int c = 0; c < nchunks; ++c) {
         float sacc[4][4];
 #pragma unroll
@@ -206,31 +191,21 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
           mma16816(sacc[nt], qa[0], b0, b1);
           mma16816(sacc[nt], qa[1], b2, b3);
         }
+        // window / step mask and bias from the tile-shape tap table
         float cmax[2] = {-INFINITY, -INFINITY};
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
           for (int b = 0; b < 2; ++b) {
-            const int ky = hy_band + hr[nt][b], kx = hx0 + hc[nt][b];
-            const bool in_grid = hr[nt][b] < RPW + 6 && static_cast<unsigned>(ky) < static_cast<unsigned>(a.H) &&
-                                 static_cast<unsigned>(kx) < static_cast<unsigned>(a.W);
-            const int ks = pow2 ? ((ky + kx) & (a.s - 1)) : (ky + kx) % a.s;
+            const int bk = c * kChunk + nt * 8 + (lane & 3) * 2 + b;
+            const bool kin = skv[key0 + bk] != 0;
 #pragma unroll
             for (int ri = 0; ri < 2; ++ri) {
-              const int dy = hr[nt][b] - qhr[ri], dx = hc[nt][b] - qhc[ri];
-              bool ok = in_grid && static_cast<unsigned>(dy + 3) < 7u && static_cast<unsigned>(dx + 3) < 7u;
-              if (a.mask == 1) ok = ok && ks <= qs[ri];
-              if (a.mask == 2) ok = ok && ks < qs[ri];
+              const int tap = stt[bk * 16 + r0 + 8 * ri];
               const int e = ri * 2 + b;
-              const float v = ok ? sacc[nt][e] * qscale + sbias[tap_base + (dy + 3) * 7 + dx + 3] : -INFINITY;
+              const float v = (kin && tap >= 0) ? sacc[nt][e] * qscale + sb[tap] : -INFINITY;
               sacc[nt][e] = v;
               cmax[ri] = fmaxf(cmax[ri], v);
-            }
-            hc[nt][b] += kChunk - kHaloW;  // advance one chunk: +32 keys = +1 row, +10 cols
-            hr[nt][b] += 1;
-            if (hc[nt][b] >= kHaloW) {
-              hc[nt][b] -= kHaloW;
-              hr[nt][b] += 1;
             }
           }
         float alpha[2];
@@ -302,7 +277,8 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
 }
 
 int smem_bytes(int halo_keys, bool three_d) {
-  return (three_d ? 4 : 2) * halo_keys * kHD * 2 + 256 * 4;
+  // K/V buffers + bias (256 floats) + tap table (<= 224 x 16 B) + key flags
+  return (three_d ? 4 : 2) * halo_keys * kHD * 2 + 256 * 4 + 256 * 16 + halo_keys;
 }
 
 }  // namespace
@@ -327,12 +303,13 @@ int window_attention_tiles_smem(int halo_rows, bool three_d) {
 }
 
 void window_attention_tiles(const __half* q, int ldq, const int32_t* qinfo, const int32_t* tiles,
-                            int ntiles, int warps_per_tile, int halo_rows, const __half* kv,
-                            int ldkv, int kv_slot_stride, int H, int W, int heads, int wt, int mask,
-                            int s, const float* bias, __half* out, int ldo, cudaStream_t st) {
+                            int ntiles, int warps_per_tile, int halo_rows, const int8_t* taps,
+                            const __half* kv, int ldkv, int kv_slot_stride, int H, int W,
+                            int heads, int wt, int mask, int s, const float* bias, __half* out,
+                            int ldo, cudaStream_t st) {
   if (ntiles <= 0) return;
   AttnArgs a{q, ldq, qinfo, tiles, ntiles, kv, ldkv, kv_slot_stride, H, W, wt, mask, s,
-             heads * kHD, bias, out, ldo, window_attention_halo_keys(halo_rows)};
+             heads * kHD, bias, out, ldo, window_attention_halo_keys(halo_rows), taps};
   dim3 grid(ntiles, heads);
   launch_k(window_attn_mma_kernel, grid, dim3(warps_per_tile * 32), smem_bytes(a.halo_keys, wt > 0), st, a);
   PSWA_LAUNCH_CHECK();

@@ -55,10 +55,15 @@ constexpr int kAttnTileInts = 8 + 16 * 8;
 bool window_attention_tiles_supported(int hd, int win_h, int win_w);
 int window_attention_tiles_smem(int halo_rows, bool three_d);
 void window_attention_tiles_init(int max_smem_bytes);
+// taps: [band keys rounded to 32][16] int8 for this tile shape: window tap
+// (dy+3)*7+(dx+3) of (band key, query slot), or -1 when the window or the step
+// mask excludes it (position independent because tiles are aligned; grid
+// bounds are applied separately). Built by the engine.
 void window_attention_tiles(const __half* q, int ldq, const int32_t* qinfo, const int32_t* tiles,
-                            int ntiles, int warps_per_tile, int halo_rows, const __half* kv,
-                            int ldkv, int kv_slot_stride, int H, int W, int heads, int wt, int mask,
-                            int s, const float* bias, __half* out, int ldo, cudaStream_t st);
+                            int ntiles, int warps_per_tile, int halo_rows, const int8_t* taps,
+                            const __half* kv, int ldkv, int kv_slot_stride, int H, int W,
+                            int heads, int wt, int mask, int s, const float* bias, __half* out,
+                            int ldo, cudaStream_t st);
 
 // ---- convolutions for the hyperprior (conv.cu) ---------------------------
 // NHWC fp32 input [h][w][c] -> fp16 patches [oh*ow][kcols], K order

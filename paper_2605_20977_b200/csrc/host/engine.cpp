@@ -119,7 +119,9 @@ void Engine::alloc_all() {
     for (int j = 0; j < T; ++j)
       for (int p = 0; p < HW; ++p) qi[static_cast<size_t>(j) * HW + p] = (j << 24) | ((p / D.W) << 12) | (p % D.W);
     ctx_qinfo_ = up(qi);
-    mma_attn_ = pswa_dev::window_attention_tiles_supported(D.hd, D.c.win_h, D.c.win_w);
+    // tap tables and aligned tiles assume s = 4 (4x16 step blocks repeat the
+    // same query / step pattern); other schedules use the SIMT kernel
+    mma_attn_ = pswa_dev::window_attention_tiles_supported(D.hd, D.c.win_h, D.c.win_w) && D.c.s == 4;
     if (mma_attn_) {
       constexpr int TI = pswa_dev::kAttnTileInts;
       // context: CTA = 8 warps x (1 row x 16 cols) query strips of one slot
@@ -163,18 +165,59 @@ void Engine::alloc_all() {
             tt[4] = 0;
             tt[5] = kStepWarps;
             int total = 0;
-            for (int w = 0; w < kStepWarps; ++w) {
-              int n = 0;
-              for (int y = by + 4 * w; y < std::min(D.H, by + 4 * w + 4); ++y)
-                for (int x = bx; x < std::min(D.W, bx + 16); ++x)
-                  if (idx[y * D.W + x] >= 0) tt[8 + 16 * w + n++] = idx[y * D.W + x];
-              total += n;
-            }
+            for (int w = 0; w < kStepWarps; ++w)
+              for (int ry = 0; ry < 4; ++ry)
+                for (int jq = 0; jq < 4; ++jq) {  // canonical slot ry*4 + jq (tap table order)
+                  const int y = by + 4 * w + ry;
+                  const int x = bx + 4 * jq + ((t - ry) % 4 + 4) % 4;
+                  if (y < D.H && x < D.W && idx[y * D.W + x] >= 0) {
+                    tt[8 + 16 * w + ry * 4 + jq] = idx[y * D.W + x];
+                    ++total;
+                  }
+                }
             if (total == 0) continue;
             v.insert(v.end(), tt.begin(), tt.end());
           }
         n_step_tiles_[t] = static_cast<int>(v.size()) / TI;
         step_tiles_[t] = up(v);
+      }
+      // tap tables: [band key][16 query slots] int8, -1 = excluded by the
+      // window or the step mask (grid bounds are applied in the kernel)
+      {
+        auto table = [&](int band_rows, auto tap_of) {
+          const int keys = (band_rows * 22 + 31) / 32 * 32;
+          std::vector<int8_t> tb(static_cast<size_t>(keys) * 16, -1);
+          for (int bk = 0; bk < band_rows * 22; ++bk)
+            for (int qs = 0; qs < 16; ++qs) tb[static_cast<size_t>(bk) * 16 + qs] = tap_of(bk / 22, bk % 22, qs);
+          return tb;
+        };
+        std::vector<int8_t> all_t;
+        auto push = [&](const std::vector<int8_t>& tb) {
+          const size_t off = all_t.size();
+          all_t.insert(all_t.end(), tb.begin(), tb.end());
+          return off;
+        };
+        // context strip: query slot q at band row 3, column q + 3
+        const size_t off_ctx = push(table(7, [](int hr, int hc, int q) -> int8_t {
+          const int dy = hr - 3, dx = hc - 3 - q;
+          return (dx < -3 || dx > 3) ? -1 : static_cast<int8_t>((dy + 3) * 7 + dx + 3);
+        }));
+        size_t off_step[16][3];
+        for (int t = 0; t < 4; ++t)
+          for (int mk = 0; mk < 3; ++mk)
+            off_step[t][mk] = push(table(10, [=](int hr, int hc, int q) -> int8_t {
+              const int ry = q / 4, rx = 4 * (q % 4) + ((t - ry) % 4 + 4) % 4;
+              const int dy = hr - 3 - ry, dx = hc - 3 - rx;
+              if (dy < -3 || dy > 3 || dx < -3 || dx > 3) return -1;
+              const int ks = ((hr - 3 + hc - 3) % 4 + 4) % 4;
+              if ((mk == 1 && ks > t) || (mk == 2 && ks >= t)) return -1;
+              return static_cast<int8_t>((dy + 3) * 7 + dx + 3);
+            }));
+        int8_t* dt = dalloc<int8_t>(all_t.size());
+        PSWA_CUDA(cudaMemcpyAsync(dt, all_t.data(), all_t.size(), cudaMemcpyHostToDevice, st_));
+        taps_ctx_ = dt + off_ctx;
+        for (int t = 0; t < 4; ++t)
+          for (int mk = 0; mk < 3; ++mk) taps_step_[t][mk] = dt + off_step[t][mk];
       }
       pswa_dev::window_attention_tiles_init(
           std::max(pswa_dev::window_attention_tiles_smem(kCtxWarps + 6, true),
@@ -473,17 +516,17 @@ GemmEpi swiglu_out(void* out, int ld) {
 // Windowed attention: tensor-core warp tiles when the shape allows
 // (head_dim 32, 7x7), the SIMT kernel otherwise (desk preset, head_dim 4).
 void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq,
-                       const int32_t* tiles, int ntiles, const __half* kv, int slot_stride, int wt,
-                       int mask, const float* bias, __half* out) {
+                       const int32_t* tiles, int ntiles, const int8_t* taps, const __half* kv,
+                       int slot_stride, int wt, int mask, const float* bias, __half* out) {
   const Dims& D = D_;
   const int d = D.d;
   if (mma_attn_) {
     const int warps = wt > 0 ? kCtxWarps : kStepWarps;
     const int halo_rows = wt > 0 ? kCtxWarps + 6 : 4 * kStepWarps + 6;
     add(P, [=](cudaStream_t s) {
-      pswa_dev::window_attention_tiles(q, d, qinfo, tiles, ntiles, warps, halo_rows, kv, 2 * d,
-                                       slot_stride, D.H, D.W, D.heads, wt, mask, D.c.s, bias, out,
-                                       d, s);
+      pswa_dev::window_attention_tiles(q, d, qinfo, tiles, ntiles, warps, halo_rows, taps, kv,
+                                       2 * d, slot_stride, D.H, D.W, D.heads, wt, mask, D.c.s, bias,
+                                       out, d, s);
     });
   } else {
     add(P, [=](cudaStream_t s) {
@@ -507,8 +550,9 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
     e.row_map = rows;  // K/V of this step's positions into the frame cache
     gemm(P, bxn_, d, M, B.wkv, d, e);
   }
-  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], B.kv_cache, 0, 0, B.cross ? 0 : 1,
-            B.pos, batt_);
+  const int mk = B.cross ? 0 : 1;
+  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], taps_step_[t][mk], B.kv_cache, 0, 0,
+            mk, B.pos, batt_);
   gemm(P, batt_, d, M, B.wo, d, f32_acc(bx_, d));
   const float* g2 = B.g2;
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, g2, bxn_, d, s); });
@@ -531,7 +575,8 @@ void Engine::build_ctx(Program& P) {
     gemm(P, ctx_xn_, d, n, B.wkv, d, f16_out(ctx_kv_, 2 * d));
     gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, f16_out(ctx_q_, d));
     attention(P, ctx_q_, ctx_qinfo_ + q0, nq, last ? ctx_tiles_last_ : ctx_tiles_,
-              last ? n_ctx_tiles_last_ : n_ctx_tiles_, ctx_kv_, HW, D.c.win_t, 0, pos, ctx_att_);
+              last ? n_ctx_tiles_last_ : n_ctx_tiles_, taps_ctx_, ctx_kv_, HW, D.c.win_t, 0, pos,
+              ctx_att_);
     float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
     __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;
     gemm(P, ctx_att_, d, nq, B.wo, d, f32_acc(xq, d));
@@ -670,7 +715,8 @@ void Engine::build_step(Program& P, int t, int mode) {
   // accumulator: A = Hq + xattn(Q = Hq, KV = S1 of strictly earlier steps)
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(hq_, d, rows, M, d, d, acc_.g1, bxn_, d, s); });
   gemm(P, bxn_, d, M, acc_.wq, d, f16_out(bq_, d));
-  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], acc_kv_, 0, 0, 2, acc_.pos, batt_);
+  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], taps_step_[t][2], acc_kv_, 0, 0, 2,
+            acc_.pos, batt_);
   add(P, [=, this](cudaStream_t s) { pswa_dev::gather_rows_f32(hq_, d, rows, M, d, bx_, d, s); });
   gemm(P, batt_, d, M, acc_.wo, d, f32_acc(bx_, d));
   const bool taps = mode == 1 && want_musig_;  // debug taps in forward_params only
