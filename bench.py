@@ -37,7 +37,8 @@ sys.path.insert(0, ROOT)
 
 H, W = 68, 120          # 1080p / 16 (1920 x 1088 padded)
 GOP_INDEX = 4           # P-frame with 4 past frames
-LANES, HYPER_LANES = 4096, 1024
+LANES = int(os.environ.get("PSWA_BENCH_LANES", 8192))
+HYPER_LANES = 1024
 FLOP_PER_LATENT = 296.0e6   # 148.0 MMAC minimal work per position (paper)
 METRIC = "1080p P-frame entropy decode ms/frame and latents/s at 1/2/4/8 B200 vs CPU"
 

@@ -86,6 +86,10 @@ __device__ double d_erf(double x) {
   return x < 0.0 ? -y : y;
 }
 
+__device__ __forceinline__ double sym_bits(uint32_t freq) {
+  return 16.0 - log2(static_cast<double>(freq));
+}
+
 __global__ void build_cdf_kernel(float* scales, uint32_t* cdf) {
   pdl_wait();
   pdl_trigger();
@@ -113,6 +117,8 @@ __global__ void build_cdf_kernel(float* scales, uint32_t* cdf) {
   uint32_t* c = cdf + idx * (kSyms + 1);
   c[0] = 0;
   for (int k = 0; k < kSyms; ++k) c[k + 1] = c[k] + freq[k];
+  double* bt = reinterpret_cast<double*>(cdf + kScales * (kSyms + 1)) + idx * kSyms;
+  for (int k = 0; k < kSyms; ++k) bt[k] = sym_bits(freq[k]);
 }
 
 // ------------------------------------------------------------ helpers -----
@@ -167,14 +173,18 @@ __device__ __forceinline__ int dec_sym(const uint8_t* pl, LaneState& s, const ui
   return lo;
 }
 
-__device__ __forceinline__ double sym_bits(uint32_t freq) {
-  return 16.0 - log2(static_cast<double>(freq));
+// -log2(freq / 65536) of every (table, symbol), appended after the 64 CDF
+// tables (see build_cdf_tables): one load per decoded symbol instead of an
+// fp64 log2 on the lane's critical path.
+__device__ __forceinline__ const double* bits_table(const uint32_t* cdf) {
+  return reinterpret_cast<const double*>(cdf + kScales * (kSyms + 1));
 }
 
 // Decodes one value (escape + Exp-Golomb included); returns v.
-__device__ int32_t dec_value(const uint8_t* pl, LaneState& s, const uint32_t* cdf_row, int& err) {
+__device__ int32_t dec_value(const uint8_t* pl, LaneState& s, const uint32_t* cdf_row,
+                             const double* bits_row, int& err) {
   const int k = dec_sym(pl, s, cdf_row, kSyms, err);
-  s.bits += sym_bits(__ldg(cdf_row + k + 1) - __ldg(cdf_row + k));
+  s.bits += __ldg(bits_row + k);
   if (k < kEscLo) return k - 127;
   int nb = 0;
   while (dec_sym(pl, s, kBitCum, 2, err) == 0) {
@@ -265,7 +275,7 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
     const float mu = musig[static_cast<size_t>(k) * ldms + j];
     const float sg = musig[static_cast<size_t>(k) * ldms + sig_off + j];
     const int idx = scale_index(scales, sg);
-    const int32_t v = dec_value(pl, s, cdf + idx * (kSyms + 1), err);
+    const int32_t v = dec_value(pl, s, cdf + idx * (kSyms + 1), bits_table(cdf) + idx * kSyms, err);
     const int32_t y = v + __float2int_rn(mu);
     yhat[static_cast<size_t>(rows[k]) * C + c0 + j] = y;
     if (yhat16) yhat16[static_cast<size_t>(k) * ld16 + c0 + j] = __int2half_rn(y);
@@ -288,7 +298,7 @@ __global__ void decode_hyper_kernel(const uint8_t* __restrict__ pl, LaneState* _
   for (int i = l; i < n; i += L) {
     const int ch = i / per_ch;
     const int idx = scale_index(scales, scale[ch]);
-    const int32_t v = dec_value(pl, s, cdf + idx * (kSyms + 1), err);
+    const int32_t v = dec_value(pl, s, cdf + idx * (kSyms + 1), bits_table(cdf) + idx * kSyms, err);
     zhat[i] = v + __float2int_rn(loc[ch]);
   }
   lanes[l] = s;
@@ -381,7 +391,7 @@ __global__ void encode_lanes_kernel(const int32_t* __restrict__ sym_v, const uin
     const int k = v < -127 ? kEscLo : (v > 127 ? kEscHi : v + 127);
     const uint32_t c0 = __ldg(c + k), c1 = __ldg(c + k + 1);
     e.put(c0, c1 - c0);
-    b += sym_bits(c1 - c0);
+    b += __ldg(bits_table(cdf) + sym_idx[o] * kSyms + k);
     if (k >= kEscLo) {
       const uint64_t x = static_cast<uint64_t>(v < 0 ? -static_cast<int64_t>(v) : v) - 128 + 1;
       int nb = 0;

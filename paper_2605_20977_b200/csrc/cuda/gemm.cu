@@ -38,7 +38,9 @@ enum EpiKind : int { kEpiF16 = 0, kEpiF32 = 1, kEpiSwiGLU = 2, kEpiHead = 3 };
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int kStages = BN == 256 ? 3 : 4;
+  // as deep as shared memory allows (<= 227 KB with the epilogue staging):
+  // the small-M step GEMMs are latency bound, so all K blocks in flight helps
+  static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;

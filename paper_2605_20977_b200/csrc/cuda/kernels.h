@@ -83,7 +83,9 @@ void round_to_zhat(const float* x, int c, int hw, int32_t* z, cudaStream_t st);
 constexpr int kScales = 64;
 constexpr int kSyms = 257;  // v in [-127,127] + 2 escapes
 // Builds the 64 scale entries and 64 x 258 cumulative tables on the device
-// in fp64 with IEEE round-to-nearest ops only (bit-exact with the host rule).
+// in fp64 with IEEE round-to-nearest ops only (bit-exact with the host rule),
+// followed (at cdf + 64*258, 8-byte aligned) by 64 x 257 fp64 symbol costs.
+constexpr size_t kCdfWords = static_cast<size_t>(kScales) * (kSyms + 1) + 2 * kScales * kSyms;
 void build_cdf_tables(float* scales, uint32_t* cdf, cudaStream_t st);
 
 struct LaneState {

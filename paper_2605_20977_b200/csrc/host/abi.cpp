@@ -168,7 +168,7 @@ int pswa_gpu_op_build_cdf(uint32_t* cdf_out, float* scales_out) {
     float* ds = nullptr;
     uint32_t* dc = nullptr;
     PSWA_CUDA(cudaMalloc(&ds, sizeof(float) * pswa_dev::kScales));
-    PSWA_CUDA(cudaMalloc(&dc, sizeof(uint32_t) * pswa_dev::kScales * (pswa_dev::kSyms + 1)));
+    PSWA_CUDA(cudaMalloc(&dc, sizeof(uint32_t) * pswa_dev::kCdfWords));
     pswa_dev::build_cdf_tables(ds, dc, nullptr);
     PSWA_CUDA(cudaMemcpy(scales_out, ds, sizeof(float) * pswa_dev::kScales, cudaMemcpyDeviceToHost));
     PSWA_CUDA(cudaMemcpy(cdf_out, dc, sizeof(uint32_t) * pswa_dev::kScales * (pswa_dev::kSyms + 1),

@@ -229,7 +229,7 @@ void Engine::alloc_all() {
     crop_rows_ = up(crop);
   }
   scales_ = dalloc<float>(pswa_dev::kScales);
-  cdf_ = dalloc<uint32_t>(pswa_dev::kScales * (pswa_dev::kSyms + 1));
+  cdf_ = dalloc<uint32_t>(pswa_dev::kCdfWords);
 
   cur_rsi_ = dalloc<float>(d);
   cur_rsh_ = dalloc<float>(d);

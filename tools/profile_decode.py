@@ -12,7 +12,7 @@ from paper_2605_20977_b200.codec import GpuCodec, gen_weights, make_cfg, synth_l
 
 H, W = int(os.environ.get("PH", 68)), int(os.environ.get("PW", 120))
 N = int(os.environ.get("PN", 1))
-cfg = make_cfg(os.environ.get("PRESET", "paper"), H, W, lanes=4096, hyper_lanes=1024)
+cfg = make_cfg(os.environ.get("PRESET", "paper"), H, W, lanes=8192, hyper_lanes=1024)
 blob = gen_weights(cfg, 1)
 frames = [synth_latent(cfg, 0, f) for f in range(5)]
 enc = GpuCodec(cfg, blob)
