@@ -32,6 +32,8 @@ constexpr int kHD = 32;     // head dim handled by this kernel
 constexpr int kHaloW = 22;  // 16 query columns + 2*3 window margin
 constexpr int kChunk = 32;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kMaxBandKeys = 224;  // 10 x 22 band rounded to the 32-key chunk
+constexpr int kTblStride = 20;     // floats per band key: 16 queries + pad (conflict-free LDS)
 
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
@@ -110,15 +112,16 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
 
   const int band_keys = (RPW + 6) * kHaloW;
   const int nchunks = (band_keys + kChunk - 1) / kChunk;
-  int8_t* stt = reinterpret_cast<int8_t*>(sbias + 256);       // [nchunks*32][16]
-  uint8_t* skv = reinterpret_cast<uint8_t*>(stt + nchunks * kChunk * 16);  // [halo_keys]
+  const int nbk = nchunks * kChunk;
+  // per-slot score-offset table [band key][kTblStride]: log2e * bias of the
+  // (key, query) window tap, -inf where the window / step mask excludes it
+  float* stbl = sbias + 256;
+  uint8_t* skv = reinterpret_cast<uint8_t*>(stbl + kMaxBandKeys * kTblStride);  // [halo_keys]
 
-  // ---- stage the bias row of this head (pre-scaled by log2 e), the tap
-  // table of this tile shape and the per-key in-grid flags
+  // ---- stage the bias row of this head (pre-scaled by log2 e) and the
+  // per-key in-grid flags
   for (int i = threadIdx.x; i < taps_total; i += blockDim.x)
     sbias[i] = a.bias[h * taps_total + i] * kLog2e;
-  for (int i = threadIdx.x; i < nchunks * kChunk * 4; i += blockDim.x)
-    reinterpret_cast<uint32_t*>(stt)[i] = reinterpret_cast<const uint32_t*>(a.taps)[i];
   const int hkeys = HR * kHaloW;
   for (int key = threadIdx.x; key < a.halo_keys; key += blockDim.x) {
     const int ky = hy0 + key / kHaloW, kx = hx0 + key % kHaloW;
@@ -176,9 +179,17 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
     } else {
       cp_wait<0>();
     }
+    // score-offset table of this slot (the bias slice depends on the slot)
+    {
+      const float* sb = sbias + (a.wt > 0 ? (j - sl + a.wt - 1) * 49 : 0);
+      if (js > 0) __syncthreads();  // previous slot's readers are done
+      for (int i = threadIdx.x; i < nbk * 16; i += blockDim.x) {
+        const int tap = a.taps[i];
+        stbl[(i >> 4) * kTblStride + (i & 15)] = tap >= 0 ? sb[tap] : -INFINITY;
+      }
+    }
     __syncthreads();
     const uint32_t sK = sbase + buf * 2 * kbuf, sV = sK + kbuf;
-    const float* sb = sbias + (a.wt > 0 ? (j - sl + a.wt - 1) * 49 : 0);
     if (live) {
       for (int c = 0; c < nchunks; ++c) {
         float sacc[4][4];
@@ -199,11 +210,11 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
           for (int b = 0; b < 2; ++b) {
             const int bk = c * kChunk + nt * 8 + (lane & 3) * 2 + b;
             const bool kin = skv[key0 + bk] != 0;
+            const float* trow = stbl + bk * kTblStride + r0;
 #pragma unroll
             for (int ri = 0; ri < 2; ++ri) {
-              const int tap = stt[bk * 16 + r0 + 8 * ri];
               const int e = ri * 2 + b;
-              const float v = (kin && tap >= 0) ? sacc[nt][e] * qscale + sb[tap] : -INFINITY;
+              const float v = kin ? fmaf(sacc[nt][e], qscale, trow[8 * ri]) : -INFINITY;
               sacc[nt][e] = v;
               cmax[ri] = fmaxf(cmax[ri], v);
             }
@@ -277,8 +288,9 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
 }
 
 int smem_bytes(int halo_keys, bool three_d) {
-  // K/V buffers + bias (256 floats) + tap table (<= 224 x 16 B) + key flags
-  return (three_d ? 4 : 2) * halo_keys * kHD * 2 + 256 * 4 + 256 * 16 + halo_keys;
+  // K/V buffers + bias (256 floats) + score-offset table + key flags
+  return (three_d ? 4 : 2) * halo_keys * kHD * 2 + 256 * 4 + kMaxBandKeys * kTblStride * 4 +
+         halo_keys;
 }
 
 }  // namespace

@@ -19,17 +19,45 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const int* 
   if (row >= M) return;
   const float* xr = x + static_cast<size_t>(src ? src[row] : row) * ldx;
   __half* yr = y + static_cast<size_t>(row) * ldy;
+  const bool vec = (group & 127) == 0 && (ldx & 3) == 0 && (ldy & 3) == 0;
   for (int g0 = 0; g0 < d; g0 += group) {
-    float ss = 0.0f;
-    for (int i = lane; i < group; i += 32) {
-      const float v = xr[g0 + i];
-      ss += v * v;
-    }
+    if (vec) {
+      // group is a multiple of 128: each lane owns group/128 float4 quads,
+      // all loaded before the reduction (one round trip per row)
+      constexpr int kMaxQ = 8;  // group <= 1024
+      float4 v[kMaxQ];
+      const int nq = group >> 7;
+      float ss = 0.0f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    const float inv = 1.0f / sqrtf(ss / static_cast<float>(group) + 1e-5f);
-    for (int i = lane; i < group; i += 32)
-      yr[g0 + i] = __float2half_rn(gain[g0 + i] * xr[g0 + i] * inv);
+      for (int k = 0; k < kMaxQ; ++k)
+        if (k < nq) {
+          v[k] = *reinterpret_cast<const float4*>(xr + g0 + (k * 32 + lane) * 4);
+          ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const float inv = 1.0f / sqrtf(ss / static_cast<float>(group) + 1e-5f);
+#pragma unroll
+      for (int k = 0; k < kMaxQ; ++k)
+        if (k < nq) {
+          const int c = g0 + (k * 32 + lane) * 4;
+          const float4 gv = *reinterpret_cast<const float4*>(gain + c);
+          __half2 h[2] = {__floats2half2_rn(gv.x * v[k].x * inv, gv.y * v[k].y * inv),
+                          __floats2half2_rn(gv.z * v[k].z * inv, gv.w * v[k].w * inv)};
+          *reinterpret_cast<uint2*>(yr + c) = *reinterpret_cast<uint2*>(h);
+        }
+    } else {
+      float ss = 0.0f;
+      for (int i = lane; i < group; i += 32) {
+        const float v = xr[g0 + i];
+        ss += v * v;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const float inv = 1.0f / sqrtf(ss / static_cast<float>(group) + 1e-5f);
+      for (int i = lane; i < group; i += 32)
+        yr[g0 + i] = __float2half_rn(gain[g0 + i] * xr[g0 + i] * inv);
+    }
   }
 }
 

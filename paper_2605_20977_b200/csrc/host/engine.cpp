@@ -185,7 +185,7 @@ void Engine::alloc_all() {
       // window or the step mask (grid bounds are applied in the kernel)
       {
         auto table = [&](int band_rows, auto tap_of) {
-          const int keys = (band_rows * 22 + 31) / 32 * 32;
+          const int keys = (band_rows * 22 + 31) / 32 * 32;  // attention key chunk = 32
           std::vector<int8_t> tb(static_cast<size_t>(keys) * 16, -1);
           for (int bk = 0; bk < band_rows * 22; ++bk)
             for (int qs = 0; qs < 16; ++qs) tb[static_cast<size_t>(bk) * 16 + qs] = tap_of(bk / 22, bk % 22, qs);
