@@ -19,6 +19,7 @@
 // per-offset bias is added to the scaled score, softmax in fp32, a query
 // with no allowed key outputs zeros.
 #include <cfloat>
+#include <cstdlib>
 
 #include "check.h"
 #include "kernels.h"
@@ -93,6 +94,7 @@ struct AttnArgs {
   int ldo;
   int halo_keys;  // staged keys per slot buffer (>= halo rows * 22, multiple of 32, + slack)
   const int8_t* taps;  // [band keys (chunk-padded)][16 queries]: tap index or -1 (masked)
+  int dbuf;            // double-buffer the slot halos (3D); 0 = stage each slot in place
 };
 
 __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) {
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
   const int nslots = a.wt > 0 ? min(sl + 1, a.wt) : 1;
   const int j0 = sl - nslots + 1;
   const int kbuf = a.halo_keys * kHD * 2;  // bytes of one K (or V) buffer
-  float* sbias = reinterpret_cast<float*>(smem + (a.wt > 0 ? 4 : 2) * kbuf);  // 2 slot buffers in 3D
+  float* sbias = reinterpret_cast<float*>(smem + (a.wt > 0 && a.dbuf ? 4 : 2) * kbuf);
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
 
   const int band_keys = (RPW + 6) * kHaloW;
@@ -172,8 +174,9 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
   float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.0f, 0.0f};
 
   for (int js = 0; js < nslots; ++js) {
-    const int j = j0 + js, buf = js & 1;
-    if (js + 1 < nslots) {
+    const int j = j0 + js, buf = a.dbuf ? (js & 1) : 0;
+    if (!a.dbuf && js > 0) stage(j, 0);  // previous slot fully consumed (barrier below)
+    if (a.dbuf && js + 1 < nslots) {
       stage(j + 1, buf ^ 1);  // prefetch the next slot's halo
       cp_wait<1>();
     } else {
@@ -287,10 +290,18 @@ __global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) 
   }
 }
 
+// Double-buffering the 3D slot halos overlaps staging with compute but halves
+// the CTAs per SM; measured slower (3.68 vs 3.42 ms / frame), so off unless
+// PSWA_ATTN_DBUF=1.
+bool attn_dbuf() {
+  static const bool on = std::getenv("PSWA_ATTN_DBUF") != nullptr;
+  return on;
+}
+
 int smem_bytes(int halo_keys, bool three_d) {
   // K/V buffers + bias (256 floats) + score-offset table + key flags
-  return (three_d ? 4 : 2) * halo_keys * kHD * 2 + 256 * 4 + kMaxBandKeys * kTblStride * 4 +
-         halo_keys;
+  return (three_d && attn_dbuf() ? 4 : 2) * halo_keys * kHD * 2 + 256 * 4 +
+         kMaxBandKeys * kTblStride * 4 + halo_keys;
 }
 
 }  // namespace
@@ -321,7 +332,8 @@ void window_attention_tiles(const __half* q, int ldq, const int32_t* qinfo, cons
                             int ldo, cudaStream_t st) {
   if (ntiles <= 0) return;
   AttnArgs a{q, ldq, qinfo, tiles, ntiles, kv, ldkv, kv_slot_stride, H, W, wt, mask, s,
-             heads * kHD, bias, out, ldo, window_attention_halo_keys(halo_rows), taps};
+             heads * kHD, bias, out, ldo, window_attention_halo_keys(halo_rows), taps,
+             attn_dbuf() ? 1 : 0};
   dim3 grid(ntiles, heads);
   launch_k(window_attn_mma_kernel, grid, dim3(warps_per_tile * 32), smem_bytes(a.halo_keys, wt > 0), st, a);
   PSWA_LAUNCH_CHECK();
