@@ -7,9 +7,8 @@
 //   warp 1    : TMEM allocator + MMA issuer (one elected lane)
 //   warps 2-9 : epilogue. Two TMEM accumulators (2 x BN columns) let the
 //               epilogue of tile i overlap the MMAs of tile i+1. Each warp
-//               drains one 32-lane quarter x one column half, transposes its
-//               32 x 32 chunk through shared memory and writes whole row
-//               segments (coalesced 64/128 B per row).
+//               drains one 32-lane quarter x one column half; lane = output
+//               row, written with 16 B stores straight from registers.
 // The epilogue kind is a template parameter (no per-element mode branches).
 // K is walked in ascending 64-wide blocks and never split: every output
 // element has one fixed reduction order, so results are bitwise identical run
@@ -17,6 +16,7 @@
 // symmetry contract).
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "check.h"
@@ -32,7 +32,6 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 fp16 = 128 B = one SWIZZLE_128B row
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr int kStageBytesOut = 32 * 33 * 4;  // per-warp 32x32 fp32 transpose buffer (+pad)
 
 enum EpiKind : int { kEpiF16 = 0, kEpiF32 = 1, kEpiSwiGLU = 2, kEpiHead = 3 };
 
@@ -41,13 +40,14 @@ struct GemmCfg {
   // as deep as shared memory allows (<= 227 KB with the epilogue staging):
   // the small-M step GEMMs are latency bound, so all K blocks in flight helps
   static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static_assert(kStages * (kBM * kBK * 2 + BN * kBK * 2) + 1280 <= 227 * 1024, "smem");
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kSmem = kStages * kStageBytes + kEpiWarps * kStageBytesOut + 1024 + 256;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
 };
 
-__device__ __forceinline__ float silu_f(float v) { return v / (1.0f + __expf(-v)); }
+__device__ __forceinline__ float silu_f(float v) { return __fdividef(v, 1.0f + __expf(-v)); }
 __device__ __forceinline__ float softplus_f(float v) {
   if (v > 30.0f) return v;
   if (v < -30.0f) return __expf(v);
@@ -102,104 +102,72 @@ __device__ __forceinline__ void epi_values(const GemmEpi& ep, int n0, float (&v)
   }
 }
 
-// Residual rows of one 32x32 fp32 chunk in the coalesced store mapping,
-// loaded ahead of time (independent of the accumulator) so their latency
-// overlaps the MMA / TMEM wait instead of serialising the epilogue.
-__device__ __forceinline__ void prefetch_residual(const GemmEpi& ep, int M, int m0w, int oc0,
-                                                  int lane, float4 (&res)[8]) {
+// Residual segment (32 fp32 of output row `orow` at column oc0) loaded ahead
+// of the accumulator wait so its latency overlaps the MMAs.
+__device__ __forceinline__ void prefetch_residual(const GemmEpi& ep, int orow, int oc0,
+                                                  float4 (&res)[8]) {
 #pragma unroll
-  for (int pass = 0; pass < 8; ++pass) {
-    const int r = pass * 4 + (lane >> 3), c = (lane & 7) * 4;
-    const int m = m0w + r;
-    res[pass] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (m >= M || oc0 + c + 4 > ep.n_store) continue;
-    const int orow = ep.row_map ? ep.row_map[m] : m;
-    if (orow < 0) continue;
-    res[pass] = *reinterpret_cast<const float4*>(static_cast<const float*>(ep.out) +
-                                                 static_cast<size_t>(orow) * ep.ld_out + oc0 + c);
-  }
+  for (int q = 0; q < 8; ++q) res[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (orow < 0 || oc0 + 32 > ep.n_store) return;
+  const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(ep.out) +
+                                                      static_cast<size_t>(orow) * ep.ld_out + oc0);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) res[q] = src[q];
 }
 
-// Drain one 32 x 32 accumulator chunk (rows m0w..m0w+31 of this warp,
-// accumulator columns n0..n0+31): values -> smem transpose -> coalesced rows.
+// Drain one accumulator row segment: lane = TMEM lane = output row, columns
+// n0..n0+31; fused op, then straight 16 B stores from registers (each lane
+// writes whole 32 B sectors of its own row).
 template <int EPI>
-__device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int M, int m0w, int n0, int lane,
-                                          float* stage, const uint32_t (&raw)[32],
-                                          const float4 (&res)[8]) {
+__device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
+                                          const uint32_t (&raw)[32], const float4 (&res)[8]) {
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
   epi_values<EPI>(ep, n0, v);
-  // columns produced by this chunk and where they start in the output row
+  if (orow < 0) return;
   const int ncols = EPI == kEpiSwiGLU ? 16 : 32;
   const int oc0 = EPI == kEpiSwiGLU ? (n0 >> 1) : n0;
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = v[j];  // row = lane
-  __syncwarp();
   if (oc0 >= ep.n_store) return;
-  const int nvalid = min(ncols, ep.n_store - oc0);
-  if (EPI == kEpiF32) {
-    // 8 lanes per row (4 floats each), 4 rows per pass; the residual (when
-    // accumulating) was prefetched into `res` before the accumulator wait
+  const bool full = oc0 + ncols <= ep.n_store;
+  if (EPI == kEpiF32 || EPI == kEpiHead) {
+    float* dst = static_cast<float*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0;
+    if (EPI == kEpiF32 && full) {
+      float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
-    for (int pass = 0; pass < 8; ++pass) {
-      const int r = pass * 4 + (lane >> 3), c = (lane & 7) * 4;
-      const int m = m0w + r;
-      if (m >= M) continue;
-      const int orow = ep.row_map ? ep.row_map[m] : m;
-      if (orow < 0) continue;
-      float* dst = static_cast<float*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0 + c;
-      const float* s = stage + r * 33 + c;
-      if (c + 4 <= nvalid) {
-        float4 o = make_float4(s[0], s[1], s[2], s[3]);
+      for (int q = 0; q < 8; ++q) {
+        float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         if (ep.accumulate) {
-          o.x += res[pass].x;
-          o.y += res[pass].y;
-          o.z += res[pass].z;
-          o.w += res[pass].w;
+          o.x += res[q].x;
+          o.y += res[q].y;
+          o.z += res[q].z;
+          o.w += res[q].w;
         }
-        *reinterpret_cast<float4*>(dst) = o;
-      } else {
-        for (int k = 0; k < 4 && c + k < nvalid; ++k) dst[k] = ep.accumulate ? dst[k] + s[k] : s[k];
+        d4[q] = o;
       }
-    }
-  } else if (EPI == kEpiHead) {
-    for (int idx = lane; idx < 32 * nvalid; idx += 32) {
-      const int r = idx / nvalid, c = idx % nvalid;
-      const int m = m0w + r;
-      if (m >= M) continue;
-      const int orow = ep.row_map ? ep.row_map[m] : m;
-      if (orow < 0) continue;
-      static_cast<float*>(ep.out)[static_cast<size_t>(orow) * ep.ld_out + oc0 + c] = stage[r * 33 + c];
+    } else {
+      for (int j = 0; j < 32 && oc0 + j < ep.n_store; ++j)
+        dst[j] = (EPI == kEpiF32 && ep.accumulate) ? dst[j] + v[j] : v[j];
     }
   } else {
-    // fp16 rows: 32 cols = 64 B -> 4 lanes x 16 B per row, 8 rows per pass;
-    // SwiGLU rows: 16 cols = 32 B -> 2 lanes per row, 16 rows per pass
-    constexpr int kLanesPerRow = EPI == kEpiSwiGLU ? 2 : 4;
-    constexpr int kRowsPerPass = 32 / kLanesPerRow;
+    __half* dst = static_cast<__half*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0;
+    uint32_t hp[16];
 #pragma unroll
-    for (int pass = 0; pass < 32 / kRowsPerPass; ++pass) {
-      const int r = pass * kRowsPerPass + lane / kLanesPerRow, c = (lane % kLanesPerRow) * 8;
-      const int m = m0w + r;
-      if (m >= M) continue;
-      const int orow = ep.row_map ? ep.row_map[m] : m;
-      if (orow < 0) continue;
-      __half* dst = static_cast<__half*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0 + c;
-      const float* s = stage + r * 33 + c;
-      if (c + 8 <= nvalid) {
-        __half2 h[4];
+    for (int j = 0; j < ncols / 2; ++j) {
+      __half2 h2 = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
+      hp[j] = *reinterpret_cast<uint32_t*>(&h2);
+    }
+    if (full) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) h[k] = __floats2half2_rn(s[2 * k], s[2 * k + 1]);
-        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(h);
-      } else {
-        for (int k = 0; k < 8 && c + k < nvalid; ++k) dst[k] = __float2half_rn(s[k]);
-      }
+      for (int q = 0; q < ncols / 8; ++q) d4[q] = make_uint4(hp[4 * q], hp[4 * q + 1], hp[4 * q + 2], hp[4 * q + 3]);
+    } else {
+      for (int j = 0; j < ncols && oc0 + j < ep.n_store; ++j) dst[j] = __float2half_rn(v[j]);
     }
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                    int M, int K, int tiles_m, int num_tiles, const __grid_constant__ GemmEpi ep) {
@@ -210,8 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sa = smem;
   uint8_t* sb = smem + S * Cfg::kABytes;
-  float* sout = reinterpret_cast<float*>(smem + S * Cfg::kStageBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sout + kEpiWarps * kStageBytesOut / 4);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -220,13 +187,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int kblocks = K / kBK;
+  // tile schedule: CL CTAs of a cluster take adjacent M tiles of one N tile
+  const int rank = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int tiles_mp = (tiles_m + CL - 1) / CL;
+  const int n_units = tiles_mp * (num_tiles / tiles_m);
+  const int unit0 = blockIdx.x / CL, unit_step = gridDim.x / CL;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tma);
     tma_prefetch(&tmb);
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // released by the MMAs of every CTA reading it
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -236,7 +208,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
   tc_fence_before();
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync();  // peer barriers initialised before any multicast
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // everything above overlaps the previous kernel (PDL); inputs are read below
@@ -246,14 +221,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       int g = 0;  // global k-block counter across tiles
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m0 = (t % tiles_m) * kBM, n0 = (t / tiles_m) * BN;
+      for (int u = unit0; u < n_units; u += unit_step) {
+        const int m0 = ((u % tiles_mp) * CL + rank) * kBM, n0 = (u / tiles_mp) * BN;
         for (int kb = 0; kb < kblocks; ++kb, ++g) {
           const int s = g % S, round = g / S;
           if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
           mbar_expect_tx(&full[s], Cfg::kStageBytes);
           tma_load_2d(sa + s * Cfg::kABytes, &tma, &full[s], kb * kBK, m0);
-          tma_load_2d(sb + s * Cfg::kBBytes, &tmb, &full[s], kb * kBK, n0);
+          if (CL > 1)
+            tma_load_2d_mc(sb + s * Cfg::kBBytes + rank * (Cfg::kBBytes / CL), &tmb, &full[s],
+                           kb * kBK, n0 + rank * (BN / CL), static_cast<uint16_t>((1u << CL) - 1));
+          else
+            tma_load_2d(sb + s * Cfg::kBBytes, &tmb, &full[s], kb * kBK, n0);
         }
       }
     }
@@ -261,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_f16_f32(kBM, BN);
       int g = 0, it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      for (int u = unit0; u < n_units; u += unit_step, ++it) {
         const int buf = it & 1, use = it >> 1;
         if (use > 0) mbar_wait(&tempty[buf], (use - 1) & 1);  // epilogue drained it
         tc_fence_after();
@@ -276,7 +255,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < kBK / 16; ++kk)
             tc_mma_f16(acc, umma_desc_k_sw128(a_base + kk * 32), umma_desc_k_sw128(b_base + kk * 32),
                        idesc, (kb | kk) != 0 ? 1u : 0u);
-          tc_commit(&empty[s]);
+          if (CL > 1)
+            tc_commit_mc(&empty[s], static_cast<uint16_t>((1u << CL) - 1));
+          else
+            tc_commit(&empty[s]);
         }
         tc_commit(&tfull[buf]);
       }
@@ -285,15 +267,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 2;
     const int q = warp & 3;                // TMEM lane quarter this warp may access
     const int half = ew >> 2;              // column half of the tile
-    float* stage = sout + ew * (kStageBytesOut / 4);
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int u = unit0; u < n_units; u += unit_step, ++it) {
       const int buf = it & 1, use = it >> 1;
-      const int m0 = (t % tiles_m) * kBM, n0 = (t / tiles_m) * BN;
+      const int m0 = ((u % tiles_mp) * CL + rank) * kBM, n0 = (u / tiles_mp) * BN;
       const int c0 = half * (BN / 64), c1 = (half + 1) * (BN / 64);
+      const int m = m0 + q * 32 + lane;
+      const int orow = m < M ? (ep.row_map ? ep.row_map[m] : m) : -1;
       float4 res[8];
       const bool acc_res = EPI == kEpiF32 && ep.accumulate;
-      if (acc_res) prefetch_residual(ep, M, m0 + q * 32, n0 + c0 * 32, lane, res);
+      if (acc_res) prefetch_residual(ep, orow, n0 + c0 * 32, res);
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const uint32_t acc = tmem + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
@@ -302,16 +285,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t raw[32];
         tmem_ld_32x32(acc + c * 32, raw);
         tc_wait_ld();
-        epi_chunk<EPI>(ep, M, m0 + q * 32, n0 + c * 32, lane, stage, raw, res);
-        if (acc_res && c + 1 < c1) prefetch_residual(ep, M, m0 + q * 32, n0 + (c + 1) * 32, lane, res);
+        if (c + 1 == c1) {
+          // accumulator fully read: hand it back to the MMA warp early
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[buf]);
+        }
+        epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res);
+        if (acc_res && c + 1 < c1) prefetch_residual(ep, orow, n0 + (c + 1) * 32, res);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync();  // no multicast / remote arrive can still target this CTA
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_free(tmem, 2 * BN);
@@ -364,7 +353,9 @@ template <int BN, int EPI>
 void set_attr() {
   static std::once_flag once;
   std::call_once(once, [] {
-    PSWA_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>,
+    PSWA_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, 1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kSmem));
+    PSWA_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, 2>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kSmem));
   });
 }
@@ -385,29 +376,30 @@ void prep(int kind) {
   }
 }
 
-template <int BN>
-void launch(const GemmPlan& p, int kind, cudaStream_t st) {
+template <int BN, int EPI>
+void launch_epi(const GemmPlan& p, cudaStream_t st) {
   const int tiles_m = (p.M + kBM - 1) / kBM;
   const int tiles = tiles_m * (p.N / BN);
-  const int grid = tiles < sm_count() ? tiles : sm_count();
   const int smem = GemmCfg<BN>::kSmem;
+  if (p.cluster == 2) {
+    const int units = (tiles_m + 1) / 2 * (p.N / BN);
+    const int clusters = units < sm_count() / 2 ? units : sm_count() / 2;
+    launch_kc(gemm_tc_kernel<BN, EPI, 2>, dim3(2 * clusters), dim3(kThreads), smem, st, 2u, p.ta,
+              p.tb, p.M, p.K, tiles_m, tiles, p.epi);
+  } else {
+    const int grid = tiles < sm_count() ? tiles : sm_count();
+    launch_k(gemm_tc_kernel<BN, EPI, 1>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.M,
+             p.K, tiles_m, tiles, p.epi);
+  }
+}
+
+template <int BN>
+void launch(const GemmPlan& p, int kind, cudaStream_t st) {
   switch (kind) {
-    case kEpiF16:
-      launch_k(gemm_tc_kernel<BN, kEpiF16>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.M, p.K,
-               tiles_m, tiles, p.epi);
-      break;
-    case kEpiF32:
-      launch_k(gemm_tc_kernel<BN, kEpiF32>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.M, p.K,
-               tiles_m, tiles, p.epi);
-      break;
-    case kEpiSwiGLU:
-      launch_k(gemm_tc_kernel<BN, kEpiSwiGLU>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.M, p.K,
-               tiles_m, tiles, p.epi);
-      break;
-    default:
-      launch_k(gemm_tc_kernel<BN, kEpiHead>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.M, p.K,
-               tiles_m, tiles, p.epi);
-      break;
+    case kEpiF16: launch_epi<BN, kEpiF16>(p, st); break;
+    case kEpiF32: launch_epi<BN, kEpiF32>(p, st); break;
+    case kEpiSwiGLU: launch_epi<BN, kEpiSwiGLU>(p, st); break;
+    default: launch_epi<BN, kEpiHead>(p, st); break;
   }
 }
 
@@ -436,8 +428,13 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   p->K = K;
   p->BN = bn;
   p->epi = epi;
+  // CTA pairs sharing B through TMA multicast: correct and available, but
+  // measured neutral-to-slower on B200 (the L2 already dedups concurrent B
+  // reads; 10.56 vs 10.44 ms / frame), so opt-in via PSWA_GEMM_CLUSTER=1.
+  static const bool use_cluster = std::getenv("PSWA_GEMM_CLUSTER") != nullptr;
+  p->cluster = (use_cluster && M > kBM) ? 2 : 1;
   make_tmap(&p->ta, A, lda, M, K, kBM);
-  make_tmap(&p->tb, B, ldb, N, K, bn);
+  make_tmap(&p->tb, B, ldb, N, K, bn / p->cluster);
   const int kind = epi_kind(epi);
   if (bn == 64) prep<64>(kind);
   if (bn == 128) prep<128>(kind);

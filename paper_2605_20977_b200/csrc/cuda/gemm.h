@@ -37,6 +37,7 @@ struct GemmPlan {
   CUtensorMap ta;
   CUtensorMap tb;
   int M = 0, N = 0, K = 0, BN = 0;
+  int cluster = 1;  // 2: CTA pairs multicasting the shared B tile
   GemmEpi epi;
 };
 
