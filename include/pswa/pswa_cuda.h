@@ -121,6 +121,40 @@ int pswa_gpu_last_launch_count(pswa_gpu* h);
 /* Stream the handle runs on (cudaStream_t as void*). */
 void* pswa_gpu_stream(pswa_gpu* h);
 
+/* ---- row bands (BASELINE config 5) -----------------------
+ * One frame decoded as n row bands, one device handle per band (bands may
+ * share a device). Band b owns latent rows [row0, row1) (multiples of 4); its
+ * halo K/V rows are pushed by the neighbours after every layer (P2P stores
+ * over NVLink when they sit on different GPUs). Results are bitwise those of
+ * the single-handle decode. The main payload is the banded container
+ * "PSWB" | u32 n | u64 len[n] | band payloads, each band's symbols in the
+ * canonical order restricted to its rows (band-local coder lanes); the hyper
+ * payload is shared. Host frame buffers are full frames [C][H][W].
+ * Replaces decode_frame_wavefront / encode_frame for a
+ * frame too large for one device's wavefront, e.g. 4K (240x136 latents).  */
+int pswa_band_rows(int height, int n_bands, int band_idx, int* row0, int* row1);
+
+typedef struct pswa_group pswa_group;
+int pswa_group_create(const int* devices, int n_bands, const pswa_cfg* cfg, const void* psww_blob,
+                      size_t blob_len, pswa_group** out);
+void pswa_group_destroy(pswa_group* g);
+int pswa_group_reset_gop(pswa_group* g);
+int pswa_group_push_frame(pswa_group* g, const int32_t* yhat, int rate_idx);
+/* zhat: nullable (computed by the hyper encoder over the gathered S1). */
+int pswa_group_encode_frame(pswa_group* g, const int32_t* yhat, const int32_t* zhat, int rate_idx,
+                            int frame_idx_in_gop, uint8_t* hyper_out, size_t hyper_cap,
+                            size_t* hyper_len, uint8_t* main_out, size_t main_cap, size_t* main_len,
+                            double* bits_out /* [2], nullable */);
+int pswa_group_decode_frame(pswa_group* g, const uint8_t* hyper, size_t hyper_len,
+                            const uint8_t* main_payload, size_t main_len, int rate_idx,
+                            int frame_idx_in_gop, int advance_state, int32_t* yhat_out,
+                            double* bits_out /* [2], nullable */);
+int pswa_group_forward_params(pswa_group* g, const int32_t* yhat, const int32_t* zhat, int rate_idx,
+                              int frame_idx_in_gop, float* mu_out, float* sigma_out,
+                              double* bits_out /* [2], nullable */);
+int pswa_group_last_zhat(pswa_group* g, int32_t* zhat_out);
+int pswa_group_last_launch_count(pswa_group* g);
+
 /* ---- operator-level entry points (device pointers, on `stream`) -------- */
 /* C[M,N] = A[M,K] . B[N,K]^T, fp16 in, fp32 accumulate; out fp16 or fp32. */
 int pswa_gpu_op_gemm_f16(const void* A, int lda, int M, const void* B, int ldb, int N, int K,

@@ -58,6 +58,17 @@ _SIGS = {
     "pswa_gpu_op_window_attn": (_I, [_VP, _I, _VP, _I, _VP, _I, _I, _I, _I, _I, _I, _I, _I, _I,
                                      _I, _I, _VP, _VP, _I, _VP]),
     "pswa_gpu_op_build_cdf": (_I, [_VP, _VP]),
+    "pswa_band_rows": (_I, [_I, _I, _I, C.POINTER(_I), C.POINTER(_I)]),
+    "pswa_group_create": (_I, [_VP, _I, C.POINTER(PswaCfg), _VP, _SZ, C.POINTER(_VP)]),
+    "pswa_group_destroy": (None, [_VP]),
+    "pswa_group_reset_gop": (_I, [_VP]),
+    "pswa_group_push_frame": (_I, [_VP, _VP, _I]),
+    "pswa_group_encode_frame": (_I, [_VP, _VP, _VP, _I, _I, _VP, _SZ, C.POINTER(_SZ), _VP, _SZ,
+                                     C.POINTER(_SZ), _D]),
+    "pswa_group_decode_frame": (_I, [_VP, _VP, _SZ, _VP, _SZ, _I, _I, _I, _VP, _D]),
+    "pswa_group_forward_params": (_I, [_VP, _VP, _VP, _I, _I, _VP, _VP, _D]),
+    "pswa_group_last_zhat": (_I, [_VP, _VP]),
+    "pswa_group_last_launch_count": (_I, [_VP]),
 }
 
 

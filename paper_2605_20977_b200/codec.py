@@ -137,3 +137,87 @@ class GpuCodec:
 
     def stream(self) -> int:
         return lib().pswa_gpu_stream(self.h)
+
+
+def band_rows(height: int, n_bands: int, band: int) -> tuple[int, int]:
+    """Latent rows [r0, r1) of band `band` of `n_bands` (multiples of 4)."""
+    r0, r1 = C.c_int(), C.c_int()
+    check(lib().pswa_band_rows(height, n_bands, band, C.byref(r0), C.byref(r1)))
+    return r0.value, r1.value
+
+
+class BandGroupCodec:
+    """One frame as row bands: one device handle per band, the
+    halo K/V rows pushed between neighbours after every layer. Same frame API
+    as GpuCodec; the main payload is the banded container (band-local lanes).
+    `devices` lists the device of each band (bands may share a device)."""
+
+    def __init__(self, cfg: PswaCfg, weights: bytes, devices):
+        self.cfg = cfg
+        self.n = len(devices)
+        self._w = (C.c_uint8 * len(weights)).from_buffer_copy(weights)
+        devs = (C.c_int * self.n)(*devices)
+        h = C.c_void_p()
+        check(lib().pswa_group_create(devs, self.n, C.byref(cfg), self._w, len(weights),
+                                      C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().pswa_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    shape = GpuCodec.shape
+    zshape = GpuCodec.zshape
+
+    def reset_gop(self):
+        check(lib().pswa_group_reset_gop(self.h))
+
+    def push_frame(self, yhat: np.ndarray, rate: int = 0):
+        y = np.ascontiguousarray(yhat, np.int32)
+        check(lib().pswa_group_push_frame(self.h, _ptr(y), rate))
+
+    def encode_frame(self, yhat: np.ndarray, rate: int = 0, fidx: int = 0, zhat=None):
+        y = np.ascontiguousarray(yhat, np.int32)
+        z = None if zhat is None else np.ascontiguousarray(zhat, np.int32)
+        cap = 20 * y.size + (1 << 20)
+        hb = np.zeros(cap, np.uint8)
+        mb = np.zeros(cap, np.uint8)
+        hl, ml = C.c_size_t(), C.c_size_t()
+        bits = np.zeros(2, np.float64)
+        check(lib().pswa_group_encode_frame(self.h, _ptr(y), None if z is None else _ptr(z), rate,
+                                            fidx, _ptr(hb), cap, C.byref(hl), _ptr(mb), cap,
+                                            C.byref(ml), bits.ctypes.data_as(C.POINTER(C.c_double))))
+        return bytes(hb[:hl.value]), bytes(mb[:ml.value]), bits
+
+    def last_zhat(self) -> np.ndarray:
+        z = np.zeros(self.zshape, np.int32)
+        check(lib().pswa_group_last_zhat(self.h, _ptr(z)))
+        return z
+
+    def decode_frame(self, hyper: bytes, main: bytes, rate: int = 0, fidx: int = 0,
+                     advance: bool = True):
+        hb = np.frombuffer(hyper, np.uint8)
+        mb = np.frombuffer(main, np.uint8)
+        y = np.zeros(self.shape, np.int32)
+        bits = np.zeros(2, np.float64)
+        check(lib().pswa_group_decode_frame(self.h, _ptr(hb), len(hyper), _ptr(mb), len(main),
+                                            rate, fidx, int(advance), _ptr(y),
+                                            bits.ctypes.data_as(C.POINTER(C.c_double))))
+        return y, bits
+
+    def forward_params(self, yhat: np.ndarray, zhat: np.ndarray, rate: int = 0, fidx: int = 0):
+        y = np.ascontiguousarray(yhat, np.int32)
+        z = np.ascontiguousarray(zhat, np.int32)
+        mu = np.zeros(self.shape, np.float32)
+        sg = np.zeros(self.shape, np.float32)
+        bits = np.zeros(2, np.float64)
+        check(lib().pswa_group_forward_params(self.h, _ptr(y), _ptr(z), rate, fidx, _ptr(mu),
+                                              _ptr(sg), bits.ctypes.data_as(C.POINTER(C.c_double))))
+        return mu, sg, bits
+
+    def last_launch_count(self) -> int:
+        return lib().pswa_group_last_launch_count(self.h)

@@ -32,6 +32,12 @@ void scatter_rows_f32(const float* src, int lds, const int* rows, int M, int n, 
 void scatter_rows_f16(const __half* src, int lds, const int* rows, int M, int n, __half* dst,
                       int ldd, cudaStream_t st);
 
+// Band halo exchange: dst[pairs[i].y][0:ld] = src[pairs[i].x][0:ld]
+// (fp16 rows, ld a multiple of 8). dst may be a peer device's buffer: the
+// rows then travel as NVLink P2P stores straight into the neighbour's K/V
+// cache, no staging copy.
+void halo_push(const __half* src, __half* dst, int ld, const int2* pairs, int n, cudaStream_t st);
+
 // ---- windowed attention (attention.cu) -----------------------------------
 // Queries: rows of q (fp16, head h at columns h*hd), qinfo[i] = slot<<24 |
 // y<<12 | x. Keys/values: kv rows (slot*kv_slot_stride + y*W + x), K at

@@ -202,6 +202,24 @@ void fill_context_slots(const float* const* ring, const int* slot_src, const flo
   PSWA_LAUNCH_CHECK();
 }
 
+__global__ void halo_push_kernel(const __half* __restrict__ src, __half* __restrict__ dst, int ld,
+                                 const int2* __restrict__ pairs, int n) {
+  pdl_wait();
+  pdl_trigger();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const int2 p = pairs[warp];
+  const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<size_t>(p.x) * ld);
+  uint4* d = reinterpret_cast<uint4*>(dst + static_cast<size_t>(p.y) * ld);
+  for (int i = lane; i < ld / 8; i += 32) d[i] = s[i];
+}
+
+void halo_push(const __half* src, __half* dst, int ld, const int2* pairs, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  launch_k(halo_push_kernel, dim3((n + 7) / 8), dim3(256), 0, st, src, dst, ld, pairs, n);
+  PSWA_LAUNCH_CHECK();
+}
+
 void yhat_to_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st) {
   dim3 grid((C + 31) / 32, (HW + 31) / 32);
   launch_k(transpose_i32_kernel, dim3(grid), dim3(32, 8), 0, st, src, HW, C, dst);

@@ -8,11 +8,15 @@
 #include "../cuda/kernels.h"
 #include "abi_util.h"
 #include "engine.h"
+#include "group.h"
 #include "model_spec.h"
 #include "pswa/pswa_cuda.h"
 
 struct pswa_gpu {
   std::unique_ptr<pswa_host::Engine> eng;
+};
+struct pswa_group {
+  std::unique_ptr<pswa_host::BandGroup> grp;
 };
 
 using pswa_abi::guard;
@@ -141,6 +145,83 @@ int pswa_gpu_debug_fetch(pswa_gpu* h, const char* name, void* out, size_t cap, s
 int pswa_gpu_last_launch_count(pswa_gpu* h) { return h->eng->last_launches(); }
 
 void* pswa_gpu_stream(pswa_gpu* h) { return h->eng->stream(); }
+
+// ---- row bands --------------------------------------------------------------
+int pswa_band_rows(int height, int n_bands, int band_idx, int* row0, int* row1) {
+  return guard([&] { pswa_host::band_rows(height, n_bands, band_idx, row0, row1); });
+}
+
+int pswa_group_create(const int* devices, int n_bands, const pswa_cfg* cfg, const void* blob,
+                      size_t len, pswa_group** out) {
+  *out = nullptr;
+  return guard([&] {
+    if (n_bands < 1) throw std::invalid_argument("n_bands < 1");
+    auto g = std::make_unique<pswa_group>();
+    g->grp = std::make_unique<pswa_host::BandGroup>(std::vector<int>(devices, devices + n_bands),
+                                                    *cfg, blob, len);
+    *out = g.release();
+  });
+}
+
+void pswa_group_destroy(pswa_group* g) { delete g; }
+
+int pswa_group_reset_gop(pswa_group* g) {
+  return guard([&] { g->grp->reset_gop(); });
+}
+
+int pswa_group_push_frame(pswa_group* g, const int32_t* yhat, int rate_idx) {
+  return guard([&] { g->grp->push_frame(yhat, rate_idx); });
+}
+
+int pswa_group_encode_frame(pswa_group* g, const int32_t* yhat, const int32_t* zhat, int rate_idx,
+                            int frame_idx_in_gop, uint8_t* hyper_out, size_t hyper_cap,
+                            size_t* hyper_len, uint8_t* main_out, size_t main_cap, size_t* main_len,
+                            double* bits_out) {
+  return guard([&] {
+    const auto r = g->grp->encode(yhat, rate_idx, frame_idx_in_gop, zhat, nullptr, nullptr,
+                                  hyper_out, hyper_cap, main_out, main_cap, /*advance=*/true);
+    *hyper_len = r.hyper_len;
+    *main_len = r.main_len;
+    if (bits_out) {
+      bits_out[0] = r.bits[0];
+      bits_out[1] = r.bits[1];
+    }
+  });
+}
+
+int pswa_group_decode_frame(pswa_group* g, const uint8_t* hyper, size_t hyper_len,
+                            const uint8_t* main_payload, size_t main_len, int rate_idx,
+                            int frame_idx_in_gop, int advance_state, int32_t* yhat_out,
+                            double* bits_out) {
+  return guard([&] {
+    const auto r = g->grp->decode(hyper, hyper_len, main_payload, main_len, rate_idx,
+                                  frame_idx_in_gop, advance_state != 0, yhat_out);
+    if (bits_out) {
+      bits_out[0] = r.bits[0];
+      bits_out[1] = r.bits[1];
+    }
+  });
+}
+
+int pswa_group_forward_params(pswa_group* g, const int32_t* yhat, const int32_t* zhat, int rate_idx,
+                              int frame_idx_in_gop, float* mu_out, float* sigma_out,
+                              double* bits_out) {
+  return guard([&] {
+    if (!mu_out || !sigma_out || !zhat) throw std::invalid_argument("zhat / mu_out / sigma_out required");
+    const auto r = g->grp->encode(yhat, rate_idx, frame_idx_in_gop, zhat, mu_out, sigma_out, nullptr,
+                                  0, nullptr, 0, /*advance=*/false);
+    if (bits_out) {
+      bits_out[0] = r.bits[0];
+      bits_out[1] = r.bits[1];
+    }
+  });
+}
+
+int pswa_group_last_zhat(pswa_group* g, int32_t* zhat_out) {
+  return guard([&] { g->grp->band(0).last_zhat(zhat_out); });
+}
+
+int pswa_group_last_launch_count(pswa_group* g) { return g->grp->last_launches(); }
 
 // ---- operator-level -------------------------------------------------------
 int pswa_gpu_op_rmsnorm(const float* x, int ld_x, int M, int d, int group, const float* gain,

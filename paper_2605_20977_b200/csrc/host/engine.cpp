@@ -38,15 +38,24 @@ void put_linear(std::vector<__half>& dst, int ldk, const float* src, int in, int
 constexpr int kCtxWarps = 8;   // attention CTA shape for the 3D context window
 constexpr int kStepWarps = 4;  // ... and for the step-batched 2D windows
 
-std::vector<int> positions(int H, int W, int s, int t) {
+// Step-t positions of the own rows of a band, as local raster indices, in
+// raster order: the canonical symbol order restricted to the band.
+std::vector<int> positions(const Band& b, int W, int s, int t) {
   std::vector<int> v;
-  for (int y = 0; y < H; ++y)
+  for (int y = b.r0; y < b.r1; ++y)
     for (int x = 0; x < W; ++x)
-      if ((y + x) % s == t) v.push_back(y * W + x);
+      if ((y + x) % s == t) v.push_back((y - b.lo) * W + x);
   return v;
 }
 
 }  // namespace
+
+void band_rows(int H, int n, int b, int* r0, int* r1) {
+  const int q = (H + 3) / 4;  // 4-row units
+  if (n < 1 || b < 0 || b >= n || n > q) throw std::invalid_argument("band_rows: bad band split");
+  *r0 = 4 * static_cast<int>(static_cast<long>(b) * q / n);
+  *r1 = b == n - 1 ? H : 4 * static_cast<int>(static_cast<long>(b + 1) * q / n);
+}
 
 template <class T>
 T* Engine::dalloc(size_t n) {
@@ -58,11 +67,23 @@ T* Engine::dalloc(size_t n) {
   return static_cast<T*>(p);
 }
 
-Engine::Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len)
+Engine::Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len, int band_idx,
+               int n_bands)
     : D_((validate_cfg(cfg), cfg)), device_(device) {
   if (D_.c.ctx_blocks > 16 || D_.c.s1_blocks > 16 || D_.c.s2_blocks > 16 || D_.c.s > 16 ||
       D_.N > 8 || D_.c.ch_blocks > 4)
     throw std::invalid_argument("pswa_cfg: block / group counts exceed engine limits");
+  B_.idx = band_idx;
+  B_.n = n_bands;
+  band_rows(D_.H, n_bands, band_idx, &B_.r0, &B_.r1);
+  if (n_bands > 1 && (D_.c.s != 4 || D_.c.win_h != 7 || B_.r1 - B_.r0 < kHaloRows))
+    throw std::invalid_argument("band mode needs s = 4, a 7-row window and >= 3 rows per band");
+  B_.lo = n_bands > 1 ? std::max(0, B_.r0 - kHaloTop) : 0;
+  B_.Hl = (n_bands > 1 ? std::min(D_.H, B_.r1 + kHaloBottom) : D_.H) - B_.lo;
+  B_.own0 = B_.r0 - B_.lo;
+  B_.nown = B_.r1 - B_.r0;
+  HWl_ = B_.Hl * D_.W;
+  HWo_ = B_.nown * D_.W;
   PSWA_CUDA(cudaSetDevice(device));
   PSWA_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   const WeightMap w = parse_psww(cfg, blob, len);
@@ -75,7 +96,8 @@ Engine::Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len)
 
 Engine::~Engine() {
   for (auto& kv : progs_)
-    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (auto ex : kv.second.execs)
+      if (ex) cudaGraphExecDestroy(ex);
   if (st_) cudaStreamSynchronize(st_);
   for (void* p : allocs_) cudaFree(p);
   if (st_) cudaStreamDestroy(st_);
@@ -87,14 +109,15 @@ void Engine::build_tables() {
   step_rows_h_.clear();
   nmax_ = 0;
   for (int t = 0; t < D.c.s; ++t) {
-    step_rows_h_.push_back(positions(D.H, D.W, D.c.s, t));
+    step_rows_h_.push_back(positions(B_, D.W, D.c.s, t));
     nmax_ = std::max<int>(nmax_, static_cast<int>(step_rows_h_.back().size()));
   }
 }
 
 void Engine::alloc_all() {
   const Dims& D = D_;
-  const int d = D.d, HW = D.HW, T = D.T, C = D.C;
+  const int d = D.d, T = D.T, C = D.C;
+  const int HWl = HWl_, HWo = HWo_, own0 = B_.own0;
   const size_t HWp = static_cast<size_t>(D.Hp) * D.Wp;
   const int L = D.c.lanes, Lz = D.c.hyper_lanes;
   auto up = [&](const std::vector<int>& v) {
@@ -106,19 +129,24 @@ void Engine::alloc_all() {
     const auto& r = step_rows_h_[t];
     std::vector<int> qi(r.size()), rp(r.size());
     for (size_t k = 0; k < r.size(); ++k) {
-      const int y = r[k] / D.W, x = r[k] % D.W;
+      const int y = r[k] / D.W, x = r[k] % D.W;  // local row
       qi[k] = (y << 12) | x;
-      rp[k] = y * D.Wp + x;
+      rp[k] = (y + B_.lo) * D.Wp + x;  // padded global hyper grid
     }
     step_rows_[t] = up(r);
     step_qinfo_[t] = up(qi);
     step_rows_pad_[t] = up(rp);
   }
   {
-    std::vector<int> qi(static_cast<size_t>(T) * HW);
+    // context queries: own rows of every slot, [T][HWo]; local coordinates
+    std::vector<int> qi(static_cast<size_t>(T) * HWo), km(static_cast<size_t>(T) * HWo);
     for (int j = 0; j < T; ++j)
-      for (int p = 0; p < HW; ++p) qi[static_cast<size_t>(j) * HW + p] = (j << 24) | ((p / D.W) << 12) | (p % D.W);
+      for (int p = 0; p < HWo; ++p) {
+        qi[static_cast<size_t>(j) * HWo + p] = (j << 24) | ((own0 + p / D.W) << 12) | (p % D.W);
+        km[static_cast<size_t>(j) * HWo + p] = j * HWl + own0 * D.W + p;
+      }
     ctx_qinfo_ = up(qi);
+    if (B_.n > 1) ctx_kv_map_ = up(km);
     // tap tables and aligned tiles assume s = 4 (4x16 step blocks repeat the
     // same query / step pattern); other schedules use the SIMT kernel
     mma_attn_ = pswa_dev::window_attention_tiles_supported(D.hd, D.c.win_h, D.c.win_w) && D.c.s == 4;
@@ -127,8 +155,9 @@ void Engine::alloc_all() {
       // context: CTA = 8 warps x (1 row x 16 cols) query strips of one slot
       auto ctx_tiles = [&](int slot_from, int row_base) {
         std::vector<int> v;
+        const int yend = own0 + B_.nown;
         for (int j = slot_from; j < T; ++j)
-          for (int y0 = 0; y0 < D.H; y0 += kCtxWarps)
+          for (int y0 = own0; y0 < yend; y0 += kCtxWarps)
             for (int x0 = 0; x0 < D.W; x0 += 16) {
               std::vector<int> t(TI, -1);
               t[0] = y0 - 3;
@@ -136,15 +165,15 @@ void Engine::alloc_all() {
               t[2] = kCtxWarps + 6;
               t[3] = 1;
               t[4] = j;
-              t[5] = std::min(kCtxWarps, D.H - y0);
+              t[5] = std::min(kCtxWarps, yend - y0);
               for (int w = 0; w < t[5]; ++w)
                 for (int x = x0, i = 0; x < std::min(D.W, x0 + 16); ++x, ++i)
-                  t[8 + 16 * w + i] = j * HW + (y0 + w) * D.W + x - row_base;
+                  t[8 + 16 * w + i] = j * HWo + (y0 - own0 + w) * D.W + x - row_base;
               v.insert(v.end(), t.begin(), t.end());
             }
         return v;
       };
-      const auto all = ctx_tiles(0, 0), last = ctx_tiles(T - 1, (T - 1) * HW);
+      const auto all = ctx_tiles(0, 0), last = ctx_tiles(T - 1, (T - 1) * HWo);
       n_ctx_tiles_ = static_cast<int>(all.size()) / TI;
       n_ctx_tiles_last_ = static_cast<int>(last.size()) / TI;
       ctx_tiles_ = up(all);
@@ -152,10 +181,11 @@ void Engine::alloc_all() {
       // step batches: CTA = 4 warps stacked vertically, warp = the step-t
       // positions of a 4x16 block (16 when the block is inside the grid)
       for (int t = 0; t < D.c.s; ++t) {
-        std::vector<int> idx(static_cast<size_t>(HW), -1);
+        std::vector<int> idx(static_cast<size_t>(HWl), -1);
         for (size_t k = 0; k < step_rows_h_[t].size(); ++k) idx[step_rows_h_[t][k]] = static_cast<int>(k);
         std::vector<int> v;
-        for (int by = 0; by < D.H; by += 4 * kStepWarps)
+        // warp blocks stay anchored to global rows = 0 mod 4 (lo = 0 mod 4)
+        for (int by = own0; by < own0 + B_.nown; by += 4 * kStepWarps)
           for (int bx = 0; bx < D.W; bx += 16) {
             std::vector<int> tt(TI, -1);
             tt[0] = by - 3;
@@ -170,7 +200,7 @@ void Engine::alloc_all() {
                 for (int jq = 0; jq < 4; ++jq) {  // canonical slot ry*4 + jq (tap table order)
                   const int y = by + 4 * w + ry;
                   const int x = bx + 4 * jq + ((t - ry) % 4 + 4) % 4;
-                  if (y < D.H && x < D.W && idx[y * D.W + x] >= 0) {
+                  if (y < B_.Hl && x < D.W && idx[y * D.W + x] >= 0) {
                     tt[8 + 16 * w + ry * 4 + jq] = idx[y * D.W + x];
                     ++total;
                   }
@@ -225,7 +255,9 @@ void Engine::alloc_all() {
     }
     std::vector<int> crop(HWp);
     for (int y = 0; y < D.Hp; ++y)
-      for (int x = 0; x < D.Wp; ++x) crop[static_cast<size_t>(y) * D.Wp + x] = (y < D.H && x < D.W) ? y * D.W + x : -1;
+      for (int x = 0; x < D.Wp; ++x)  // padded global hyper grid -> own local rows
+        crop[static_cast<size_t>(y) * D.Wp + x] =
+            (y >= B_.r0 && y < B_.r1 && x < D.W) ? (y - B_.lo) * D.W + x : -1;
     crop_rows_ = up(crop);
   }
   scales_ = dalloc<float>(pswa_dev::kScales);
@@ -238,24 +270,25 @@ void Engine::alloc_all() {
   cur_scale_ = dalloc<float>(D.hc);
   slot_src_ = dalloc<int>(T);
   ring_.clear();
-  for (int j = 0; j < T; ++j) ring_.push_back(dalloc<float>(static_cast<size_t>(HW) * d));
+  for (int j = 0; j < T; ++j) ring_.push_back(dalloc<float>(static_cast<size_t>(HWo) * d));
   ring_ptrs_ = dalloc<float*>(T);
   PSWA_CUDA(cudaMemcpyAsync(ring_ptrs_, ring_.data(), sizeof(float*) * T, cudaMemcpyHostToDevice, st_));
 
-  yfr_ = dalloc<int32_t>(static_cast<size_t>(HW) * C);
-  ychw_ = dalloc<int32_t>(static_cast<size_t>(HW) * C);
+  yfr_ = dalloc<int32_t>(static_cast<size_t>(HWl) * C);
+  ychw_ = dalloc<int32_t>(static_cast<size_t>(HWo) * C);
   zhat_ = dalloc<int32_t>(static_cast<size_t>(D.hc) * D.zh * D.zw);
-  emb_cur_ = dalloc<float>(static_cast<size_t>(HW) * d);
-  hq_ = dalloc<float>(static_cast<size_t>(HW) * d);
-  const size_t TH = static_cast<size_t>(T) * HW;
+  emb_cur_ = dalloc<float>(static_cast<size_t>(HWl) * d);
+  hq_ = dalloc<float>(static_cast<size_t>(HWl) * d);
+  const size_t TH = static_cast<size_t>(T) * HWo, THl = static_cast<size_t>(T) * HWl;
   ctx_x_ = dalloc<float>(TH * d);
   ctx_xn_ = dalloc<__half>(TH * d);
-  ctx_kv_ = dalloc<__half>(TH * 2 * d);
+  ctx_kv_ = dalloc<__half>(THl * 2 * d);
+  if (B_.n > 1) ctx_kv2_ = dalloc<__half>(THl * 2 * d);
   ctx_q_ = dalloc<__half>(TH * d);
   ctx_att_ = dalloc<__half>(TH * d);
   ctx_h_ = dalloc<__half>(TH * D.fp);
-  ctx16_ = dalloc<__half>(static_cast<size_t>(HW) * d);
-  acc_kv_ = dalloc<__half>(static_cast<size_t>(HW) * 2 * d);
+  ctx16_ = dalloc<__half>(static_cast<size_t>(HWl) * d);
+  acc_kv_ = dalloc<__half>(static_cast<size_t>(HWl) * 2 * d);
 
   hx_ = dalloc<float>(HWp * D.hc);
   hu_ = dalloc<float>(HWp * D.hc);
@@ -282,7 +315,7 @@ void Engine::alloc_all() {
   const int ms = (2 * D.Cg + 63) / 64 * 64;
   musig_ = dalloc<float>(nb * ms);
 
-  const size_t nsym = static_cast<size_t>(HW) * C, nz = static_cast<size_t>(D.hc) * D.zh * D.zw;
+  const size_t nsym = static_cast<size_t>(HWo) * C, nz = static_cast<size_t>(D.hc) * D.zh * D.zw;
   main_cap_ = 8 + 4ull * L + 6 * static_cast<size_t>(L) + 16 * nsym;
   hyper_cap_ = 8 + 4ull * Lz + 6 * static_cast<size_t>(Lz) + 16 * nz;
   d_main_ = dalloc<uint8_t>(main_cap_);
@@ -306,10 +339,10 @@ void Engine::alloc_all() {
   enc_hbits_ = dalloc<double>(Lz);
   pack_total_ = dalloc<unsigned long long>(2);
   pack_offs_ = dalloc<uint64_t>(std::max(L, Lz));
-  mu_full_ = dalloc<float>(nsym);
-  sg_full_ = dalloc<float>(nsym);
-  afull_ = dalloc<float>(static_cast<size_t>(HW) * d);
-  s2full_ = dalloc<__half>(static_cast<size_t>(HW) * d);
+  mu_full_ = dalloc<float>(static_cast<size_t>(HWl) * C);
+  sg_full_ = dalloc<float>(static_cast<size_t>(HWl) * C);
+  afull_ = dalloc<float>(static_cast<size_t>(HWl) * d);
+  s2full_ = dalloc<__half>(static_cast<size_t>(HWl) * d);
 }
 
 // ------------------------------------------------------------ weights ----
@@ -364,7 +397,7 @@ void Engine::upload_weights(const WeightMap& w) {
       B.g1 = upload_f(fv(p + ".norm1.g"), d);
       B.g2 = upload_f(fv(p + ".norm2.g"), d);
       B.pos = upload_f(fv(p + ".pos"), fsize(p + ".pos"));
-      if (spatial) B.kv_cache = dalloc<__half>(static_cast<size_t>(D.HW) * 2 * d);
+      if (spatial) B.kv_cache = dalloc<__half>(static_cast<size_t>(HWl_) * 2 * d);
     }
   };
   stack("ctx", D.c.ctx_blocks, ctx_, false);
@@ -519,18 +552,18 @@ void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq
                        const int32_t* tiles, int ntiles, const int8_t* taps, const __half* kv,
                        int slot_stride, int wt, int mask, const float* bias, __half* out) {
   const Dims& D = D_;
-  const int d = D.d;
+  const int d = D.d, Hl = B_.Hl;  // key grid bounds: the band's local grid
   if (mma_attn_) {
     const int warps = wt > 0 ? kCtxWarps : kStepWarps;
     const int halo_rows = wt > 0 ? kCtxWarps + 6 : 4 * kStepWarps + 6;
     add(P, [=](cudaStream_t s) {
       pswa_dev::window_attention_tiles(q, d, qinfo, tiles, ntiles, warps, halo_rows, taps, kv,
-                                       2 * d, slot_stride, D.H, D.W, D.heads, wt, mask, D.c.s, bias,
+                                       2 * d, slot_stride, Hl, D.W, D.heads, wt, mask, D.c.s, bias,
                                        out, d, s);
     });
   } else {
     add(P, [=](cudaStream_t s) {
-      pswa_dev::window_attention(q, d, qinfo, Mq, kv, 2 * d, slot_stride, D.H, D.W, D.heads, D.hd,
+      pswa_dev::window_attention(q, d, qinfo, Mq, kv, 2 * d, slot_stride, Hl, D.W, D.heads, D.hd,
                                  D.c.win_h, D.c.win_w, wt, mask, D.c.s, bias, out, d, s);
     });
   }
@@ -549,6 +582,7 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
     GemmEpi e = f16_out(B.kv_cache, 2 * d);
     e.row_map = rows;  // K/V of this step's positions into the frame cache
     gemm(P, bxn_, d, M, B.wkv, d, e);
+    exchange(P, xid_of(B), t);  // band mode: step-t K/V of the boundary rows
   }
   const int mk = B.cross ? 0 : 1;
   attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], taps_step_[t][mk], B.kv_cache, 0, 0,
@@ -562,20 +596,27 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
 
 void Engine::build_ctx(Program& P) {
   const Dims& D = D_;
-  const int d = D.d, HW = D.HW, T = D.T, n = T * HW;
+  const int d = D.d, HWo = HWo_, T = D.T, n = T * HWo;
   add(P, [=, this](cudaStream_t s) {
-    pswa_dev::fill_context_slots(ring_ptrs_, slot_src_, pad_, T, HW, d, ctx_x_, s);
+    pswa_dev::fill_context_slots(ring_ptrs_, slot_src_, pad_, T, HWo, d, ctx_x_, s);
   });
   for (int b = 0; b < D.c.ctx_blocks; ++b) {
     const Block& B = ctx_[b];
     const bool last = b == D.c.ctx_blocks - 1;
-    const int q0 = last ? (T - 1) * HW : 0, nq = n - q0;
+    const int q0 = last ? (T - 1) * HWo : 0, nq = n - q0;
     const float *g1 = B.g1, *g2 = B.g2, *pos = B.pos;
+    // band mode: K/V of the own rows into the local [T][HWl] grid, the halo
+    // rows pushed by the neighbours; buffers alternate by layer so a
+    // neighbour's push of layer b+1 never lands in the buffer read by layer b
+    __half* kv = (B_.n > 1 && b % 2) ? ctx_kv2_ : ctx_kv_;
     add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(ctx_x_, d, nullptr, n, d, d, g1, ctx_xn_, d, s); });
-    gemm(P, ctx_xn_, d, n, B.wkv, d, f16_out(ctx_kv_, 2 * d));
+    GemmEpi ekv = f16_out(kv, 2 * d);
+    ekv.row_map = ctx_kv_map_;
+    gemm(P, ctx_xn_, d, n, B.wkv, d, ekv);
+    exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
     gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, f16_out(ctx_q_, d));
     attention(P, ctx_q_, ctx_qinfo_ + q0, nq, last ? ctx_tiles_last_ : ctx_tiles_,
-              last ? n_ctx_tiles_last_ : n_ctx_tiles_, taps_ctx_, ctx_kv_, HW, D.c.win_t, 0, pos,
+              last ? n_ctx_tiles_last_ : n_ctx_tiles_, taps_ctx_, kv, HWl_, D.c.win_t, 0, pos,
               ctx_att_);
     float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
     __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;
@@ -584,13 +625,16 @@ void Engine::build_ctx(Program& P) {
     gemm(P, xnq, d, nq, B.wgu, d, swiglu_out(ctx_h_, D.fp));
     gemm(P, ctx_h_, D.fp, nq, B.wd, D.fp, f32_acc(xq, d));
   }
-  const float* last = ctx_x_ + static_cast<size_t>(T - 1) * HW * d;
-  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(last, d, nullptr, HW, d, d, ctx_gout_, ctx16_, d, s); });
-  // cross-attention K/V of every cross block, once per frame (K7)
+  const float* last = ctx_x_ + static_cast<size_t>(T - 1) * HWo * d;
+  __half* c16 = ctx16_ + static_cast<size_t>(B_.own0) * D.W * d;
+  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(last, d, nullptr, HWo, d, d, ctx_gout_, c16, d, s); });
+  exchange(P, kXidCtx16, kXAll);  // band mode: normed context of the boundary rows
+  // cross-attention K/V of every cross block, once per frame (K7), over the
+  // whole local grid (own rows + the halo received above)
   for (Block* stackp : {s1_, s2_}) {
     const int nb = stackp == s1_ ? D.c.s1_blocks : D.c.s2_blocks;
     for (int b = 0; b < nb; ++b)
-      if (stackp[b].cross) gemm(P, ctx16_, d, HW, stackp[b].wkv, d, f16_out(stackp[b].kv_cache, 2 * d));
+      if (stackp[b].cross) gemm(P, ctx16_, d, HWl_, stackp[b].wkv, d, f16_out(stackp[b].kv_cache, 2 * d));
   }
 }
 
@@ -701,10 +745,12 @@ void Engine::build_s1(Program& P, int t, bool encoder) {
   GemmEpi e = f16_out(acc_kv_, 2 * d);
   e.row_map = rows;
   gemm(P, bs1n_, d, M, acc_.wkv, d, e);
-  if (encoder) {
+  if (encoder) {  // full-frame S1 for the hyper encoder (band mode: band 0 gathers it)
     const int* rp = step_rows_pad_[t];
-    add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f16(bs1n_, d, rp, M, d, s1full_, d, s); });
+    __half* dst = band0_ ? band0_->s1full_ : s1full_;
+    add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f16(bs1n_, d, rp, M, d, dst, d, s); });
   }
+  exchange(P, kXidAcc, t);
 }
 
 void Engine::build_step(Program& P, int t, int mode) {
@@ -793,8 +839,9 @@ Program& Engine::program(const std::string& key) {
   if (it != progs_.end()) return it->second;
   Program& P = progs_[key];
   const Dims& D = D_;
-  const int HW = D.HW, C = D.C, L = D.c.lanes, Lz = D.c.hyper_lanes;
+  const int HW = HWo_, C = D.C, L = D.c.lanes, Lz = D.c.hyper_lanes;  // HW: own positions
   const int nz = D.hc * D.zh * D.zw;
+  const size_t yoff = static_cast<size_t>(B_.own0) * D.W * C;  // own rows in yfr_
   const std::string base = key.substr(0, key.find('+'));  // "+ms": mu/sigma outputs
   if (base == "decode") {
     add(P, [=, this](cudaStream_t s) {
@@ -815,10 +862,10 @@ Program& Engine::program(const std::string& key) {
       build_step(P, t, 0);
     }
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_lane_bits(lanes_, L, bits_ + 1, s); });
-    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_to_chw(yfr_, HW, C, ychw_, s); });
+    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_to_chw(yfr_ + yoff, HW, C, ychw_, s); });
   } else if (base == "encode" || base == "encode_z") {
     const bool zgiven = base == "encode_z";
-    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_from_chw(ychw_, HW, C, yfr_, s); });
+    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_from_chw(ychw_, HW, C, yfr_ + yoff, s); });
     build_ctx(P);
     for (int t = 0; t < D.c.s; ++t) {
       const int M = static_cast<int>(step_rows_h_[t].size());
@@ -827,7 +874,22 @@ Program& Engine::program(const std::string& key) {
       build_embed(P, t);
       build_s1(P, t, true);
     }
-    if (!zgiven) build_hyper_encode(P);
+    if (!zgiven) {
+      if (B_.n > 1) {
+        // every band has scattered its S1 rows into band 0's full-frame
+        // buffer; each band then runs the (small) hyper encoder on a local
+        // copy, so z_hat is bitwise identical on every band
+        cut(P, true);
+        if (band0_ && band0_ != this) {
+          const __half* src = band0_->s1full_;
+          const size_t bytes = static_cast<size_t>(D.Hp) * D.Wp * D.d * sizeof(__half);
+          add(P, [=, this](cudaStream_t s) {
+            PSWA_CUDA(cudaMemcpyAsync(s1full_, src, bytes, cudaMemcpyDefault, s));
+          }, 0);
+        }
+      }
+      build_hyper_encode(P);
+    }
     add(P, [=, this](cudaStream_t s) {
       pswa_dev::quantize_hyper(zhat_, nz, D.zh * D.zw, cur_loc_, cur_scale_, scales_, hsym_v_,
                                hsym_idx_, s);
@@ -853,7 +915,7 @@ Program& Engine::program(const std::string& key) {
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_doubles(enc_hbits_, Lz, bits_, s); });
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_doubles(enc_bits_, L, bits_ + 1, s); });
   } else if (base == "push") {
-    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_from_chw(ychw_, HW, C, yfr_, s); });
+    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_from_chw(ychw_, HW, C, yfr_ + yoff, s); });
     for (int t = 0; t < D.c.s; ++t) {
       const int M = static_cast<int>(step_rows_h_[t].size());
       const int* rows = step_rows_[t];
@@ -866,28 +928,114 @@ Program& Engine::program(const std::string& key) {
   return P;
 }
 
-void Engine::run(Program& P) {
+// One graph per segment (a single segment unless band mode). The graphs are
+// captured lazily on first use.
+void Engine::launch_segment(Program& P, int k) {
   static const bool no_graph = std::getenv("PSWA_NO_GRAPH") != nullptr;
-  last_launches_ = P.launches;
+  const size_t b = k == 0 ? 0 : P.cuts[k - 1].at;
+  const size_t e = k + 1 < segments(P) ? P.cuts[k].at : P.ops.size();
   if (no_graph) {
-    for (auto& op : P.ops) op(st_);
+    for (size_t i = b; i < e; ++i) P.ops[i](st_);
     return;
   }
-  if (!P.exec) {
+  if (P.execs.empty()) P.execs.assign(segments(P), nullptr);
+  if (!P.execs[k]) {
     cudaGraph_t g = nullptr;
     PSWA_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
     try {
-      for (auto& op : P.ops) op(st_);
+      for (size_t i = b; i < e; ++i) P.ops[i](st_);
     } catch (...) {
       cudaStreamEndCapture(st_, &g);
       if (g) cudaGraphDestroy(g);
       throw;
     }
     PSWA_CUDA(cudaStreamEndCapture(st_, &g));
-    PSWA_CUDA(cudaGraphInstantiate(&P.exec, g, 0));
+    PSWA_CUDA(cudaGraphInstantiate(&P.execs[k], g, 0));
     PSWA_CUDA(cudaGraphDestroy(g));
   }
-  PSWA_CUDA(cudaGraphLaunch(P.exec, st_));
+  PSWA_CUDA(cudaGraphLaunch(P.execs[k], st_));
+}
+
+void Engine::run(Program& P) {
+  if (B_.n > 1) throw std::logic_error("band engines are run by their BandGroup");
+  last_launches_ = P.launches;
+  launch_segment(P, 0);
+}
+
+// ------------------------------------------------------------ band mode ---
+void Engine::cut(Program& P, bool global) {
+  if (B_.n > 1) P.cuts.push_back(Cut{P.ops.size(), global});
+}
+
+__half* Engine::xbuf(int id) {
+  if (id < 16) return s1_[id].kv_cache;
+  if (id < 32) return s2_[id - 16].kv_cache;
+  if (id == kXidAcc) return acc_kv_;
+  if (id == kXidCtx0) return ctx_kv_;
+  if (id == kXidCtx1) return ctx_kv2_;
+  return ctx16_;
+}
+
+int Engine::xld(int id) const { return id == kXidCtx16 ? D_.d : 2 * D_.d; }
+
+// Row pairs (my local row, the neighbour's local row) of the kHaloRows
+// boundary rows each neighbour needs: my top rows into the upper band's
+// bottom halo, my bottom rows into the lower band's top halo. Kinds: step t
+// (positions with (y + x) mod s == t), all positions, or all positions of
+// every context slot (slot strides HWl of each side).
+void Engine::build_pairs() {
+  const Dims& D = D_;
+  for (int side = 0; side < 2; ++side) {
+    Engine* nb = side == 0 ? up_ : down_;
+    for (int k = 0; k < 18; ++k) {
+      nxpairs_[side][k] = 0;
+      xpairs_[side][k] = nullptr;
+    }
+    if (!nb) continue;
+    const int g0 = side == 0 ? B_.r0 : B_.r1 - kHaloRows;  // global rows sent
+    std::vector<int2> v[18];
+    for (int y = g0; y < g0 + kHaloRows; ++y)
+      for (int x = 0; x < D.W; ++x) {
+        const int src = (y - B_.lo) * D.W + x, dst = (y - nb->B_.lo) * D.W + x;
+        v[(y + x) % D.c.s].push_back(make_int2(src, dst));
+        v[kXAll].push_back(make_int2(src, dst));
+        for (int j = 0; j < D.T; ++j)
+          v[kXCtx].push_back(make_int2(j * HWl_ + src, j * nb->HWl_ + dst));
+      }
+    for (int k = 0; k < 18; ++k) {
+      if (v[k].empty()) continue;
+      int2* p = dalloc<int2>(v[k].size());
+      PSWA_CUDA(cudaMemcpyAsync(p, v[k].data(), v[k].size() * sizeof(int2), cudaMemcpyHostToDevice, st_));
+      xpairs_[side][k] = p;
+      nxpairs_[side][k] = static_cast<int>(v[k].size());
+    }
+  }
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Engine::exchange(Program& P, int id, int kind) {
+  if (B_.n <= 1) return;
+  for (int side = 0; side < 2; ++side) {
+    Engine* nb = side == 0 ? up_ : down_;
+    if (!nb || !nxpairs_[side][kind]) continue;
+    const __half* src = xbuf(id);
+    __half* dst = nb->xbuf(id);
+    const int ld = xld(id), n = nxpairs_[side][kind];
+    const int2* pairs = xpairs_[side][kind];
+    add(P, [=](cudaStream_t s) { pswa_dev::halo_push(src, dst, ld, pairs, n, s); });
+  }
+  cut(P, false);
+}
+
+void Engine::link(Engine* up, Engine* down, Engine* band0) {
+  up_ = up;
+  down_ = down;
+  band0_ = band0;
+  build_pairs();
+  for (auto& kv : progs_)
+    for (auto ex : kv.second.execs)
+      if (ex) cudaGraphExecDestroy(ex);
+  progs_.clear();
 }
 
 // ---------------------------------------------------------- frame API ----
@@ -915,8 +1063,8 @@ void Engine::set_frame_params(int rate, int fidx) {
 }
 
 void Engine::advance_ring() {
-  PSWA_CUDA(cudaMemcpyAsync(ring_[head_], emb_cur_, sizeof(float) * D_.HW * D_.d,
-                            cudaMemcpyDeviceToDevice, st_));
+  PSWA_CUDA(cudaMemcpyAsync(ring_[head_], emb_cur_ + static_cast<size_t>(B_.own0) * D_.W * D_.d,
+                            sizeof(float) * HWo_ * D_.d, cudaMemcpyDeviceToDevice, st_));
   head_ = (head_ + 1) % D_.T;
   npast_ = std::min(npast_ + 1, D_.T);
 }
@@ -926,29 +1074,46 @@ void Engine::reset_gop() {
   npast_ = 0;
 }
 
+// Own rows of a full-frame [planes][H][W] int32 host/device buffer into (or,
+// with dst == nullptr semantics reversed by the callers) the compact
+// [planes][nown][W] device layout.
+void Engine::copy_rows_in(int32_t* dst, const int32_t* src_full, int planes, bool device) {
+  const size_t row = static_cast<size_t>(HWo_) * sizeof(int32_t);
+  const cudaMemcpyKind k = device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (B_.n == 1) {
+    PSWA_CUDA(cudaMemcpyAsync(dst, src_full, row * planes, k, st_));
+  } else {
+    PSWA_CUDA(cudaMemcpy2DAsync(dst, row, src_full + static_cast<size_t>(B_.r0) * D_.W,
+                                static_cast<size_t>(D_.HW) * sizeof(int32_t), row, planes, k, st_));
+  }
+}
+
 void Engine::push_frame(const int32_t* yhat_chw, int rate) {
   set_frame_params(rate, 0);
-  PSWA_CUDA(cudaMemcpyAsync(ychw_, yhat_chw, sizeof(int32_t) * D_.HW * D_.C, cudaMemcpyHostToDevice, st_));
-  run(program("push"));
+  copy_rows_in(ychw_, yhat_chw, D_.C, false);
+  Program& P = program("push");
+  last_launches_ = P.launches;
+  launch_segment(P, 0);  // no exchanges: embeddings are per position
   advance_ring();
   PSWA_CUDA(cudaStreamSynchronize(st_));
 }
 
-FrameResult Engine::encode(const int32_t* yhat_chw, int rate, int fidx, const int32_t* zhat_in,
-                           float* mu_out, float* sigma_out, uint8_t* hyper_out, size_t hyper_cap,
-                           uint8_t* main_out, size_t main_cap, bool advance) {
-  const Dims& D = D_;
-  const size_t nsym = static_cast<size_t>(D.HW) * D.C;
-  const size_t nz = static_cast<size_t>(D.hc) * D.zh * D.zw;
+std::string Engine::encode_key(bool zgiven, bool musig) {
+  return std::string(zgiven ? "encode_z" : "encode") + (musig ? "+ms" : "");
+}
+
+void Engine::prep_encode(const int32_t* yhat_chw, int rate, int fidx, const int32_t* zhat_in) {
   set_frame_params(rate, fidx);
-  PSWA_CUDA(cudaMemcpyAsync(ychw_, yhat_chw, sizeof(int32_t) * nsym, cudaMemcpyHostToDevice, st_));
+  copy_rows_in(ychw_, yhat_chw, D_.C, false);
   if (zhat_in)
-    PSWA_CUDA(cudaMemcpyAsync(zhat_, zhat_in, sizeof(int32_t) * nz, cudaMemcpyHostToDevice, st_));
-  want_musig_ = mu_out != nullptr;
-  // the mu/sigma output pointers are baked into the captured graph, so the
-  // two variants are separate programs
-  const std::string key = std::string(zhat_in ? "encode_z" : "encode") + (want_musig_ ? "+ms" : "");
-  run(program(key));
+    PSWA_CUDA(cudaMemcpyAsync(zhat_, zhat_in, sizeof(int32_t) * D_.hc * D_.zh * D_.zw,
+                              cudaMemcpyHostToDevice, st_));
+}
+
+FrameResult Engine::finish_encode(float* mu_out, float* sigma_out, uint8_t* hyper_out,
+                                  size_t hyper_cap, uint8_t* main_out, size_t main_cap,
+                                  bool advance) {
+  const Dims& D = D_;
   FrameResult r;
   unsigned long long tot[2];
   PSWA_CUDA(cudaMemcpyAsync(tot, pack_total_, sizeof(tot), cudaMemcpyDeviceToHost, st_));
@@ -966,15 +1131,17 @@ FrameResult Engine::encode(const int32_t* yhat_chw, int rate, int fidx, const in
     if (main_cap < r.main_len) throw std::invalid_argument("main output buffer too small");
     PSWA_CUDA(cudaMemcpyAsync(main_out, d_main_, r.main_len, cudaMemcpyDeviceToHost, st_));
   }
-  if (mu_out) {
-    std::vector<float> a(nsym), b(nsym);
-    PSWA_CUDA(cudaMemcpyAsync(a.data(), mu_full_, sizeof(float) * nsym, cudaMemcpyDeviceToHost, st_));
-    PSWA_CUDA(cudaMemcpyAsync(b.data(), sg_full_, sizeof(float) * nsym, cudaMemcpyDeviceToHost, st_));
+  if (mu_out) {  // [HWl][C] device -> own rows of the [C][H][W] host frame
+    const size_t n = static_cast<size_t>(HWl_) * D.C;
+    std::vector<float> a(n), b(n);
+    PSWA_CUDA(cudaMemcpyAsync(a.data(), mu_full_, sizeof(float) * n, cudaMemcpyDeviceToHost, st_));
+    PSWA_CUDA(cudaMemcpyAsync(b.data(), sg_full_, sizeof(float) * n, cudaMemcpyDeviceToHost, st_));
     PSWA_CUDA(cudaStreamSynchronize(st_));
-    for (int p = 0; p < D.HW; ++p)
+    const size_t o = static_cast<size_t>(B_.own0) * D.W, g = static_cast<size_t>(B_.r0) * D.W;
+    for (int p = 0; p < HWo_; ++p)
       for (int c = 0; c < D.C; ++c) {
-        mu_out[static_cast<size_t>(c) * D.HW + p] = a[static_cast<size_t>(p) * D.C + c];
-        sigma_out[static_cast<size_t>(c) * D.HW + p] = b[static_cast<size_t>(p) * D.C + c];
+        mu_out[static_cast<size_t>(c) * D.HW + g + p] = a[(o + p) * D.C + c];
+        sigma_out[static_cast<size_t>(c) * D.HW + g + p] = b[(o + p) * D.C + c];
       }
   }
   if (advance) advance_ring();
@@ -982,21 +1149,51 @@ FrameResult Engine::encode(const int32_t* yhat_chw, int rate, int fidx, const in
   return r;
 }
 
-FrameResult Engine::decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
-                           int rate, int fidx, bool advance, int32_t* yhat_out, bool device) {
-  const Dims& D = D_;
+void Engine::fetch_payloads(uint8_t* hyper_out, size_t hyper_cap, const FrameResult& r,
+                            uint8_t* main_out) {
+  if (hyper_out) {
+    if (hyper_cap < r.hyper_len) throw std::invalid_argument("hyper output buffer too small");
+    PSWA_CUDA(cudaMemcpyAsync(hyper_out, d_hyper_, r.hyper_len, cudaMemcpyDeviceToHost, st_));
+  }
+  if (main_out) PSWA_CUDA(cudaMemcpyAsync(main_out, d_main_, r.main_len, cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+}
+
+FrameResult Engine::encode(const int32_t* yhat_chw, int rate, int fidx, const int32_t* zhat_in,
+                           float* mu_out, float* sigma_out, uint8_t* hyper_out, size_t hyper_cap,
+                           uint8_t* main_out, size_t main_cap, bool advance) {
+  prep_encode(yhat_chw, rate, fidx, zhat_in);
+  want_musig_ = mu_out != nullptr;
+  // the mu/sigma output pointers are baked into the captured graph, so the
+  // two variants are separate programs
+  run(program(encode_key(zhat_in != nullptr, want_musig_)));
+  return finish_encode(mu_out, sigma_out, hyper_out, hyper_cap, main_out, main_cap, advance);
+}
+
+void Engine::prep_decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
+                         int rate, int fidx, bool device) {
   if (hyper_len > hyper_cap_ || main_len > main_cap_)
     throw pswa_abi::TruncatedError("payload larger than the decoder's capacity");
   set_frame_params(rate, fidx);
   const cudaMemcpyKind in_kind = device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   PSWA_CUDA(cudaMemcpyAsync(d_hyper_, hyper, hyper_len, in_kind, st_));
   PSWA_CUDA(cudaMemcpyAsync(d_main_, main_pl, main_len, in_kind, st_));
-  uint32_t lens[2] = {static_cast<uint32_t>(hyper_len), static_cast<uint32_t>(main_len)};
-  PSWA_CUDA(cudaMemcpyAsync(d_lens_, lens, sizeof(lens), cudaMemcpyHostToDevice, st_));
-  run(program("decode"));
+  lens_h_[0] = static_cast<uint32_t>(hyper_len);
+  lens_h_[1] = static_cast<uint32_t>(main_len);
+  PSWA_CUDA(cudaMemcpyAsync(d_lens_, lens_h_, sizeof(lens_h_), cudaMemcpyHostToDevice, st_));
+}
+
+FrameResult Engine::finish_decode(bool advance, int32_t* yhat_out, bool device) {
+  const Dims& D = D_;
   FrameResult r;
-  PSWA_CUDA(cudaMemcpyAsync(yhat_out, ychw_, sizeof(int32_t) * D.HW * D.C,
-                            device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st_));
+  const size_t row = static_cast<size_t>(HWo_) * sizeof(int32_t);
+  const cudaMemcpyKind k = device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (B_.n == 1)
+    PSWA_CUDA(cudaMemcpyAsync(yhat_out, ychw_, row * D.C, k, st_));
+  else
+    PSWA_CUDA(cudaMemcpy2DAsync(yhat_out + static_cast<size_t>(B_.r0) * D.W,
+                                static_cast<size_t>(D.HW) * sizeof(int32_t), ychw_, row, row, D.C,
+                                k, st_));
   PSWA_CUDA(cudaMemcpyAsync(r.bits, bits_, sizeof(r.bits), cudaMemcpyDeviceToHost, st_));
   PSWA_CUDA(cudaMemcpyAsync(&r.status, status_, sizeof(int), cudaMemcpyDeviceToHost, st_));
   PSWA_CUDA(cudaStreamSynchronize(st_));
@@ -1009,12 +1206,20 @@ FrameResult Engine::decode(const void* hyper, size_t hyper_len, const void* main
   return r;
 }
 
+FrameResult Engine::decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
+                           int rate, int fidx, bool advance, int32_t* yhat_out, bool device) {
+  prep_decode(hyper, hyper_len, main_pl, main_len, rate, fidx, device);
+  run(program("decode"));
+  return finish_decode(advance, yhat_out, device);
+}
+
+
 size_t Engine::debug_fetch(const std::string& name, void* out, size_t cap) {
-  const size_t hwd = static_cast<size_t>(D_.HW) * D_.d;
+  const size_t hwd = static_cast<size_t>(HWl_) * D_.d;
   const void* src = nullptr;
   size_t bytes = 0;
   if (name == "ctx") src = ctx16_, bytes = hwd * 2;
-  else if (name == "emb") src = emb_cur_, bytes = hwd * 4;
+  else if (name == "emb") src = emb_cur_, bytes = hwd * 4;  // local grid in band mode
   else if (name == "hq") src = hq_, bytes = hwd * 4;
   else if (name == "s1") src = s1full_, bytes = static_cast<size_t>(D_.Hp) * D_.Wp * D_.d * 2;
   else if (name == "a") src = afull_, bytes = hwd * 4;

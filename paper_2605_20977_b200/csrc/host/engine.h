@@ -39,10 +39,34 @@ struct Block {  // one transformer block of ctx / s1 / s2
   __half* kv_cache = nullptr;  // self layers of s1/s2: [HW][2d]; cross: ctx K/V
 };
 
+// Row band of a banded frame (BASELINE config 5). A band owns
+// global latent rows [r0, r1) (multiples of 4) and keeps a local grid of rows
+// [lo, lo + Hl): its own rows plus a halo of kHaloTop rows above (3 needed by
+// the 7x7 window, 4 so that local row 0 keeps the global (y + x) mod 4 step
+// pattern) and kHaloBottom below. Halo rows are never computed or coded
+// locally; the neighbour pushes their K/V after every layer that produces them.
+constexpr int kHaloTop = 4, kHaloBottom = 3, kHaloRows = 3;
+struct Band {
+  int idx = 0, n = 1;
+  int r0 = 0, r1 = 0;       // own rows (global)
+  int lo = 0, Hl = 0;       // local grid: global rows [lo, lo + Hl)
+  int own0 = 0, nown = 0;   // own rows in local coordinates
+};
+// Deterministic partition of H latent rows into n bands at multiples of 4.
+void band_rows(int H, int n, int b, int* r0, int* r1);
+
+// A program is a list of launches, split into segments at halo exchanges in
+// band mode (a segment ends with the pushes into the neighbours' halos;
+// `global` cuts wait for every band, not just the neighbours).
+struct Cut {
+  size_t at;
+  bool global;
+};
 struct Program {
   std::vector<std::function<void(cudaStream_t)>> ops;
+  std::vector<Cut> cuts;
   int launches = 0;
-  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaGraphExec_t> execs;  // one graph per segment
 };
 
 struct FrameResult {
@@ -53,7 +77,8 @@ struct FrameResult {
 
 class Engine {
  public:
-  Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len);
+  Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len, int band_idx = 0,
+         int n_bands = 1);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -62,6 +87,11 @@ class Engine {
   cudaStream_t stream() const { return st_; }
   int last_launches() const { return last_launches_; }
 
+  const Band& band() const { return B_; }
+  int device() const { return device_; }
+
+  // Host frame buffers are full-frame [C][H][W] (z_hat [hc][zh][zw]); a band
+  // reads and writes only its own rows.
   void reset_gop();
   void push_frame(const int32_t* yhat_chw_host, int rate);
   // Encoder (teacher forced). zhat_in: nullable host [hc][zh][zw]; mu/sigma
@@ -74,6 +104,28 @@ class Engine {
   FrameResult decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
                      int rate, int fidx, bool advance, int32_t* yhat_out, bool device);
   void last_zhat(int32_t* out_host);
+
+  // ---- band mode (driven by BandGroup) ----------------------------------
+  // Neighbours above / below (nullable) and band 0 (holder of the gathered
+  // full-frame S1 for the hyper encoder). Peers may live on other devices
+  // (peer access enabled by the group). Invalidates built programs.
+  void link(Engine* up, Engine* down, Engine* band0);
+  // Split-phase frame API: prep_* stage inputs on the stream, the group runs
+  // the program's segments on every band, finish_* collects the outputs.
+  void prep_decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
+                   int rate, int fidx, bool device);
+  FrameResult finish_decode(bool advance, int32_t* yhat_out, bool device);
+  void prep_encode(const int32_t* yhat_chw_host, int rate, int fidx, const int32_t* zhat_in);
+  FrameResult finish_encode(float* mu_out, float* sigma_out, uint8_t* hyper_out, size_t hyper_cap,
+                            uint8_t* main_out, size_t main_cap, bool advance);
+  std::string encode_key(bool zgiven, bool musig);
+  void set_want_musig(bool on) { want_musig_ = on; }
+  // Copies the payloads of the last finish_encode to host buffers (nullable).
+  void fetch_payloads(uint8_t* hyper_out, size_t hyper_cap, const FrameResult& r, uint8_t* main_out);
+  Program& program(const std::string& key);
+  int segments(const Program& P) const { return static_cast<int>(P.cuts.size()) + 1; }
+  bool cut_global(const Program& P, int k) const { return P.cuts[k].global; }
+  void launch_segment(Program& P, int k);
   // Debug taps (filled by forward_params): ctx, emb, hq, s1 (padded grid),
   // a, s2. Returns the byte size; copies when out != nullptr.
   size_t debug_fetch(const std::string& name, void* out, size_t cap);
@@ -99,9 +151,28 @@ class Engine {
   void run(Program& P);
   void set_frame_params(int rate, int fidx);
   void advance_ring();
-  Program& program(const std::string& key);
+  // band mode: push the halo rows of exchange buffer `id` (kind: step t in
+  // 0..3, kAll, kCtx) into the neighbours and end the segment
+  enum { kXAll = 16, kXCtx = 17 };
+  enum { kXidAcc = 32, kXidCtx0 = 33, kXidCtx1 = 34, kXidCtx16 = 35 };
+  int xid_of(const Block& b) const {
+    return (&b >= s1_ && &b < s1_ + 16) ? static_cast<int>(&b - s1_) : 16 + static_cast<int>(&b - s2_);
+  }
+  void exchange(Program& P, int id, int kind);
+  void cut(Program& P, bool global);
+  __half* xbuf(int id);
+  int xld(int id) const;
+  void build_pairs();
+  void copy_rows_in(int32_t* dst, const int32_t* src_full, int per_row_planes, bool device);
 
   Dims D_;
+  Band B_;
+  int HWl_ = 0, HWo_ = 0;  // local grid / own positions (== HW when unbanded)
+  Engine *up_ = nullptr, *down_ = nullptr, *band0_ = nullptr;
+  int2* xpairs_[2][18] = {};  // [side: 0 up, 1 down][kind] (src local, dst peer-local) rows
+  int nxpairs_[2][18] = {};
+  int* ctx_kv_map_ = nullptr;  // own ctx rows -> local K/V rows (band mode)
+  __half* ctx_kv2_ = nullptr;  // second context K/V buffer (band mode: layer parity)
   int device_ = 0;
   cudaStream_t st_ = nullptr;
   std::vector<void*> allocs_;
@@ -172,6 +243,7 @@ class Engine {
   uint8_t *d_hyper_ = nullptr, *d_main_ = nullptr;
   size_t hyper_cap_ = 0, main_cap_ = 0;
   uint32_t* d_lens_ = nullptr;  // [2] payload lengths (hyper, main)
+  uint32_t lens_h_[2] = {0, 0};  // host staging of d_lens_ (stable address for async copies)
   pswa_dev::LaneState *lanes_ = nullptr, *hlanes_ = nullptr;
   int* status_ = nullptr;
   double* bits_ = nullptr;  // [2]

@@ -58,3 +58,23 @@ def test_bad_config_rejected():
     cfg = make_cfg("desk", 16, 16, win_h=6)
     with pytest.raises(PswaError):
         gen_weights(cfg, 1)
+
+
+@pytest.mark.parametrize("H,n", [(68, 1), (68, 2), (136, 8), (16, 4), (17, 2), (120, 7)])
+def test_band_rows_partition(H, n):
+    """Row bands tile the grid, start at multiples of 4 (the hyperprior and
+    the s = 4 wavefront pattern) and hold >= 3 rows (the 7x7 halo)."""
+    from paper_2605_20977_b200.codec import band_rows
+    rows = [band_rows(H, n, b) for b in range(n)]
+    assert rows[0][0] == 0 and rows[-1][1] == H
+    for (a0, a1), (b0, _) in zip(rows, rows[1:]):
+        assert a1 == b0
+    for r0, r1 in rows:
+        assert r0 % 4 == 0 and r1 - r0 >= 3
+
+
+def test_band_rows_rejects_too_many_bands():
+    from paper_2605_20977_b200 import PswaError
+    from paper_2605_20977_b200.codec import band_rows
+    with pytest.raises(PswaError):
+        band_rows(16, 5, 0)
