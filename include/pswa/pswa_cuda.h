@@ -155,6 +155,19 @@ int pswa_group_forward_params(pswa_group* g, const int32_t* yhat, const int32_t*
 int pswa_group_last_zhat(pswa_group* g, int32_t* zhat_out);
 int pswa_group_last_launch_count(pswa_group* g);
 
+/* One band per process (torchrun: rank r = band r on its own GPU). Create
+ * the band handle, export its exchange buffers (CUDA-IPC handles, an opaque
+ * blob), pass every band its neighbours' blobs (NULL at the frame edges),
+ * then use the frame API above on the handle with the band's own payload of
+ * the PSWB container. Segments are chained on the device by mailbox flags
+ * (no host round trip per exchange). Encoding through band handles needs
+ * z_hat (pswa_gpu_forward_params); produce banded bitstreams with a group. */
+int pswa_gpu_create_band(int device, const pswa_cfg* cfg, const void* psww_blob, size_t blob_len,
+                         int band_idx, int n_bands, pswa_gpu** out);
+int pswa_gpu_band_export(pswa_gpu* h, void* out, size_t cap, size_t* len);
+int pswa_gpu_band_link(pswa_gpu* h, const void* up_blob, size_t up_len, const void* down_blob,
+                       size_t down_len);
+
 /* ---- operator-level entry points (device pointers, on `stream`) -------- */
 /* C[M,N] = A[M,K] . B[N,K]^T, fp16 in, fp32 accumulate; out fp16 or fp32. */
 int pswa_gpu_op_gemm_f16(const void* A, int lda, int M, const void* B, int ldb, int N, int K,

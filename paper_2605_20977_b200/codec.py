@@ -51,12 +51,29 @@ def _ptr(a: np.ndarray):
 class GpuCodec:
     """One device handle: weights, K/V caches, temporal ring, coder lanes."""
 
-    def __init__(self, cfg: PswaCfg, weights: bytes, device: int = 0):
+    def __init__(self, cfg: PswaCfg, weights: bytes, device: int = 0, band: int = 0,
+                 n_bands: int = 1):
         self.cfg = cfg
         self._w = (C.c_uint8 * len(weights)).from_buffer_copy(weights)
         h = C.c_void_p()
-        check(lib().pswa_gpu_create(device, C.byref(cfg), self._w, len(weights), C.byref(h)))
+        if n_bands == 1:
+            check(lib().pswa_gpu_create(device, C.byref(cfg), self._w, len(weights), C.byref(h)))
+        else:  # one band of a cross-process group (link it with band_link)
+            check(lib().pswa_gpu_create_band(device, C.byref(cfg), self._w, len(weights), band,
+                                             n_bands, C.byref(h)))
         self.h = h
+        self.band, self.n_bands = band, n_bands
+
+    def band_export(self) -> bytes:
+        n = C.c_size_t()
+        check(lib().pswa_gpu_band_export(self.h, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        check(lib().pswa_gpu_band_export(self.h, buf, n.value, C.byref(n)))
+        return bytes(buf)
+
+    def band_link(self, up: bytes | None, down: bytes | None):
+        check(lib().pswa_gpu_band_link(self.h, up, len(up) if up else 0, down,
+                                       len(down) if down else 0))
 
     def close(self):
         if getattr(self, "h", None):
@@ -137,6 +154,22 @@ class GpuCodec:
 
     def stream(self) -> int:
         return lib().pswa_gpu_stream(self.h)
+
+
+def split_banded(main: bytes, n: int) -> list[bytes]:
+    """Band payloads of a PSWB container ("PSWB" | u32 n | u64 len[n] | ...)."""
+    if len(main) < 8 + 8 * n or main[:4] != b"PSWB":
+        raise ValueError("not a banded payload")
+    if int.from_bytes(main[4:8], "little") != n:
+        raise ValueError("band count differs")
+    lens = [int.from_bytes(main[8 + 8 * b:16 + 8 * b], "little") for b in range(n)]
+    off, out = 8 + 8 * n, []
+    for l in lens:
+        if off + l > len(main):
+            raise ValueError("truncated banded payload")
+        out.append(main[off:off + l])
+        off += l
+    return out
 
 
 def band_rows(height: int, n_bands: int, band: int) -> tuple[int, int]:

@@ -37,6 +37,15 @@ void scatter_rows_f16(const __half* src, int lds, const int* rows, int M, int n,
 // rows then travel as NVLink P2P stores straight into the neighbour's K/V
 // cache, no staging copy.
 void halo_push(const __half* src, __half* dst, int ld, const int2* pairs, int n, cudaStream_t st);
+// Cross-process band chaining (one process per GPU): after a segment's
+// pushes, increment the neighbours' mailbox counters (system scope); before
+// the next segment, spin until every present neighbour has signalled as many
+// times as this band has waited (wait_ctr, device-resident so captured
+// graphs can be replayed). A wait longer than ~20 s sets status |= 8 and
+// returns instead of hanging the device.
+void band_signal(unsigned* to_up, unsigned* to_down, cudaStream_t st);
+void band_wait(const unsigned* mbox, unsigned* wait_ctr, bool need_up, bool need_down, int* status,
+               cudaStream_t st);
 
 // ---- windowed attention (attention.cu) -----------------------------------
 // Queries: rows of q (fp16, head h at columns h*hd), qinfo[i] = slot<<24 |

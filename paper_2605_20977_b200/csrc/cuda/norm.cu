@@ -212,11 +212,59 @@ __global__ void halo_push_kernel(const __half* __restrict__ src, __half* __restr
   const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<size_t>(p.x) * ld);
   uint4* d = reinterpret_cast<uint4*>(dst + static_cast<size_t>(p.y) * ld);
   for (int i = lane; i < ld / 8; i += 32) d[i] = s[i];
+  __threadfence_system();  // peer stores performed before any later signal
+}
+
+__global__ void band_signal_kernel(unsigned* to_up, unsigned* to_down) {
+  pdl_wait();
+  __threadfence_system();
+  if (to_up) atomicAdd_system(to_up, 1u);
+  if (to_down) atomicAdd_system(to_down, 1u);
+}
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void band_wait_kernel(const unsigned* mbox, unsigned* wait_ctr, int need_up,
+                                 int need_down, int* status) {
+  pdl_wait();
+  const unsigned e = ++wait_ctr[0];
+  if (*reinterpret_cast<volatile int*>(status) & 8) return;  // a wait already timed out: fail fast
+  const unsigned long long t0 = globaltimer();
+  auto behind = [&](int i) { return static_cast<int>(ld_acquire_sys(mbox + i) - e) < 0; };
+  while ((need_up && behind(0)) || (need_down && behind(1))) {
+    __nanosleep(200);
+    if (globaltimer() - t0 > 20000000000ull) {
+      atomicOr(status, 8);
+      break;
+    }
+  }
+  __threadfence();
 }
 
 void halo_push(const __half* src, __half* dst, int ld, const int2* pairs, int n, cudaStream_t st) {
   if (n <= 0) return;
   launch_k(halo_push_kernel, dim3((n + 7) / 8), dim3(256), 0, st, src, dst, ld, pairs, n);
+  PSWA_LAUNCH_CHECK();
+}
+
+void band_signal(unsigned* to_up, unsigned* to_down, cudaStream_t st) {
+  launch_k(band_signal_kernel, dim3(1), dim3(1), 0, st, to_up, to_down);
+  PSWA_LAUNCH_CHECK();
+}
+
+void band_wait(const unsigned* mbox, unsigned* wait_ctr, bool need_up, bool need_down, int* status,
+               cudaStream_t st) {
+  launch_k(band_wait_kernel, dim3(1), dim3(1), 0, st, mbox, wait_ctr, need_up ? 1 : 0,
+           need_down ? 1 : 0, status);
   PSWA_LAUNCH_CHECK();
 }
 

@@ -74,6 +74,36 @@ int pswa_gpu_create(int device, const pswa_cfg* cfg, const void* blob, size_t le
 
 void pswa_gpu_destroy(pswa_gpu* h) { delete h; }
 
+int pswa_gpu_create_band(int device, const pswa_cfg* cfg, const void* blob, size_t len, int band_idx,
+                         int n_bands, pswa_gpu** out) {
+  *out = nullptr;
+  return guard([&] {
+    auto h = std::make_unique<pswa_gpu>();
+    h->eng = std::make_unique<pswa_host::Engine>(device, *cfg, blob, len, band_idx, n_bands);
+    *out = h.release();
+  });
+}
+
+int pswa_gpu_band_export(pswa_gpu* h, void* out, size_t cap, size_t* len) {
+  return guard([&] {
+    PSWA_CUDA(cudaSetDevice(h->eng->device()));
+    const auto b = h->eng->ipc_export();
+    *len = b.size();
+    if (out) {
+      if (cap < b.size()) throw std::invalid_argument("pswa_gpu_band_export: buffer too small");
+      std::memcpy(out, b.data(), b.size());
+    }
+  });
+}
+
+int pswa_gpu_band_link(pswa_gpu* h, const void* up, size_t up_len, const void* down, size_t down_len) {
+  return guard([&] {
+    PSWA_CUDA(cudaSetDevice(h->eng->device()));
+    h->eng->link_ipc(static_cast<const uint8_t*>(up), up_len, static_cast<const uint8_t*>(down),
+                     down_len);
+  });
+}
+
 int pswa_gpu_reset_gop(pswa_gpu* h) {
   return guard([&] { h->eng->reset_gop(); });
 }

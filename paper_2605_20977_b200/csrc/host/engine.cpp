@@ -99,6 +99,7 @@ Engine::~Engine() {
     for (auto ex : kv.second.execs)
       if (ex) cudaGraphExecDestroy(ex);
   if (st_) cudaStreamSynchronize(st_);
+  for (void* p : ipc_mapped_) cudaIpcCloseMemHandle(p);
   for (void* p : allocs_) cudaFree(p);
   if (st_) cudaStreamDestroy(st_);
 }
@@ -260,6 +261,8 @@ void Engine::alloc_all() {
             (y >= B_.r0 && y < B_.r1 && x < D.W) ? (y - B_.lo) * D.W + x : -1;
     crop_rows_ = up(crop);
   }
+  mbox_ = dalloc<unsigned>(2);
+  wait_ctr_ = dalloc<unsigned>(1);
   scales_ = dalloc<float>(pswa_dev::kScales);
   cdf_ = dalloc<uint32_t>(pswa_dev::kCdfWords);
 
@@ -747,7 +750,7 @@ void Engine::build_s1(Program& P, int t, bool encoder) {
   gemm(P, bs1n_, d, M, acc_.wkv, d, e);
   if (encoder) {  // full-frame S1 for the hyper encoder (band mode: band 0 gathers it)
     const int* rp = step_rows_pad_[t];
-    __half* dst = band0_ ? band0_->s1full_ : s1full_;
+    __half* dst = band0_s1_ ? band0_s1_ : s1full_;
     add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f16(bs1n_, d, rp, M, d, dst, d, s); });
   }
   exchange(P, kXidAcc, t);
@@ -879,9 +882,10 @@ Program& Engine::program(const std::string& key) {
         // every band has scattered its S1 rows into band 0's full-frame
         // buffer; each band then runs the (small) hyper encoder on a local
         // copy, so z_hat is bitwise identical on every band
+        if (ipc_) throw std::invalid_argument("cross-process band encode needs z_hat (encode_z)");
         cut(P, true);
-        if (band0_ && band0_ != this) {
-          const __half* src = band0_->s1full_;
+        if (band0_s1_ && band0_s1_ != s1full_) {
+          const __half* src = band0_s1_;
           const size_t bytes = static_cast<size_t>(D.Hp) * D.Wp * D.d * sizeof(__half);
           add(P, [=, this](cudaStream_t s) {
             PSWA_CUDA(cudaMemcpyAsync(s1full_, src, bytes, cudaMemcpyDefault, s));
@@ -957,7 +961,7 @@ void Engine::launch_segment(Program& P, int k) {
 }
 
 void Engine::run(Program& P) {
-  if (B_.n > 1) throw std::logic_error("band engines are run by their BandGroup");
+  if (B_.n > 1 && !ipc_) throw std::logic_error("in-process band engines are run by their BandGroup");
   last_launches_ = P.launches;
   launch_segment(P, 0);
 }
@@ -986,21 +990,21 @@ int Engine::xld(int id) const { return id == kXidCtx16 ? D_.d : 2 * D_.d; }
 void Engine::build_pairs() {
   const Dims& D = D_;
   for (int side = 0; side < 2; ++side) {
-    Engine* nb = side == 0 ? up_ : down_;
+    const PeerInfo& nb = peer_[side];
     for (int k = 0; k < 18; ++k) {
       nxpairs_[side][k] = 0;
       xpairs_[side][k] = nullptr;
     }
-    if (!nb) continue;
+    if (!nb.present) continue;
     const int g0 = side == 0 ? B_.r0 : B_.r1 - kHaloRows;  // global rows sent
     std::vector<int2> v[18];
     for (int y = g0; y < g0 + kHaloRows; ++y)
       for (int x = 0; x < D.W; ++x) {
-        const int src = (y - B_.lo) * D.W + x, dst = (y - nb->B_.lo) * D.W + x;
+        const int src = (y - B_.lo) * D.W + x, dst = (y - nb.lo) * D.W + x;
         v[(y + x) % D.c.s].push_back(make_int2(src, dst));
         v[kXAll].push_back(make_int2(src, dst));
         for (int j = 0; j < D.T; ++j)
-          v[kXCtx].push_back(make_int2(j * HWl_ + src, j * nb->HWl_ + dst));
+          v[kXCtx].push_back(make_int2(j * HWl_ + src, j * nb.HWl + dst));
       }
     for (int k = 0; k < 18; ++k) {
       if (v[k].empty()) continue;
@@ -1016,21 +1020,110 @@ void Engine::build_pairs() {
 void Engine::exchange(Program& P, int id, int kind) {
   if (B_.n <= 1) return;
   for (int side = 0; side < 2; ++side) {
-    Engine* nb = side == 0 ? up_ : down_;
-    if (!nb || !nxpairs_[side][kind]) continue;
+    const PeerInfo& nb = peer_[side];
+    if (!nb.present || !nxpairs_[side][kind]) continue;
     const __half* src = xbuf(id);
-    __half* dst = nb->xbuf(id);
+    __half* dst = nb.buf[id];
     const int ld = xld(id), n = nxpairs_[side][kind];
     const int2* pairs = xpairs_[side][kind];
     add(P, [=](cudaStream_t s) { pswa_dev::halo_push(src, dst, ld, pairs, n, s); });
   }
-  cut(P, false);
+  if (ipc_) {
+    // the band above counts my pushes in its "from below" slot and v.v.
+    unsigned* to_up = peer_[0].present ? peer_[0].mbox + 1 : nullptr;
+    unsigned* to_down = peer_[1].present ? peer_[1].mbox : nullptr;
+    const bool need_up = peer_[0].present, need_down = peer_[1].present;
+    add(P, [=](cudaStream_t s) { pswa_dev::band_signal(to_up, to_down, s); });
+    add(P, [=, this](cudaStream_t s) {
+      pswa_dev::band_wait(mbox_, wait_ctr_, need_up, need_down, status_, s);
+    });
+  } else {
+    cut(P, false);
+  }
+}
+
+PeerInfo Engine::self_info() {
+  PeerInfo p;
+  p.present = true;
+  p.lo = B_.lo;
+  p.HWl = HWl_;
+  for (int id = 0; id < kXids; ++id) p.buf[id] = xbuf(id);  // null for absent blocks
+  p.s1full = s1full_;
+  p.mbox = mbox_;
+  return p;
 }
 
 void Engine::link(Engine* up, Engine* down, Engine* band0) {
-  up_ = up;
-  down_ = down;
-  band0_ = band0;
+  peer_[0] = up ? up->self_info() : PeerInfo{};
+  peer_[1] = down ? down->self_info() : PeerInfo{};
+  band0_s1_ = band0 ? band0->s1full_ : nullptr;
+  ipc_ = false;
+  build_pairs();
+  for (auto& kv : progs_)
+    for (auto ex : kv.second.execs)
+      if (ex) cudaGraphExecDestroy(ex);
+  progs_.clear();
+}
+
+// ---- CUDA-IPC blob: "PSWI" | i32 band, n, lo, HWl | handles of the
+// exchange buffers (kXids), band 0's S1 gather buffer and the mailbox
+namespace {
+struct IpcBlob {
+  char magic[4];
+  int band, n, lo, HWl;
+  int has[kXids + 2];
+  cudaIpcMemHandle_t h[kXids + 2];
+};
+}  // namespace
+
+std::vector<uint8_t> Engine::ipc_export() {
+  if (B_.n <= 1) throw std::invalid_argument("ipc_export: not a band handle");
+  IpcBlob b{};
+  std::memcpy(b.magic, "PSWI", 4);
+  b.band = B_.idx;
+  b.n = B_.n;
+  b.lo = B_.lo;
+  b.HWl = HWl_;
+  const PeerInfo me = self_info();
+  for (int i = 0; i < kXids + 2; ++i) {
+    void* p = i < kXids ? static_cast<void*>(me.buf[i]) : i == kXids ? static_cast<void*>(s1full_) : mbox_;
+    b.has[i] = p != nullptr;
+    if (p) PSWA_CUDA(cudaIpcGetMemHandle(&b.h[i], p));
+  }
+  std::vector<uint8_t> out(sizeof(b));
+  std::memcpy(out.data(), &b, sizeof(b));
+  return out;
+}
+
+void Engine::link_ipc(const uint8_t* up, size_t up_len, const uint8_t* down, size_t down_len) {
+  auto open = [&](const uint8_t* blob, size_t len, int want_band) {
+    PeerInfo p;
+    if (!blob) return p;
+    IpcBlob b;
+    if (len != sizeof(b)) throw std::invalid_argument("link_ipc: bad blob size");
+    std::memcpy(&b, blob, sizeof(b));
+    if (std::memcmp(b.magic, "PSWI", 4) != 0 || b.band != want_band || b.n != B_.n)
+      throw std::invalid_argument("link_ipc: blob is not the neighbouring band of this group");
+    p.present = true;
+    p.lo = b.lo;
+    p.HWl = b.HWl;
+    for (int i = 0; i < kXids + 2; ++i) {
+      if (!b.has[i]) continue;
+      void* q = nullptr;
+      PSWA_CUDA(cudaIpcOpenMemHandle(&q, b.h[i], cudaIpcMemLazyEnablePeerAccess));
+      ipc_mapped_.push_back(q);
+      if (i < kXids) p.buf[i] = static_cast<__half*>(q);
+      else if (i == kXids) p.s1full = static_cast<__half*>(q);
+      else p.mbox = static_cast<unsigned*>(q);
+    }
+    return p;
+  };
+  if ((B_.idx > 0) != (up != nullptr) || (B_.idx + 1 < B_.n) != (down != nullptr))
+    throw std::invalid_argument("link_ipc: neighbour blobs do not match the band position");
+  peer_[0] = open(up, up_len, B_.idx - 1);
+  peer_[1] = open(down, down_len, B_.idx + 1);
+  band0_s1_ = nullptr;
+  ipc_ = true;
   build_pairs();
   for (auto& kv : progs_)
     for (auto ex : kv.second.execs)

@@ -52,6 +52,17 @@ struct Band {
   int lo = 0, Hl = 0;       // local grid: global rows [lo, lo + Hl)
   int own0 = 0, nown = 0;   // own rows in local coordinates
 };
+// What a band needs to know about a neighbour: its local grid origin and the
+// device addresses, valid in this process (same device, peer device, or a
+// CUDA-IPC mapping of another process's memory), of its exchange buffers.
+constexpr int kXids = 36;
+struct PeerInfo {
+  bool present = false;
+  int lo = 0, HWl = 0;
+  __half* buf[kXids] = {};
+  __half* s1full = nullptr;
+  unsigned* mbox = nullptr;  // [2] pushes received from above / below (IPC mode)
+};
 // Deterministic partition of H latent rows into n bands at multiples of 4.
 void band_rows(int H, int n, int b, int* r0, int* r1);
 
@@ -110,6 +121,12 @@ class Engine {
   // full-frame S1 for the hyper encoder). Peers may live on other devices
   // (peer access enabled by the group). Invalidates built programs.
   void link(Engine* up, Engine* down, Engine* band0);
+  // Cross-process linking (one process per GPU): export this band's
+  // exchange buffers as CUDA-IPC handles, then map the neighbours' blobs.
+  // Segments are then chained inside one graph by device-side mailbox
+  // flags (signal after the pushes, spin-wait before the next segment).
+  std::vector<uint8_t> ipc_export();
+  void link_ipc(const uint8_t* up, size_t up_len, const uint8_t* down, size_t down_len);
   // Split-phase frame API: prep_* stage inputs on the stream, the group runs
   // the program's segments on every band, finish_* collects the outputs.
   void prep_decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
@@ -168,7 +185,12 @@ class Engine {
   Dims D_;
   Band B_;
   int HWl_ = 0, HWo_ = 0;  // local grid / own positions (== HW when unbanded)
-  Engine *up_ = nullptr, *down_ = nullptr, *band0_ = nullptr;
+  PeerInfo peer_[2];               // [0] band above, [1] band below
+  PeerInfo self_info();
+  __half* band0_s1_ = nullptr;     // band 0's full-frame S1 (encoder gather)
+  bool ipc_ = false;
+  unsigned *mbox_ = nullptr, *wait_ctr_ = nullptr;
+  std::vector<void*> ipc_mapped_;
   int2* xpairs_[2][18] = {};  // [side: 0 up, 1 down][kind] (src local, dst peer-local) rows
   int nxpairs_[2][18] = {};
   int* ctx_kv_map_ = nullptr;  // own ctx rows -> local K/V rows (band mode)

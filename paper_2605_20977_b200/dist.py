@@ -62,3 +62,26 @@ def max_over_ranks(value: float, dist=None, device=None) -> float:
 def barrier(dist=None):
     if dist is not None:
         dist.barrier()
+
+
+def neighbour_blobs(blobs: list[bytes], rank: int) -> tuple[bytes | None, bytes | None]:
+    """(band above, band below) of `rank` from the all-gathered export blobs;
+    None at the frame edges. Row band r is owned by rank r."""
+    up = blobs[rank - 1] if rank > 0 else None
+    down = blobs[rank + 1] if rank + 1 < len(blobs) else None
+    return up, down
+
+
+def link_band(codec, dist=None):
+    """Cross-process row bands: all-gather every rank's CUDA-IPC
+    export blob over torch.distributed, then map the neighbours' exchange
+    buffers into this rank's band handle. The halo exchange itself never
+    touches torch.distributed: it is P2P stores + device mailbox flags."""
+    blob = codec.band_export()
+    if dist is None:
+        raise ValueError("link_band needs an initialised process group")
+    blobs = [None] * dist.get_world_size()
+    dist.all_gather_object(blobs, blob)
+    up, down = neighbour_blobs(blobs, dist.get_rank())
+    codec.band_link(up, down)
+    return blobs

@@ -58,3 +58,43 @@ def test_two_rank_gloo_max_and_shards():
     assert [r[1] for r in res] == [15.0, 15.0]  # every rank reports the slowest
     assert sorted(res[0][2] + res[1][2]) == list(range(64))
     assert not set(res[0][2]) & set(res[1][2])
+
+
+def _band_link_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    from paper_2605_20977_b200 import dist as pdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    class FakeBand:  # stands in for a GPU band handle: the host logic only
+        def band_export(self):
+            return f"blob{rank}".encode()
+
+        def band_link(self, up, down):
+            q.put((rank, up, down))
+
+    pdist.link_band(FakeBand(), dist)
+    dist.destroy_process_group()
+
+
+def test_band_link_exchanges_neighbour_blobs():
+    """world-size-3 gloo: every rank is linked to exactly its row-band
+    neighbours' export blobs (None at the frame edges)."""
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_band_link_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in ps:
+        p.start()
+    got = dict((r, (u, d)) for r, u, d in (q.get(timeout=120) for _ in ps))
+    for p in ps:
+        p.join(60)
+        assert p.exitcode == 0
+    assert got[0] == (None, b"blob1")
+    assert got[1] == (b"blob0", b"blob2")
+    assert got[2] == (b"blob1", None)

@@ -84,3 +84,27 @@ def test_band_gop_sequence():
         h, m, _ = enc.encode_frame(y, fidx=f)
         yd, _ = dec.decode_frame(h, m, fidx=f)
         assert np.array_equal(yd, y), f
+
+
+@pytest.mark.parametrize("preset,H,W,n", [("desk", 16, 16, 2), ("paper", 24, 16, 3)])
+def test_bands_cross_process(tmp_path, preset, H, W, n):
+    """One process per band (torchrun), all on cuda:0 here: the exchange runs
+    through CUDA-IPC mappings and device mailbox flags, as across GPUs."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = tmp_path / "res.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(root, "tools", "band_ranks.py"), "--same-device", "--preset", preset,
+           "--height", str(H), "--width", str(W), "--out", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    res = json.load(open(out))
+    assert res["bit_exact"]
