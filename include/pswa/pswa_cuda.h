@@ -112,12 +112,26 @@ int pswa_gpu_push_frame(pswa_gpu* h, const int32_t* yhat, int rate_idx);
 int pswa_gpu_decode_frame_device(pswa_gpu* h, const void* d_hyper, size_t hyper_len,
                                  const void* d_main, size_t main_len, int rate_idx,
                                  int frame_idx_in_gop, int advance_state, void* d_yhat_out);
+/* Asynchronous variant: enqueues the decode on the handle's stream and
+ * returns; pswa_gpu_finish() waits and reports the status and bits. Handles
+ * on separate streams then overlap on one GPU (independent GOPs, BASELINE
+ * config 4). The temporal ring is not advanced. */
+int pswa_gpu_decode_frame_async(pswa_gpu* h, const void* d_hyper, size_t hyper_len,
+                                const void* d_main, size_t main_len, int rate_idx,
+                                int frame_idx_in_gop, void* d_yhat_out);
+int pswa_gpu_finish(pswa_gpu* h, double* bits_out /* [2], nullable */);
 /* Intermediate activations of the last forward_params call, for parity
  * triage: "ctx", "emb", "hq", "a" (fp32 / fp16 [H*W][d]) and "s1" (fp16, padded
  * hyper grid). *bytes gets the size; out may be NULL to query it. */
 int pswa_gpu_debug_fetch(pswa_gpu* h, const char* name, void* out, size_t cap, size_t* bytes);
 /* Number of kernels the last frame call launched (graph nodes included). */
 int pswa_gpu_last_launch_count(pswa_gpu* h);
+/* Replays one production launch of the last decode (warm, real operands)
+ * `reps` times between CUDA events on the handle's stream: "ctx_attn",
+ * "ctx_ffn_gu", "step_attn", "step_wq". us per launch and the launch's
+ * algorithmic FLOPs (mask-allowed keys only) feed bench.py's roofline. */
+int pswa_gpu_bench_op(pswa_gpu* h, const char* name, int reps, double* us_per_launch,
+                      double* flops_per_launch);
 /* Stream the handle runs on (cudaStream_t as void*). */
 void* pswa_gpu_stream(pswa_gpu* h);
 

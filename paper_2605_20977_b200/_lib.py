@@ -52,6 +52,9 @@ _SIGS = {
     "pswa_gpu_debug_fetch": (_I, [_VP, C.c_char_p, _VP, _SZ, C.POINTER(_SZ)]),
     "pswa_gpu_last_launch_count": (_I, [_VP]),
     "pswa_gpu_stream": (_VP, [_VP]),
+    "pswa_gpu_bench_op": (_I, [_VP, C.c_char_p, _I, _D, _D]),
+    "pswa_gpu_decode_frame_async": (_I, [_VP, _VP, _SZ, _VP, _SZ, _I, _I, _VP]),
+    "pswa_gpu_finish": (_I, [_VP, _D]),
     "pswa_gpu_op_gemm_f16": (_I, [_VP, _I, _I, _VP, _I, _I, _I, _VP, _I, _I, _I, _VP, _VP, _I,
                                   _I, _VP]),
     "pswa_gpu_op_rmsnorm": (_I, [_VP, _I, _I, _I, _I, _VP, _VP, _I, _VP]),

@@ -141,6 +141,16 @@ class GpuCodec:
         check(lib().pswa_gpu_decode_frame_device(self.h, d_hyper, hyper_len, d_main, main_len,
                                                  rate, fidx, int(advance), d_out))
 
+    def decode_async(self, d_hyper: int, hyper_len: int, d_main: int, main_len: int, rate: int,
+                     fidx: int, d_out: int):
+        check(lib().pswa_gpu_decode_frame_async(self.h, d_hyper, hyper_len, d_main, main_len,
+                                                rate, fidx, d_out))
+
+    def finish(self):
+        bits = np.zeros(2, np.float64)
+        check(lib().pswa_gpu_finish(self.h, bits.ctypes.data_as(C.POINTER(C.c_double))))
+        return bits
+
     def debug_fetch(self, name: str) -> np.ndarray:
         n = C.c_size_t()
         check(lib().pswa_gpu_debug_fetch(self.h, name.encode(), None, 0, C.byref(n)))
@@ -151,6 +161,12 @@ class GpuCodec:
 
     def last_launch_count(self) -> int:
         return lib().pswa_gpu_last_launch_count(self.h)
+
+    def bench_op(self, name: str, reps: int = 50) -> tuple[float, float]:
+        """(us per launch, algorithmic FLOPs per launch) of one production op."""
+        us, fl = C.c_double(), C.c_double()
+        check(lib().pswa_gpu_bench_op(self.h, name.encode(), reps, C.byref(us), C.byref(fl)))
+        return us.value, fl.value
 
     def stream(self) -> int:
         return lib().pswa_gpu_stream(self.h)

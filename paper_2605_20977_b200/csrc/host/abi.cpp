@@ -150,6 +150,25 @@ int pswa_gpu_decode_frame_device(pswa_gpu* h, const void* d_hyper, size_t hyper_
   });
 }
 
+int pswa_gpu_decode_frame_async(pswa_gpu* h, const void* d_hyper, size_t hyper_len,
+                                const void* d_main, size_t main_len, int rate_idx,
+                                int frame_idx_in_gop, void* d_yhat_out) {
+  return guard([&] {
+    h->eng->decode_async(d_hyper, hyper_len, d_main, main_len, rate_idx, frame_idx_in_gop,
+                         static_cast<int32_t*>(d_yhat_out));
+  });
+}
+
+int pswa_gpu_finish(pswa_gpu* h, double* bits_out) {
+  return guard([&] {
+    const auto r = h->eng->finish_async();
+    if (bits_out) {
+      bits_out[0] = r.bits[0];
+      bits_out[1] = r.bits[1];
+    }
+  });
+}
+
 int pswa_gpu_forward_params(pswa_gpu* h, const int32_t* yhat, const int32_t* zhat, int rate_idx,
                             int frame_idx_in_gop, float* mu_out, float* sigma_out,
                             double* bits_out) {
@@ -173,6 +192,10 @@ int pswa_gpu_debug_fetch(pswa_gpu* h, const char* name, void* out, size_t cap, s
 }
 
 int pswa_gpu_last_launch_count(pswa_gpu* h) { return h->eng->last_launches(); }
+
+int pswa_gpu_bench_op(pswa_gpu* h, const char* name, int reps, double* us, double* flops) {
+  return guard([&] { *us = h->eng->bench_op(name, reps, flops); });
+}
 
 void* pswa_gpu_stream(pswa_gpu* h) { return h->eng->stream(); }
 

@@ -581,6 +581,8 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
   const float* g1 = B.g1;
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, g1, bxn_, d, s); });
   gemm(P, bxn_, d, M, B.wq, d, f16_out(bq_, d));
+  const bool probe = &B == &s2_[0] && t == D.c.s - 1;  // bench_op probes (last step, S2 block 0)
+  if (probe) tag(P, "step_wq", 2.0 * M * d * d);
   if (!B.cross) {
     GemmEpi e = f16_out(B.kv_cache, 2 * d);
     e.row_map = rows;  // K/V of this step's positions into the frame cache
@@ -590,6 +592,7 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
   const int mk = B.cross ? 0 : 1;
   attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], taps_step_[t][mk], B.kv_cache, 0, 0,
             mk, B.pos, batt_);
+  if (probe) tag(P, "step_attn", attn_flops(t, mk, 0));
   gemm(P, batt_, d, M, B.wo, d, f32_acc(bx_, d));
   const float* g2 = B.g2;
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, g2, bxn_, d, s); });
@@ -621,11 +624,13 @@ void Engine::build_ctx(Program& P) {
     attention(P, ctx_q_, ctx_qinfo_ + q0, nq, last ? ctx_tiles_last_ : ctx_tiles_,
               last ? n_ctx_tiles_last_ : n_ctx_tiles_, taps_ctx_, kv, HWl_, D.c.win_t, 0, pos,
               ctx_att_);
+    if (b == 0) tag(P, "ctx_attn", attn_flops(-1, 0, 0));
     float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
     __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;
     gemm(P, ctx_att_, d, nq, B.wo, d, f32_acc(xq, d));
     add(P, [=](cudaStream_t s) { pswa_dev::rmsnorm_rows(xq, d, nullptr, nq, d, d, g2, xnq, d, s); });
     gemm(P, xnq, d, nq, B.wgu, d, swiglu_out(ctx_h_, D.fp));
+    if (b == 0) tag(P, "ctx_ffn_gu", 2.0 * nq * (2.0 * D.f) * d);
     gemm(P, ctx_h_, D.fp, nq, B.wd, D.fp, f32_acc(xq, d));
   }
   const float* last = ctx_x_ + static_cast<size_t>(T - 1) * HWo * d;
@@ -966,6 +971,57 @@ void Engine::run(Program& P) {
   launch_segment(P, 0);
 }
 
+// ------------------------------------------------------------ probes ------
+void Engine::tag(Program& P, const std::string& name, double flops) {
+  probes_[name] = {P.ops.back(), flops};
+}
+
+// Algorithmic attention FLOPs of one launch: 4 * d per (query, allowed key)
+// (QK^T and PV, 2 d each), counting in-grid, in-window, mask-allowed keys only
+// (SURVEY §8(d)). t < 0: the 3D context window over all T slots.
+double Engine::attn_flops(int t, int mask, int) const {
+  const Dims& D = D_;
+  const int rh = D.c.win_h / 2, rw = D.c.win_w / 2;
+  double keys = 0;
+  for (int y = B_.own0; y < B_.own0 + B_.nown; ++y)
+    for (int x = 0; x < D.W; ++x) {
+      const int gy = y + B_.lo;
+      if (t >= 0 && (gy + x) % D.c.s != t) continue;
+      int n = 0;
+      for (int ky = std::max(0, y - rh); ky <= std::min(B_.Hl - 1, y + rh); ++ky)
+        for (int kx = std::max(0, x - rw); kx <= std::min(D.W - 1, x + rw); ++kx) {
+          const int ks = (ky + B_.lo + kx) % D.c.s;
+          if (t >= 0 && ((mask == 1 && ks > t) || (mask == 2 && ks >= t))) continue;
+          ++n;
+        }
+      if (t >= 0) keys += n;
+      else
+        for (int j = 0; j < D.T; ++j) keys += static_cast<double>(n) * std::min(j + 1, D.c.win_t);
+    }
+  return 4.0 * D.d * keys;
+}
+
+double Engine::bench_op(const std::string& name, int reps, double* flops) {
+  auto it = probes_.find(name);
+  if (it == probes_.end())
+    throw std::invalid_argument("bench_op: unknown probe (run a decode first): " + name);
+  auto& op = it->second.first;
+  for (int i = 0; i < 3; ++i) op(st_);
+  cudaEvent_t a, b;
+  PSWA_CUDA(cudaEventCreate(&a));
+  PSWA_CUDA(cudaEventCreate(&b));
+  PSWA_CUDA(cudaEventRecord(a, st_));
+  for (int i = 0; i < reps; ++i) op(st_);
+  PSWA_CUDA(cudaEventRecord(b, st_));
+  PSWA_CUDA(cudaEventSynchronize(b));
+  float ms = 0;
+  PSWA_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (flops) *flops = it->second.second;
+  return 1e3 * ms / reps;  // us per launch
+}
+
 // ------------------------------------------------------------ band mode ---
 void Engine::cut(Program& P, bool global) {
   if (B_.n > 1) P.cuts.push_back(Cut{P.ops.size(), global});
@@ -1296,6 +1352,25 @@ FrameResult Engine::finish_decode(bool advance, int32_t* yhat_out, bool device) 
     advance_ring();
     PSWA_CUDA(cudaStreamSynchronize(st_));
   }
+  return r;
+}
+
+void Engine::decode_async(const void* d_hyper, size_t hyper_len, const void* d_main,
+                          size_t main_len, int rate, int fidx, int32_t* d_yhat_out) {
+  if (B_.n > 1) throw std::invalid_argument("decode_async: not for band handles");
+  prep_decode(d_hyper, hyper_len, d_main, main_len, rate, fidx, true);
+  run(program("decode"));
+  PSWA_CUDA(cudaMemcpyAsync(d_yhat_out, ychw_, sizeof(int32_t) * HWo_ * D_.C,
+                            cudaMemcpyDeviceToDevice, st_));
+}
+
+FrameResult Engine::finish_async() {
+  FrameResult r;
+  PSWA_CUDA(cudaMemcpyAsync(r.bits, bits_, sizeof(r.bits), cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaMemcpyAsync(&r.status, status_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+  if (r.status) throw pswa_abi::TruncatedError("corrupt or truncated payload (status " +
+                                               std::to_string(r.status) + ")");
   return r;
 }
 

@@ -132,6 +132,12 @@ class Engine {
   void prep_decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
                    int rate, int fidx, bool device);
   FrameResult finish_decode(bool advance, int32_t* yhat_out, bool device);
+  // Asynchronous device-resident decode (no host sync; ring not advanced):
+  // several handles on their own streams overlap on one GPU (GOP batches,
+  // BASELINE config 4). finish_async() syncs and checks the status.
+  void decode_async(const void* d_hyper, size_t hyper_len, const void* d_main, size_t main_len,
+                    int rate, int fidx, int32_t* d_yhat_out);
+  FrameResult finish_async();
   void prep_encode(const int32_t* yhat_chw_host, int rate, int fidx, const int32_t* zhat_in);
   FrameResult finish_encode(float* mu_out, float* sigma_out, uint8_t* hyper_out, size_t hyper_cap,
                             uint8_t* main_out, size_t main_cap, bool advance);
@@ -143,6 +149,13 @@ class Engine {
   int segments(const Program& P) const { return static_cast<int>(P.cuts.size()) + 1; }
   bool cut_global(const Program& P, int k) const { return P.cuts[k].global; }
   void launch_segment(Program& P, int k);
+
+  // Replays one production launch of the last-built decode program `reps`
+  // times on the handle's stream between CUDA events (warm, real operands):
+  // "ctx_attn" (context block 0 attention), "ctx_ffn_gu" (its SwiGLU gate|up
+  // GEMM), "step_attn" / "step_wq" (S2 block 0, last step). Returns us per
+  // launch; *flops = the algorithmic FLOPs of one launch.
+  double bench_op(const std::string& name, int reps, double* flops);
   // Debug taps (filled by forward_params): ctx, emb, hq, s1 (padded grid),
   // a, s2. Returns the byte size; copies when out != nullptr.
   size_t debug_fetch(const std::string& name, void* out, size_t cap);
@@ -166,6 +179,9 @@ class Engine {
   void build_step(Program& P, int t, int mode /*0 decode, 1 encode*/);
   void build_embed(Program& P, int t);
   void run(Program& P);
+  void tag(Program& P, const std::string& name, double flops);
+  double attn_flops(int t, int mask, int unused) const;
+  std::map<std::string, std::pair<std::function<void(cudaStream_t)>, double>> probes_;
   void set_frame_params(int rate, int fidx);
   void advance_ring();
   // band mode: push the halo rows of exchange buffer `id` (kind: step t in
