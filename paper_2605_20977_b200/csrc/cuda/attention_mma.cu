@@ -1,40 +1,44 @@
-// Tensor-core windowed attention (head_dim 32, 7x7 window): FlashAttention-2
-// style online softmax, QK^T and PV on the tensor cores (mma.sync m16n8k16,
-// fp16 operands, fp32 accumulate), masks evaluated in registers.
+// Tensor-core windowed attention (head_dim 32, 7x7 window), transposed
+// FlashAttention-2 formulation: per warp 8 queries, scores computed as
+// S^T = K . Q^T (keys on the MMA's M side, queries on N), probabilities moved
+// into the PV operand with movmatrix, O^T = V^T . P^T; mma.sync m16n8k16, fp16
+// operands, fp32 accumulation, masks and bias from a per-shape table.
 //
-// Work decomposition. A CTA owns a rectangle of query rows and stages the
-// K/V halo of the whole rectangle once per key slot into shared memory with
-// cp.async (zero-filled outside the grid, double-buffered across the slots of
-// the 3D context window). Each warp owns 16 queries whose windows lie in
-// RPW+6 consecutive halo rows, and walks only that band in 32-key chunks:
-//   * context (3D): warp = a 1x16 query strip, band = 7 x 22 keys per slot;
-//   * step batches (2D): warp = the 16 step-t positions of a 4x16 block,
-//     band = 10 x 22 keys.
-// 32-44% of the scanned scores are in-window. 128-row tcgen05 tiles would
-// scan >= 14x22 keys per slot for the same queries (16% useful), so this
-// operator uses warp-level MMA; every dense projection is on tcgen05.
+// Why transposed. m16n8k16 needs 16 rows on M but only 8 columns on N. With
+// the keys on M, a warp owns 8 queries, which fit in a compact 2x4 block
+// (context) or the 8 step-t positions of a 4x8 block (step batches). The key
+// union a warp scans shrinks accordingly:
+//   * context, 2x4 queries: an 8x10 band, 80 keys per slot for 49 in-window
+//     (61%; the previous 1x16-strip, 16-query layout scanned 160);
+//   * step batches: a 10x14 band, keys sorted by wavefront step class so the
+//     masked classes (<= t for S1/S2 self, < t for the
+//     accumulator) are never scanned: step 0 scans 48 keys, not 140.
+// Work is a list of CTA tiles x head groups: the CTA walks (head, slot)
+// stages; each stage's K/V halo of its query rectangle is one pair of 4D TMA
+// boxes (zero-filled outside the grid, SWIZZLE_128B) issued by one thread
+// and double-buffered so the next halo loads while this one is consumed.
+// Each warp walks only its band, in 16-key chunks, two passes per slot
+// (scores + max, then exp + PV) so the softmax reductions happen once per
+// slot rather than once per chunk.
 //
 // Semantics match SPEC.md:221-256 and the oracle: out-of-grid keys are
-// masked (not padded), step masks <= / < per wavefront.h:34-43, the learned
-// per-offset bias is added to the scaled score, softmax in fp32, a query
-// with no allowed key outputs zeros.
+// masked (not padded), the learned per-offset bias is added to the scaled
+// score, softmax in fp32, a query with no allowed key outputs zeros.
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 
 #include "check.h"
 #include "kernels.h"
 #include "launch.cuh"
+#include "ptx.cuh"
 
 namespace pswa_dev {
 
 namespace {
 
-constexpr int kHD = 32;     // head dim handled by this kernel
-constexpr int kHaloW = 22;  // 16 query columns + 2*3 window margin
-constexpr int kChunk = 32;
+constexpr int kHD = 32;  // head dim handled by this kernel
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kMaxBandKeys = 224;  // 10 x 22 band rounded to the 32-key chunk
-constexpr int kTblStride = 20;     // floats per band key: 16 queries + pad (conflict-free LDS)
 
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
@@ -53,255 +57,295 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
-                                        uint32_t& r3) {
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(addr));
 }
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
-                                          uint32_t& r3) {
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(addr));
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes)
-               : "memory");
+// 8x8 b16 transpose across the warp (C-fragment layout in, transposed out)
+__device__ __forceinline__ uint32_t movtrans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// byte offset of (key, 16 B chunk) in a [key][32 halves] tile, chunk
-// XOR-swizzled by (key >> 1) & 3: conflict-free ldmatrix over 8 keys.
-__device__ __forceinline__ uint32_t sw(int key, int chunk) {
-  return static_cast<uint32_t>(key * 64 + ((chunk ^ ((key >> 1) & 3)) << 4));
+// Byte offset of (halo key, 16 B chunk) in a [key][32 halves] halo buffer
+// written by TMA with SWIZZLE_64B (64 B rows): address bits [4:5] ^= bits
+// [7:8]. With the band orders used (column-major context bands over a
+// 23-wide halo, step-class-sorted bands over a 24-wide halo) the 8 rows of an
+// ldmatrix phase land on distinct 16 B bank groups (context) or at most
+// 2-way (steps).
+__device__ __forceinline__ uint32_t swz(int key, int chunk) {
+  const uint32_t off = static_cast<uint32_t>(key * 64 + chunk * 16);
+  return off ^ (((off >> 7) & 3u) << 4);
 }
 
 struct AttnArgs {
   const __half* q;
   int ldq;
-  const int32_t* qinfo;
   const int32_t* tiles;
-  int ntiles;
-  const __half* kv;
-  int ldkv, kv_slot_stride, H, W, wt, mask, s, d;
-  const float* bias;
+  int d;
+  int wt;  // > 0: 3D context window over wt slots
+  const float* tables;  // [heads][nsl][nbk][8] score offsets (build_score_tables)
+  int nsl;              // slot offsets per head in `tables` (wt for 3D, 1 for 2D)
   __half* out;
   int ldo;
-  int halo_keys;  // staged keys per slot buffer (>= halo rows * 22, multiple of 32, + slack)
-  const int8_t* taps;  // [band keys (chunk-padded)][16 queries]: tap index or -1 (masked)
-  int dbuf;            // double-buffer the slot halos (3D); 0 = stage each slot in place
+  AttnShape shape;
+  int hw;      // halo width (keys per halo row)
+  int kbuf;    // bytes of one K (or V) halo buffer (1024-aligned)
+  int dbuf;    // double-buffer the (head, slot) halos
+  int hpc;     // heads per CTA (pipelined)
 };
 
-__global__ void __launch_bounds__(256) window_attn_mma_kernel(const AttnArgs a) {
-  pdl_wait();
-  pdl_trigger();
-  extern __shared__ __align__(128) uint8_t smem[];
+template <int NCH>
+__global__ void __launch_bounds__(256, NCH <= 5 ? 3 : 2)
+    window_attn_t8_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap kvmap) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = blockIdx.y;
+  const int h0 = blockIdx.y * a.hpc;  // this CTA's heads: [h0, h0 + hpc)
   const int32_t* T = a.tiles + blockIdx.x * kAttnTileInts;
-  const int hy0 = T[0], hx0 = T[1], HR = T[2], RPW = T[3], sl = T[4];
-  const int taps_total = a.wt > 0 ? a.wt * 49 : 49;
+  const int hy0 = T[0], hx0 = T[1], HR = T[2], sl = T[3], nw = T[4];
   const int nslots = a.wt > 0 ? min(sl + 1, a.wt) : 1;
   const int j0 = sl - nslots + 1;
-  const int kbuf = a.halo_keys * kHD * 2;  // bytes of one K (or V) buffer
-  float* sbias = reinterpret_cast<float*>(smem + (a.wt > 0 && a.dbuf ? 4 : 2) * kbuf);
-  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int nstages = a.hpc * nslots;  // pipeline over (head, slot)
+  const int nbuf = a.dbuf ? 2 : 1;
+  const uint32_t sraw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;  // swizzled TMA boxes: 1024 B aligned
+  uint8_t* smem = smem_raw + (sbase - sraw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + nbuf * 2 * a.kbuf);  // [2] stage-full barriers
+  float* stbl0 = reinterpret_cast<float*>(bars + 2);  // [nbuf][kAttnMaxBandKeys][8] score offsets
+  int16_t* sbk = reinterpret_cast<int16_t*>(stbl0 + 2 * kAttnMaxBandKeys * 8);  // band key: row<<8 | col
+  const int nbk = a.shape.nbk;
+  const uint32_t box_bytes = static_cast<uint32_t>(HR * a.hw * 64);
+  const uint32_t tbl_bytes = static_cast<uint32_t>(nbk * 8 * 4);
+  const CUtensorMap* kvm = &kvmap;  // param-space address (never copied to local memory)
 
-  const int band_keys = (RPW + 6) * kHaloW;
-  const int nchunks = (band_keys + kChunk - 1) / kChunk;
-  const int nbk = nchunks * kChunk;
-  // per-slot score-offset table [band key][kTblStride]: log2e * bias of the
-  // (key, query) window tap, -inf where the window / step mask excludes it
-  float* stbl = sbias + 256;
-  uint8_t* skv = reinterpret_cast<uint8_t*>(stbl + kMaxBandKeys * kTblStride);  // [halo_keys]
-
-  // ---- stage the bias row of this head (pre-scaled by log2 e) and the
-  // per-key in-grid flags
-  for (int i = threadIdx.x; i < taps_total; i += blockDim.x)
-    sbias[i] = a.bias[h * taps_total + i] * kLog2e;
-  const int hkeys = HR * kHaloW;
-  for (int key = threadIdx.x; key < a.halo_keys; key += blockDim.x) {
-    const int ky = hy0 + key / kHaloW, kx = hx0 + key % kHaloW;
-    skv[key] = key < hkeys && ky >= 0 && ky < a.H && kx >= 0 && kx < a.W;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    tma_prefetch(kvm);
   }
+  // the band keys are constants: safe to read before the PDL wait
+  for (int i = threadIdx.x; i < nbk; i += blockDim.x) sbk[i] = a.shape.bkey[i];
+  pdl_wait();  // K/V and Q come from the previous kernels
+  pdl_trigger();
+  __syncthreads();
 
-  auto stage = [&](int j, int buf) {
-    const uint32_t kb = sbase + buf * 2 * kbuf, vb = kb + kbuf;
-    for (int idx = threadIdx.x; idx < a.halo_keys * 4; idx += blockDim.x) {
-      const int key = idx >> 2, ch = idx & 3;
-      const int ky = hy0 + key / kHaloW, kx = hx0 + key % kHaloW;
-      const bool ok = key < hkeys && ky >= 0 && ky < a.H && kx >= 0 && kx < a.W;
-      const __half* src = a.kv + (ok ? static_cast<size_t>(j * a.kv_slot_stride + ky * a.W + kx) * a.ldkv +
-                                           h * kHD + ch * 8
-                                     : 0);
-      cp_async16(kb + sw(key, ch), src, ok ? 16 : 0);
-      cp_async16(vb + sw(key, ch), src + (ok ? a.d : 0), ok ? 16 : 0);
+  // one elected thread stages (head h, slot j): two 4D TMA boxes (K, V) and
+  // the (head, slot offset) score-offset table, on one mbarrier
+  auto stage = [&](int h, int j, int buf) {
+#ifdef PSWA_ATTN_DEBUG
+    if (threadIdx.x == 0 && blockIdx.x < 2 && blockIdx.y == 0)
+      printf("blk %d h %d j %d buf %d sraw %u sbase %u kbuf %d box %u HR %d hw %d hx0 %d hy0 %d dyn %u\n", blockIdx.x, h, j, buf, sraw, sbase, a.kbuf, box_bytes, HR, a.hw, hx0, hy0, 0u);
+#endif
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();  // prior ldmatrix reads of this buffer before the overwrite
+      const uint32_t kb = sbase + buf * 2 * a.kbuf;
+      mbar_expect_tx(&bars[buf], 2 * box_bytes + tbl_bytes);
+      tma_load_4d(kb, kvm, &bars[buf], h * kHD, hx0, hy0, j);
+      tma_load_4d(kb + a.kbuf, kvm, &bars[buf], a.d + h * kHD, hx0, hy0, j);
+      const int so = a.wt > 0 ? j - sl + a.wt - 1 : 0;
+      if (tbl_bytes)
+        bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(stbl0 + buf * kAttnMaxBandKeys * 8)),
+                  a.tables + (static_cast<size_t>(h) * a.nsl + so) * nbk * 8, tbl_bytes, &bars[buf]);
     }
-    cp_commit();
   };
-  stage(j0, 0);
+  uint32_t phase = 0;  // bit b: parity of the next completion of bars[b]
+  auto wait_buf = [&](int buf) {
+    mbar_wait(&bars[buf], (phase >> buf) & 1u);
+    phase ^= 1u << buf;
+  };
+  stage(h0, j0, 0);
 
-  // ---- my 16 queries: fragment rows r0 = lane/4, r1 = r0 + 8
-  const int32_t* Q = T + 8 + warp * 16;
-  const int r0 = lane >> 2;
-  const int qr[2] = {warp < T[5] ? Q[r0] : -1, warp < T[5] ? Q[r0 + 8] : -1};
-  uint32_t qa[2][4];
-  {
-    const int kc = (lane & 3) * 2;
+  const int32_t* Wd = T + 8 + warp * 10;
+  const int br = warp < nw ? Wd[0] : 0, bc = warp < nw ? Wd[1] : 0;  // band origin in the halo
+  const int qrow = warp < nw ? Wd[2 + (lane >> 2)] : -1;  // query n = lane/4 (B-operand column)
+  const bool live = __any_sync(0xffffffffu, qrow >= 0);
+
+  // per-lane ldmatrix row keys (K: non-transposed A operand; V: transposed,
+  // read per chunk) and the in-grid bits of the two score rows per chunk
+  const int nch = nbk / 16;
+  auto halo_key = [&](int bk) {
+    const int v = sbk[bk];
+    return (br + (v >> 8)) * a.hw + bc + (v & 255);
+  };
+  int hk[NCH], hv[NCH];
+  uint32_t inb = 0;
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks)
+  for (int c = 0; c < NCH; ++c) {
+    hk[c] = hv[c] = 0;
+    if (c < nch) {
+      hk[c] = halo_key(c * 16 + (lane & 7) + ((lane >> 3) & 1) * 8);
+      hv[c] = halo_key(c * 16 + (lane & 7) + ((lane >> 4) & 1) * 8);
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const __half* qp = a.q + static_cast<size_t>(qr[i] < 0 ? 0 : qr[i]) * a.ldq + h * kHD + ks * 16 + kc;
-        qa[ks][i] = qr[i] >= 0 ? *reinterpret_cast<const uint32_t*>(qp) : 0u;
-        qa[ks][i + 2] = qr[i] >= 0 ? *reinterpret_cast<const uint32_t*>(qp + 8) : 0u;
+      for (int rr = 0; rr < 2; ++rr) {
+        const int v = sbk[c * 16 + (lane >> 2) + 8 * rr];
+        const int ky = hy0 + br + (v >> 8), kx = hx0 + bc + (v & 255);
+        if (ky >= 0 && ky < a.shape.H && kx >= 0 && kx < a.shape.W) inb |= 1u << (2 * c + rr);
       }
+    }
   }
-  const bool live = __any_sync(0xffffffffu, qr[0] >= 0 || qr[1] >= 0);
-  const float qscale = 0.17677669529663687f * kLog2e;  // log2(e) / sqrt(32)
-  const int key0 = warp * RPW * kHaloW;  // first key of my band in the CTA halo
+  const int qc = (lane & 3) * 2;                         // my two query columns in C fragments
+  const float qscale = 0.17677669529663687f * kLog2e;    // log2(e) / sqrt(32)
+  uint32_t qb[2][2];
+  float o[2][4];
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
 
-  float o[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) o[i][e] = 0.0f;
-  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.0f, 0.0f};
-
-  for (int js = 0; js < nslots; ++js) {
-    const int j = j0 + js, buf = a.dbuf ? (js & 1) : 0;
-    if (!a.dbuf && js > 0) stage(j, 0);  // previous slot fully consumed (barrier below)
-    if (a.dbuf && js + 1 < nslots) {
-      stage(j + 1, buf ^ 1);  // prefetch the next slot's halo
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
+  int hi = 0, js = 0;  // stage st = (head h0 + hi, slot j0 + js)
+  for (int st = 0; st < nstages; ++st) {
+    const int h = h0 + hi, j = j0 + js;
+    const int buf = nbuf == 2 ? (st & 1) : 0;
+    if (nbuf == 1 && st > 0) stage(h, j, 0);  // previous stage fully consumed (barrier below)
+    if (nbuf == 2 && st + 1 < nstages) {
+      const bool wrap = js + 1 == nslots;  // prefetch the next (head, slot) halo
+      stage(wrap ? h + 1 : h, wrap ? j0 : j + 1, buf ^ 1);
     }
-    // score-offset table of this slot (the bias slice depends on the slot)
-    {
-      const float* sb = sbias + (a.wt > 0 ? (j - sl + a.wt - 1) * 49 : 0);
-      if (js > 0) __syncthreads();  // previous slot's readers are done
-      for (int i = threadIdx.x; i < nbk * 16; i += blockDim.x) {
-        const int tap = a.taps[i];
-        stbl[(i >> 4) * kTblStride + (i & 15)] = tap >= 0 ? sb[tap] : -INFINITY;
+    if (js == 0) {  // new head: my queries' fragments, fresh softmax state
+      const __half* qp = a.q + static_cast<size_t>(qrow < 0 ? 0 : qrow) * a.ldq + h * kHD + qc;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        qb[ks][0] = qrow >= 0 ? *reinterpret_cast<const uint32_t*>(qp + ks * 16) : 0u;
+        qb[ks][1] = qrow >= 0 ? *reinterpret_cast<const uint32_t*>(qp + ks * 16 + 8) : 0u;
       }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[i][e] = 0.0f;
+      m0 = m1 = -INFINITY;
+      l0 = l1 = 0.0f;
     }
-    __syncthreads();
-    const uint32_t sK = sbase + buf * 2 * kbuf, sV = sK + kbuf;
+    wait_buf(buf);  // halo and score-offset table of this stage landed
+    const uint32_t sK = sbase + buf * 2 * a.kbuf, sV = sK + a.kbuf;
+    const float* stbl = stbl0 + buf * kAttnMaxBandKeys * 8;
     if (live) {
-      for (int c = 0; c < nchunks; ++c) {
-        float sacc[4][4];
+      // pass 1: scores and their per-query max over this slot
+      float s[NCH][4];
+      float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) sacc[nt][e] = 0.0f;
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4(sK + sw(key0 + c * kChunk + nt * 8 + (lane & 7), lane >> 3), b0, b1, b2, b3);
-          mma16816(sacc[nt], qa[0], b0, b1);
-          mma16816(sacc[nt], qa[1], b2, b3);
+      for (int c = 0; c < NCH; ++c) {
+        if (c < nch) {
+          float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          uint32_t fa[4];
+          ldsm_x4(sK + swz(hk[c], lane >> 4), fa);
+          mma16816(acc, fa, qb[0][0], qb[0][1]);
+          ldsm_x4(sK + swz(hk[c], (lane >> 4) + 2), fa);
+          mma16816(acc, fa, qb[1][0], qb[1][1]);
+          const int r0 = c * 16 + (lane >> 2);
+          const float2 t0 = *reinterpret_cast<const float2*>(stbl + r0 * 8 + qc);
+          const float2 t1 = *reinterpret_cast<const float2*>(stbl + (r0 + 8) * 8 + qc);
+          const bool k0 = (inb >> (2 * c)) & 1u, k1 = (inb >> (2 * c + 1)) & 1u;
+          s[c][0] = k0 ? fmaf(acc[0], qscale, t0.x) : -INFINITY;
+          s[c][1] = k0 ? fmaf(acc[1], qscale, t0.y) : -INFINITY;
+          s[c][2] = k1 ? fmaf(acc[2], qscale, t1.x) : -INFINITY;
+          s[c][3] = k1 ? fmaf(acc[3], qscale, t1.y) : -INFINITY;
+          mx0 = fmaxf(mx0, fmaxf(s[c][0], s[c][2]));
+          mx1 = fmaxf(mx1, fmaxf(s[c][1], s[c][3]));
         }
-        // window / step mask and bias from the tile-shape tap table
-        float cmax[2] = {-INFINITY, -INFINITY};
+      }
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+      for (int off = 4; off < 32; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float al0 = mn0 == -INFINITY ? 1.0f : ex2(m0 - mn0);  // ex2(-inf) = 0
+      const float al1 = mn1 == -INFINITY ? 1.0f : ex2(m1 - mn1);
+      m0 = mn0;
+      m1 = mn1;
+      // exp offsets: a query with no allowed key yet keeps m = -inf; use 0
+      // so that ex2(-inf - 0) = 0 instead of NaN
+      const float ms0 = mn0 == -INFINITY ? 0.0f : mn0, ms1 = mn1 == -INFINITY ? 0.0f : mn1;
+      l0 *= al0;
+      l1 *= al1;
 #pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            const int bk = c * kChunk + nt * 8 + (lane & 3) * 2 + b;
-            const bool kin = skv[key0 + bk] != 0;
-            const float* trow = stbl + bk * kTblStride + r0;
+      for (int mt = 0; mt < 2; ++mt) {
+        o[mt][0] *= al0;
+        o[mt][1] *= al1;
+        o[mt][2] *= al0;
+        o[mt][3] *= al1;
+      }
+      // pass 2: probabilities (fp16) and O^T += V^T P^T
 #pragma unroll
-            for (int ri = 0; ri < 2; ++ri) {
-              const int e = ri * 2 + b;
-              const float v = kin ? fmaf(sacc[nt][e], qscale, trow[8 * ri]) : -INFINITY;
-              sacc[nt][e] = v;
-              cmax[ri] = fmaxf(cmax[ri], v);
-            }
-          }
-        float alpha[2];
+      for (int c = 0; c < NCH; ++c) {
+        if (c < nch) {
+          const float p0 = ex2(s[c][0] - ms0), p1 = ex2(s[c][1] - ms1);
+          const float p2 = ex2(s[c][2] - ms0), p3 = ex2(s[c][3] - ms1);
+          l0 += p0 + p2;
+          l1 += p1 + p3;
+          const uint32_t b0 = movtrans(pack_h2(p0, p1)), b1 = movtrans(pack_h2(p2, p3));
 #pragma unroll
-        for (int ri = 0; ri < 2; ++ri) {
-          cmax[ri] = fmaxf(cmax[ri], __shfl_xor_sync(0xffffffffu, cmax[ri], 1));
-          cmax[ri] = fmaxf(cmax[ri], __shfl_xor_sync(0xffffffffu, cmax[ri], 2));
-          const float mn = fmaxf(m[ri], cmax[ri]);
-          alpha[ri] = mn == -INFINITY ? 1.0f : ex2(m[ri] - mn);  // ex2(-inf) = 0
-          m[ri] = mn;
-        }
-        float rs[2] = {0.0f, 0.0f};
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int ri = e >> 1;
-            const float p = sacc[nt][e] == -INFINITY ? 0.0f : ex2(sacc[nt][e] - m[ri]);
-            sacc[nt][e] = p;
-            rs[ri] += p;
-          }
-#pragma unroll
-        for (int ri = 0; ri < 2; ++ri) {
-          rs[ri] += __shfl_xor_sync(0xffffffffu, rs[ri], 1);
-          rs[ri] += __shfl_xor_sync(0xffffffffu, rs[ri], 2);
-          l[ri] = l[ri] * alpha[ri] + rs[ri];
-        }
-#pragma unroll
-        for (int nd = 0; nd < 4; ++nd) {
-          o[nd][0] *= alpha[0];
-          o[nd][1] *= alpha[0];
-          o[nd][2] *= alpha[1];
-          o[nd][3] *= alpha[1];
-        }
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          uint32_t pa[4];
-          pa[0] = pack_h2(sacc[2 * kk][0], sacc[2 * kk][1]);
-          pa[1] = pack_h2(sacc[2 * kk][2], sacc[2 * kk][3]);
-          pa[2] = pack_h2(sacc[2 * kk + 1][0], sacc[2 * kk + 1][1]);
-          pa[3] = pack_h2(sacc[2 * kk + 1][2], sacc[2 * kk + 1][3]);
-          const int mi = lane >> 3;
-          const int key = key0 + c * kChunk + kk * 16 + (mi & 1) * 8 + (lane & 7);
-#pragma unroll
-          for (int nd = 0; nd < 4; nd += 2) {
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(sV + sw(key, nd + (mi >> 1)), b0, b1, b2, b3);
-            mma16816(o[nd], pa, b0, b1);
-            mma16816(o[nd + 1], pa, b2, b3);
+          for (int mt = 0; mt < 2; ++mt) {
+            uint32_t fv[4];
+            ldsm_x4_t(sV + swz(hv[c], ((lane >> 3) & 1) + 2 * mt), fv);
+            mma16816(o[mt], fv, b0, b1);
           }
         }
       }
-    }
-    __syncthreads();  // buffer `buf` is refilled two slots later
-  }
-  if (!live) return;
-  const float inv0 = l[0] > 0.0f ? 1.0f / l[0] : 0.0f;
-  const float inv1 = l[1] > 0.0f ? 1.0f / l[1] : 0.0f;
+      if (js == nslots - 1) {  // head done: normalise and store
+        float t0 = l0, t1 = l1;
 #pragma unroll
-  for (int nd = 0; nd < 4; ++nd) {
-    const int col = h * kHD + nd * 8 + (lane & 3) * 2;
-    if (qr[0] >= 0)
-      *reinterpret_cast<uint32_t*>(a.out + static_cast<size_t>(qr[0]) * a.ldo + col) =
-          pack_h2(o[nd][0] * inv0, o[nd][1] * inv0);
-    if (qr[1] >= 0)
-      *reinterpret_cast<uint32_t*>(a.out + static_cast<size_t>(qr[1]) * a.ldo + col) =
-          pack_h2(o[nd][2] * inv1, o[nd][3] * inv1);
+        for (int off = 4; off < 32; off <<= 1) {
+          t0 += __shfl_xor_sync(0xffffffffu, t0, off);
+          t1 += __shfl_xor_sync(0xffffffffu, t1, off);
+        }
+        const float inv0 = t0 > 0.0f ? 1.0f / t0 : 0.0f;
+        const float inv1 = t1 > 0.0f ? 1.0f / t1 : 0.0f;
+        // O^T blocks (8 dims x 8 queries) -> row-major O rows via movmatrix
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int hb = 0; hb < 2; ++hb) {
+            const uint32_t v = movtrans(pack_h2(o[mt][2 * hb] * inv0, o[mt][2 * hb + 1] * inv1));
+            if (qrow >= 0)
+              *reinterpret_cast<uint32_t*>(a.out + static_cast<size_t>(qrow) * a.ldo + h * kHD +
+                                           mt * 16 + hb * 8 + (lane & 3) * 2) = v;
+          }
+      }
+    }
+    __syncthreads();  // buffer `buf` (halo + table) is rewritten by a later stage
+    if (++js == nslots) {
+      js = 0;
+      ++hi;
+    }
   }
 }
 
-// Double-buffering the 3D slot halos overlaps staging with compute but halves
-// the CTAs per SM; measured slower (3.68 vs 3.42 ms / frame), so off unless
-// PSWA_ATTN_DBUF=1.
-bool attn_dbuf() {
-  static const bool on = std::getenv("PSWA_ATTN_DBUF") != nullptr;
-  return on;
+// Per-shape launch policy: heads per CTA (their halos pipelined through
+// two buffers) and double buffering. PSWA_ATTN_HPC / PSWA_ATTN_DBUF override
+// for experiments.
+int env_int(const char* n, int dflt) {
+  const char* e = std::getenv(n);
+  return e ? std::atoi(e) : dflt;
 }
 
-int smem_bytes(int halo_keys, bool three_d) {
-  // K/V buffers + bias (256 floats) + score-offset table + key flags
-  return (three_d && attn_dbuf() ? 4 : 2) * halo_keys * kHD * 2 + 256 * 4 +
-         kMaxBandKeys * kTblStride * 4 + halo_keys;
+int box_buf_bytes(int halo_keys) { return (halo_keys * 64 + 1023) / 1024 * 1024; }
+
+int smem_bytes(int halo_keys, int dbuf) {
+  // alignment slack + K/V buffers + barriers + 2 score-offset tables + band keys
+  return 1024 + (dbuf ? 4 : 2) * box_buf_bytes(halo_keys) + 16 + 2 * kAttnMaxBandKeys * 8 * 4 +
+         kAttnMaxBandKeys * 2;
+}
+
+__global__ void score_table_kernel(const float* __restrict__ bias, int taps_total, const int8_t* __restrict__ taps,
+                                   int n, int nsl, float* __restrict__ out) {
+  // out[h][k][i] = log2e * bias[h][k*49 + taps[i]] or -inf (i < n = nbk*8)
+  const int h = blockIdx.y, k = blockIdx.z;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int t = taps[i];
+    out[(static_cast<size_t>(h) * nsl + k) * n + i] = t >= 0 ? bias[h * taps_total + k * 49 + t] * kLog2e : -INFINITY;
+  }
+}
+
+template <int NCH>
+void launch_t8(const AttnArgs& a, const CUtensorMap& map, int halo_keys, int ntiles, int heads,
+               int warps, cudaStream_t st) {
+  launch_k(window_attn_t8_kernel<NCH>, dim3(ntiles, heads / a.hpc), dim3(warps * 32),
+           smem_bytes(halo_keys, a.dbuf), st, a, map);
 }
 
 }  // namespace
@@ -310,32 +354,39 @@ bool window_attention_tiles_supported(int hd, int win_h, int win_w) {
   return hd == kHD && win_h == 7 && win_w == 7;
 }
 
-int window_attention_halo_keys(int halo_rows) {
-  // staged keys: whole halo rounded to chunks, plus one chunk of slack for the
-  // last warp's band overrun (those keys are masked)
-  return (halo_rows * kHaloW + kChunk - 1) / kChunk * kChunk + kChunk;
+int window_attention_tiles_smem(int halo_keys, bool) { return smem_bytes(halo_keys, 1); }
+
+void build_score_tables(const float* bias, int heads, int wt, AttnShape shape, float* out,
+                        cudaStream_t st) {
+  const int nsl = wt > 0 ? wt : 1, n = shape.nbk * 8;
+  if (n == 0) return;
+  score_table_kernel<<<dim3((n + 255) / 256, heads, nsl), 256, 0, st>>>(bias, nsl * 49, shape.taps, n,
+                                                                       nsl, out);
+  PSWA_LAUNCH_CHECK();
 }
 
 void window_attention_tiles_init(int max_smem_bytes) {
-  PSWA_CUDA(cudaFuncSetAttribute(window_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PSWA_CUDA(cudaFuncSetAttribute(window_attn_t8_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 max_smem_bytes));
+  PSWA_CUDA(cudaFuncSetAttribute(window_attn_t8_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  max_smem_bytes));
 }
 
-int window_attention_tiles_smem(int halo_rows, bool three_d) {
-  return smem_bytes(window_attention_halo_keys(halo_rows), three_d);
-}
-
-void window_attention_tiles(const __half* q, int ldq, const int32_t* qinfo, const int32_t* tiles,
-                            int ntiles, int warps_per_tile, int halo_rows, const int8_t* taps,
-                            const __half* kv, int ldkv, int kv_slot_stride, int H, int W,
-                            int heads, int wt, int mask, int s, const float* bias, __half* out,
-                            int ldo, cudaStream_t st) {
+void window_attention_tiles(const __half* q, int ldq, const int32_t* tiles, int ntiles,
+                            int warps_per_tile, int halo_rows, int halo_width, AttnShape shape,
+                            const CUtensorMap& kv_map, int heads, int wt, const float* tables,
+                            __half* out, int ldo, cudaStream_t st) {
   if (ntiles <= 0) return;
-  AttnArgs a{q, ldq, qinfo, tiles, ntiles, kv, ldkv, kv_slot_stride, H, W, wt, mask, s,
-             heads * kHD, bias, out, ldo, window_attention_halo_keys(halo_rows), taps,
-             attn_dbuf() ? 1 : 0};
-  dim3 grid(ntiles, heads);
-  launch_k(window_attn_mma_kernel, grid, dim3(warps_per_tile * 32), smem_bytes(a.halo_keys, wt > 0), st, a);
+  if (shape.nbk % 16 || shape.nbk > kAttnMaxBandKeys) throw std::invalid_argument("attention shape");
+  static const int hpc3 = env_int("PSWA_ATTN_HPC", 2), hpc2 = env_int("PSWA_ATTN_HPC2", 1);
+  static const int dbuf3 = env_int("PSWA_ATTN_DBUF", 1), dbuf2 = env_int("PSWA_ATTN_DBUF2", 0);
+  int hpc = wt > 0 ? hpc3 : hpc2;
+  while (heads % hpc) --hpc;
+  const int hk = halo_rows * halo_width;
+  AttnArgs a{q, ldq, tiles, heads * kHD, wt, tables, wt > 0 ? wt : 1, out, ldo, shape, halo_width,
+             box_buf_bytes(hk), wt > 0 ? dbuf3 : dbuf2, hpc};
+  if (shape.nbk <= 80) launch_t8<5>(a, kv_map, hk, ntiles, heads, warps_per_tile, st);
+  else launch_t8<9>(a, kv_map, hk, ntiles, heads, warps_per_tile, st);
   PSWA_LAUNCH_CHECK();
 }
 

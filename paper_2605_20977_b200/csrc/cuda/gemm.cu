@@ -405,6 +405,22 @@ void launch(const GemmPlan& p, int kind, cudaStream_t st) {
 
 }  // namespace
 
+void make_kv_tmap(CUtensorMap* m, const __half* kv, int ld, int W, int H, int slots,
+                  long slot_stride_rows, int box_w, int box_h) {
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(W),
+                        static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(slots)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld) * 2, static_cast<cuuint64_t>(W) * ld * 2,
+                           static_cast<cuuint64_t>(slot_stride_rows) * ld * 2};
+  cuuint32_t box[4] = {32, static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half*>(kv), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw CudaError("cuTensorMapEncodeTiled (kv) failed (code " + std::to_string(int(r)) + ")");
+}
+
 void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, int ldb, int N,
                int K, const GemmEpi& epi, int force_bn) {
   if (K % kBK != 0 || N % 64 != 0 || lda % 8 != 0 || ldb % 8 != 0 || M <= 0)

@@ -47,6 +47,11 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
                int K, const GemmEpi& epi, int force_bn = 0);
 void gemm_run(const GemmPlan& p, cudaStream_t stream);
 
+// TMA map of a frame K/V cache [slots][H][W][ld] fp16 for the attention halo
+// loads: box = 32 channels (one head) x box_w x box_h x 1 slot, SWIZZLE_64B.
+void make_kv_tmap(CUtensorMap* m, const __half* kv, int ld, int W, int H, int slots,
+                  long slot_stride_rows, int box_w, int box_h);
+
 // Number of kernel launches gemm_run issues (always 1); used by launch accounting.
 constexpr int kGemmLaunches = 1;
 

@@ -1,5 +1,6 @@
 // Launchers for the non-GEMM sm_100a kernels of the decode path.
 #pragma once
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -59,26 +60,34 @@ void window_attention(const __half* q, int ldq, const int32_t* qinfo, int Mq, co
                       int win_w, int win_t, int mask, int s, const float* bias, __half* out,
                       int ldo, cudaStream_t st);
 
-// Tensor-core variant (attention_mma.cu) for head_dim 32 and 7x7 windows.
-// Work is a list of CTA tiles, kAttnTileInts ints each: [0] halo top row,
-// [1] halo left col (halo is 22 columns wide), [2] halo rows, [3] query rows
-// per warp (RPW; warp w's band is halo rows [w*RPW, w*RPW+RPW+6)), [4] query
-// slot, [5] warps with queries, [8 + 16*w + i] query row i of warp w (-1 =
-// none). Every query of warp w must lie in halo rows [w*RPW+3, w*RPW+RPW+3)
-// and halo columns [3, 19). Same contract as window_attention otherwise.
-constexpr int kAttnTileInts = 8 + 16 * 8;
+// Tensor-core variant (attention_mma.cu) for head_dim 32 and 7x7 windows:
+// warps of 8 queries, keys on the MMA's M side. Work is a list of CTA tiles,
+// kAttnTileInts ints each: [0] halo top row, [1] halo left col, [2] halo
+// rows, [3] query slot, [4] warps with queries, then per warp w at
+// [8 + 10w]: band origin (row, col) inside the halo and 8 query rows of q /
+// out (-1 = none). All warps of a launch share one band shape:
+constexpr int kAttnTileInts = 8 + 10 * 16;
+constexpr int kAttnMaxBandKeys = 144;
+struct AttnShape {
+  const int8_t* taps;   // [nbk][8]: window tap (dy+3)*7+(dx+3) of (band key, query), -1 = excluded
+  const int16_t* bkey;  // [nbk]: band key -> row << 8 | col relative to the band origin
+  int nbk;              // band keys scanned (multiple of 16, <= kAttnMaxBandKeys; 0 = none)
+  int H, W;             // key grid bounds (keys outside are masked)
+};
 bool window_attention_tiles_supported(int hd, int win_h, int win_w);
-int window_attention_tiles_smem(int halo_rows, bool three_d);
+int window_attention_tiles_smem(int halo_keys, bool three_d);
 void window_attention_tiles_init(int max_smem_bytes);
-// taps: [band keys rounded to 32][16] int8 for this tile shape: window tap
-// (dy+3)*7+(dx+3) of (band key, query slot), or -1 when the window or the step
-// mask excludes it (position independent because tiles are aligned; grid
-// bounds are applied separately). Built by the engine.
-void window_attention_tiles(const __half* q, int ldq, const int32_t* qinfo, const int32_t* tiles,
-                            int ntiles, int warps_per_tile, int halo_rows, const int8_t* taps,
-                            const __half* kv, int ldkv, int kv_slot_stride, int H, int W,
-                            int heads, int wt, int mask, int s, const float* bias, __half* out,
-                            int ldo, cudaStream_t st);
+// Score-offset tables of one attention layer and band shape, built once from
+// the layer's relative-position bias [heads][wt*49 or 49]: out[h][slot
+// offset][band key][query] = log2(e) * bias of the tap, -inf where the
+// window or mask excludes the pair. [heads][max(wt,1)][nbk][8] floats.
+void build_score_tables(const float* bias, int heads, int wt, AttnShape shape, float* out,
+                        cudaStream_t st);
+// kv_map: make_kv_tmap() of the K/V cache (gemm.h); halos are staged by TMA.
+void window_attention_tiles(const __half* q, int ldq, const int32_t* tiles, int ntiles,
+                            int warps_per_tile, int halo_rows, int halo_width, AttnShape shape,
+                            const CUtensorMap& kv_map, int heads, int wt, const float* tables,
+                            __half* out, int ldo, cudaStream_t st);
 
 // ---- convolutions for the hyperprior (conv.cu) ---------------------------
 // NHWC fp32 input [h][w][c] -> fp16 patches [oh*ow][kcols], K order

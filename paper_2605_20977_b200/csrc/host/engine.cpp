@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
+#include <tuple>
 
 #include "../cuda/check.h"
 #include "abi_util.h"
@@ -35,8 +36,12 @@ void put_linear(std::vector<__half>& dst, int ldk, const float* src, int in, int
           __float2half_rn(src[static_cast<size_t>(i) * out + o]);
 }
 
-constexpr int kCtxWarps = 8;   // attention CTA shape for the 3D context window
-constexpr int kStepWarps = 4;  // ... and for the step-batched 2D windows
+// tensor-core attention CTA halos (8 warps each): context 4 x 16 queries,
+// step batches 16 x 16 positions; +3 rows / columns of window margin
+// halo widths 22 + pad columns: spread the ldmatrix rows over the banks
+// under the TMA 64 B swizzle (see attention_mma.cu)
+constexpr int kCtxHaloRows = 10, kCtxHaloW = 23;
+constexpr int kStepHaloRows = 22, kStepHaloW = 24;
 
 // Step-t positions of the own rows of a band, as local raster indices, in
 // raster order: the canonical symbol order restricted to the band.
@@ -148,28 +153,35 @@ void Engine::alloc_all() {
       }
     ctx_qinfo_ = up(qi);
     if (B_.n > 1) ctx_kv_map_ = up(km);
-    // tap tables and aligned tiles assume s = 4 (4x16 step blocks repeat the
+    // tap tables and aligned tiles assume s = 4 (4-row step blocks repeat the
     // same query / step pattern); other schedules use the SIMT kernel
     mma_attn_ = pswa_dev::window_attention_tiles_supported(D.hd, D.c.win_h, D.c.win_w) && D.c.s == 4;
     if (mma_attn_) {
       constexpr int TI = pswa_dev::kAttnTileInts;
-      // context: CTA = 8 warps x (1 row x 16 cols) query strips of one slot
+      // context: CTA = 8 warps as 2 x 4 blocks of 2x4 queries (a 4 x 16 query
+      // rectangle of one slot), halo 10 rows x 23 columns
       auto ctx_tiles = [&](int slot_from, int row_base) {
         std::vector<int> v;
         const int yend = own0 + B_.nown;
         for (int j = slot_from; j < T; ++j)
-          for (int y0 = own0; y0 < yend; y0 += kCtxWarps)
+          for (int y0 = own0; y0 < yend; y0 += 4)
             for (int x0 = 0; x0 < D.W; x0 += 16) {
               std::vector<int> t(TI, -1);
               t[0] = y0 - 3;
               t[1] = x0 - 3;
-              t[2] = kCtxWarps + 6;
-              t[3] = 1;
-              t[4] = j;
-              t[5] = std::min(kCtxWarps, yend - y0);
-              for (int w = 0; w < t[5]; ++w)
-                for (int x = x0, i = 0; x < std::min(D.W, x0 + 16); ++x, ++i)
-                  t[8 + 16 * w + i] = j * HWo + (y0 - own0 + w) * D.W + x - row_base;
+              t[2] = kCtxHaloRows;
+              t[3] = j;
+              t[4] = 8;
+              for (int w = 0; w < 8; ++w) {
+                const int wy = w / 4, wx = w % 4;
+                int* W8 = &t[8 + 10 * w];
+                W8[0] = 2 * wy;
+                W8[1] = 4 * wx;
+                for (int i = 0; i < 8; ++i) {
+                  const int y = y0 + 2 * wy + i / 4, x = x0 + 4 * wx + i % 4;
+                  W8[2 + i] = (y < yend && x < D.W) ? j * HWo + (y - own0) * D.W + x - row_base : -1;
+                }
+              }
               v.insert(v.end(), t.begin(), t.end());
             }
         return v;
@@ -179,80 +191,116 @@ void Engine::alloc_all() {
       n_ctx_tiles_last_ = static_cast<int>(last.size()) / TI;
       ctx_tiles_ = up(all);
       ctx_tiles_last_ = up(last);
-      // step batches: CTA = 4 warps stacked vertically, warp = the step-t
-      // positions of a 4x16 block (16 when the block is inside the grid)
+      // step batches: CTA = 8 warps as 4 x 2 blocks of 4x8 (a 16 x 16
+      // rectangle); a warp owns the 8 step-t positions of its 4x8 block
       for (int t = 0; t < D.c.s; ++t) {
         std::vector<int> idx(static_cast<size_t>(HWl), -1);
         for (size_t k = 0; k < step_rows_h_[t].size(); ++k) idx[step_rows_h_[t][k]] = static_cast<int>(k);
         std::vector<int> v;
-        // warp blocks stay anchored to global rows = 0 mod 4 (lo = 0 mod 4)
-        for (int by = own0; by < own0 + B_.nown; by += 4 * kStepWarps)
+        // blocks stay anchored to global rows = 0 mod 4 (lo = 0 mod 4)
+        for (int by = own0; by < own0 + B_.nown; by += 16)
           for (int bx = 0; bx < D.W; bx += 16) {
             std::vector<int> tt(TI, -1);
             tt[0] = by - 3;
             tt[1] = bx - 3;
-            tt[2] = 4 * kStepWarps + 6;
-            tt[3] = 4;
-            tt[4] = 0;
-            tt[5] = kStepWarps;
+            tt[2] = kStepHaloRows;
+            tt[3] = 0;
+            tt[4] = 8;
             int total = 0;
-            for (int w = 0; w < kStepWarps; ++w)
-              for (int ry = 0; ry < 4; ++ry)
-                for (int jq = 0; jq < 4; ++jq) {  // canonical slot ry*4 + jq (tap table order)
-                  const int y = by + 4 * w + ry;
-                  const int x = bx + 4 * jq + ((t - ry) % 4 + 4) % 4;
-                  if (y < B_.Hl && x < D.W && idx[y * D.W + x] >= 0) {
-                    tt[8 + 16 * w + ry * 4 + jq] = idx[y * D.W + x];
-                    ++total;
-                  }
+            for (int w = 0; w < 8; ++w) {
+              const int wy = w / 2, wx = w % 2;
+              int* W8 = &tt[8 + 10 * w];
+              W8[0] = 4 * wy;
+              W8[1] = 8 * wx;
+              for (int i = 0; i < 8; ++i) {
+                const int ry = i / 2, jj = i % 2;
+                const int y = by + 4 * wy + ry;
+                const int x = bx + 8 * wx + 4 * jj + ((t - ry) % 4 + 4) % 4;
+                W8[2 + i] = -1;
+                if (y < B_.Hl && x < D.W && idx[y * D.W + x] >= 0) {
+                  W8[2 + i] = idx[y * D.W + x];
+                  ++total;
                 }
+              }
+            }
             if (total == 0) continue;
             v.insert(v.end(), tt.begin(), tt.end());
           }
         n_step_tiles_[t] = static_cast<int>(v.size()) / TI;
         step_tiles_[t] = up(v);
       }
-      // tap tables: [band key][16 query slots] int8, -1 = excluded by the
-      // window or the step mask (grid bounds are applied in the kernel)
+      // band shapes: the keys a warp scans (band order) and their taps per
+      // query, -1 where the window or the step mask excludes the pair (grid
+      // bounds are applied in the kernel). Keys no query can use are dropped.
       {
-        auto table = [&](int band_rows, auto tap_of) {
-          const int keys = (band_rows * 22 + 31) / 32 * 32;  // attention key chunk = 32
-          std::vector<int8_t> tb(static_cast<size_t>(keys) * 16, -1);
-          for (int bk = 0; bk < band_rows * 22; ++bk)
-            for (int qs = 0; qs < 16; ++qs) tb[static_cast<size_t>(bk) * 16 + qs] = tap_of(bk / 22, bk % 22, qs);
-          return tb;
+        std::vector<int8_t> all_taps;
+        std::vector<int16_t> all_keys;
+        struct Pending { size_t tap_off, key_off; int nbk; };
+        auto add_shape = [&](std::vector<std::pair<int, int>> keys /* (row, col) in band */,
+                             auto query_pos, int t, int mk) {
+          std::vector<std::pair<int, int>> used;
+          std::vector<int8_t> taps;
+          for (auto [kr, kc] : keys) {
+            int8_t row[8];
+            bool any = false;
+            for (int i = 0; i < 8; ++i) {
+              const auto [qr, qc] = query_pos(i);
+              const int dy = kr - qr, dx = kc - qc;
+              row[i] = -1;
+              if (dy < -3 || dy > 3 || dx < -3 || dx > 3) continue;
+              const int ks = ((kr - 3 + kc - 3) % 4 + 4) % 4;  // band origin = block origin - 3
+              if (t >= 0 && ((mk == 1 && ks > t) || (mk == 2 && ks >= t))) continue;
+              row[i] = static_cast<int8_t>((dy + 3) * 7 + dx + 3);
+              any = true;
+            }
+            if (!any) continue;
+            used.push_back({kr, kc});
+            taps.insert(taps.end(), row, row + 8);
+          }
+          while (used.size() % 16) {  // pad to whole 16-key chunks (all taps -1)
+            used.push_back({0, 0});
+            taps.insert(taps.end(), 8, int8_t(-1));
+          }
+          Pending p{all_taps.size(), all_keys.size(), static_cast<int>(used.size())};
+          all_taps.insert(all_taps.end(), taps.begin(), taps.end());
+          for (auto [kr, kc] : used) all_keys.push_back(static_cast<int16_t>(kr << 8 | kc));
+          return p;
         };
-        std::vector<int8_t> all_t;
-        auto push = [&](const std::vector<int8_t>& tb) {
-          const size_t off = all_t.size();
-          all_t.insert(all_t.end(), tb.begin(), tb.end());
-          return off;
+        // context: 8 x 10 band, column-major (conflict-free ldmatrix with a
+        // 23-wide halo and the TMA 64 B swizzle); query i at (3 + i/4, 3 + i%4)
+        std::vector<std::pair<int, int>> ck;
+        for (int c = 0; c < 10; ++c)
+          for (int r = 0; r < 8; ++r) ck.push_back({r, c});
+        const Pending pc = add_shape(ck, [](int i) { return std::make_pair(3 + i / 4, 3 + i % 4); }, -1, 0);
+        // steps: 10 x 14 band sorted by step class, then row, column
+        Pending ps[4][3];
+        for (int t = 0; t < 4; ++t)
+          for (int mk = 0; mk < 3; ++mk) {
+            std::vector<std::tuple<int, int, int>> sk;
+            for (int r = 0; r < 10; ++r)
+              for (int c = 0; c < 14; ++c) sk.emplace_back(((r + c - 6) % 4 + 4) % 4, r, c);
+            std::sort(sk.begin(), sk.end());
+            std::vector<std::pair<int, int>> keys;
+            for (auto [cls, r, c] : sk) keys.push_back({r, c});
+            ps[t][mk] = add_shape(keys, [t](int i) {
+              const int ry = i / 2, jj = i % 2;
+              return std::make_pair(3 + ry, 3 + 4 * jj + ((t - ry) % 4 + 4) % 4);
+            }, t, mk);
+          }
+        int8_t* dt = dalloc<int8_t>(all_taps.size());
+        int16_t* dk = dalloc<int16_t>(all_keys.size());
+        PSWA_CUDA(cudaMemcpyAsync(dt, all_taps.data(), all_taps.size(), cudaMemcpyHostToDevice, st_));
+        PSWA_CUDA(cudaMemcpyAsync(dk, all_keys.data(), all_keys.size() * 2, cudaMemcpyHostToDevice, st_));
+        auto shape = [&](const Pending& p) {
+          return pswa_dev::AttnShape{dt + p.tap_off, dk + p.key_off, p.nbk, B_.Hl, D.W};
         };
-        // context strip: query slot q at band row 3, column q + 3
-        const size_t off_ctx = push(table(7, [](int hr, int hc, int q) -> int8_t {
-          const int dy = hr - 3, dx = hc - 3 - q;
-          return (dx < -3 || dx > 3) ? -1 : static_cast<int8_t>((dy + 3) * 7 + dx + 3);
-        }));
-        size_t off_step[16][3];
+        shape_ctx_ = shape(pc);
         for (int t = 0; t < 4; ++t)
-          for (int mk = 0; mk < 3; ++mk)
-            off_step[t][mk] = push(table(10, [=](int hr, int hc, int q) -> int8_t {
-              const int ry = q / 4, rx = 4 * (q % 4) + ((t - ry) % 4 + 4) % 4;
-              const int dy = hr - 3 - ry, dx = hc - 3 - rx;
-              if (dy < -3 || dy > 3 || dx < -3 || dx > 3) return -1;
-              const int ks = ((hr - 3 + hc - 3) % 4 + 4) % 4;
-              if ((mk == 1 && ks > t) || (mk == 2 && ks >= t)) return -1;
-              return static_cast<int8_t>((dy + 3) * 7 + dx + 3);
-            }));
-        int8_t* dt = dalloc<int8_t>(all_t.size());
-        PSWA_CUDA(cudaMemcpyAsync(dt, all_t.data(), all_t.size(), cudaMemcpyHostToDevice, st_));
-        taps_ctx_ = dt + off_ctx;
-        for (int t = 0; t < 4; ++t)
-          for (int mk = 0; mk < 3; ++mk) taps_step_[t][mk] = dt + off_step[t][mk];
+          for (int mk = 0; mk < 3; ++mk) shape_step_[t][mk] = shape(ps[t][mk]);
       }
       pswa_dev::window_attention_tiles_init(
-          std::max(pswa_dev::window_attention_tiles_smem(kCtxWarps + 6, true),
-                   pswa_dev::window_attention_tiles_smem(4 * kStepWarps + 6, false)));
+          std::max(pswa_dev::window_attention_tiles_smem(kCtxHaloRows * kCtxHaloW, true),
+                   pswa_dev::window_attention_tiles_smem(kStepHaloRows * kStepHaloW, false)));
     }
     std::vector<int> crop(HWp);
     for (int y = 0; y < D.Hp; ++y)
@@ -552,16 +600,27 @@ GemmEpi swiglu_out(void* out, int ld) {
 // Windowed attention: tensor-core warp tiles when the shape allows
 // (head_dim 32, 7x7), the SIMT kernel otherwise (desk preset, head_dim 4).
 void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq,
-                       const int32_t* tiles, int ntiles, const int8_t* taps, const __half* kv,
-                       int slot_stride, int wt, int mask, const float* bias, __half* out) {
+                       const int32_t* tiles, int ntiles, const pswa_dev::AttnShape* shape,
+                       const __half* kv, int slot_stride, int wt, int mask, const float* bias,
+                       __half* out) {
   const Dims& D = D_;
   const int d = D.d, Hl = B_.Hl;  // key grid bounds: the band's local grid
   if (mma_attn_) {
-    const int warps = wt > 0 ? kCtxWarps : kStepWarps;
-    const int halo_rows = wt > 0 ? kCtxWarps + 6 : 4 * kStepWarps + 6;
+    const pswa_dev::AttnShape sh = *shape;
+    const int hr = wt > 0 ? kCtxHaloRows : kStepHaloRows, hw = wt > 0 ? kCtxHaloW : kStepHaloW;
+    CUtensorMap map;  // halo boxes of this K/V buffer: 32 channels x hw x hr x 1 slot
+    pswa_dev::make_kv_tmap(&map, kv, 2 * d, D.W, Hl, wt > 0 ? D.T : 1, slot_stride > 0 ? slot_stride : HWl_,
+                           hw, hr);
+    // score-offset tables of (layer bias, band shape): built once, reused by
+    // every program that launches this layer on this shape
+    float*& tab = score_tables_[{bias, shape}];
+    if (!tab && sh.nbk > 0) {
+      tab = dalloc<float>(static_cast<size_t>(D.heads) * std::max(wt, 1) * sh.nbk * 8);
+      pswa_dev::build_score_tables(bias, D.heads, wt, sh, tab, st_);
+    }
+    const float* tables = tab;
     add(P, [=](cudaStream_t s) {
-      pswa_dev::window_attention_tiles(q, d, qinfo, tiles, ntiles, warps, halo_rows, taps, kv,
-                                       2 * d, slot_stride, Hl, D.W, D.heads, wt, mask, D.c.s, bias,
+      pswa_dev::window_attention_tiles(q, d, tiles, ntiles, 8, hr, hw, sh, map, D.heads, wt, tables,
                                        out, d, s);
     });
   } else {
@@ -590,7 +649,7 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
     exchange(P, xid_of(B), t);  // band mode: step-t K/V of the boundary rows
   }
   const int mk = B.cross ? 0 : 1;
-  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], taps_step_[t][mk], B.kv_cache, 0, 0,
+  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], &shape_step_[t][mk], B.kv_cache, 0, 0,
             mk, B.pos, batt_);
   if (probe) tag(P, "step_attn", attn_flops(t, mk, 0));
   gemm(P, batt_, d, M, B.wo, d, f32_acc(bx_, d));
@@ -622,7 +681,7 @@ void Engine::build_ctx(Program& P) {
     exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
     gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, f16_out(ctx_q_, d));
     attention(P, ctx_q_, ctx_qinfo_ + q0, nq, last ? ctx_tiles_last_ : ctx_tiles_,
-              last ? n_ctx_tiles_last_ : n_ctx_tiles_, taps_ctx_, kv, HWl_, D.c.win_t, 0, pos,
+              last ? n_ctx_tiles_last_ : n_ctx_tiles_, &shape_ctx_, kv, HWl_, D.c.win_t, 0, pos,
               ctx_att_);
     if (b == 0) tag(P, "ctx_attn", attn_flops(-1, 0, 0));
     float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
@@ -769,7 +828,7 @@ void Engine::build_step(Program& P, int t, int mode) {
   // accumulator: A = Hq + xattn(Q = Hq, KV = S1 of strictly earlier steps)
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(hq_, d, rows, M, d, d, acc_.g1, bxn_, d, s); });
   gemm(P, bxn_, d, M, acc_.wq, d, f16_out(bq_, d));
-  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], taps_step_[t][2], acc_kv_, 0, 0, 2,
+  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], &shape_step_[t][2], acc_kv_, 0, 0, 2,
             acc_.pos, batt_);
   add(P, [=, this](cudaStream_t s) { pswa_dev::gather_rows_f32(hq_, d, rows, M, d, bx_, d, s); });
   gemm(P, batt_, d, M, acc_.wo, d, f32_acc(bx_, d));

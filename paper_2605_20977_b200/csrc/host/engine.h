@@ -252,11 +252,12 @@ class Engine {
   int n_ctx_tiles_ = 0, n_ctx_tiles_last_ = 0;
   int32_t* step_tiles_[16] = {};
   int n_step_tiles_[16] = {};
-  const int8_t* taps_ctx_ = nullptr;
-  const int8_t* taps_step_[4][3] = {};  // [t][mask: none, <=, <]
+  pswa_dev::AttnShape shape_ctx_{};
+  std::map<std::pair<const float*, const pswa_dev::AttnShape*>, float*> score_tables_;
+  pswa_dev::AttnShape shape_step_[4][3] = {};  // [t][mask: none, <=, <]
   void attention(struct Program& P, const __half* q, const int32_t* qinfo, int Mq, const int32_t* tiles,
-                 int ntiles, const int8_t* taps, const __half* kv, int slot_stride, int wt, int mask,
-                 const float* bias, __half* out);
+                 int ntiles, const pswa_dev::AttnShape* shape, const __half* kv, int slot_stride,
+                 int wt, int mask, const float* bias, __half* out);
   int* crop_rows_ = nullptr;  // padded hyper grid index -> raster index (-1: pad)
   float* scales_ = nullptr;
   uint32_t* cdf_ = nullptr;
