@@ -120,10 +120,11 @@ __device__ __forceinline__ void prefetch_residual(const GemmEpi& ep, int orow, i
 // writes whole 32 B sectors of its own row).
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
-                                          const uint32_t (&raw)[32], const float4 (&res)[8]) {
+                                          const uint32_t (&raw)[32], const float4 (&res)[8],
+                                          float row_scale) {
   float v[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]) * row_scale;
   epi_values<EPI>(ep, n0, v);
   if (orow < 0) return;
   const int ncols = EPI == kEpiSwiGLU ? 16 : 32;
@@ -134,6 +135,8 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
     float* dst = static_cast<float*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0;
     if (EPI == kEpiF32 && full) {
       float4* d4 = reinterpret_cast<float4*>(dst);
+      float ss = 0.0f;
+      uint32_t hp[16];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -144,7 +147,20 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
           o.w += res[q].w;
         }
         d4[q] = o;
+        ss = fmaf(o.x, o.x, ss);
+        ss = fmaf(o.y, o.y, ss);
+        ss = fmaf(o.z, o.z, ss);
+        ss = fmaf(o.w, o.w, ss);
+        __half2 h0 = __floats2half2_rn(o.x, o.y), h1 = __floats2half2_rn(o.z, o.w);
+        hp[2 * q] = *reinterpret_cast<uint32_t*>(&h0);
+        hp[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h1);
       }
+      if (ep.x16_out) {  // next RMSNorm's input: fp16 copy of the updated row
+        uint4* h4 = reinterpret_cast<uint4*>(ep.x16_out + static_cast<size_t>(orow) * ep.ld_x16 + oc0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) h4[q] = make_uint4(hp[4 * q], hp[4 * q + 1], hp[4 * q + 2], hp[4 * q + 3]);
+      }
+      if (ep.ssq_out) ep.ssq_out[static_cast<size_t>(orow) * ep.ld_ssq + (oc0 >> 5)] = ss;
     } else {
       for (int j = 0; j < 32 && oc0 + j < ep.n_store; ++j)
         dst[j] = (EPI == kEpiF32 && ep.accumulate) ? dst[j] + v[j] : v[j];
@@ -277,6 +293,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       float4 res[8];
       const bool acc_res = EPI == kEpiF32 && ep.accumulate;
       if (acc_res) prefetch_residual(ep, orow, n0 + c0 * 32, res);
+      float row_scale = 1.0f;  // folded RMSNorm of A's row m
+      if (ep.rms_ssq && m < M) {
+        const float* sp = ep.rms_ssq + static_cast<size_t>(m) * ep.ld_rms;
+        float ss = 0.0f;
+        if ((ep.rms_parts & 3) == 0 && (ep.ld_rms & 3) == 0) {  // 16 B loads (the row's 64 B)
+          for (int k = 0; k < ep.rms_parts; k += 4) {
+            const float4 q4 = *reinterpret_cast<const float4*>(sp + k);
+            ss += q4.x;
+            ss += q4.y;
+            ss += q4.z;
+            ss += q4.w;
+          }
+        } else {
+          for (int k = 0; k < ep.rms_parts; ++k) ss += sp[k];
+        }
+        row_scale = 1.0f / sqrtf(ss * ep.rms_inv_d + 1e-5f);
+      }
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const uint32_t acc = tmem + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
@@ -291,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);
         }
-        epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res);
+        epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res, row_scale);
         if (acc_res && c + 1 < c1) prefetch_residual(ep, orow, n0 + (c + 1) * 32, res);
       }
     }

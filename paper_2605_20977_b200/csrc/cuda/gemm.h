@@ -31,6 +31,20 @@ struct GemmEpi {
   int split = 0;                 // kActHead: first sigma column
   const int* row_map = nullptr;  // nullable: output row = row_map[m] (< 0: skip)
   int n_store = 1 << 30;         // output columns >= n_store are not written
+  // RMSNorm folded into the GEMMs around it (tensor.cpp:81-86):
+  //  * producer (fp32 accumulate epilogue, the residual add): also writes an
+  //    fp16 copy of each updated row and its sum of squares per 32-column
+  //    chunk (fixed order, no atomics), the next norm's inputs;
+  //  * consumer (A = that fp16 copy, gain folded into the packed weight):
+  //    every output row is scaled by 1/sqrt(sum(ssq[m][0:parts]) / d + 1e-5)
+  //    before bias / activation.
+  __half* x16_out = nullptr;
+  int ld_x16 = 0;
+  float* ssq_out = nullptr;
+  int ld_ssq = 0;
+  const float* rms_ssq = nullptr;  // consumer: [M][ld_rms] partial sums of squares of A's rows
+  int ld_rms = 0, rms_parts = 0;
+  float rms_inv_d = 0.0f;
 };
 
 struct GemmPlan {

@@ -13,6 +13,11 @@ namespace pswa_dev {
 // Matches tensor.cpp:81-86 (eps 1e-5) up to reduction order.
 void rmsnorm_rows(const float* x, int ldx, const int* src_rows, int M, int d, int group,
                   const float* gain, __half* y, int ldy, cudaStream_t st);
+// Inputs of a folded RMSNorm (see GemmEpi::rms_ssq) for M rows of x
+// (gathered through src_rows when given): optional fp32 copy, fp16 copy and
+// sums of squares per 32 columns. d % 128 == 0 or d % 32 == 0 (slow path).
+void rms_prep(const float* x, int ldx, const int* src_rows, int M, int d, float* xcopy, int ldc,
+              __half* x16, int ld16, float* ssq, int ld_ssq, cudaStream_t st);
 // dst[i][0:n] = src[rows ? rows[i] : i][0:n] (fp32)
 void gather_rows_f32(const float* src, int lds, const int* rows, int M, int n, float* dst,
                      int ldd, cudaStream_t st);

@@ -61,6 +61,41 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const int* 
   }
 }
 
+__global__ void rms_prep_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ src,
+                                int M, int d, float* __restrict__ xc, int ldc, __half* __restrict__ x16,
+                                int ld16, float* __restrict__ ssq, int ld_ssq) {
+  pdl_wait();
+  pdl_trigger();
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float* xr = x + static_cast<size_t>(src ? src[row] : row) * ldx;
+  if ((d & 127) == 0) {
+    for (int c0 = 0; c0 < d; c0 += 128) {  // lane owns 4 columns; 8 lanes = one 32-column chunk
+      const int c = c0 + lane * 4;
+      const float4 v = *reinterpret_cast<const float4*>(xr + c);
+      if (xc) *reinterpret_cast<float4*>(xc + static_cast<size_t>(row) * ldc + c) = v;
+      __half2 h[2] = {__floats2half2_rn(v.x, v.y), __floats2half2_rn(v.z, v.w)};
+      *reinterpret_cast<uint2*>(x16 + static_cast<size_t>(row) * ld16 + c) = *reinterpret_cast<uint2*>(h);
+      float ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+      ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+      ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+      if ((lane & 7) == 0) ssq[static_cast<size_t>(row) * ld_ssq + (c >> 5)] = ss;
+    }
+  } else {
+    for (int c0 = 0; c0 < d; c0 += 32) {  // one chunk per pass, lane = column
+      const float v = xr[c0 + lane];
+      if (xc) xc[static_cast<size_t>(row) * ldc + c0 + lane] = v;
+      x16[static_cast<size_t>(row) * ld16 + c0 + lane] = __float2half_rn(v);
+      float ss = v * v;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) ssq[static_cast<size_t>(row) * ld_ssq + (c0 >> 5)] = ss;
+    }
+  }
+}
+
 __global__ void gather_f32_kernel(const float* __restrict__ src, int lds, const int* __restrict__ rows,
                                   int M, int n, float* __restrict__ dst, int ldd) {
   pdl_wait();
@@ -265,6 +300,15 @@ void band_wait(const unsigned* mbox, unsigned* wait_ctr, bool need_up, bool need
                cudaStream_t st) {
   launch_k(band_wait_kernel, dim3(1), dim3(1), 0, st, mbox, wait_ctr, need_up ? 1 : 0,
            need_down ? 1 : 0, status);
+  PSWA_LAUNCH_CHECK();
+}
+
+void rms_prep(const float* x, int ldx, const int* src_rows, int M, int d, float* xcopy, int ldc,
+              __half* x16, int ld16, float* ssq, int ld_ssq, cudaStream_t st) {
+  if (M <= 0) return;
+  if (d % 32) throw std::invalid_argument("rms_prep: d % 32");
+  launch_k(rms_prep_kernel, dim3((M + 7) / 8), dim3(256), 0, st, x, ldx, src_rows, M, d, xcopy, ldc,
+           x16, ld16, ssq, ld_ssq);
   PSWA_LAUNCH_CHECK();
 }
 

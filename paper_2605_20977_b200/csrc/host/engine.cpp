@@ -27,13 +27,16 @@ const HostTensor& W(const WeightMap& w, const std::string& n) {
 }
 
 // Host-side fp16 packing: dst[(row_off + o) * ldk + col_off + i] = src[i][o]
-// for a linear layer stored [in][out] (reference matmul convention).
+// for a linear layer stored [in][out] (reference matmul convention). `gain`
+// (nullable, [in]) folds a preceding RMSNorm gain into the weight:
+// rmsnorm(x) . W = (x . diag(g) W) / rms(x), the 1/rms applied in the GEMM
+// epilogue (GemmEpi::rms_ssq).
 void put_linear(std::vector<__half>& dst, int ldk, const float* src, int in, int out, int row_off,
-                int col_off) {
+                int col_off, const float* gain = nullptr) {
   for (int o = 0; o < out; ++o)
     for (int i = 0; i < in; ++i)
       dst[static_cast<size_t>(row_off + o) * ldk + col_off + i] =
-          __float2half_rn(src[static_cast<size_t>(i) * out + o]);
+          __float2half_rn(src[static_cast<size_t>(i) * out + o] * (gain ? gain[i] : 1.0f));
 }
 
 // tensor-core attention CTA halos (8 warps each): context 4 x 16 queries,
@@ -333,6 +336,7 @@ void Engine::alloc_all() {
   const size_t TH = static_cast<size_t>(T) * HWo, THl = static_cast<size_t>(T) * HWl;
   ctx_x_ = dalloc<float>(TH * d);
   ctx_xn_ = dalloc<__half>(TH * d);
+  ctx_ssq_ = dalloc<float>(TH * (d / 32));
   ctx_kv_ = dalloc<__half>(THl * 2 * d);
   if (B_.n > 1) ctx_kv2_ = dalloc<__half>(THl * 2 * d);
   ctx_q_ = dalloc<__half>(TH * d);
@@ -351,6 +355,7 @@ void Engine::alloc_all() {
   const size_t nb = static_cast<size_t>(nmax_);
   bx_ = dalloc<float>(nb * d);
   bxn_ = dalloc<__half>(nb * d);
+  bssq_ = dalloc<float>(nb * (d / 32));
   bq_ = dalloc<__half>(nb * d);
   batt_ = dalloc<__half>(nb * d);
   bh_ = dalloc<__half>(nb * D.fp);
@@ -412,26 +417,28 @@ void Engine::upload_weights(const WeightMap& w) {
   };
   auto fv = [&](const std::string& n) { return W(w, n).v.data(); };
   auto fsize = [&](const std::string& n) { return W(w, n).v.size(); };
-  auto linear = [&](const std::string& n, int in, int out, int Np, int Kp) {
+  auto linear = [&](const std::string& n, int in, int out, int Np, int Kp, const float* gain = nullptr) {
     std::vector<__half> h(static_cast<size_t>(Np) * Kp, __float2half_rn(0.0f));
-    put_linear(h, Kp, fv(n), in, out, 0, 0);
+    put_linear(h, Kp, fv(n), in, out, 0, 0, gain);
     return PW{upload_h(h), Np, Kp};
   };
-  auto kv = [&](const std::string& k, const std::string& v) {
+  auto kv = [&](const std::string& k, const std::string& v, const float* gain = nullptr) {
     std::vector<__half> h(static_cast<size_t>(2 * d) * d, __float2half_rn(0.0f));
-    put_linear(h, d, fv(k), d, d, 0, 0);
-    put_linear(h, d, fv(v), d, d, d, 0);
+    put_linear(h, d, fv(k), d, d, 0, 0, gain);
+    put_linear(h, d, fv(v), d, d, d, 0, gain);
     return PW{upload_h(h), 2 * d, d};
   };
   // SwiGLU gate/up interleaved by output column: rows 2j (gate), 2j+1 (up).
-  auto gate_up = [&](const std::string& g, const std::string& u, int in, int f, int fp, int Kp) {
+  auto gate_up = [&](const std::string& g, const std::string& u, int in, int f, int fp, int Kp,
+                     const float* gain = nullptr) {
     std::vector<__half> h(static_cast<size_t>(2 * fp) * Kp, __float2half_rn(0.0f));
     const float* G = fv(g);
     const float* U = fv(u);
     for (int j = 0; j < f; ++j)
       for (int i = 0; i < in; ++i) {
-        h[static_cast<size_t>(2 * j) * Kp + i] = __float2half_rn(G[static_cast<size_t>(i) * f + j]);
-        h[static_cast<size_t>(2 * j + 1) * Kp + i] = __float2half_rn(U[static_cast<size_t>(i) * f + j]);
+        const float gi = gain ? gain[i] : 1.0f;
+        h[static_cast<size_t>(2 * j) * Kp + i] = __float2half_rn(G[static_cast<size_t>(i) * f + j] * gi);
+        h[static_cast<size_t>(2 * j + 1) * Kp + i] = __float2half_rn(U[static_cast<size_t>(i) * f + j] * gi);
       }
     return PW{upload_h(h), 2 * fp, Kp};
   };
@@ -440,10 +447,13 @@ void Engine::upload_weights(const WeightMap& w) {
       const std::string p = std::string(tag) + ".b" + std::to_string(b);
       Block& B = out[b];
       B.cross = spatial && (b % 2 == 1);
-      B.wq = linear(p + ".wq", d, d, d, d);
-      B.wkv = kv(p + ".wk", p + ".wv");
+      // norm1 / norm2 gains folded into the projections they feed
+      const float* g1 = fv(p + ".norm1.g");
+      const float* g2 = fv(p + ".norm2.g");
+      B.wq = linear(p + ".wq", d, d, d, d, g1);
+      B.wkv = kv(p + ".wk", p + ".wv", g1);
       B.wo = linear(p + ".wo", d, d, d, d);
-      B.wgu = gate_up(p + ".ffn.wg", p + ".ffn.wu", d, D.f, D.fp, d);
+      B.wgu = gate_up(p + ".ffn.wg", p + ".ffn.wu", d, D.f, D.fp, d, g2);
       B.wd = linear(p + ".ffn.wd", D.f, d, d, D.fp);
       B.g1 = upload_f(fv(p + ".norm1.g"), d);
       B.g2 = upload_f(fv(p + ".norm2.g"), d);
@@ -504,7 +514,7 @@ void Engine::upload_weights(const WeightMap& w) {
     he_in_b_ = upload_f(fv("he.in.b"), D.hc, D.hcp);
   }
   // accumulator
-  acc_.wq = linear("acc.wq", d, d, d, d);
+  acc_.wq = linear("acc.wq", d, d, d, d, fv("acc.normq.g"));  // normq gain folded
   acc_.wkv = kv("acc.wk", "acc.wv");
   acc_.wo = linear("acc.wo", d, d, d, d);
   acc_.g1 = upload_f(fv("acc.normq.g"), d);
@@ -588,6 +598,14 @@ GemmEpi f32_acc(void* out, int ld, int n_store = 1 << 30) {
   e.n_store = n_store;
   return e;
 }
+// folded RMSNorm (GemmEpi::rms_ssq): producer / consumer sides
+GemmEpi rms_out(GemmEpi e, __half* x16, float* ssq) {
+  e.x16_out = x16;
+  e.ld_x16 = e.ld_out;
+  e.ssq_out = ssq;
+  e.ld_ssq = e.ld_out / 32;
+  return e;
+}
 GemmEpi swiglu_out(void* out, int ld) {
   GemmEpi e;
   e.out = out;
@@ -596,6 +614,14 @@ GemmEpi swiglu_out(void* out, int ld) {
   return e;
 }
 }  // namespace
+
+GemmEpi Engine::rms_in(GemmEpi e, const float* ssq) const {
+  e.rms_ssq = ssq;
+  e.ld_rms = D_.d / 32;
+  e.rms_parts = D_.d / 32;
+  e.rms_inv_d = 1.0f / static_cast<float>(D_.d);
+  return e;
+}
 
 // Windowed attention: tensor-core warp tiles when the shape allows
 // (head_dim 32, 7x7), the SIMT kernel otherwise (desk preset, head_dim 4).
@@ -637,13 +663,13 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
   const int d = D.d, M = static_cast<int>(step_rows_h_[t].size());
   const int* rows = step_rows_[t];
   const int32_t* qinfo = step_qinfo_[t];
-  const float* g1 = B.g1;
-  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, g1, bxn_, d, s); });
-  gemm(P, bxn_, d, M, B.wq, d, f16_out(bq_, d));
+  // norm1 is folded: bxn_ holds the fp16 residual stream and bssq_ its
+  // sums of squares (from the previous residual GEMM or rms_prep)
+  gemm(P, bxn_, d, M, B.wq, d, rms_in(f16_out(bq_, d), bssq_));
   const bool probe = &B == &s2_[0] && t == D.c.s - 1;  // bench_op probes (last step, S2 block 0)
   if (probe) tag(P, "step_wq", 2.0 * M * d * d);
   if (!B.cross) {
-    GemmEpi e = f16_out(B.kv_cache, 2 * d);
+    GemmEpi e = rms_in(f16_out(B.kv_cache, 2 * d), bssq_);
     e.row_map = rows;  // K/V of this step's positions into the frame cache
     gemm(P, bxn_, d, M, B.wkv, d, e);
     exchange(P, xid_of(B), t);  // band mode: step-t K/V of the boundary rows
@@ -652,11 +678,9 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
   attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], &shape_step_[t][mk], B.kv_cache, 0, 0,
             mk, B.pos, batt_);
   if (probe) tag(P, "step_attn", attn_flops(t, mk, 0));
-  gemm(P, batt_, d, M, B.wo, d, f32_acc(bx_, d));
-  const float* g2 = B.g2;
-  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, g2, bxn_, d, s); });
-  gemm(P, bxn_, d, M, B.wgu, d, swiglu_out(bh_, D.fp));
-  gemm(P, bh_, D.fp, M, B.wd, D.fp, f32_acc(bx_, d));
+  gemm(P, batt_, d, M, B.wo, d, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + norm2 inputs
+  gemm(P, bxn_, d, M, B.wgu, d, rms_in(swiglu_out(bh_, D.fp), bssq_));
+  gemm(P, bh_, D.fp, M, B.wd, D.fp, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + next norm1 inputs
 }
 
 void Engine::build_ctx(Program& P) {
@@ -665,32 +689,35 @@ void Engine::build_ctx(Program& P) {
   add(P, [=, this](cudaStream_t s) {
     pswa_dev::fill_context_slots(ring_ptrs_, slot_src_, pad_, T, HWo, d, ctx_x_, s);
   });
+  // block 0 norm1 inputs; later norms come out of the residual GEMMs
+  add(P, [=, this](cudaStream_t s) {
+    pswa_dev::rms_prep(ctx_x_, d, nullptr, n, d, nullptr, 0, ctx_xn_, d, ctx_ssq_, d / 32, s);
+  });
   for (int b = 0; b < D.c.ctx_blocks; ++b) {
     const Block& B = ctx_[b];
     const bool last = b == D.c.ctx_blocks - 1;
     const int q0 = last ? (T - 1) * HWo : 0, nq = n - q0;
-    const float *g1 = B.g1, *g2 = B.g2, *pos = B.pos;
+    const float* pos = B.pos;
     // band mode: K/V of the own rows into the local [T][HWl] grid, the halo
     // rows pushed by the neighbours; buffers alternate by layer so a
     // neighbour's push of layer b+1 never lands in the buffer read by layer b
     __half* kv = (B_.n > 1 && b % 2) ? ctx_kv2_ : ctx_kv_;
-    add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(ctx_x_, d, nullptr, n, d, d, g1, ctx_xn_, d, s); });
-    GemmEpi ekv = f16_out(kv, 2 * d);
+    GemmEpi ekv = rms_in(f16_out(kv, 2 * d), ctx_ssq_);
     ekv.row_map = ctx_kv_map_;
     gemm(P, ctx_xn_, d, n, B.wkv, d, ekv);
     exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
-    gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, f16_out(ctx_q_, d));
+    float* ssq_q = ctx_ssq_ + static_cast<size_t>(q0) * (d / 32);
+    gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, rms_in(f16_out(ctx_q_, d), ssq_q));
     attention(P, ctx_q_, ctx_qinfo_ + q0, nq, last ? ctx_tiles_last_ : ctx_tiles_,
               last ? n_ctx_tiles_last_ : n_ctx_tiles_, &shape_ctx_, kv, HWl_, D.c.win_t, 0, pos,
               ctx_att_);
     if (b == 0) tag(P, "ctx_attn", attn_flops(-1, 0, 0));
     float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
     __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;
-    gemm(P, ctx_att_, d, nq, B.wo, d, f32_acc(xq, d));
-    add(P, [=](cudaStream_t s) { pswa_dev::rmsnorm_rows(xq, d, nullptr, nq, d, d, g2, xnq, d, s); });
-    gemm(P, xnq, d, nq, B.wgu, d, swiglu_out(ctx_h_, D.fp));
+    gemm(P, ctx_att_, d, nq, B.wo, d, rms_out(f32_acc(xq, d), xnq, ssq_q));
+    gemm(P, xnq, d, nq, B.wgu, d, rms_in(swiglu_out(ctx_h_, D.fp), ssq_q));
     if (b == 0) tag(P, "ctx_ffn_gu", 2.0 * nq * (2.0 * D.f) * d);
-    gemm(P, ctx_h_, D.fp, nq, B.wd, D.fp, f32_acc(xq, d));
+    gemm(P, ctx_h_, D.fp, nq, B.wd, D.fp, rms_out(f32_acc(xq, d), xnq, ssq_q));
   }
   const float* last = ctx_x_ + static_cast<size_t>(T - 1) * HWo * d;
   __half* c16 = ctx16_ + static_cast<size_t>(B_.own0) * D.W * d;
@@ -806,7 +833,9 @@ void Engine::build_s1(Program& P, int t, bool encoder) {
   const Dims& D = D_;
   const int d = D.d, M = static_cast<int>(step_rows_h_[t].size());
   const int* rows = step_rows_[t];
-  add(P, [=, this](cudaStream_t s) { pswa_dev::gather_rows_f32(emb_cur_, d, rows, M, d, bx_, d, s); });
+  add(P, [=, this](cudaStream_t s) {  // gather + block 0 norm1 inputs
+    pswa_dev::rms_prep(emb_cur_, d, rows, M, d, bx_, d, bxn_, d, bssq_, d / 32, s);
+  });
   for (int b = 0; b < D.c.s1_blocks; ++b) block_step(P, s1_[b], t, "s1", true);
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, s1_gout_, bs1n_, d, s); });
   GemmEpi e = f16_out(acc_kv_, 2 * d);
@@ -826,12 +855,13 @@ void Engine::build_step(Program& P, int t, int mode) {
   const int* rows = step_rows_[t];
   const int32_t* qinfo = step_qinfo_[t];
   // accumulator: A = Hq + xattn(Q = Hq, KV = S1 of strictly earlier steps)
-  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(hq_, d, rows, M, d, d, acc_.g1, bxn_, d, s); });
-  gemm(P, bxn_, d, M, acc_.wq, d, f16_out(bq_, d));
+  add(P, [=, this](cudaStream_t s) {  // residual = Hq rows, normq folded into acc.wq
+    pswa_dev::rms_prep(hq_, d, rows, M, d, bx_, d, bxn_, d, bssq_, d / 32, s);
+  });
+  gemm(P, bxn_, d, M, acc_.wq, d, rms_in(f16_out(bq_, d), bssq_));
   attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], &shape_step_[t][2], acc_kv_, 0, 0, 2,
             acc_.pos, batt_);
-  add(P, [=, this](cudaStream_t s) { pswa_dev::gather_rows_f32(hq_, d, rows, M, d, bx_, d, s); });
-  gemm(P, batt_, d, M, acc_.wo, d, f32_acc(bx_, d));
+  gemm(P, batt_, d, M, acc_.wo, d, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + S2 norm1 inputs
   const bool taps = mode == 1 && want_musig_;  // debug taps in forward_params only
   if (taps)
     add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f32(bx_, d, rows, M, d, afull_, d, s); });

@@ -255,6 +255,8 @@ class Engine {
   pswa_dev::AttnShape shape_ctx_{};
   std::map<std::pair<const float*, const pswa_dev::AttnShape*>, float*> score_tables_;
   pswa_dev::AttnShape shape_step_[4][3] = {};  // [t][mask: none, <=, <]
+  pswa_dev::GemmEpi rms_in(pswa_dev::GemmEpi e, const float* ssq) const;
+  float *bssq_ = nullptr, *ctx_ssq_ = nullptr;  // folded-RMSNorm sums of squares [rows][d/32]
   void attention(struct Program& P, const __half* q, const int32_t* qinfo, int Mq, const int32_t* tiles,
                  int ntiles, const pswa_dev::AttnShape* shape, const __half* kv, int slot_stride,
                  int wt, int mask, const float* bias, __half* out);
