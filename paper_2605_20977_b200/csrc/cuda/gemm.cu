@@ -102,6 +102,20 @@ __device__ __forceinline__ void epi_values(const GemmEpi& ep, int n0, float (&v)
   }
 }
 
+// 256-bit global accesses (sm_100): one lane moves a whole 32 B sector per
+// instruction, so the row-per-lane epilogue writes full sectors.
+__device__ __forceinline__ void st_v8(void* p, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                      uint32_t a4, uint32_t a5, uint32_t a6, uint32_t a7) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a0), "r"(a1),
+               "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
+               : "memory");
+}
+__device__ __forceinline__ void ld_v8(const void* p, float4& x, float4& y) {
+  asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w), "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
+               : "l"(p));
+}
+
 // Residual segment (32 fp32 of output row `orow` at column oc0) loaded ahead
 // of the accumulator wait so its latency overlaps the MMAs.
 __device__ __forceinline__ void prefetch_residual(const GemmEpi& ep, int orow, int oc0,
@@ -111,8 +125,13 @@ __device__ __forceinline__ void prefetch_residual(const GemmEpi& ep, int orow, i
   if (orow < 0 || oc0 + 32 > ep.n_store) return;
   const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(ep.out) +
                                                       static_cast<size_t>(orow) * ep.ld_out + oc0);
+  if (ep.v8) {
 #pragma unroll
-  for (int q = 0; q < 8; ++q) res[q] = src[q];
+    for (int q = 0; q < 8; q += 2) ld_v8(src + q, res[q], res[q + 1]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) res[q] = src[q];
+  }
 }
 
 // Drain one accumulator row segment: lane = TMEM lane = output row, columns
@@ -137,6 +156,7 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
       float4* d4 = reinterpret_cast<float4*>(dst);
       float ss = 0.0f;
       uint32_t hp[16];
+      float4 ov[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -146,7 +166,8 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
           o.z += res[q].z;
           o.w += res[q].w;
         }
-        d4[q] = o;
+        ov[q] = o;
+        if (!ep.v8) d4[q] = o;
         ss = fmaf(o.x, o.x, ss);
         ss = fmaf(o.y, o.y, ss);
         ss = fmaf(o.z, o.z, ss);
@@ -155,10 +176,22 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
         hp[2 * q] = *reinterpret_cast<uint32_t*>(&h0);
         hp[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h1);
       }
+      if (ep.v8) {
+#pragma unroll
+        for (int q = 0; q < 8; q += 2)
+          st_v8(d4 + q, __float_as_uint(ov[q].x), __float_as_uint(ov[q].y), __float_as_uint(ov[q].z),
+                __float_as_uint(ov[q].w), __float_as_uint(ov[q + 1].x), __float_as_uint(ov[q + 1].y),
+                __float_as_uint(ov[q + 1].z), __float_as_uint(ov[q + 1].w));
+      }
       if (ep.x16_out) {  // next RMSNorm's input: fp16 copy of the updated row
         uint4* h4 = reinterpret_cast<uint4*>(ep.x16_out + static_cast<size_t>(orow) * ep.ld_x16 + oc0);
+        if (ep.v8) {
+          st_v8(h4, hp[0], hp[1], hp[2], hp[3], hp[4], hp[5], hp[6], hp[7]);
+          st_v8(h4 + 2, hp[8], hp[9], hp[10], hp[11], hp[12], hp[13], hp[14], hp[15]);
+        } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) h4[q] = make_uint4(hp[4 * q], hp[4 * q + 1], hp[4 * q + 2], hp[4 * q + 3]);
+          for (int q = 0; q < 4; ++q) h4[q] = make_uint4(hp[4 * q], hp[4 * q + 1], hp[4 * q + 2], hp[4 * q + 3]);
+        }
       }
       if (ep.ssq_out) ep.ssq_out[static_cast<size_t>(orow) * ep.ld_ssq + (oc0 >> 5)] = ss;
     } else {
@@ -173,7 +206,12 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
       __half2 h2 = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
       hp[j] = *reinterpret_cast<uint32_t*>(&h2);
     }
-    if (full) {
+    if (full && ep.v8) {
+#pragma unroll
+      for (int q = 0; q < ncols / 16; ++q)
+        st_v8(dst + 16 * q, hp[8 * q], hp[8 * q + 1], hp[8 * q + 2], hp[8 * q + 3], hp[8 * q + 4],
+              hp[8 * q + 5], hp[8 * q + 6], hp[8 * q + 7]);
+    } else if (full) {
       uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
       for (int q = 0; q < ncols / 8; ++q) d4[q] = make_uint4(hp[4 * q], hp[4 * q + 1], hp[4 * q + 2], hp[4 * q + 3]);
@@ -477,6 +515,16 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   p->K = K;
   p->BN = bn;
   p->epi = epi;
+  {  // 256-bit epilogue accesses when every row segment is 32 B aligned
+    const size_t es = epi.out_f32 || epi.act == kActHead ? 4 : 2;
+    auto al = [](const void* ptr, size_t ld_bytes) {
+      return ptr == nullptr || (reinterpret_cast<uintptr_t>(ptr) % 32 == 0 && ld_bytes % 32 == 0);
+    };
+    p->epi.v8 = al(epi.out, epi.ld_out * es) && al(epi.x16_out, static_cast<size_t>(epi.ld_x16) * 2) &&
+                        !std::getenv("PSWA_GEMM_NO_V8")
+                    ? 1
+                    : 0;
+  }
   // CTA pairs sharing B through TMA multicast: correct and available, but
   // measured neutral-to-slower on B200 (the L2 already dedups concurrent B
   // reads; 10.56 vs 10.44 ms / frame), so opt-in via PSWA_GEMM_CLUSTER=1.

@@ -45,6 +45,7 @@ struct GemmEpi {
   const float* rms_ssq = nullptr;  // consumer: [M][ld_rms] partial sums of squares of A's rows
   int ld_rms = 0, rms_parts = 0;
   float rms_inv_d = 0.0f;
+  int v8 = 0;  // set by gemm_plan: every output row segment is 32 B aligned (256-bit ld/st)
 };
 
 struct GemmPlan {
