@@ -140,7 +140,7 @@ __device__ __forceinline__ void prefetch_residual(const GemmEpi& ep, int orow, i
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
                                           const uint32_t (&raw)[32], const float4 (&res)[8],
-                                          float row_scale) {
+                                          float row_scale, bool side2) {
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]) * row_scale;
@@ -199,7 +199,8 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
         dst[j] = (EPI == kEpiF32 && ep.accumulate) ? dst[j] + v[j] : v[j];
     }
   } else {
-    __half* dst = static_cast<__half*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0;
+    __half* dst = side2 ? static_cast<__half*>(ep.out2) + static_cast<size_t>(orow) * ep.ld_out2 + oc0 - ep.split_n
+                        : static_cast<__half*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0;
     uint32_t hp[16];
 #pragma unroll
     for (int j = 0; j < ncols / 2; ++j) {
@@ -327,7 +328,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = ((u % tiles_mp) * CL + rank) * kBM, n0 = (u / tiles_mp) * BN;
       const int c0 = half * (BN / 64), c1 = (half + 1) * (BN / 64);
       const int m = m0 + q * 32 + lane;
-      const int orow = m < M ? (ep.row_map ? ep.row_map[m] : m) : -1;
+      const bool side2 = ep.out2 != nullptr && n0 >= ep.split_n;  // fused second output
+      const int* rmap = side2 ? ep.row_map2 : ep.row_map;
+      const int orow = m < M ? (rmap ? rmap[m] : m) : -1;
       float4 res[8];
       const bool acc_res = EPI == kEpiF32 && ep.accumulate;
       if (acc_res) prefetch_residual(ep, orow, n0 + c0 * 32, res);
@@ -362,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);
         }
-        epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res, row_scale);
+        epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res, row_scale, side2);
         if (acc_res && c + 1 < c1) prefetch_residual(ep, orow, n0 + (c + 1) * 32, res);
       }
     }
@@ -510,6 +513,8 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   }
   if (N % bn != 0 || (bn != 64 && bn != 128 && bn != 256))
     throw std::invalid_argument("gemm_plan: bad BN");
+  if (epi.out2 && (epi.out_f32 || epi.act != kActNone || epi.split_n % bn != 0))
+    throw std::invalid_argument("gemm_plan: split output needs fp16 out and split_n % BN == 0");
   p->M = M;
   p->N = N;
   p->K = K;
@@ -521,6 +526,7 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
       return ptr == nullptr || (reinterpret_cast<uintptr_t>(ptr) % 32 == 0 && ld_bytes % 32 == 0);
     };
     p->epi.v8 = al(epi.out, epi.ld_out * es) && al(epi.x16_out, static_cast<size_t>(epi.ld_x16) * 2) &&
+                        al(epi.out2, static_cast<size_t>(epi.ld_out2) * 2) &&
                         !std::getenv("PSWA_GEMM_NO_V8")
                     ? 1
                     : 0;

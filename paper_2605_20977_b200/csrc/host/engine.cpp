@@ -422,6 +422,13 @@ void Engine::upload_weights(const WeightMap& w) {
     put_linear(h, Kp, fv(n), in, out, 0, 0, gain);
     return PW{upload_h(h), Np, Kp};
   };
+  auto qkv = [&](const std::string& q, const std::string& k, const std::string& v, const float* gain) {
+    std::vector<__half> h(static_cast<size_t>(3 * d) * d, __float2half_rn(0.0f));
+    put_linear(h, d, fv(q), d, d, 0, 0, gain);
+    put_linear(h, d, fv(k), d, d, d, 0, gain);
+    put_linear(h, d, fv(v), d, d, 2 * d, 0, gain);
+    return PW{upload_h(h), 3 * d, d};
+  };
   auto kv = [&](const std::string& k, const std::string& v, const float* gain = nullptr) {
     std::vector<__half> h(static_cast<size_t>(2 * d) * d, __float2half_rn(0.0f));
     put_linear(h, d, fv(k), d, d, 0, 0, gain);
@@ -452,6 +459,7 @@ void Engine::upload_weights(const WeightMap& w) {
       const float* g2 = fv(p + ".norm2.g");
       B.wq = linear(p + ".wq", d, d, d, d, g1);
       B.wkv = kv(p + ".wk", p + ".wv", g1);
+      if (!B.cross) B.wqkv = qkv(p + ".wq", p + ".wk", p + ".wv", g1);
       B.wo = linear(p + ".wo", d, d, d, d);
       B.wgu = gate_up(p + ".ffn.wg", p + ".ffn.wu", d, D.f, D.fp, d, g2);
       B.wd = linear(p + ".ffn.wd", D.f, d, d, D.fp);
@@ -665,14 +673,20 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
   const int32_t* qinfo = step_qinfo_[t];
   // norm1 is folded: bxn_ holds the fp16 residual stream and bssq_ its
   // sums of squares (from the previous residual GEMM or rms_prep)
-  gemm(P, bxn_, d, M, B.wq, d, rms_in(f16_out(bq_, d), bssq_));
   const bool probe = &B == &s2_[0] && t == D.c.s - 1;  // bench_op probes (last step, S2 block 0)
-  if (probe) tag(P, "step_wq", 2.0 * M * d * d);
   if (!B.cross) {
-    GemmEpi e = rms_in(f16_out(B.kv_cache, 2 * d), bssq_);
-    e.row_map = rows;  // K/V of this step's positions into the frame cache
-    gemm(P, bxn_, d, M, B.wkv, d, e);
+    // one GEMM for Q | K V: Q rows to the batch, K/V of this step's
+    // positions into the frame cache (row map)
+    GemmEpi e = rms_in(f16_out(bq_, d), bssq_);
+    e.out2 = B.kv_cache;
+    e.ld_out2 = 2 * d;
+    e.split_n = d;
+    e.row_map2 = rows;
+    gemm(P, bxn_, d, M, B.wqkv, d, e);
+    if (probe) tag(P, "step_wq", 2.0 * M * 3.0 * d * d);
     exchange(P, xid_of(B), t);  // band mode: step-t K/V of the boundary rows
+  } else {
+    gemm(P, bxn_, d, M, B.wq, d, rms_in(f16_out(bq_, d), bssq_));
   }
   const int mk = B.cross ? 0 : 1;
   attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], &shape_step_[t][mk], B.kv_cache, 0, 0,
@@ -702,12 +716,22 @@ void Engine::build_ctx(Program& P) {
     // rows pushed by the neighbours; buffers alternate by layer so a
     // neighbour's push of layer b+1 never lands in the buffer read by layer b
     __half* kv = (B_.n > 1 && b % 2) ? ctx_kv2_ : ctx_kv_;
-    GemmEpi ekv = rms_in(f16_out(kv, 2 * d), ctx_ssq_);
-    ekv.row_map = ctx_kv_map_;
-    gemm(P, ctx_xn_, d, n, B.wkv, d, ekv);
-    exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
     float* ssq_q = ctx_ssq_ + static_cast<size_t>(q0) * (d / 32);
-    gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, rms_in(f16_out(ctx_q_, d), ssq_q));
+    if (!last) {  // Q | K V in one GEMM over all slots
+      GemmEpi e = rms_in(f16_out(ctx_q_, d), ctx_ssq_);
+      e.out2 = kv;
+      e.ld_out2 = 2 * d;
+      e.split_n = d;
+      e.row_map2 = ctx_kv_map_;
+      gemm(P, ctx_xn_, d, n, B.wqkv, d, e);
+      exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
+    } else {  // last block: K/V of every slot, queries of the last slot only
+      GemmEpi ekv = rms_in(f16_out(kv, 2 * d), ctx_ssq_);
+      ekv.row_map = ctx_kv_map_;
+      gemm(P, ctx_xn_, d, n, B.wkv, d, ekv);
+      exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
+      gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, rms_in(f16_out(ctx_q_, d), ssq_q));
+    }
     attention(P, ctx_q_, ctx_qinfo_ + q0, nq, last ? ctx_tiles_last_ : ctx_tiles_,
               last ? n_ctx_tiles_last_ : n_ctx_tiles_, &shape_ctx_, kv, HWl_, D.c.win_t, 0, pos,
               ctx_att_);

@@ -35,6 +35,7 @@ struct PW {  // packed weight: fp16 [N][K] row-major (K-major operand)
 struct Block {  // one transformer block of ctx / s1 / s2
   bool cross = false;
   PW wq, wkv, wo, wgu, wd;
+  PW wqkv;  // [wq; wk; wv] stacked (self blocks): one GEMM, Q to the batch, K/V to the cache
   float *g1 = nullptr, *g2 = nullptr, *pos = nullptr;
   __half* kv_cache = nullptr;  // self layers of s1/s2: [HW][2d]; cross: ctx K/V
 };
