@@ -90,7 +90,7 @@ struct AttnArgs {
   const int32_t* tiles;
   int d;
   int wt;  // > 0: 3D context window over wt slots
-  const float* tables;  // [heads][nsl][nbk][8] score offsets (build_score_tables)
+  const __half* tables;  // [heads][nsl][nbk][8] score offsets (build_score_tables)
   int nsl;              // slot offsets per head in `tables` (wt for 3D, 1 for 2D)
   __half* out;
   int ldo;
@@ -116,12 +116,13 @@ __global__ void __launch_bounds__(256, NCH <= 5 ? 3 : 2)
   const uint32_t sraw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
   const uint32_t sbase = (sraw + 1023u) & ~1023u;  // swizzled TMA boxes: 1024 B aligned
   uint8_t* smem = smem_raw + (sbase - sraw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + nbuf * 2 * a.kbuf);  // [2] stage-full barriers
-  float* stbl0 = reinterpret_cast<float*>(bars + 2);  // [nbuf][kAttnMaxBandKeys][8] score offsets
-  int16_t* sbk = reinterpret_cast<int16_t*>(stbl0 + 2 * kAttnMaxBandKeys * 8);  // band key: row<<8 | col
+  // [2][kAttnMaxBandKeys][8] fp16 score offsets (128 B aligned), then barriers, band keys
+  __half* stbl0 = reinterpret_cast<__half*>(smem + nbuf * 2 * a.kbuf);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stbl0 + 2 * kAttnMaxBandKeys * 8);  // [2] stage-full
+  int16_t* sbk = reinterpret_cast<int16_t*>(bars + 2);  // band key: row<<8 | col
   const int nbk = a.shape.nbk;
   const uint32_t box_bytes = static_cast<uint32_t>(HR * a.hw * 64);
-  const uint32_t tbl_bytes = static_cast<uint32_t>(nbk * 8 * 4);
+  const uint32_t tbl_bytes = static_cast<uint32_t>(nbk * 8 * 2);
   const CUtensorMap* kvm = &kvmap;  // param-space address (never copied to local memory)
 
   if (threadIdx.x == 0) {
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(256, NCH <= 5 ? 3 : 2)
     }
     wait_buf(buf);  // halo and score-offset table of this stage landed
     const uint32_t sK = sbase + buf * 2 * a.kbuf, sV = sK + a.kbuf;
-    const float* stbl = stbl0 + buf * kAttnMaxBandKeys * 8;
+    const __half* stbl = stbl0 + buf * kAttnMaxBandKeys * 8;
     if (live) {
       // pass 1: scores and their per-query max over this slot
       float s[NCH][4];
@@ -236,8 +237,8 @@ __global__ void __launch_bounds__(256, NCH <= 5 ? 3 : 2)
           ldsm_x4(sK + swz(hk[c], (lane >> 4) + 2), fa);
           mma16816(acc, fa, qb[1][0], qb[1][1]);
           const int r0 = c * 16 + (lane >> 2);
-          const float2 t0 = *reinterpret_cast<const float2*>(stbl + r0 * 8 + qc);
-          const float2 t1 = *reinterpret_cast<const float2*>(stbl + (r0 + 8) * 8 + qc);
+          const float2 t0 = __half22float2(*reinterpret_cast<const __half2*>(stbl + r0 * 8 + qc));
+          const float2 t1 = __half22float2(*reinterpret_cast<const __half2*>(stbl + (r0 + 8) * 8 + qc));
           const bool k0 = (inb >> (2 * c)) & 1u, k1 = (inb >> (2 * c + 1)) & 1u;
           s[c][0] = k0 ? fmaf(acc[0], qscale, t0.x) : -INFINITY;
           s[c][1] = k0 ? fmaf(acc[1], qscale, t0.y) : -INFINITY;
@@ -326,18 +327,19 @@ int env_int(const char* n, int dflt) {
 int box_buf_bytes(int halo_keys) { return (halo_keys * 64 + 1023) / 1024 * 1024; }
 
 int smem_bytes(int halo_keys, int dbuf) {
-  // alignment slack + K/V buffers + barriers + 2 score-offset tables + band keys
-  return 1024 + (dbuf ? 4 : 2) * box_buf_bytes(halo_keys) + 16 + 2 * kAttnMaxBandKeys * 8 * 4 +
+  // alignment slack + K/V buffers + 2 fp16 score-offset tables + barriers + band keys
+  return 1024 + (dbuf ? 4 : 2) * box_buf_bytes(halo_keys) + 2 * kAttnMaxBandKeys * 8 * 2 + 16 +
          kAttnMaxBandKeys * 2;
 }
 
 __global__ void score_table_kernel(const float* __restrict__ bias, int taps_total, const int8_t* __restrict__ taps,
-                                   int n, int nsl, float* __restrict__ out) {
-  // out[h][k][i] = log2e * bias[h][k*49 + taps[i]] or -inf (i < n = nbk*8)
+                                   int n, int nsl, __half* __restrict__ out) {
+  // out[h][k][i] = half(log2e * bias[h][k*49 + taps[i]]) or -inf (i < n = nbk*8)
   const int h = blockIdx.y, k = blockIdx.z;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int t = taps[i];
-    out[(static_cast<size_t>(h) * nsl + k) * n + i] = t >= 0 ? bias[h * taps_total + k * 49 + t] * kLog2e : -INFINITY;
+    out[(static_cast<size_t>(h) * nsl + k) * n + i] =
+        __float2half_rn(t >= 0 ? bias[h * taps_total + k * 49 + t] * kLog2e : -INFINITY);
   }
 }
 
@@ -356,7 +358,7 @@ bool window_attention_tiles_supported(int hd, int win_h, int win_w) {
 
 int window_attention_tiles_smem(int halo_keys, bool) { return smem_bytes(halo_keys, 1); }
 
-void build_score_tables(const float* bias, int heads, int wt, AttnShape shape, float* out,
+void build_score_tables(const float* bias, int heads, int wt, AttnShape shape, __half* out,
                         cudaStream_t st) {
   const int nsl = wt > 0 ? wt : 1, n = shape.nbk * 8;
   if (n == 0) return;
@@ -374,7 +376,7 @@ void window_attention_tiles_init(int max_smem_bytes) {
 
 void window_attention_tiles(const __half* q, int ldq, const int32_t* tiles, int ntiles,
                             int warps_per_tile, int halo_rows, int halo_width, AttnShape shape,
-                            const CUtensorMap& kv_map, int heads, int wt, const float* tables,
+                            const CUtensorMap& kv_map, int heads, int wt, const __half* tables,
                             __half* out, int ldo, cudaStream_t st) {
   if (ntiles <= 0) return;
   if (shape.nbk % 16 || shape.nbk > kAttnMaxBandKeys) throw std::invalid_argument("attention shape");

@@ -1,8 +1,11 @@
 // tcgen05 / TMA GEMM for sm_100a. See gemm.h for the contract.
 //
 // Persistent kernel, one CTA per SM, 128 x BN output tiles (cta_group::1,
-// UMMA M=128, N=BN, K=16 per instruction), tiles walked M-fastest so the CTAs
-// in flight share their B (weight) panel in L2. Warp roles:
+// UMMA M=128, N=BN, K=16 per instruction), tiles walked N-fastest: the
+// weights (<= 3 MB) stay L2-resident and the CTAs in flight share each
+// activation row panel, which is then read from HBM once (M-fastest order
+// re-streamed the whole activation matrix from HBM for every N tile of the
+// 32640-row context GEMMs). Warp roles:
 //   warp 0    : TMA producer (one elected lane), STAGES-deep smem ring
 //   warp 1    : TMEM allocator + MMA issuer (one elected lane)
 //   warps 2-9 : epilogue. Two TMEM accumulators (2 x BN columns) let the
@@ -244,8 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kblocks = K / kBK;
   // tile schedule: CL CTAs of a cluster take adjacent M tiles of one N tile
   const int rank = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
-  const int tiles_mp = (tiles_m + CL - 1) / CL;
-  const int n_units = tiles_mp * (num_tiles / tiles_m);
+  const int tiles_mp = (tiles_m + CL - 1) / CL, tiles_n = num_tiles / tiles_m;
+  const int n_units = tiles_mp * tiles_n;
   const int unit0 = blockIdx.x / CL, unit_step = gridDim.x / CL;
 
   if (warp == 0 && lane == 0) {
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int g = 0;  // global k-block counter across tiles
       for (int u = unit0; u < n_units; u += unit_step) {
-        const int m0 = ((u % tiles_mp) * CL + rank) * kBM, n0 = (u / tiles_mp) * BN;
+        const int m0 = ((u / tiles_n) * CL + rank) * kBM, n0 = (u % tiles_n) * BN;
         for (int kb = 0; kb < kblocks; ++kb, ++g) {
           const int s = g % S, round = g / S;
           if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
@@ -325,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0;
     for (int u = unit0; u < n_units; u += unit_step, ++it) {
       const int buf = it & 1, use = it >> 1;
-      const int m0 = ((u % tiles_mp) * CL + rank) * kBM, n0 = (u / tiles_mp) * BN;
+      const int m0 = ((u / tiles_n) * CL + rank) * kBM, n0 = (u % tiles_n) * BN;
       const int c0 = half * (BN / 64), c1 = (half + 1) * (BN / 64);
       const int m = m0 + q * 32 + lane;
       const bool side2 = ep.out2 != nullptr && n0 >= ep.split_n;  // fused second output

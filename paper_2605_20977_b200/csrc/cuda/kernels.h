@@ -85,13 +85,14 @@ void window_attention_tiles_init(int max_smem_bytes);
 // Score-offset tables of one attention layer and band shape, built once from
 // the layer's relative-position bias [heads][wt*49 or 49]: out[h][slot
 // offset][band key][query] = log2(e) * bias of the tap, -inf where the
-// window or mask excludes the pair. [heads][max(wt,1)][nbk][8] floats.
-void build_score_tables(const float* bias, int heads, int wt, AttnShape shape, float* out,
+// window or mask excludes the pair. [heads][max(wt,1)][nbk][8] fp16 (the
+// bias enters the fp32 score as its fp16 rounding, < 1e-3 relative).
+void build_score_tables(const float* bias, int heads, int wt, AttnShape shape, __half* out,
                         cudaStream_t st);
 // kv_map: make_kv_tmap() of the K/V cache (gemm.h); halos are staged by TMA.
 void window_attention_tiles(const __half* q, int ldq, const int32_t* tiles, int ntiles,
                             int warps_per_tile, int halo_rows, int halo_width, AttnShape shape,
-                            const CUtensorMap& kv_map, int heads, int wt, const float* tables,
+                            const CUtensorMap& kv_map, int heads, int wt, const __half* tables,
                             __half* out, int ldo, cudaStream_t st);
 
 // ---- convolutions for the hyperprior (conv.cu) ---------------------------

@@ -647,12 +647,12 @@ void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq
                            hw, hr);
     // score-offset tables of (layer bias, band shape): built once, reused by
     // every program that launches this layer on this shape
-    float*& tab = score_tables_[{bias, shape}];
+    __half*& tab = score_tables_[{bias, shape}];
     if (!tab && sh.nbk > 0) {
-      tab = dalloc<float>(static_cast<size_t>(D.heads) * std::max(wt, 1) * sh.nbk * 8);
+      tab = dalloc<__half>(static_cast<size_t>(D.heads) * std::max(wt, 1) * sh.nbk * 8);
       pswa_dev::build_score_tables(bias, D.heads, wt, sh, tab, st_);
     }
-    const float* tables = tab;
+    const __half* tables = tab;
     add(P, [=](cudaStream_t s) {
       pswa_dev::window_attention_tiles(q, d, tiles, ntiles, 8, hr, hw, sh, map, D.heads, wt, tables,
                                        out, d, s);

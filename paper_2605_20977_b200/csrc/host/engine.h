@@ -254,7 +254,7 @@ class Engine {
   int32_t* step_tiles_[16] = {};
   int n_step_tiles_[16] = {};
   pswa_dev::AttnShape shape_ctx_{};
-  std::map<std::pair<const float*, const pswa_dev::AttnShape*>, float*> score_tables_;
+  std::map<std::pair<const float*, const pswa_dev::AttnShape*>, __half*> score_tables_;
   pswa_dev::AttnShape shape_step_[4][3] = {};  // [t][mask: none, <=, <]
   pswa_dev::GemmEpi rms_in(pswa_dev::GemmEpi e, const float* ssq) const;
   float *bssq_ = nullptr, *ctx_ssq_ = nullptr;  // folded-RMSNorm sums of squares [rows][d/32]

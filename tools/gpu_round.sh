@@ -10,8 +10,8 @@ timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.json 2> gpu
 PSWA_NO_PDL=1 PN=5 timeout 300 python tools/kernel_times.py > gpurun_out/kt.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches.csv python tools/profile_decode.py > gpurun_out/ncu_launch.log 2>&1
 NCU="ncu --set full --clock-control none --import-source on --profile-from-start off"
-timeout 600 $NCU -k regex:window_attn_mma -c 1 -o gpurun_out/ncu_ctx_attn python tools/profile_decode.py > /dev/null 2>&1
-timeout 600 $NCU -k regex:window_attn_mma -s 66 -c 1 -o gpurun_out/ncu_step_attn python tools/profile_decode.py > /dev/null 2>&1
+timeout 600 $NCU -k regex:window_attn -c 1 -o gpurun_out/ncu_ctx_attn python tools/profile_decode.py > /dev/null 2>&1
+timeout 600 $NCU -k regex:window_attn -s 66 -c 1 -o gpurun_out/ncu_step_attn python tools/profile_decode.py > /dev/null 2>&1
 # gemm launch order of a decode: 0-4 hyper, 5-9 context block 0 (kv, q, wo, gate|up, down), ...,
 # 53 = accumulator Q projection of step 0 (M=2040 N=K=512, the step_wq shape)
 timeout 600 $NCU -k regex:gemm_tc_kernel -s 8 -c 1 -o gpurun_out/ncu_ctx_ffn_gu python tools/profile_decode.py > /dev/null 2>&1
