@@ -148,8 +148,35 @@ __device__ __forceinline__ uint32_t next_byte(const uint8_t* pl, LaneState& s, i
   return 0;
 }
 
-__device__ __forceinline__ int dec_sym(const uint8_t* pl, LaneState& s, const uint32_t* cum,
-                                       int nsym, int& err) {
+// Payload byte readers: direct (one global load per byte) and a 16 B
+// window (one aligned 16 B load per 16 bytes of a lane's stream: the
+// renormalisation byte reads are on the lane's sequential critical path).
+struct ByteDirect {
+  const uint8_t* pl;
+  __device__ __forceinline__ uint32_t get(LaneState& s, int& err) { return next_byte(pl, s, err); }
+};
+struct ByteWin {
+  const uint8_t* pl;
+  uint4 w;
+  uint32_t base;
+  __device__ __forceinline__ uint32_t get(LaneState& s, int& err) {
+    if (s.pos < s.end) {
+      const uint32_t b = s.pos & ~15u;
+      if (b != base) {  // the payload buffer extends >= 16 B past its end (capacity)
+        base = b;
+        w = __ldg(reinterpret_cast<const uint4*>(pl + b));
+      }
+      const uint32_t off = s.pos & 15u;
+      ++s.pos;
+      const uint32_t word = off < 8 ? (off < 4 ? w.x : w.y) : (off < 12 ? w.z : w.w);
+      return (word >> ((off & 3u) * 8u)) & 0xffu;
+    }
+    return next_byte(pl, s, err);  // implicit zero bytes / truncation
+  }
+};
+
+template <class R>
+__device__ __forceinline__ int dec_sym(R& rd, LaneState& s, const uint32_t* cum, int nsym, int& err) {
   const uint64_t r = s.range >> 16;
   if (s.code >= (r << 16)) {
     err = 1;
@@ -158,16 +185,16 @@ __device__ __forceinline__ int dec_sym(const uint8_t* pl, LaneState& s, const ui
   int lo = 0, hi = nsym;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (r * __ldg(cum + mid) <= s.code)
+    if (r * cum[mid] <= s.code)
       lo = mid;
     else
       hi = mid;
   }
-  const uint32_t c0 = __ldg(cum + lo), c1 = __ldg(cum + lo + 1);
+  const uint32_t c0 = cum[lo], c1 = cum[lo + 1];
   s.code -= r * c0;
   s.range = r * (c1 - c0);
   while (s.range < kBot) {
-    s.code = (s.code << 8) | next_byte(pl, s, err);
+    s.code = (s.code << 8) | rd.get(s, err);
     s.range <<= 8;
   }
   return lo;
@@ -181,20 +208,21 @@ __device__ __forceinline__ const double* bits_table(const uint32_t* cdf) {
 }
 
 // Decodes one value (escape + Exp-Golomb included); returns v.
-__device__ int32_t dec_value(const uint8_t* pl, LaneState& s, const uint32_t* cdf_row,
-                             const double* bits_row, int& err) {
-  const int k = dec_sym(pl, s, cdf_row, kSyms, err);
+template <class R>
+__device__ int32_t dec_value(R& rd, LaneState& s, const uint32_t* cdf_row, const double* bits_row,
+                             int& err) {
+  const int k = dec_sym(rd, s, cdf_row, kSyms, err);
   s.bits += __ldg(bits_row + k);
   if (k < kEscLo) return k - 127;
   int nb = 0;
-  while (dec_sym(pl, s, kBitCum, 2, err) == 0) {
+  while (dec_sym(rd, s, kBitCum, 2, err) == 0) {
     if (++nb > 31 || err) {
       err = 1;
       return 0;
     }
   }
   uint64_t x = 1;
-  for (int i = 0; i < nb; ++i) x = (x << 1) | static_cast<uint64_t>(dec_sym(pl, s, kBitCum, 2, err));
+  for (int i = 0; i < nb; ++i) x = (x << 1) | static_cast<uint64_t>(dec_sym(rd, s, kBitCum, 2, err));
   s.bits += 2 * nb + 1;
   const long long m = static_cast<long long>(x) - 1 + 128;
   return static_cast<int32_t>(k == kEscLo ? -m : m);
@@ -259,8 +287,18 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
                                     const float* __restrict__ scales, const uint32_t* __restrict__ cdf,
                                     const int* __restrict__ rows, int32_t* __restrict__ yhat, int C,
                                     int c0, __half* __restrict__ yhat16, int ld16, int* status) {
+  // the 64 scale thresholds and the 64 cumulative tables (66 KB) staged in
+  // shared memory: the sigma -> table and symbol binary searches are
+  // dependent-load chains that otherwise run at L2 latency
+  extern __shared__ uint4 s_raw[];
+  uint32_t* s_cdf = reinterpret_cast<uint32_t*>(s_raw);
+  float* s_scales = reinterpret_cast<float*>(s_cdf + kScales * (kSyms + 1));
+  constexpr int kCdf4 = kScales * (kSyms + 1) / 4;
+  for (int i = threadIdx.x; i < kCdf4; i += blockDim.x) s_raw[i] = reinterpret_cast<const uint4*>(cdf)[i];
+  for (int i = threadIdx.x; i < kScales; i += blockDim.x) s_scales[i] = scales[i];
   pdl_wait();
   pdl_trigger();
+  __syncthreads();
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
   const uint64_t total = static_cast<uint64_t>(n) * per;
@@ -269,16 +307,35 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
   if (first >= o0 + total) return;
   LaneState s = lanes[l];
   int err = 0;
-  for (uint64_t o = first; o < o0 + total; o += L) {
-    const int i = static_cast<int>(o - o0);
-    const int k = i / per, j = i - k * per;
-    const float mu = musig[static_cast<size_t>(k) * ldms + j];
-    const float sg = musig[static_cast<size_t>(k) * ldms + sig_off + j];
-    const int idx = scale_index(scales, sg);
-    const int32_t v = dec_value(pl, s, cdf + idx * (kSyms + 1), bits_table(cdf) + idx * kSyms, err);
-    const int32_t y = v + __float2int_rn(mu);
-    yhat[static_cast<size_t>(rows[k]) * C + c0 + j] = y;
-    if (yhat16) yhat16[static_cast<size_t>(k) * ld16 + c0 + j] = __int2half_rn(y);
+  ByteWin rd{pl, make_uint4(0, 0, 0, 0), 0xffffffffu};
+  // the parameters (mu, table index) of a lane's next symbols do not depend
+  // on the coder state: gather them in a batch (loads in flight together),
+  // then run the sequential decode chain
+  constexpr int kB = 8;
+  const uint64_t end = o0 + total;
+  for (uint64_t base = first; base < end; base += static_cast<uint64_t>(kB) * L) {
+    int mu_r[kB], idx[kB], dst[kB], k16[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const uint64_t o = base + static_cast<uint64_t>(q) * L;
+      idx[q] = -1;
+      if (o < end) {
+        const int i = static_cast<int>(o - o0);
+        const int k = i / per, j = i - k * per;
+        mu_r[q] = __float2int_rn(musig[static_cast<size_t>(k) * ldms + j]);
+        idx[q] = scale_index(s_scales, musig[static_cast<size_t>(k) * ldms + sig_off + j]);
+        dst[q] = rows[k] * C + c0 + j;
+        k16[q] = k * ld16 + c0 + j;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      if (idx[q] < 0) break;
+      const int32_t v = dec_value(rd, s, s_cdf + idx[q] * (kSyms + 1), bits_table(cdf) + idx[q] * kSyms, err);
+      const int32_t y = v + mu_r[q];
+      yhat[dst[q]] = y;
+      if (yhat16) yhat16[k16[q]] = __int2half_rn(y);
+    }
   }
   lanes[l] = s;
   if (err) atomicOr(status, 2);
@@ -298,7 +355,8 @@ __global__ void decode_hyper_kernel(const uint8_t* __restrict__ pl, LaneState* _
   for (int i = l; i < n; i += L) {
     const int ch = i / per_ch;
     const int idx = scale_index(scales, scale[ch]);
-    const int32_t v = dec_value(pl, s, cdf + idx * (kSyms + 1), bits_table(cdf) + idx * kSyms, err);
+    ByteDirect rd{pl};
+    const int32_t v = dec_value(rd, s, cdf + idx * (kSyms + 1), bits_table(cdf) + idx * kSyms, err);
     zhat[i] = v + __float2int_rn(loc[ch]);
   }
   lanes[l] = s;
@@ -449,7 +507,13 @@ void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_
                         const uint32_t* cdf, const int* rows, int32_t* yhat, int C, int c0,
                         __half* yhat16, int ld16, int* status, cudaStream_t st) {
   if (n <= 0) return;
-  launch_k(decode_phase_kernel, dim3(blocks(L)), dim3(128), 0, st, payload, lanes, L, o0, n, per, musig, ldms,
+  constexpr int smem = (kScales * (kSyms + 1) + kScales) * 4;
+  static const bool attr = [] {
+    PSWA_CUDA(cudaFuncSetAttribute(decode_phase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    return true;
+  }();
+  (void)attr;
+  launch_k(decode_phase_kernel, dim3(blocks(L)), dim3(128), smem, st, payload, lanes, L, o0, n, per, musig, ldms,
                                                   sig_off, scales, cdf, rows, yhat, C, c0, yhat16,
                                                   ld16, status);
   PSWA_LAUNCH_CHECK();

@@ -1,7 +1,4 @@
 mkdir -p gpurun_out
-timeout 300 python tools/probe_ops.py 2>&1 | tail -1
-timeout 900 python -m pytest tests/test_gpu_pipeline.py tests/test_gpu_bands.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "gpu rc=$?"
-tail -3 gpurun_out/pytest_gpu.log
-python -c "
-import json; d=json.load(open('gpurun_out/parity.json'))
-for k,v in d.items(): print(k, {a:v[a] for a in ('mu_max_abs','sigma_max_rel','rate_rel_err','frac_within_tol') if a in v})"
+PSWA_NO_PDL=1 PN=5 timeout 300 python tools/kernel_times.py 2>&1 | grep -v Warn | grep -E "warm|decode_phase"
+timeout 900 python -m pytest tests/test_gpu_pipeline.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "gpu rc=$?"
+tail -2 gpurun_out/pytest_gpu.log
