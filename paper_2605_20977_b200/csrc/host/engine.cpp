@@ -94,6 +94,9 @@ Engine::Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len, in
   HWo_ = B_.nown * D_.W;
   PSWA_CUDA(cudaSetDevice(device));
   PSWA_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  PSWA_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  PSWA_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  PSWA_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   const WeightMap w = parse_psww(cfg, blob, len);
   build_tables();
   alloc_all();
@@ -109,6 +112,9 @@ Engine::~Engine() {
   if (st_) cudaStreamSynchronize(st_);
   for (void* p : ipc_mapped_) cudaIpcCloseMemHandle(p);
   for (void* p : allocs_) cudaFree(p);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
+  if (side_) cudaStreamDestroy(side_);
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -584,6 +590,26 @@ void Engine::add(Program& P, std::function<void(cudaStream_t)> op, int launches)
   P.launches += launches;
 }
 
+// Moves ops [from, end) onto the side stream: a fork (event record on the
+// main stream, wait on the side stream) precedes them; join_side() later
+// makes the main stream wait for the side stream. Both are capturable.
+void Engine::to_side(Program& P, size_t from) {
+  std::vector<std::function<void(cudaStream_t)>> moved(P.ops.begin() + from, P.ops.end());
+  P.ops.resize(from);
+  P.ops.push_back([this](cudaStream_t s) {
+    PSWA_CUDA(cudaEventRecord(ev_fork_, s));
+    PSWA_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+  });
+  for (auto& op : moved) P.ops.push_back([op, this](cudaStream_t) { op(side_); });
+}
+
+void Engine::join_side(Program& P) {
+  P.ops.push_back([this](cudaStream_t s) {
+    PSWA_CUDA(cudaEventRecord(ev_join_, side_));
+    PSWA_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+  });
+}
+
 void Engine::gemm(Program& P, const __half* A, int lda, int M, const PW& B, int K, const GemmEpi& ep) {
   pswa_dev::GemmPlan plan;
   pswa_dev::gemm_plan(&plan, A, lda, M, B.p, B.K, B.N, K, ep);
@@ -965,6 +991,11 @@ Program& Engine::program(const std::string& key) {
   const size_t yoff = static_cast<size_t>(B_.own0) * D.W * C;  // own rows in yfr_
   const std::string base = key.substr(0, key.find('+'));  // "+ms": mu/sigma outputs
   if (base == "decode") {
+    // the hyperprior branch (z_hat lanes -> hyper decoder -> Hq) does not
+    // depend on the context transformer: it runs on a side stream of the
+    // same graph and joins before the first Hq consumer (band mode: before
+    // the first exchange, since each segment is its own graph)
+    const size_t side_from = P.ops.size();
     add(P, [=, this](cudaStream_t s) {
       pswa_dev::lanes_init(d_hyper_, d_lens_, Lz, static_cast<uint32_t>(nz), hlanes_, status_, s);
     });
@@ -973,11 +1004,14 @@ Program& Engine::program(const std::string& key) {
                                    scales_, cdf_, zhat_, status_, s);
     });
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_lane_bits(hlanes_, Lz, bits_, s); });
+    build_hyper_decode(P);
+    to_side(P, side_from);
+    if (B_.n > 1) join_side(P);
     add(P, [=, this](cudaStream_t s) {
       pswa_dev::lanes_init(d_main_, d_lens_ + 1, L, static_cast<uint32_t>(HW) * C, lanes_, status_, s);
     });
-    build_hyper_decode(P);
     build_ctx(P);
+    if (B_.n == 1) join_side(P);
     for (int t = 0; t < D.c.s; ++t) {
       if (t > 0) build_s1(P, t - 1, false);
       build_step(P, t, 0);

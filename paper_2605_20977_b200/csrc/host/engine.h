@@ -180,6 +180,10 @@ class Engine {
   void build_step(Program& P, int t, int mode /*0 decode, 1 encode*/);
   void build_embed(Program& P, int t);
   void run(Program& P);
+  void to_side(Program& P, size_t from);
+  void join_side(Program& P);
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   void tag(Program& P, const std::string& name, double flops);
   double attn_flops(int t, int mask, int unused) const;
   std::map<std::string, std::pair<std::function<void(cudaStream_t)>, double>> probes_;
