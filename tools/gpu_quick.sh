@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 300 python tools/probe_ops.py 2>&1 | tail -1
+PSWA_NO_PDL=1 PN=5 timeout 300 python tools/kernel_times.py 2>&1 | grep -v Warn | grep -E "warm|decode_phase"
 timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu --no-config4 --no-config5 > gpurun_out/bench_q.json 2> gpurun_out/bench_q.err; echo "bench rc=$?"; tail -3 gpurun_out/bench_q.err
 python -c "
 import json; d=json.load(open('gpurun_out/bench_q.json'))
