@@ -65,6 +65,10 @@ typedef struct pswa_cfg {
   int height, width;/* latent grid H x W (multiples of 4) */
   int lanes;        /* main-payload coder lanes          */
   int hyper_lanes;  /* hyper-payload coder lanes         */
+  int prior;        /* main-latent parameter head: 0 Gaussian,
+                       1 Laplace with scale b = the head's sigma output
+                       (north_star "Gaussian or Laplace parameter head");
+                       the hyperprior stays Gaussian */
 } pswa_cfg;
 
 /* Fill the paper (preset=1) or desk (preset=0) defaults for an H x W grid. */
@@ -198,6 +202,8 @@ int pswa_gpu_op_window_attn(const void* q, int ld_q, const int32_t* qinfo, int M
                             int s, const float* bias, void* out, int ld_out, void* stream);
 /* 64 cumulative tables x 258 u32, built on the device. */
 int pswa_gpu_op_build_cdf(uint32_t* cdf_out /* host [64*258] */, float* scales_out /* [64] */);
+/* laplace = 1: the Laplace tables of the prior = 1 parameter head. */
+int pswa_gpu_op_build_cdf_family(uint32_t* cdf_out, float* scales_out, int laplace);
 
 #ifdef __cplusplus
 }

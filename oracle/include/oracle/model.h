@@ -23,6 +23,7 @@ struct Config {
   int wh = 7, ww = 7, wt = 5, T = 4, rates = 4;
   int H = 16, W = 16;
   int lanes = 1, hyper_lanes = 1;
+  int prior = 0;  // main-latent head: 0 Gaussian, 1 Laplace (tables offset kScales)
   int hd() const { return d / heads; }
   int f() const { return ffn_hidden(d); }
   int slot() const { return d_ch / N; }
@@ -83,13 +84,19 @@ Weights from_psww(const Config& c, const uint8_t* data, size_t n);
 constexpr int kScales = 64;
 constexpr int kSupport = 127;          // v in [-127, 127]
 constexpr int kSyms = 2 * kSupport + 3;  // 255 in-range + 2 escapes = 257
+// Tables: [0, 64) discretised Gaussian, [64, 128) the
+// Laplace family of the prior = 1 head (scale b = the table sigma).
 struct Tables {
   float scale[kScales];
-  uint32_t cdf[kScales][kSyms + 1];  // cumulative, c[0]=0, c[257]=65536
+  uint32_t cdf[2 * kScales][kSyms + 1];  // cumulative, c[0]=0, c[257]=65536
 };
 const Tables& tables();
 int scale_index(float sigma);  // smallest i with scale[i] >= sigma, else 63
-void build_cdf(int idx, uint32_t* cum /* kSyms+1 */);
+// Table of a main-latent symbol: the sigma index in the head's family.
+inline int main_index(const Config& c, float sigma) {
+  return scale_index(sigma) + (c.prior ? kScales : 0);
+}
+void build_cdf(int idx, uint32_t* cum /* kSyms+1 */);  // idx >= kScales: Laplace
 
 struct CodedSym {  // one latent symbol ready for the coder
   int32_t v;        // y_hat - round(mu)  (escape when |v| > 127)

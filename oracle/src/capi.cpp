@@ -1,5 +1,5 @@
 // ORACLE — test infrastructure only: C entry points for tests/ (ctypes) and
-// bench.py's cpu_baseline leg. Config is passed as the 20 ints of pswa_cfg.
+// bench.py's cpu_baseline leg. Config is passed as the 21 ints of pswa_cfg.
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -34,6 +34,7 @@ Config to_cfg(const int* a) {
   c.W = a[17];
   c.lanes = a[18];
   c.hyper_lanes = a[19];
+  c.prior = a[20];
   return c;
 }
 
@@ -134,7 +135,10 @@ int oracle_validate_schedule(int H, int W, int s, int wh, int ww, int N, int* st
 
 // ---- coder -----------------------------------------------------------------
 void oracle_scale_table(float* out) { std::memcpy(out, tables().scale, sizeof(float) * kScales); }
-void oracle_cdf_tables(uint32_t* out) { std::memcpy(out, tables().cdf, sizeof(tables().cdf)); }
+void oracle_cdf_tables(uint32_t* out) { std::memcpy(out, tables().cdf, sizeof(tables().cdf) / 2); }
+void oracle_cdf_tables_family(int laplace, uint32_t* out) {
+  std::memcpy(out, tables().cdf[laplace ? kScales : 0], sizeof(tables().cdf) / 2);
+}
 int oracle_scale_index(float s) { return scale_index(s); }
 int oracle_encode_lanes(const int32_t* v, const int32_t* idx, size_t n, int lanes, uint8_t* out,
                         size_t cap, size_t* len) {

@@ -23,6 +23,8 @@ int sym_of(int32_t v) {
 
 void build_cdf(int idx, uint32_t* cum) {
   // scale table: 64 log-spaced sigmas in [0.11, 64]
+  const bool laplace = idx >= kScales;
+  if (laplace) idx -= kScales;
   const double ratio = det::log(64.0 / 0.11);
   const double sigma = static_cast<float>(0.11 * det::exp(ratio * idx / 63.0));
   const double inv = 1.0 / (sigma * 1.4142135623730951);
@@ -31,12 +33,25 @@ void build_cdf(int idx, uint32_t* cum) {
     if (p < 0.0) p = 0.0;
     return 1u + static_cast<uint32_t>(std::floor(p * 65279.0));
   };
-  freq[kSupport] = q(det::erf(0.5 * inv));
-  for (int v = 1; v <= kSupport; ++v) {
-    const double p = 0.5 * (det::erf((v + 0.5) * inv) - det::erf((v - 0.5) * inv));
-    freq[kSupport + v] = freq[kSupport - v] = q(p);
+  if (!laplace) {
+    freq[kSupport] = q(det::erf(0.5 * inv));
+    for (int v = 1; v <= kSupport; ++v) {
+      const double p = 0.5 * (det::erf((v + 0.5) * inv) - det::erf((v - 0.5) * inv));
+      freq[kSupport + v] = freq[kSupport - v] = q(p);
+    }
+    freq[kEscLo] = freq[kEscHi] = q(0.5 * (1.0 - det::erf((kSupport + 0.5) * inv)));
+  } else {
+    // discretised Laplace with scale b = sigma: F(x) = 1 - exp(-x / b) / 2,
+    // x >= 0, so p(0) = 1 - exp(-1/(2b)), p(v) = (exp(-(v-1/2)/b) -
+    // exp(-(v+1/2)/b)) / 2, tail = exp(-(127+1/2)/b) / 2
+    const double ib = 1.0 / sigma;
+    freq[kSupport] = q(1.0 - det::exp(-0.5 * ib));
+    for (int v = 1; v <= kSupport; ++v) {
+      const double p = 0.5 * (det::exp(-(v - 0.5) * ib) - det::exp(-(v + 0.5) * ib));
+      freq[kSupport + v] = freq[kSupport - v] = q(p);
+    }
+    freq[kEscLo] = freq[kEscHi] = q(0.5 * det::exp(-(kSupport + 0.5) * ib));
   }
-  freq[kEscLo] = freq[kEscHi] = q(0.5 * (1.0 - det::erf((kSupport + 0.5) * inv)));
   uint32_t sum = 0;
   for (int k = 0; k < kSyms; ++k) sum += freq[k];
   freq[kSupport] += 65536u - sum;  // deficit to the mode keeps symmetry
@@ -52,6 +67,7 @@ const Tables& tables() {
     for (int i = 0; i < kScales; ++i) {
       t.scale[i] = static_cast<float>(0.11 * det::exp(ratio * i / 63.0));
       build_cdf(i, t.cdf[i]);
+      build_cdf(kScales + i, t.cdf[kScales + i]);
     }
   });
   return t;

@@ -53,7 +53,7 @@ std::vector<CodedSym> main_symbols(const Model& m, const int32_t* yhat, const fl
       for (int p : pos)
         for (int j = 0; j < Cg; ++j) {
           const size_t e = static_cast<size_t>(g * Cg + j) * hw + p;
-          out.push_back({yhat[e] - rint_i(mu[e]), scale_index(sigma[e])});
+          out.push_back({yhat[e] - rint_i(mu[e]), main_index(c, sigma[e])});
         }
   }
   return out;
@@ -136,7 +136,7 @@ Decoded decode_wavefront(const Model& m, const Payload& pl, int rate, int fidx,
         for (int j = 0; j < Cg; ++j) {
           const int ch = g * Cg + j;
           const float mv = mu[k * c.C + ch];
-          const int idx = scale_index(sg[k * c.C + ch]);
+          const int idx = main_index(c, sg[k * c.C + ch]);
           const int32_t v = dec.decode(ordinal++, idx);
           out.yhat[static_cast<size_t>(ch) * hw + pos[k]] = v + rint_i(mv);
           out.main_bits += bits_of({v, idx});
@@ -174,7 +174,7 @@ Decoded decode_serial(const Model& m, const Payload& pl, int rate, int fidx,
         channel_heads(m, s2, out.yhat.data(), {p}, rate, g + 1, mu, sg);
         for (int j = 0; j < Cg; ++j) {
           const int ch = g * Cg + j;
-          const int idx = scale_index(sg[ch]);
+          const int idx = main_index(c, sg[ch]);
           const int32_t v = dec.decode(ordinal++, idx);
           out.yhat[static_cast<size_t>(ch) * hw + p] = v + rint_i(mu[ch]);
           out.main_bits += bits_of({v, idx});

@@ -24,7 +24,7 @@ class PswaCfg(C.Structure):
     _fields_ = [(n, C.c_int) for n in (
         "d_spatial", "heads", "ctx_blocks", "s1_blocks", "s2_blocks", "d_channel",
         "ch_blocks", "hyper_ch", "latent_ch", "s", "n_groups", "win_h", "win_w", "win_t",
-        "ctx_slots", "rate_points", "height", "width", "lanes", "hyper_lanes")]
+        "ctx_slots", "rate_points", "height", "width", "lanes", "hyper_lanes", "prior")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -61,6 +61,7 @@ _SIGS = {
     "pswa_gpu_op_window_attn": (_I, [_VP, _I, _VP, _I, _VP, _I, _I, _I, _I, _I, _I, _I, _I, _I,
                                      _I, _I, _VP, _VP, _I, _VP]),
     "pswa_gpu_op_build_cdf": (_I, [_VP, _VP]),
+    "pswa_gpu_op_build_cdf_family": (_I, [_VP, _VP, _I]),
     "pswa_band_rows": (_I, [_I, _I, _I, C.POINTER(_I), C.POINTER(_I)]),
     "pswa_group_create": (_I, [_VP, _I, C.POINTER(PswaCfg), _VP, _SZ, C.POINTER(_VP)]),
     "pswa_group_destroy": (None, [_VP]),

@@ -90,7 +90,7 @@ __device__ __forceinline__ double sym_bits(uint32_t freq) {
   return 16.0 - log2(static_cast<double>(freq));
 }
 
-__global__ void build_cdf_kernel(float* scales, uint32_t* cdf) {
+__global__ void build_cdf_kernel(float* scales, uint32_t* cdf, int laplace) {
   pdl_wait();
   pdl_trigger();
   const int idx = threadIdx.x;
@@ -105,12 +105,22 @@ __global__ void build_cdf_kernel(float* scales, uint32_t* cdf) {
     if (p < 0.0) p = 0.0;
     return 1u + static_cast<uint32_t>(floor(p * 65279.0));
   };
-  freq[127] = q(d_erf(0.5 * inv));
-  for (int v = 1; v <= 127; ++v) {
-    const double p = 0.5 * (d_erf((v + 0.5) * inv) - d_erf((v - 0.5) * inv));
-    freq[127 + v] = freq[127 - v] = q(p);
+  if (!laplace) {  // Gaussian: p(v) = Phi((v+1/2)/sigma) - Phi((v-1/2)/sigma)
+    freq[127] = q(d_erf(0.5 * inv));
+    for (int v = 1; v <= 127; ++v) {
+      const double p = 0.5 * (d_erf((v + 0.5) * inv) - d_erf((v - 0.5) * inv));
+      freq[127 + v] = freq[127 - v] = q(p);
+    }
+    freq[kEscLo] = freq[kEscHi] = q(0.5 * (1.0 - d_erf(127.5 * inv)));
+  } else {  // Laplace, scale b = sigma: F(x) = 1 - exp(-x/b) / 2 for x >= 0
+    const double ib = 1.0 / sigma;
+    freq[127] = q(1.0 - d_exp(-0.5 * ib));
+    for (int v = 1; v <= 127; ++v) {
+      const double p = 0.5 * (d_exp(-(v - 0.5) * ib) - d_exp(-(v + 0.5) * ib));
+      freq[127 + v] = freq[127 - v] = q(p);
+    }
+    freq[kEscLo] = freq[kEscHi] = q(0.5 * d_exp(-127.5 * ib));
   }
-  freq[kEscLo] = freq[kEscHi] = q(0.5 * (1.0 - d_erf(127.5 * inv)));
   uint32_t sum = 0;
   for (int k = 0; k < kSyms; ++k) sum += freq[k];
   freq[127] += 65536u - sum;
@@ -491,8 +501,8 @@ inline int blocks(long n, int t = 128) { return static_cast<int>((n + t - 1) / t
 
 }  // namespace
 
-void build_cdf_tables(float* scales, uint32_t* cdf, cudaStream_t st) {
-  launch_k(build_cdf_kernel, dim3(1), dim3(kScales), 0, st, scales, cdf);
+void build_cdf_tables(float* scales, uint32_t* cdf, cudaStream_t st, int laplace) {
+  launch_k(build_cdf_kernel, dim3(1), dim3(kScales), 0, st, scales, cdf, laplace);
   PSWA_LAUNCH_CHECK();
 }
 

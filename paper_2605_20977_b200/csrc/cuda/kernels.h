@@ -116,7 +116,9 @@ constexpr int kSyms = 257;  // v in [-127,127] + 2 escapes
 // in fp64 with IEEE round-to-nearest ops only (bit-exact with the host rule),
 // followed (at cdf + 64*258, 8-byte aligned) by 64 x 257 fp64 symbol costs.
 constexpr size_t kCdfWords = static_cast<size_t>(kScales) * (kSyms + 1) + 2 * kScales * kSyms;
-void build_cdf_tables(float* scales, uint32_t* cdf, cudaStream_t st);
+// laplace = 1: discretised Laplace with scale b = sigma instead (same 64
+// scales, same quantisation rule).
+void build_cdf_tables(float* scales, uint32_t* cdf, cudaStream_t st, int laplace = 0);
 
 struct LaneState {
   uint64_t code, range;  // decoder: code; encoder: low

@@ -298,12 +298,16 @@ int pswa_gpu_op_window_attn(const void* q, int ld_q, const int32_t* qinfo, int M
 }
 
 int pswa_gpu_op_build_cdf(uint32_t* cdf_out, float* scales_out) {
+  return pswa_gpu_op_build_cdf_family(cdf_out, scales_out, 0);
+}
+
+int pswa_gpu_op_build_cdf_family(uint32_t* cdf_out, float* scales_out, int laplace) {
   return guard([&] {
     float* ds = nullptr;
     uint32_t* dc = nullptr;
     PSWA_CUDA(cudaMalloc(&ds, sizeof(float) * pswa_dev::kScales));
     PSWA_CUDA(cudaMalloc(&dc, sizeof(uint32_t) * pswa_dev::kCdfWords));
-    pswa_dev::build_cdf_tables(ds, dc, nullptr);
+    pswa_dev::build_cdf_tables(ds, dc, nullptr, laplace);
     PSWA_CUDA(cudaMemcpy(scales_out, ds, sizeof(float) * pswa_dev::kScales, cudaMemcpyDeviceToHost));
     PSWA_CUDA(cudaMemcpy(cdf_out, dc, sizeof(uint32_t) * pswa_dev::kScales * (pswa_dev::kSyms + 1),
                          cudaMemcpyDeviceToHost));

@@ -101,7 +101,14 @@ Engine::Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len, in
   build_tables();
   alloc_all();
   upload_weights(w);
-  pswa_dev::build_cdf_tables(scales_, cdf_, st_);
+  pswa_dev::build_cdf_tables(scales_, cdf_, st_);  // Gaussian (hyperprior, and main when prior = 0)
+  if (D_.c.prior == 1) {
+    float* tmp_scales = dalloc<float>(pswa_dev::kScales);
+    cdf_main_ = dalloc<uint32_t>(pswa_dev::kCdfWords);
+    pswa_dev::build_cdf_tables(tmp_scales, cdf_main_, st_, 1);
+  } else {
+    cdf_main_ = cdf_;
+  }
   PSWA_CUDA(cudaStreamSynchronize(st_));
 }
 
@@ -966,7 +973,7 @@ void Engine::build_step(Program& P, int t, int mode) {
     if (mode == 0) {
       const int L = D.c.lanes;
       add(P, [=, this](cudaStream_t s) {
-        pswa_dev::lanes_decode_phase(d_main_, lanes_, L, o0, M, Cg, musig_, ms, Cg, scales_, cdf_,
+        pswa_dev::lanes_decode_phase(d_main_, lanes_, L, o0, M, Cg, musig_, ms, Cg, scales_, cdf_main_,
                                      rows, yfr_, C, c0, y16_, C, status_, s);
       });
     } else {
@@ -1061,7 +1068,7 @@ Program& Engine::program(const std::string& key) {
                            d_hyper_, hyper_cap_, pack_total_, pack_offs_, status_, s);
     }, 2);
     add(P, [=, this](cudaStream_t s) {
-      pswa_dev::lanes_encode(sym_v_, sym_idx_, static_cast<uint64_t>(HW) * C, L, cdf_, enc_lanes_,
+      pswa_dev::lanes_encode(sym_v_, sym_idx_, static_cast<uint64_t>(HW) * C, L, cdf_main_, enc_lanes_,
                              enc_cap_, enc_lens_, enc_bits_, status_, s);
     });
     add(P, [=, this](cudaStream_t s) {

@@ -268,6 +268,7 @@ class Engine {
   int* crop_rows_ = nullptr;  // padded hyper grid index -> raster index (-1: pad)
   float* scales_ = nullptr;
   uint32_t* cdf_ = nullptr;
+  uint32_t* cdf_main_ = nullptr;  // main-latent tables (== cdf_ for the Gaussian head)
 
   // frame buffers
   int32_t *yfr_ = nullptr, *ychw_ = nullptr, *zhat_ = nullptr;

@@ -65,6 +65,7 @@ void validate_cfg(const pswa_cfg& c) {
   req(c.height > 0 && c.width > 0 && c.height < 4096 && c.width < 4096, "grid");
   req(c.s >= 1 && c.ctx_slots >= 1 && c.ctx_slots < 64 && c.rate_points >= 1, "s / T / R");
   req(c.lanes >= 1 && c.hyper_lanes >= 1, "lanes");
+  req(c.prior == 0 || c.prior == 1, "prior must be 0 (Gaussian) or 1 (Laplace)");
   req(c.win_t * c.win_h * c.win_w <= 256, "window taps <= 256");
   const int hd = c.d_spatial / c.heads;
   req(hd == 4 || hd == 8 || hd == 16 || hd == 32 || hd == 64, "head_dim in {4..64}");

@@ -17,7 +17,7 @@ REF_SO = os.path.join(ROOT, "oracle", "_ref", "libpswa_ref.so")
 
 CFG_FIELDS = ("d_spatial", "heads", "ctx_blocks", "s1_blocks", "s2_blocks", "d_channel",
               "ch_blocks", "hyper_ch", "latent_ch", "s", "n_groups", "win_h", "win_w", "win_t",
-              "ctx_slots", "rate_points", "height", "width", "lanes", "hyper_lanes")
+              "ctx_slots", "rate_points", "height", "width", "lanes", "hyper_lanes", "prior")
 
 _P = C.c_void_p
 _fp = C.POINTER(C.c_float)
@@ -28,13 +28,13 @@ def preset(paper: bool, H: int, W: int, lanes: int = 1, hyper_lanes: int = 1, **
              s1_blocks=8 if paper else 2, s2_blocks=8 if paper else 2,
              d_channel=1024 if paper else 128, ch_blocks=2, hyper_ch=128 if paper else 32,
              latent_ch=192, s=4, n_groups=4, win_h=7, win_w=7, win_t=5, ctx_slots=4,
-             rate_points=4, height=H, width=W, lanes=lanes, hyper_lanes=hyper_lanes)
+             rate_points=4, height=H, width=W, lanes=lanes, hyper_lanes=hyper_lanes, prior=0)
     c.update(over)
     return c
 
 
 def cfg_array(cfg: dict):
-    return (C.c_int * 20)(*[int(cfg[f]) for f in CFG_FIELDS])
+    return (C.c_int * len(CFG_FIELDS))(*[int(cfg[f]) for f in CFG_FIELDS])
 
 
 def ptr(a: np.ndarray):
@@ -231,4 +231,11 @@ def cdf_tables() -> np.ndarray:
 def scale_table() -> np.ndarray:
     t = np.zeros(64, np.float32)
     oracle().oracle_scale_table(ptr(t))
+    return t
+
+
+def cdf_tables_family(laplace: int) -> np.ndarray:
+    """The 64 cumulative tables of the Gaussian (0) or Laplace (1) head."""
+    t = np.zeros((64, 258), np.uint32)
+    oracle().oracle_cdf_tables_family(int(laplace), ptr(t))
     return t

@@ -224,3 +224,36 @@ def test_rmsnorm_op():
     xr = x.view(300, 2, 256)
     ref = (xr / torch.sqrt((xr * xr).mean(-1, keepdim=True) + 1e-5)).view(300, 512) * g
     assert torch.allclose(y.float(), ref, atol=2e-3, rtol=2e-3)
+
+
+def test_cdf_tables_laplace_bitexact():
+    """Device-built Laplace tables (fp64, no FMA) equal the host oracle's."""
+    from oracle_api import cdf_tables_family
+    cdf = np.zeros((64, 258), np.uint32)
+    sc = np.zeros(64, np.float32)
+    check(lib().pswa_gpu_op_build_cdf_family(cdf.ctypes.data_as(C.c_void_p),
+                                             sc.ctypes.data_as(C.c_void_p), 1))
+    assert np.array_equal(cdf, cdf_tables_family(1))
+
+
+@pytest.mark.parametrize("paper,H,W", [(False, 16, 16), (True, 16, 16)])
+def test_laplace_head_roundtrip_and_rate(paper, H, W):
+    """prior = 1: GPU encode -> decode bit-exact; mu/sigma and rate vs the
+    oracle under the same tolerances as the Gaussian head."""
+    c = preset(paper, H, W, lanes=64, hyper_lanes=16, prior=1)
+    blob = gen_weights(c, 1)
+    om = OracleModel(c, blob)
+    g = GpuCodec(cfg_from_dict(c), blob)
+    rng = np.random.default_rng(11)
+    y = laplace_yhat(rng, 192, H, W)
+    hyper, main, bits_e = g.encode_frame(y, rate=0, fidx=0)
+    z = g.last_zhat()
+    g.reset_gop()
+    yd, bits_d = g.decode_frame(hyper, main, rate=0, fidx=0)
+    assert np.array_equal(yd, y)
+    g.reset_gop()
+    mu_g, sg_g, bits_g = g.forward_params(y, z, rate=0, fidx=0)
+    mu_o, sg_o, _ = om.forward(y, rate=0, zhat=z)
+    bits_o = om.encode(y, rate=0, fidx=0, zhat=z)[2]
+    compare_params(f"laplace_{'paper' if paper else 'desk'}_{H}x{W}", mu_g, sg_g, mu_o, sg_o,
+                   bits_g, bits_o)
