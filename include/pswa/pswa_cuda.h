@@ -139,6 +139,24 @@ int pswa_gpu_bench_op(pswa_gpu* h, const char* name, int reps, double* us_per_la
 /* Stream the handle runs on (cudaStream_t as void*). */
 void* pswa_gpu_stream(pswa_gpu* h);
 
+/* ---- sequences (encode_sequence / decode_sequence) -----
+ * Container layout: FORMAT.md (header "PSWA", per-frame hyper + main
+ * payloads). Frame f of the sequence has frame_idx_in_gop = f % gop_size and
+ * the temporal ring resets at every GOP start. */
+int pswa_gpu_encode_sequence(pswa_gpu* h, const int32_t* frames /* [F][C][H][W] */, int n_frames,
+                             int gop_size, int rate_idx, uint8_t* out, size_t cap, size_t* len);
+/* Decodes the whole frames present (a truncated tail frame is ignored).
+ * A frame that fails (corrupt / truncated payload) gets its status code in
+ * frame_status and decoding resumes at the next GOP boundary (frames in
+ * between get -1); the call itself fails only on a bad header, a config or
+ * weights hash mismatch (PSWA_E_HASH) or too small an output. */
+int pswa_gpu_decode_sequence(pswa_gpu* h, const uint8_t* container, size_t len, int32_t* frames_out,
+                             int max_frames, int* frame_status /* nullable [max_frames] */,
+                             double* bits_out /* nullable [max_frames][2] */, int* n_frames);
+/* Header fields: info[0..9] = version, W_px, H_px, frame_count, gop_size,
+ * rate_idx, s, N, prior, whole frames present. Host only. */
+int pswa_container_info(const uint8_t* container, size_t len, int* info);
+
 /* ---- row bands (BASELINE config 5) -----------------------
  * One frame decoded as n row bands, one device handle per band (bands may
  * share a device). Band b owns latent rows [row0, row1) (multiples of 4); its

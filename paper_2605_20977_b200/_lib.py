@@ -73,6 +73,9 @@ _SIGS = {
     "pswa_group_forward_params": (_I, [_VP, _VP, _VP, _I, _I, _VP, _VP, _D]),
     "pswa_group_last_zhat": (_I, [_VP, _VP]),
     "pswa_group_last_launch_count": (_I, [_VP]),
+    "pswa_gpu_encode_sequence": (_I, [_VP, _VP, _I, _I, _I, _VP, _SZ, C.POINTER(_SZ)]),
+    "pswa_gpu_decode_sequence": (_I, [_VP, _VP, _SZ, _VP, _I, _VP, _D, C.POINTER(_I)]),
+    "pswa_container_info": (_I, [_VP, _SZ, C.POINTER(_I)]),
     "pswa_gpu_create_band": (_I, [_I, C.POINTER(PswaCfg), _VP, _SZ, _I, _I, C.POINTER(_VP)]),
     "pswa_gpu_band_export": (_I, [_VP, _VP, _SZ, C.POINTER(_SZ)]),
     "pswa_gpu_band_link": (_I, [_VP, _VP, _SZ, _VP, _SZ]),

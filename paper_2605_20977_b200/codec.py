@@ -136,6 +136,30 @@ class GpuCodec:
                                             bits.ctypes.data_as(C.POINTER(C.c_double))))
         return mu, sg, bits
 
+    def encode_sequence(self, frames: np.ndarray, gop: int = 32, rate: int = 0) -> bytes:
+        """frames [F][C][H][W] -> PSWA container (FORMAT.md); resets the ring."""
+        f = np.ascontiguousarray(frames, np.int32)
+        n = C.c_size_t()
+        cap = 20 * f.size + (1 << 20) * max(1, f.shape[0])
+        buf = np.zeros(cap, np.uint8)
+        check(lib().pswa_gpu_encode_sequence(self.h, _ptr(f), f.shape[0], gop, rate, _ptr(buf), cap,
+                                             C.byref(n)))
+        return bytes(buf[:n.value])
+
+    def decode_sequence(self, container: bytes, max_frames: int | None = None):
+        """-> (frames [F][C][H][W], status [F] (0 ok, -1 skipped, >0 error), bits [F][2])."""
+        info = container_info(container)
+        mf = info["frames_present"] if max_frames is None else max_frames
+        out = np.zeros((max(mf, 1),) + self.shape, np.int32)
+        st = np.zeros(max(mf, 1), np.int32)
+        bits = np.zeros((max(mf, 1), 2), np.float64)
+        n = C.c_int()
+        cb = np.frombuffer(container, np.uint8)
+        check(lib().pswa_gpu_decode_sequence(self.h, _ptr(cb), len(container), _ptr(out), mf,
+                                             _ptr(st), bits.ctypes.data_as(C.POINTER(C.c_double)),
+                                             C.byref(n)))
+        return out[:n.value], st[:n.value], bits[:n.value]
+
     def decode_device(self, d_hyper: int, hyper_len: int, d_main: int, main_len: int, rate: int,
                       fidx: int, advance: bool, d_out: int):
         check(lib().pswa_gpu_decode_frame_device(self.h, d_hyper, hyper_len, d_main, main_len,
@@ -186,6 +210,15 @@ def split_banded(main: bytes, n: int) -> list[bytes]:
         out.append(main[off:off + l])
         off += l
     return out
+
+
+def container_info(container: bytes) -> dict:
+    """Header of a PSWA sequence container (FORMAT.md); host only."""
+    v = (C.c_int * 10)()
+    cb = np.frombuffer(container, np.uint8)
+    check(lib().pswa_container_info(_ptr(cb), len(container), v))
+    keys = ("version", "w_px", "h_px", "frames", "gop", "rate", "s", "N", "prior", "frames_present")
+    return dict(zip(keys, list(v)))
 
 
 def band_rows(height: int, n_bands: int, band: int) -> tuple[int, int]:

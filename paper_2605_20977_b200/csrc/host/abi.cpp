@@ -8,12 +8,16 @@
 #include "../cuda/kernels.h"
 #include "abi_util.h"
 #include "engine.h"
+#include "container.h"
 #include "group.h"
+#include "pswa/rng.h"
 #include "model_spec.h"
 #include "pswa/pswa_cuda.h"
 
 struct pswa_gpu {
   std::unique_ptr<pswa_host::Engine> eng;
+  pswa_cfg cfg{};
+  uint64_t weights_hash = 0;
 };
 struct pswa_group {
   std::unique_ptr<pswa_host::BandGroup> grp;
@@ -68,6 +72,8 @@ int pswa_gpu_create(int device, const pswa_cfg* cfg, const void* blob, size_t le
   return guard([&] {
     auto h = std::make_unique<pswa_gpu>();
     h->eng = std::make_unique<pswa_host::Engine>(device, *cfg, blob, len);
+    h->cfg = *cfg;
+    h->weights_hash = pswa::fnv1a64(blob, len);
     *out = h.release();
   });
 }
@@ -198,6 +204,91 @@ int pswa_gpu_bench_op(pswa_gpu* h, const char* name, int reps, double* us, doubl
 }
 
 void* pswa_gpu_stream(pswa_gpu* h) { return h->eng->stream(); }
+
+// ---- sequences ----------------------------------------------------------------
+int pswa_gpu_encode_sequence(pswa_gpu* h, const int32_t* frames, int n_frames, int gop_size,
+                             int rate_idx, uint8_t* out, size_t cap, size_t* len) {
+  return guard([&] {
+    if (n_frames < 0 || gop_size < 1) throw std::invalid_argument("n_frames / gop_size");
+    const pswa_cfg& c = h->cfg;
+    pswa_host::ContainerHeader hd;
+    hd.w_px = static_cast<uint32_t>(c.width) * 16;
+    hd.h_px = static_cast<uint32_t>(c.height) * 16;
+    hd.frames = static_cast<uint32_t>(n_frames);
+    hd.gop = static_cast<uint32_t>(gop_size);
+    hd.rate = static_cast<uint32_t>(rate_idx);
+    hd.s = static_cast<uint32_t>(c.s);
+    hd.N = static_cast<uint32_t>(c.n_groups);
+    hd.cfg_hash = pswa_host::stream_cfg_hash(c, 1);
+    hd.weights_hash = h->weights_hash;
+    hd.prior = static_cast<uint32_t>(c.prior);
+    std::vector<uint8_t> o;
+    pswa_host::write_header(o, hd);
+    const size_t fsz = static_cast<size_t>(c.latent_ch) * c.height * c.width;
+    const size_t pcap = 20 * fsz + (1 << 20);
+    std::vector<uint8_t> hb(pcap), mb(pcap);
+    for (int f = 0; f < n_frames; ++f) {
+      if (f % gop_size == 0) h->eng->reset_gop();
+      const auto r = h->eng->encode(frames + f * fsz, rate_idx, f % gop_size, nullptr, nullptr,
+                                    nullptr, hb.data(), pcap, mb.data(), pcap, true);
+      pswa_host::append_frame(o, hb.data(), r.hyper_len, mb.data(), r.main_len);
+    }
+    *len = o.size();
+    if (out) {
+      if (cap < o.size()) throw std::invalid_argument("encode_sequence: output buffer too small");
+      std::memcpy(out, o.data(), o.size());
+    }
+  });
+}
+
+int pswa_gpu_decode_sequence(pswa_gpu* h, const uint8_t* cont, size_t len, int32_t* frames_out,
+                             int max_frames, int* frame_status, double* bits_out, int* n_frames) {
+  return guard([&] {
+    std::vector<pswa_host::FrameRef> fr;
+    const auto hd = pswa_host::parse_container(cont, len, &fr);
+    const pswa_cfg& c = h->cfg;
+    if (hd.cfg_hash != pswa_host::stream_cfg_hash(c, static_cast<int>(hd.n_bands)) || hd.n_bands != 1)
+      throw pswa_abi::HashError("decode_sequence: stream config differs from the handle's");
+    if (hd.weights_hash != h->weights_hash)
+      throw pswa_abi::HashError("decode_sequence: stream was coded with other weights");
+    const int n = static_cast<int>(fr.size());
+    if (n > max_frames) throw std::invalid_argument("decode_sequence: output buffer too small");
+    const size_t fsz = static_cast<size_t>(c.latent_ch) * c.height * c.width;
+    int resume = 0;  // first frame to attempt (after a failure: the next GOP start)
+    for (int f = 0; f < n; ++f) {
+      if (frame_status) frame_status[f] = -1;
+      if (f < resume) continue;
+      const int fidx = static_cast<int>(f % hd.gop);
+      if (fidx == 0) h->eng->reset_gop();
+      try {
+        const auto r = h->eng->decode(cont + fr[f].hyper_off, fr[f].hyper_len, cont + fr[f].main_off,
+                                      fr[f].main_len, static_cast<int>(hd.rate), fidx, true,
+                                      frames_out + f * fsz, false);
+        if (frame_status) frame_status[f] = 0;
+        if (bits_out) {
+          bits_out[2 * f] = r.bits[0];
+          bits_out[2 * f + 1] = r.bits[1];
+        }
+      } catch (const pswa_abi::TruncatedError&) {
+        if (frame_status) frame_status[f] = PSWA_E_TRUNCATED;
+        resume = static_cast<int>((f / hd.gop + 1) * hd.gop);
+      }
+    }
+    *n_frames = n;
+  });
+}
+
+int pswa_container_info(const uint8_t* cont, size_t len, int* info) {
+  return guard([&] {
+    std::vector<pswa_host::FrameRef> fr;
+    const auto hd = pswa_host::parse_container(cont, len, &fr);
+    const int v[10] = {pswa_host::kContainerVersion, static_cast<int>(hd.w_px), static_cast<int>(hd.h_px),
+                       static_cast<int>(hd.frames), static_cast<int>(hd.gop), static_cast<int>(hd.rate),
+                       static_cast<int>(hd.s), static_cast<int>(hd.N), static_cast<int>(hd.prior),
+                       static_cast<int>(fr.size())};
+    std::memcpy(info, v, sizeof(v));
+  });
+}
 
 // ---- row bands --------------------------------------------------------------
 int pswa_band_rows(int height, int n_bands, int band_idx, int* row0, int* row1) {
