@@ -244,6 +244,34 @@ def config4_gop_batch(torch, rank, world, GpuCodec, gen_weights, make_cfg, synth
             "latents_per_s_this_rank": len(decs) * steps * H * W / (ms * 1e-3), "bit_exact": exact}
 
 
+def lrp_1080p(GpuCodec, gen_weights, make_cfg, synth_latent, frames_timed=3, blocks=4):
+    """The LRP transformer (paper scale 4 blocks) after the
+    1080p P-frame decode: decode-only vs decode + LRP in the same frame
+    program (host API, synced), eps produced on the device."""
+    cfg0 = make_cfg("paper", H, W, lanes=LANES, hyper_lanes=HYPER_LANES)
+    cfg = make_cfg("paper", H, W, lanes=LANES, hyper_lanes=HYPER_LANES, lrp_blocks=blocks)
+    blob = gen_weights(cfg, 1)
+    frames = [synth_latent(cfg, 0, f) for f in range(GOP_INDEX + 1)]
+    enc = GpuCodec(cfg, blob)
+    for f in frames[:GOP_INDEX]:
+        enc.push_frame(f)
+    h, m, _ = enc.encode_frame(frames[GOP_INDEX], fidx=GOP_INDEX)
+    enc.close()
+    dec = GpuCodec(cfg, blob)
+    for f in frames[:GOP_INDEX]:
+        dec.push_frame(f)
+    ts = []
+    for _ in range(frames_timed + 1):
+        t0 = time.perf_counter()
+        y, _ = dec.decode_frame(h, m, fidx=GOP_INDEX, advance=False)
+        ts.append(time.perf_counter() - t0)
+    eps = dec.last_eps()
+    assert np.array_equal(y, frames[GOP_INDEX]) and np.abs(eps).max() < 0.5
+    dec.close()
+    return {"workload": "1080p P-frame decode + LRP transformer (4 blocks, T+1 = 5 slots), paper scale",
+            "decode_plus_lrp_e2e_ms": 1e3 * statistics.median(ts[1:]), "lrp_blocks": blocks}
+
+
 def config5_single_gpu(GpuCodec, BandGroupCodec, gen_weights, make_cfg, synth_latent, n_bands=8,
                        frames_timed=3):
     """BASELINE config 5 on one GPU: the 4K P-frame (240x136 latents, GOP
@@ -433,6 +461,12 @@ def run_ours(args, rank, world, local):
                   "bit_exact": okr == 0.0, "timing": "CUDA events, fork/join over the handle streams, max over ranks"}
     except Exception as e:
         c4 = {"error": f"{type(e).__name__}: {e}"[:300]}
+    lrp = None
+    try:
+        if rank == 0 and not args.no_lrp:
+            lrp = lrp_1080p(GpuCodec, gen_weights, make_cfg, synth_latent)
+    except Exception as e:
+        lrp = {"error": f"{type(e).__name__}: {e}"[:300]}
     c5 = None
     try:
         if world == 1 and not args.no_config5:
@@ -478,6 +512,7 @@ def run_ours(args, rank, world, local):
         "kernel_rooflines": kroof,
         "config4_gop_batch": c4,
         "config5_4k": c5,
+        "lrp": lrp,
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": "latents/s",
                 "h2d_bytes_per_step": len(hyper) + len(main), "d2h_bytes_per_step": 192 * H * W * 4,
@@ -500,6 +535,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-config5", action="store_true", help="skip the 4K row-band measurement")
     ap.add_argument("--no-config4", action="store_true", help="skip the GOP-batch measurement")
+    ap.add_argument("--no-lrp", action="store_true", help="skip the LRP measurement")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

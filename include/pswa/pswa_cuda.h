@@ -69,6 +69,8 @@ typedef struct pswa_cfg {
                        1 Laplace with scale b = the head's sigma output
                        (north_star "Gaussian or Laplace parameter head");
                        the hyperprior stays Gaussian */
+  int lrp_blocks;   /* LRP transformer blocks; 0 = no LRP
+                       (eps = 0). Paper scale uses 4. */
 } pswa_cfg;
 
 /* Fill the paper (preset=1) or desk (preset=0) defaults for an H x W grid. */
@@ -107,6 +109,10 @@ int pswa_gpu_decode_frame(pswa_gpu* h, const uint8_t* hyper, size_t hyper_len,
 int pswa_gpu_forward_params(pswa_gpu* h, const int32_t* yhat, const int32_t* zhat, int rate_idx,
                             int frame_idx_in_gop, float* mu_out, float* sigma_out,
                             double* bits_out /* [2], nullable */);
+/* LRP transformer output eps [C][H][W] of the last frame
+ * decoded or encoded by this handle (computed in the same frame program
+ * when cfg.lrp_blocks > 0); the reconstruction input is y_hat + eps. */
+int pswa_gpu_last_eps(pswa_gpu* h, float* eps_out);
 /* Returns the z_hat the encoder produced for the last encode_frame call. */
 int pswa_gpu_last_zhat(pswa_gpu* h, int32_t* zhat_out);
 /* Append a decoded / known frame to the temporal ring. */

@@ -24,6 +24,7 @@ struct Config {
   int H = 16, W = 16;
   int lanes = 1, hyper_lanes = 1;
   int prior = 0;  // main-latent head: 0 Gaussian, 1 Laplace (tables offset kScales)
+  int lrp_blocks = 0;  // LRP transformer blocks (0: no LRP, eps = 0)
   int hd() const { return d / heads; }
   int f() const { return ffn_hidden(d); }
   int slot() const { return d_ch / N; }
@@ -143,13 +144,23 @@ Tok accumulate(const Model& m, const Tok& hq, const Tok& s1);
 // Channel transformer + heads for a set of positions. s2: [HW][d];
 // yhat [C][H][W]; writes mu/sigma [npos][C] for groups < n_groups_out.
 void channel_heads(const Model& m, const Tok& s2, const int32_t* yhat, const std::vector<int>& pos,
-                   int rate, int n_groups_out, float* mu, float* sigma);
+                   int rate, int n_groups_out, float* mu, float* sigma, Tok* final_rep = nullptr);
+
+// LRP transformer (A8): eps [C][H][W] =
+// 0.5 tanh(head(rmsnorm(x))) of the current slot after lrp_blocks of 3D SWA
+// over T + 1 slots: the T past slots carry the context transformer's inputs
+// (embedded past y_hat or the learned pad), the current slot
+// in_proj(concat(final channel representation, y_hat)).
+std::vector<float> lrp_forward(const Model& m, const Tok& final_rep /*[HW][d_ch]*/,
+                               const int32_t* yhat, const std::vector<const float*>& slots);
 
 // Full teacher-forced forward (encoder side): mu/sigma [C][H][W].
 struct Forward {
   Tok ctx, s1, hq, a, s2;
   std::vector<int32_t> zhat;
   std::vector<float> mu, sigma;
+  Tok final_rep;             // [HW][d_ch] normalised channel output (LRP input)
+  std::vector<float> eps;    // [C][H][W] (empty when lrp_blocks == 0)
 };
 // past: up to T previous y_hat frames, oldest first (empty -> I-frame).
 Forward forward(const Model& m, const int32_t* yhat, const int32_t* zhat_or_null, int rate,

@@ -1,5 +1,5 @@
 // ORACLE — test infrastructure only: C entry points for tests/ (ctypes) and
-// bench.py's cpu_baseline leg. Config is passed as the 21 ints of pswa_cfg.
+// bench.py's cpu_baseline leg. Config is passed as the 22 ints of pswa_cfg.
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -35,6 +35,7 @@ Config to_cfg(const int* a) {
   c.lanes = a[18];
   c.hyper_lanes = a[19];
   c.prior = a[20];
+  c.lrp_blocks = a[21];
   return c;
 }
 
@@ -199,6 +200,16 @@ int oracle_forward(void* h, const int32_t* yhat, const int32_t* zhat_or_null, in
     std::memcpy(sigma, f.sigma.data(), f.sigma.size() * sizeof(float));
     if (zhat_out) std::memcpy(zhat_out, f.zhat.data(), f.zhat.size() * sizeof(int32_t));
     if (s2_out) std::memcpy(s2_out, f.s2.data(), f.s2.size() * sizeof(float));
+  });
+}
+
+int oracle_lrp(void* h, const int32_t* yhat, const int32_t* zhat, int rate,
+               const int32_t* const* past, int npast, float* eps) {
+  return guard([&] {
+    const Model& m = *static_cast<Model*>(h);
+    if (m.c.lrp_blocks <= 0) throw std::invalid_argument("oracle_lrp: lrp_blocks == 0");
+    const Forward f = forward(m, yhat, zhat, rate, past_list(past, npast));
+    std::memcpy(eps, f.eps.data(), f.eps.size() * sizeof(float));
   });
 }
 

@@ -301,7 +301,7 @@ Tok accumulate(const Model& m, const Tok& hq, const Tok& s1) {
 }
 
 void channel_heads(const Model& m, const Tok& s2, const int32_t* yhat, const std::vector<int>& pos,
-                   int rate, int n_out, float* mu, float* sigma) {
+                   int rate, int n_out, float* mu, float* sigma, Tok* final_rep) {
   const Config& c = m.c;
   const int n = static_cast<int>(pos.size()), d = c.d, sl = c.slot(), Cg = c.Cg(), hw = c.HW();
   const int dch = c.d_ch;
@@ -361,6 +361,7 @@ void channel_heads(const Model& m, const Tok& s2, const int32_t* yhat, const std
   }
   (void)act;
   const Tok fo = norm_rows(x, n, dch, m.w["ch.norm_out.g"], sl);
+  if (final_rep) *final_rep = fo;
   const float* rso = m.w["rate.out"] + static_cast<size_t>(rate) * c.C;
   for (int g = 0; g < n_out; ++g) {
     const Tok fg = get_cols(fo, g * sl, sl);
@@ -411,10 +412,74 @@ Forward forward(const Model& m, const int32_t* yhat, const int32_t* zhat_or_null
   f.a = accumulate(m, f.hq, f.s1);
   f.s2 = spatial_forward(m, "s2", c.s2_blocks, f.a, f.ctx);
   std::vector<float> mu_t(static_cast<size_t>(hw) * c.C), sg_t(mu_t.size());
-  channel_heads(m, f.s2, yhat, iota(hw), rate, c.N, mu_t.data(), sg_t.data());
+  channel_heads(m, f.s2, yhat, iota(hw), rate, c.N, mu_t.data(), sg_t.data(), &f.final_rep);
   f.mu = tok_to_chw(mu_t, c.C, hw);
   f.sigma = tok_to_chw(sg_t, c.C, hw);
+  if (c.lrp_blocks > 0) f.eps = lrp_forward(m, f.final_rep, yhat, slots);
   return f;
+}
+
+std::vector<float> lrp_forward(const Model& m, const Tok& final_rep, const int32_t* yhat,
+                               const std::vector<const float*>& slots) {
+  const Config& c = m.c;
+  const int hw = c.HW(), d = c.d, T = c.T, S = T + 1, dch = c.d_ch, kin = dch + c.C;
+  // current slot: in_proj(concat(final_rep, y_hat)) + bias
+  Tok cat(static_cast<size_t>(hw) * kin);
+  for (int p = 0; p < hw; ++p) {
+    std::memcpy(cat.data() + static_cast<size_t>(p) * kin, final_rep.data() + static_cast<size_t>(p) * dch,
+                sizeof(float) * dch);
+    for (int ch = 0; ch < c.C; ++ch)
+      cat[static_cast<size_t>(p) * kin + dch + ch] = static_cast<float>(yhat[static_cast<size_t>(ch) * hw + p]);
+  }
+  Tok cur = mm(cat, hw, kin, m.w["lrp.in.w"], d);
+  const float* bin = m.w["lrp.in.b"];
+  for (int p = 0; p < hw; ++p)
+    for (int j = 0; j < d; ++j) cur[static_cast<size_t>(p) * d + j] += bin[j];
+  // slots 0..T-1: the context transformer's inputs; slot T: the current frame
+  Tok x(static_cast<size_t>(S) * hw * d);
+  const float* pad = m.w["pad"];
+  for (int t = 0; t < T; ++t)
+    for (int p = 0; p < hw; ++p)
+      std::memcpy(x.data() + (static_cast<size_t>(t) * hw + p) * d,
+                  slots[t] ? slots[t] + static_cast<size_t>(p) * d : pad, sizeof(float) * d);
+  std::memcpy(x.data() + static_cast<size_t>(T) * hw * d, cur.data(), cur.size() * sizeof(float));
+  std::vector<int> all_pos;
+  for (int t = 0; t < S; ++t)
+    for (int p = 0; p < hw; ++p) all_pos.push_back(p);
+  for (int b = 0; b < c.lrp_blocks; ++b) {
+    const std::string P = "lrp.b" + std::to_string(b);
+    const bool last = b == c.lrp_blocks - 1;
+    const int n = S * hw;
+    const Tok xn = norm_rows(x, n, d, m.w[P + ".norm1.g"], d);
+    const Tok K = mm(xn, n, d, m.w[P + ".wk"], d);
+    const Tok V = mm(xn, n, d, m.w[P + ".wv"], d);
+    const int q0 = last ? T * hw : 0;  // last block: the current slot's queries only
+    const int nq = n - q0;
+    Tok xq(xn.begin() + static_cast<size_t>(q0) * d, xn.end());
+    const Tok Q = mm(xq, nq, d, m.w[P + ".wq"], d);
+    std::vector<int> qpos(all_pos.begin() + q0, all_pos.end()), qslot(static_cast<size_t>(nq));
+    for (int i = 0; i < nq; ++i) qslot[i] = (q0 + i) / hw;
+    Tok att(static_cast<size_t>(nq) * d);
+    window_attention(c, nq, Q.data(), qpos.data(), qslot.data(), K.data(), V.data(), 1, kNone,
+                     m.w[P + ".pos"], att.data());
+    const Tok o = mm(att, nq, d, m.w[P + ".wo"], d);
+    Tok xs(x.begin() + static_cast<size_t>(q0) * d, x.end());
+    add_into(xs, o);
+    const Tok xn2 = norm_rows(xs, nq, d, m.w[P + ".norm2.g"], d);
+    add_into(xs, swiglu_rows(xn2, nq, d, c.f(), m.w[P + ".ffn.wg"], m.w[P + ".ffn.wu"],
+                             m.w[P + ".ffn.wd"]));
+    std::memcpy(x.data() + static_cast<size_t>(q0) * d, xs.data(), xs.size() * sizeof(float));
+  }
+  Tok xc(x.begin() + static_cast<size_t>(T) * hw * d, x.end());
+  const Tok xo = norm_rows(xc, hw, d, m.w["lrp.norm_out.g"], d);
+  Tok e = mm(xo, hw, d, m.w["lrp.head.w"], c.C);
+  const float* hb = m.w["lrp.head.b"];
+  for (int p = 0; p < hw; ++p)
+    for (int ch = 0; ch < c.C; ++ch) {
+      float& v = e[static_cast<size_t>(p) * c.C + ch];
+      v = 0.5f * det::tanh_f32(v + hb[ch]);
+    }
+  return tok_to_chw(e, c.C, hw);
 }
 
 }  // namespace oracle

@@ -15,6 +15,7 @@ std::string Config::canonical() const {
     << ";s2=" << s2_blocks << ";dch=" << d_ch << ";chb=" << ch_blocks << ";hc=" << hyper_ch
     << ";C=" << C << ";s=" << s << ";N=" << N << ";wh=" << wh << ";ww=" << ww << ";wt=" << wt
     << ";T=" << T << ";R=" << rates;
+  if (lrp_blocks > 0) o << ";lrp=" << lrp_blocks;
   return o.str();
 }
 
@@ -184,6 +185,26 @@ std::vector<ParamSpec> param_specs(const Config& c) {
       add(P + ".w2", {sl, Cg}, 0, sl);
       add(P + ".b2", {Cg}, 1, 1);
     }
+  if (c.lrp_blocks > 0) {  // LRP transformer (A8)
+    add("lrp.in.w", {dch + c.C, d}, 0, dch + c.C);
+    add("lrp.in.b", {d}, 1, 1);
+    for (int i = 0; i < c.lrp_blocks; ++i) {
+      const std::string P = "lrp.b" + std::to_string(i);
+      add(P + ".norm1.g", {d}, 2, 1);
+      add(P + ".wq", {d, d}, 0, d);
+      add(P + ".wk", {d, d}, 0, d);
+      add(P + ".wv", {d, d}, 0, d);
+      add(P + ".wo", {d, d}, 0, d);
+      add(P + ".pos", {h, c.taps3()}, 0, c.taps3());
+      add(P + ".norm2.g", {d}, 2, 1);
+      add(P + ".ffn.wg", {d, f}, 0, d);
+      add(P + ".ffn.wu", {d, f}, 0, d);
+      add(P + ".ffn.wd", {f, d}, 0, f);
+    }
+    add("lrp.norm_out.g", {d}, 2, 1);
+    add("lrp.head.w", {d, c.C}, 0, d);
+    add("lrp.head.b", {c.C}, 1, 1);
+  }
   return v;
 }
 

@@ -24,7 +24,7 @@ class PswaCfg(C.Structure):
     _fields_ = [(n, C.c_int) for n in (
         "d_spatial", "heads", "ctx_blocks", "s1_blocks", "s2_blocks", "d_channel",
         "ch_blocks", "hyper_ch", "latent_ch", "s", "n_groups", "win_h", "win_w", "win_t",
-        "ctx_slots", "rate_points", "height", "width", "lanes", "hyper_lanes", "prior")]
+        "ctx_slots", "rate_points", "height", "width", "lanes", "hyper_lanes", "prior", "lrp_blocks")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -47,6 +47,7 @@ _SIGS = {
     "pswa_gpu_decode_frame": (_I, [_VP, _VP, _SZ, _VP, _SZ, _I, _I, _I, _VP, _D]),
     "pswa_gpu_forward_params": (_I, [_VP, _VP, _VP, _I, _I, _VP, _VP, _D]),
     "pswa_gpu_last_zhat": (_I, [_VP, _VP]),
+    "pswa_gpu_last_eps": (_I, [_VP, _VP]),
     "pswa_gpu_push_frame": (_I, [_VP, _VP, _I]),
     "pswa_gpu_decode_frame_device": (_I, [_VP, _VP, _SZ, _VP, _SZ, _I, _I, _I, _VP]),
     "pswa_gpu_debug_fetch": (_I, [_VP, C.c_char_p, _VP, _SZ, C.POINTER(_SZ)]),

@@ -115,6 +115,12 @@ class GpuCodec:
         check(lib().pswa_gpu_last_zhat(self.h, _ptr(z)))
         return z
 
+    def last_eps(self) -> np.ndarray:
+        """LRP output eps [C][H][W] of the last decoded / encoded frame."""
+        e = np.zeros(self.shape, np.float32)
+        check(lib().pswa_gpu_last_eps(self.h, _ptr(e)))
+        return e
+
     def decode_frame(self, hyper: bytes, main: bytes, rate: int = 0, fidx: int = 0,
                      advance: bool = True):
         hb = np.frombuffer(hyper, np.uint8)

@@ -102,6 +102,9 @@ __device__ __forceinline__ void epi_values(const GemmEpi& ep, int n0, float (&v)
   if (ep.act == kActSilu) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
+  } else if (ep.act == kActTanhHalf) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = 0.5f * tanhf(v[j]);
   }
 }
 

@@ -17,6 +17,7 @@ enum GemmAct : int {
   kActSilu = 1,
   kActSwiGLU = 2,  // columns interleaved (gate_j, up_j): out_j = silu(g)*u
   kActHead = 3,    // n < split: mu = (acc+b)*scale ; else sigma = 0.11+softplus(acc+b)
+  kActTanhHalf = 4,  // 0.5 * tanh(acc * scale + b): the LRP output eps
 };
 
 struct GemmEpi {

@@ -189,6 +189,10 @@ int pswa_gpu_forward_params(pswa_gpu* h, const int32_t* yhat, const int32_t* zha
   });
 }
 
+int pswa_gpu_last_eps(pswa_gpu* h, float* eps_out) {
+  return guard([&] { h->eng->last_eps(eps_out); });
+}
+
 int pswa_gpu_last_zhat(pswa_gpu* h, int32_t* zhat_out) {
   return guard([&] { h->eng->last_zhat(zhat_out); });
 }

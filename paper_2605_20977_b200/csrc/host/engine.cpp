@@ -84,6 +84,8 @@ Engine::Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len, in
   B_.idx = band_idx;
   B_.n = n_bands;
   band_rows(D_.H, n_bands, band_idx, &B_.r0, &B_.r1);
+  if (n_bands > 1 && D_.c.lrp_blocks > 0)
+    throw std::invalid_argument("band mode does not run the LRP transformer (lrp_blocks must be 0)");
   if (n_bands > 1 && (D_.c.s != 4 || D_.c.win_h != 7 || B_.r1 - B_.r0 < kHaloRows))
     throw std::invalid_argument("band mode needs s = 4, a 7-row window and >= 3 rows per band");
   B_.lo = n_bands > 1 ? std::max(0, B_.r0 - kHaloTop) : 0;
@@ -160,14 +162,17 @@ void Engine::alloc_all() {
     step_rows_pad_[t] = up(rp);
   }
   {
-    // context queries: own rows of every slot, [T][HWo]; local coordinates
-    std::vector<int> qi(static_cast<size_t>(T) * HWo), km(static_cast<size_t>(T) * HWo);
-    for (int j = 0; j < T; ++j)
+    // 3D-stack queries: own rows of every slot, [S][HWo]; local coordinates
+    // (S = T for the context transformer, T + 1 for the LRP transformer)
+    const int Smax = T + (D.c.lrp_blocks > 0 ? 1 : 0);
+    std::vector<int> qi(static_cast<size_t>(Smax) * HWo), km(static_cast<size_t>(T) * HWo);
+    for (int j = 0; j < Smax; ++j)
       for (int p = 0; p < HWo; ++p) {
         qi[static_cast<size_t>(j) * HWo + p] = (j << 24) | ((own0 + p / D.W) << 12) | (p % D.W);
-        km[static_cast<size_t>(j) * HWo + p] = j * HWl + own0 * D.W + p;
+        if (j < T) km[static_cast<size_t>(j) * HWo + p] = j * HWl + own0 * D.W + p;
       }
     ctx_qinfo_ = up(qi);
+    tiles_ctx_.qinfo = tiles_lrp_.qinfo = ctx_qinfo_;
     if (B_.n > 1) ctx_kv_map_ = up(km);
     // tap tables and aligned tiles assume s = 4 (4-row step blocks repeat the
     // same query / step pattern); other schedules use the SIMT kernel
@@ -176,10 +181,10 @@ void Engine::alloc_all() {
       constexpr int TI = pswa_dev::kAttnTileInts;
       // context: CTA = 8 warps as 2 x 4 blocks of 2x4 queries (a 4 x 16 query
       // rectangle of one slot), halo 10 rows x 23 columns
-      auto ctx_tiles = [&](int slot_from, int row_base) {
+      auto ctx_tiles = [&](int slot_from, int row_base, int S) {
         std::vector<int> v;
         const int yend = own0 + B_.nown;
-        for (int j = slot_from; j < T; ++j)
+        for (int j = slot_from; j < S; ++j)
           for (int y0 = own0; y0 < yend; y0 += 4)
             for (int x0 = 0; x0 < D.W; x0 += 16) {
               std::vector<int> t(TI, -1);
@@ -202,11 +207,15 @@ void Engine::alloc_all() {
             }
         return v;
       };
-      const auto all = ctx_tiles(0, 0), last = ctx_tiles(T - 1, (T - 1) * HWo);
-      n_ctx_tiles_ = static_cast<int>(all.size()) / TI;
-      n_ctx_tiles_last_ = static_cast<int>(last.size()) / TI;
-      ctx_tiles_ = up(all);
-      ctx_tiles_last_ = up(last);
+      auto make = [&](int S, Tiles3d& tl) {
+        const auto all = ctx_tiles(0, 0, S), last = ctx_tiles(S - 1, (S - 1) * HWo, S);
+        tl.n_all = static_cast<int>(all.size()) / TI;
+        tl.n_last = static_cast<int>(last.size()) / TI;
+        tl.all = up(all);
+        tl.last = up(last);
+      };
+      make(T, tiles_ctx_);
+      if (D.c.lrp_blocks > 0) make(T + 1, tiles_lrp_);
       // step batches: CTA = 8 warps as 4 x 2 blocks of 4x8 (a 16 x 16
       // rectangle); a warp owns the 8 step-t positions of its 4x8 block
       for (int t = 0; t < D.c.s; ++t) {
@@ -346,7 +355,9 @@ void Engine::alloc_all() {
   zhat_ = dalloc<int32_t>(static_cast<size_t>(D.hc) * D.zh * D.zw);
   emb_cur_ = dalloc<float>(static_cast<size_t>(HWl) * d);
   hq_ = dalloc<float>(static_cast<size_t>(HWl) * d);
-  const size_t TH = static_cast<size_t>(T) * HWo, THl = static_cast<size_t>(T) * HWl;
+  // 3D-stack buffers hold S slots: T (context) or T + 1 (LRP transformer)
+  const int Sx = T + (D.c.lrp_blocks > 0 ? 1 : 0);
+  const size_t TH = static_cast<size_t>(Sx) * HWo, THl = static_cast<size_t>(Sx) * HWl;
   ctx_x_ = dalloc<float>(TH * d);
   ctx_xn_ = dalloc<__half>(TH * d);
   ctx_ssq_ = dalloc<float>(TH * (d / 32));
@@ -357,6 +368,12 @@ void Engine::alloc_all() {
   ctx_h_ = dalloc<__half>(TH * D.fp);
   ctx16_ = dalloc<__half>(static_cast<size_t>(HWl) * d);
   acc_kv_ = dalloc<__half>(static_cast<size_t>(HWl) * 2 * d);
+  if (D.c.lrp_blocks > 0) {
+    lrp_cat_ = dalloc<__half>(static_cast<size_t>(HWl) * (D.N * D.sp + C));
+    lrp16_ = dalloc<__half>(static_cast<size_t>(HWo) * d);
+    eps_ = dalloc<float>(static_cast<size_t>(HWo) * C);
+    eps_chw_ = dalloc<float>(static_cast<size_t>(HWo) * C);
+  }
 
   hx_ = dalloc<float>(HWp * D.hc);
   hu_ = dalloc<float>(HWp * D.hc);
@@ -569,6 +586,27 @@ void Engine::upload_weights(const WeightMap& w) {
     }
   }
   ch_gout_ = upload_f(fv("ch.norm_out.g"), D.dch);
+  if (c_lrp() > 0) {
+    stack("lrp", c_lrp(), lrp_, false);
+    lrp_gout_ = upload_f(fv("lrp.norm_out.g"), d);
+    // in_proj rows: the final channel representation (slot g at columns
+    // g*sp, padded) then y_hat (C columns), matching lrp_cat_
+    const int kcat = D.N * D.sp + D.C;
+    std::vector<__half> h(static_cast<size_t>(d) * kcat, __float2half_rn(0.0f));
+    const float* wi = fv("lrp.in.w");  // [dch + C][d]
+    for (int o = 0; o < d; ++o) {
+      for (int i = 0; i < D.dch; ++i)
+        h[static_cast<size_t>(o) * kcat + (i / D.slot) * D.sp + i % D.slot] =
+            __float2half_rn(wi[static_cast<size_t>(i) * d + o]);
+      for (int i = 0; i < D.C; ++i)
+        h[static_cast<size_t>(o) * kcat + D.N * D.sp + i] =
+            __float2half_rn(wi[static_cast<size_t>(D.dch + i) * d + o]);
+    }
+    lrp_in_ = PW{upload_h(h), d, kcat};
+    lrp_in_b_ = upload_f(fv("lrp.in.b"), d);
+    lrp_head_ = linear("lrp.head.w", d, D.C, D.C, d);
+    lrp_head_b_ = upload_f(fv("lrp.head.b"), D.C);
+  }
   const int ms = (2 * D.Cg + 63) / 64 * 64;
   for (int g = 0; g < N; ++g) {
     const std::string mu = "head.mu" + std::to_string(g), sg = "head.sg" + std::to_string(g);
@@ -669,14 +707,15 @@ GemmEpi Engine::rms_in(GemmEpi e, const float* ssq) const {
 void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq,
                        const int32_t* tiles, int ntiles, const pswa_dev::AttnShape* shape,
                        const __half* kv, int slot_stride, int wt, int mask, const float* bias,
-                       __half* out) {
+                       __half* out, int kv_slots) {
   const Dims& D = D_;
   const int d = D.d, Hl = B_.Hl;  // key grid bounds: the band's local grid
   if (mma_attn_) {
     const pswa_dev::AttnShape sh = *shape;
     const int hr = wt > 0 ? kCtxHaloRows : kStepHaloRows, hw = wt > 0 ? kCtxHaloW : kStepHaloW;
     CUtensorMap map;  // halo boxes of this K/V buffer: 32 channels x hw x hr x 1 slot
-    pswa_dev::make_kv_tmap(&map, kv, 2 * d, D.W, Hl, wt > 0 ? D.T : 1, slot_stride > 0 ? slot_stride : HWl_,
+    pswa_dev::make_kv_tmap(&map, kv, 2 * d, D.W, Hl, wt > 0 ? (kv_slots > 0 ? kv_slots : D.T) : 1,
+                           slot_stride > 0 ? slot_stride : HWl_,
                            hw, hr);
     // score-offset tables of (layer bias, band shape): built once, reused by
     // every program that launches this layer on this shape
@@ -724,10 +763,55 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
   const int mk = B.cross ? 0 : 1;
   attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], &shape_step_[t][mk], B.kv_cache, 0, 0,
             mk, B.pos, batt_);
-  if (probe) tag(P, "step_attn", attn_flops(t, mk, 0));
+  if (probe) tag(P, "step_attn", attn_flops(t, mk, 1));
   gemm(P, batt_, d, M, B.wo, d, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + norm2 inputs
   gemm(P, bxn_, d, M, B.wgu, d, rms_in(swiglu_out(bh_, D.fp), bssq_));
   gemm(P, bh_, D.fp, M, B.wd, D.fp, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + next norm1 inputs
+}
+
+// Blocks of time-causal 3D SWA over S slots of own rows held in ctx_x_
+// (inputs) with the norm1 inputs of block 0 already in ctx_xn_/ctx_ssq_; the
+// last block computes the queries of the last slot only. Used by the context
+// transformer (S = T) and the LRP transformer (S = T + 1).
+void Engine::run_stack3d(Program& P, const Block* blocks, int nblocks, int S, const Tiles3d& tl,
+                         bool exchange_kv, const char* probe) {
+  const Dims& D = D_;
+  const int d = D.d, HWo = HWo_, n = S * HWo;
+  for (int b = 0; b < nblocks; ++b) {
+    const Block& B = blocks[b];
+    const bool last = b == nblocks - 1;
+    const int q0 = last ? (S - 1) * HWo : 0, nq = n - q0;
+    const float* pos = B.pos;
+    // band mode: K/V of the own rows into the local [S][HWl] grid, the halo
+    // rows pushed by the neighbours; buffers alternate by layer so a
+    // neighbour's push of layer b+1 never lands in the buffer read by layer b
+    __half* kv = (B_.n > 1 && b % 2) ? ctx_kv2_ : ctx_kv_;
+    float* ssq_q = ctx_ssq_ + static_cast<size_t>(q0) * (d / 32);
+    if (!last) {  // Q | K V in one GEMM over all slots
+      GemmEpi e = rms_in(f16_out(ctx_q_, d), ctx_ssq_);
+      e.out2 = kv;
+      e.ld_out2 = 2 * d;
+      e.split_n = d;
+      e.row_map2 = ctx_kv_map_;
+      gemm(P, ctx_xn_, d, n, B.wqkv, d, e);
+      if (exchange_kv) exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
+    } else {  // last block: K/V of every slot, queries of the last slot only
+      GemmEpi ekv = rms_in(f16_out(kv, 2 * d), ctx_ssq_);
+      ekv.row_map = ctx_kv_map_;
+      gemm(P, ctx_xn_, d, n, B.wkv, d, ekv);
+      if (exchange_kv) exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
+      gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, rms_in(f16_out(ctx_q_, d), ssq_q));
+    }
+    attention(P, ctx_q_, tl.qinfo + q0, nq, last ? tl.last : tl.all, last ? tl.n_last : tl.n_all,
+              &shape_ctx_, kv, HWl_, D.c.win_t, 0, pos, ctx_att_, S);
+    if (b == 0 && probe) tag(P, std::string(probe) + "_attn", attn_flops(-1, 0, S));
+    float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
+    __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;
+    gemm(P, ctx_att_, d, nq, B.wo, d, rms_out(f32_acc(xq, d), xnq, ssq_q));
+    gemm(P, xnq, d, nq, B.wgu, d, rms_in(swiglu_out(ctx_h_, D.fp), ssq_q));
+    if (b == 0 && probe) tag(P, std::string(probe) + "_ffn_gu", 2.0 * nq * (2.0 * D.f) * d);
+    gemm(P, ctx_h_, D.fp, nq, B.wd, D.fp, rms_out(f32_acc(xq, d), xnq, ssq_q));
+  }
 }
 
 void Engine::build_ctx(Program& P) {
@@ -740,42 +824,7 @@ void Engine::build_ctx(Program& P) {
   add(P, [=, this](cudaStream_t s) {
     pswa_dev::rms_prep(ctx_x_, d, nullptr, n, d, nullptr, 0, ctx_xn_, d, ctx_ssq_, d / 32, s);
   });
-  for (int b = 0; b < D.c.ctx_blocks; ++b) {
-    const Block& B = ctx_[b];
-    const bool last = b == D.c.ctx_blocks - 1;
-    const int q0 = last ? (T - 1) * HWo : 0, nq = n - q0;
-    const float* pos = B.pos;
-    // band mode: K/V of the own rows into the local [T][HWl] grid, the halo
-    // rows pushed by the neighbours; buffers alternate by layer so a
-    // neighbour's push of layer b+1 never lands in the buffer read by layer b
-    __half* kv = (B_.n > 1 && b % 2) ? ctx_kv2_ : ctx_kv_;
-    float* ssq_q = ctx_ssq_ + static_cast<size_t>(q0) * (d / 32);
-    if (!last) {  // Q | K V in one GEMM over all slots
-      GemmEpi e = rms_in(f16_out(ctx_q_, d), ctx_ssq_);
-      e.out2 = kv;
-      e.ld_out2 = 2 * d;
-      e.split_n = d;
-      e.row_map2 = ctx_kv_map_;
-      gemm(P, ctx_xn_, d, n, B.wqkv, d, e);
-      exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
-    } else {  // last block: K/V of every slot, queries of the last slot only
-      GemmEpi ekv = rms_in(f16_out(kv, 2 * d), ctx_ssq_);
-      ekv.row_map = ctx_kv_map_;
-      gemm(P, ctx_xn_, d, n, B.wkv, d, ekv);
-      exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
-      gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, rms_in(f16_out(ctx_q_, d), ssq_q));
-    }
-    attention(P, ctx_q_, ctx_qinfo_ + q0, nq, last ? ctx_tiles_last_ : ctx_tiles_,
-              last ? n_ctx_tiles_last_ : n_ctx_tiles_, &shape_ctx_, kv, HWl_, D.c.win_t, 0, pos,
-              ctx_att_);
-    if (b == 0) tag(P, "ctx_attn", attn_flops(-1, 0, 0));
-    float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
-    __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;
-    gemm(P, ctx_att_, d, nq, B.wo, d, rms_out(f32_acc(xq, d), xnq, ssq_q));
-    gemm(P, xnq, d, nq, B.wgu, d, rms_in(swiglu_out(ctx_h_, D.fp), ssq_q));
-    if (b == 0) tag(P, "ctx_ffn_gu", 2.0 * nq * (2.0 * D.f) * d);
-    gemm(P, ctx_h_, D.fp, nq, B.wd, D.fp, rms_out(f32_acc(xq, d), xnq, ssq_q));
-  }
+  run_stack3d(P, ctx_, D.c.ctx_blocks, T, tiles_ctx_, true, "ctx");
   const float* last = ctx_x_ + static_cast<size_t>(T - 1) * HWo * d;
   __half* c16 = ctx16_ + static_cast<size_t>(B_.own0) * D.W * d;
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(last, d, nullptr, HWo, d, d, ctx_gout_, c16, d, s); });
@@ -787,6 +836,46 @@ void Engine::build_ctx(Program& P) {
     for (int b = 0; b < nb; ++b)
       if (stackp[b].cross) gemm(P, ctx16_, d, HWl_, stackp[b].wkv, d, f16_out(stackp[b].kv_cache, 2 * d));
   }
+}
+
+// LRP transformer (A8) on the decoded (or
+// teacher-forced) frame: the final channel representation was scattered
+// into lrp_cat_ during the phases; y_hat joins it here. eps -> eps_chw_.
+void Engine::build_lrp(Program& P) {
+  const Dims& D = D_;
+  const int d = D.d, HWo = HWo_, T = D.T, S = T + 1, C = D.C;
+  const int kcat = D.N * D.sp + C;
+  __half* cat_own = lrp_cat_ + static_cast<size_t>(B_.own0) * D.W * kcat;
+  const int32_t* y_own = yfr_ + static_cast<size_t>(B_.own0) * D.W * C;
+  add(P, [=](cudaStream_t s) {  // y_hat columns of the concat
+    pswa_dev::yhat_rows_f16(y_own, C, nullptr, HWo, 0, C, cat_own + D.N * D.sp, kcat, C, s);
+  });
+  add(P, [=, this](cudaStream_t s) {  // past slots: the context transformer's inputs
+    pswa_dev::fill_context_slots(ring_ptrs_, slot_src_, pad_, T, HWo, d, ctx_x_, s);
+  });
+  GemmEpi e;  // current slot: in_proj(concat(final_rep, y_hat)) + b
+  e.out = ctx_x_ + static_cast<size_t>(T) * HWo * d;
+  e.ld_out = d;
+  e.out_f32 = 1;
+  e.bias = lrp_in_b_;
+  gemm(P, cat_own, kcat, HWo, lrp_in_, kcat, e);
+  add(P, [=, this](cudaStream_t s) {
+    pswa_dev::rms_prep(ctx_x_, d, nullptr, S * HWo, d, nullptr, 0, ctx_xn_, d, ctx_ssq_, d / 32, s);
+  });
+  run_stack3d(P, lrp_, D.c.lrp_blocks, S, tiles_lrp_, false, nullptr);
+  const float* cur = ctx_x_ + static_cast<size_t>(T) * HWo * d;
+  add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(cur, d, nullptr, HWo, d, d, lrp_gout_, lrp16_, d, s); });
+  GemmEpi eh;  // eps = 0.5 tanh(head(x) + b)
+  eh.out = eps_;
+  eh.ld_out = C;
+  eh.out_f32 = 1;
+  eh.bias = lrp_head_b_;
+  eh.act = pswa_dev::kActTanhHalf;
+  gemm(P, lrp16_, d, HWo, lrp_head_, d, eh);
+  add(P, [=, this](cudaStream_t s) {  // [HWo][C] -> [C][HWo] (32-bit words)
+    pswa_dev::yhat_to_chw(reinterpret_cast<const int32_t*>(eps_), HWo, C,
+                          reinterpret_cast<int32_t*>(eps_chw_), s);
+  });
 }
 
 void Engine::build_hyper_decode(Program& P) {
@@ -954,6 +1043,11 @@ void Engine::build_step(Program& P, int t, int mode) {
     }
     const float* go = ch_gout_ + g * sl;
     add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(xg, dchp, nullptr, M, sl, sl, go, chfo_, sp, s); });
+    if (c_lrp() > 0) {  // final channel representation of slot g -> LRP input
+      const int kcat = N * sp + C;
+      __half* dst = lrp_cat_ + g * sp;
+      add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f16(chfo_, sp, rows, M, sp, dst, kcat, s); });
+    }
     GemmEpi e1 = f16_out(hh16_, 2 * sp);
     e1.bias = head_b1_[g];
     e1.act = kActSilu;
@@ -1025,6 +1119,7 @@ Program& Engine::program(const std::string& key) {
     }
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_lane_bits(lanes_, L, bits_ + 1, s); });
     add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_to_chw(yfr_ + yoff, HW, C, ychw_, s); });
+    if (c_lrp() > 0) build_lrp(P);
   } else if (base == "encode" || base == "encode_z") {
     const bool zgiven = base == "encode_z";
     add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_from_chw(ychw_, HW, C, yfr_ + yoff, s); });
@@ -1059,6 +1154,7 @@ Program& Engine::program(const std::string& key) {
     });
     build_hyper_decode(P);
     for (int t = 0; t < D.c.s; ++t) build_step(P, t, 1);
+    if (c_lrp() > 0) build_lrp(P);
     add(P, [=, this](cudaStream_t s) {
       pswa_dev::lanes_encode(hsym_v_, hsym_idx_, nz, Lz, cdf_, enc_hlanes_, enc_hcap_, enc_hlens_,
                              enc_hbits_, status_, s);
@@ -1133,7 +1229,7 @@ void Engine::tag(Program& P, const std::string& name, double flops) {
 // Algorithmic attention FLOPs of one launch: 4 * d per (query, allowed key)
 // (QK^T and PV, 2 d each), counting in-grid, in-window, mask-allowed keys only
 // (SURVEY §8(d)). t < 0: the 3D context window over all T slots.
-double Engine::attn_flops(int t, int mask, int) const {
+double Engine::attn_flops(int t, int mask, int slots) const {
   const Dims& D = D_;
   const int rh = D.c.win_h / 2, rw = D.c.win_w / 2;
   double keys = 0;
@@ -1150,7 +1246,7 @@ double Engine::attn_flops(int t, int mask, int) const {
         }
       if (t >= 0) keys += n;
       else
-        for (int j = 0; j < D.T; ++j) keys += static_cast<double>(n) * std::min(j + 1, D.c.win_t);
+        for (int j = 0; j < slots; ++j) keys += static_cast<double>(n) * std::min(j + 1, D.c.win_t);
     }
   return 4.0 * D.d * keys;
 }
@@ -1535,6 +1631,13 @@ FrameResult Engine::decode(const void* hyper, size_t hyper_len, const void* main
   return finish_decode(advance, yhat_out, device);
 }
 
+
+void Engine::last_eps(float* out_chw) {
+  if (c_lrp() <= 0) throw std::invalid_argument("last_eps: the handle has no LRP transformer (lrp_blocks = 0)");
+  const size_t row = static_cast<size_t>(HWo_) * sizeof(float);
+  PSWA_CUDA(cudaMemcpyAsync(out_chw, eps_chw_, row * D_.C, cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+}
 
 size_t Engine::debug_fetch(const std::string& name, void* out, size_t cap) {
   const size_t hwd = static_cast<size_t>(HWl_) * D_.d;

@@ -116,6 +116,8 @@ class Engine {
   FrameResult decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
                      int rate, int fidx, bool advance, int32_t* yhat_out, bool device);
   void last_zhat(int32_t* out_host);
+  // LRP output eps [C][H][W] of the last decoded / encoded frame (lrp_blocks > 0).
+  void last_eps(float* out_chw);
 
   // ---- band mode (driven by BandGroup) ----------------------------------
   // Neighbours above / below (nullable) and band 0 (holder of the gathered
@@ -185,7 +187,7 @@ class Engine {
   cudaStream_t side_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   void tag(Program& P, const std::string& name, double flops);
-  double attn_flops(int t, int mask, int unused) const;
+  double attn_flops(int t, int mask, int slots) const;  // t < 0: 3D over `slots` slots
   std::map<std::string, std::pair<std::function<void(cudaStream_t)>, double>> probes_;
   void set_frame_params(int rate, int fidx);
   void advance_ring();
@@ -252,9 +254,6 @@ class Engine {
   int32_t* ctx_qinfo_ = nullptr;
   // tensor-core attention work lists (warp tiles); empty when unsupported
   bool mma_attn_ = false;
-  int32_t* ctx_tiles_ = nullptr;        // all slots (rows relative to slot 0)
-  int32_t* ctx_tiles_last_ = nullptr;   // last slot only (rows relative to it)
-  int n_ctx_tiles_ = 0, n_ctx_tiles_last_ = 0;
   int32_t* step_tiles_[16] = {};
   int n_step_tiles_[16] = {};
   pswa_dev::AttnShape shape_ctx_{};
@@ -264,7 +263,22 @@ class Engine {
   float *bssq_ = nullptr, *ctx_ssq_ = nullptr;  // folded-RMSNorm sums of squares [rows][d/32]
   void attention(struct Program& P, const __half* q, const int32_t* qinfo, int Mq, const int32_t* tiles,
                  int ntiles, const pswa_dev::AttnShape* shape, const __half* kv, int slot_stride,
-                 int wt, int mask, const float* bias, __half* out);
+                 int wt, int mask, const float* bias, __half* out, int kv_slots = 0);
+  struct Tiles3d {  // attention work of a 3D stack: all slots / last slot only
+    const int32_t *all = nullptr, *last = nullptr, *qinfo = nullptr;
+    int n_all = 0, n_last = 0;
+  };
+  Tiles3d tiles_ctx_, tiles_lrp_;
+  void run_stack3d(Program& P, const Block* blocks, int nblocks, int S, const Tiles3d& tl,
+                   bool exchange_kv, const char* probe);
+  void build_lrp(Program& P);
+  int c_lrp() const { return D_.c.lrp_blocks; }
+  // LRP transformer
+  Block lrp_[16];
+  PW lrp_in_, lrp_head_;
+  float *lrp_in_b_ = nullptr, *lrp_gout_ = nullptr, *lrp_head_b_ = nullptr;
+  __half *lrp_cat_ = nullptr, *lrp16_ = nullptr;  // [HWl][N*sp + C] concat input; normed output
+  float *eps_ = nullptr, *eps_chw_ = nullptr;      // [HWo][C], [C][HWo]
   int* crop_rows_ = nullptr;  // padded hyper grid index -> raster index (-1: pad)
   float* scales_ = nullptr;
   uint32_t* cdf_ = nullptr;

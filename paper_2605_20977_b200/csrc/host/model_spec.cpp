@@ -66,6 +66,7 @@ void validate_cfg(const pswa_cfg& c) {
   req(c.s >= 1 && c.ctx_slots >= 1 && c.ctx_slots < 64 && c.rate_points >= 1, "s / T / R");
   req(c.lanes >= 1 && c.hyper_lanes >= 1, "lanes");
   req(c.prior == 0 || c.prior == 1, "prior must be 0 (Gaussian) or 1 (Laplace)");
+  req(c.lrp_blocks >= 0 && c.lrp_blocks <= 16, "lrp_blocks in [0, 16]");
   req(c.win_t * c.win_h * c.win_w <= 256, "window taps <= 256");
   const int hd = c.d_spatial / c.heads;
   req(hd == 4 || hd == 8 || hd == 16 || hd == 32 || hd == 64, "head_dim in {4..64}");
@@ -78,6 +79,7 @@ std::string canonical_cfg(const pswa_cfg& c) {
     << ";chb=" << c.ch_blocks << ";hc=" << c.hyper_ch << ";C=" << c.latent_ch << ";s=" << c.s
     << ";N=" << c.n_groups << ";wh=" << c.win_h << ";ww=" << c.win_w << ";wt=" << c.win_t
     << ";T=" << c.ctx_slots << ";R=" << c.rate_points;
+  if (c.lrp_blocks > 0) o << ";lrp=" << c.lrp_blocks;
   return o.str();
 }
 
@@ -163,6 +165,24 @@ std::vector<ParamDecl> param_inventory(const pswa_cfg& c) {
       linear(p + ".w2", D.slot, D.Cg);
       zeros(p + ".b2", D.Cg);
     }
+  // LRP transformer (A8)
+  if (c.lrp_blocks > 0) {
+    linear("lrp.in.w", D.dch + D.C, D.d);
+    zeros("lrp.in.b", D.d);
+    for (int b = 0; b < c.lrp_blocks; ++b) {
+      const std::string p = "lrp.b" + std::to_string(b);
+      gain(p + ".norm1.g", D.d);
+      for (const char* w : {".wq", ".wk", ".wv", ".wo"}) linear(p + w, D.d, D.d);
+      P(p + ".pos", {D.heads, D.taps3}, Init::kScaledNormal, D.taps3);
+      gain(p + ".norm2.g", D.d);
+      linear(p + ".ffn.wg", D.d, D.f);
+      linear(p + ".ffn.wu", D.d, D.f);
+      linear(p + ".ffn.wd", D.f, D.d);
+    }
+    gain("lrp.norm_out.g", D.d);
+    linear("lrp.head.w", D.d, D.C);
+    zeros("lrp.head.b", D.C);
+  }
   return v;
 }
 

@@ -17,7 +17,7 @@ REF_SO = os.path.join(ROOT, "oracle", "_ref", "libpswa_ref.so")
 
 CFG_FIELDS = ("d_spatial", "heads", "ctx_blocks", "s1_blocks", "s2_blocks", "d_channel",
               "ch_blocks", "hyper_ch", "latent_ch", "s", "n_groups", "win_h", "win_w", "win_t",
-              "ctx_slots", "rate_points", "height", "width", "lanes", "hyper_lanes", "prior")
+              "ctx_slots", "rate_points", "height", "width", "lanes", "hyper_lanes", "prior", "lrp_blocks")
 
 _P = C.c_void_p
 _fp = C.POINTER(C.c_float)
@@ -28,7 +28,8 @@ def preset(paper: bool, H: int, W: int, lanes: int = 1, hyper_lanes: int = 1, **
              s1_blocks=8 if paper else 2, s2_blocks=8 if paper else 2,
              d_channel=1024 if paper else 128, ch_blocks=2, hyper_ch=128 if paper else 32,
              latent_ch=192, s=4, n_groups=4, win_h=7, win_w=7, win_t=5, ctx_slots=4,
-             rate_points=4, height=H, width=W, lanes=lanes, hyper_lanes=hyper_lanes, prior=0)
+             rate_points=4, height=H, width=W, lanes=lanes, hyper_lanes=hyper_lanes, prior=0,
+             lrp_blocks=0)
     c.update(over)
     return c
 
@@ -151,6 +152,16 @@ class OracleModel:
                                      len(past), ptr(mu), ptr(sg), ptr(zo), None)
         assert rc == 0, oracle().oracle_last_error()
         return mu, sg, zo
+
+    def lrp(self, yhat, zhat, rate=0, past=()):
+        """LRP output eps [C][H][W] of a known frame (teacher forced)."""
+        y = np.ascontiguousarray(yhat, dtype=np.int32)
+        z = np.ascontiguousarray(zhat, dtype=np.int32)
+        eps = np.zeros(self.shape, np.float32)
+        pa, keep = _past_array(past)
+        rc = oracle().oracle_lrp(self.h, ptr(y), ptr(z), rate, pa, len(past), ptr(eps))
+        assert rc == 0, oracle().oracle_last_error()
+        return eps
 
     def forward_debug(self, yhat, zhat, rate=0, past=()):
         """Stage outputs [H*W][d]: ctx, s1, hq, a, s2 (parity triage)."""
