@@ -337,9 +337,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool side2 = ep.out2 != nullptr && n0 >= ep.split_n;  // fused second output
       const int* rmap = side2 ? ep.row_map2 : ep.row_map;
       const int orow = m < M ? (rmap ? rmap[m] : m) : -1;
-      float4 res[8];
+      // residual segments prefetched two chunks ahead (two register
+      // buffers): the row-per-lane residual read is the epilogue's HBM
+      // latency chain in the 32640-row context GEMMs
+      float4 resA[8], resB[8];
       const bool acc_res = EPI == kEpiF32 && ep.accumulate;
-      if (acc_res) prefetch_residual(ep, orow, n0 + c0 * 32, res);
+      if (acc_res) {
+        prefetch_residual(ep, orow, n0 + c0 * 32, resA);
+        if (c0 + 1 < c1) prefetch_residual(ep, orow, n0 + (c0 + 1) * 32, resB);
+      }
       float row_scale = 1.0f;  // folded RMSNorm of A's row m
       if (ep.rms_ssq && m < M) {
         const float* sp = ep.rms_ssq + static_cast<size_t>(m) * ep.ld_rms;
@@ -360,8 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const uint32_t acc = tmem + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
-#pragma unroll 1
-      for (int c = c0; c < c1; ++c) {
+      auto chunk = [&](int c, float4 (&res)[8]) {
         uint32_t raw[32];
         tmem_ld_32x32(acc + c * 32, raw);
         tc_wait_ld();
@@ -372,7 +377,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(&tempty[buf]);
         }
         epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res, row_scale, side2);
-        if (acc_res && c + 1 < c1) prefetch_residual(ep, orow, n0 + (c + 1) * 32, res);
+        if (acc_res && c + 2 < c1) prefetch_residual(ep, orow, n0 + (c + 2) * 32, res);
+      };
+#pragma unroll 1
+      for (int c = c0; c < c1; c += 2) {
+        chunk(c, resA);
+        if (c + 1 < c1) chunk(c + 1, resB);
       }
     }
   }

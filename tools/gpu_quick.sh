@@ -1,11 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "gpu rc=$?"
-tail -3 gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu --no-config4 --no-config5 > gpurun_out/bench_q.json 2> gpurun_out/bench_q.err; echo "bench rc=$?"; tail -3 gpurun_out/bench_q.err
-python -c "
-import json; d=json.load(open('gpurun_out/bench_q.json'))
-print(d['ms_per_frame'], d['e2e']['ms_per_frame'], d['lrp'])"
-python -c "
-import json; d=json.load(open('gpurun_out/parity.json'))
-for k,v in d.items():
-  if 'lrp' in k: print(k, v)"
+NCU="ncu --set full --clock-control none --import-source on --profile-from-start off"
+timeout 600 $NCU -k regex:gemm_tc_kernel -s 7 -c 1 -o gpurun_out/ncu_ctx_wo2 python tools/profile_decode.py > /dev/null 2>&1
