@@ -163,6 +163,20 @@ int pswa_gpu_decode_sequence(pswa_gpu* h, const uint8_t* container, size_t len, 
  * rate_idx, s, N, prior, whole frames present. Host only. */
 int pswa_container_info(const uint8_t* container, size_t len, int* info);
 
+/* ---- frames: PPM I/O and the toy transform --
+ * Binary P6 only (P3 and maxval != 255 rejected). pswa_pad8 replicates the
+ * edges up to multiples of 8. Analysis: per 8x8 patch and colour, the
+ * orthonormal DCT-II of pixel - 128, channel = 3 * zigzag + colour, divided
+ * by q[rate] = {8, 5, 3, 2}; y_hat = round-half-even(y). Synthesis inverts
+ * it (y_rec = y_hat + eps), clamps to [0, 255] and rounds. On the current
+ * device. rgb [H][W][3] u8, y [192][H/8][W/8] f32. */
+int pswa_read_ppm(const char* path, uint8_t* rgb /* nullable: query size */, size_t cap, int* width,
+                  int* height);
+int pswa_write_ppm(const char* path, const uint8_t* rgb, int width, int height);
+int pswa_pad8(const uint8_t* rgb, int height, int width, uint8_t* out /* nullable */, int* h8, int* w8);
+int pswa_toy_analysis(const uint8_t* rgb, int h_px, int w_px, int rate_idx, float* y_out);
+int pswa_toy_synthesis(const float* y, int h_px, int w_px, int rate_idx, uint8_t* rgb_out);
+
 /* ---- row bands (BASELINE config 5) -----------------------
  * One frame decoded as n row bands, one device handle per band (bands may
  * share a device). Band b owns latent rows [row0, row1) (multiples of 4); its

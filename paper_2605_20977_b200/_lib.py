@@ -77,6 +77,11 @@ _SIGS = {
     "pswa_gpu_encode_sequence": (_I, [_VP, _VP, _I, _I, _I, _VP, _SZ, C.POINTER(_SZ)]),
     "pswa_gpu_decode_sequence": (_I, [_VP, _VP, _SZ, _VP, _I, _VP, _D, C.POINTER(_I)]),
     "pswa_container_info": (_I, [_VP, _SZ, C.POINTER(_I)]),
+    "pswa_read_ppm": (_I, [C.c_char_p, _VP, _SZ, C.POINTER(_I), C.POINTER(_I)]),
+    "pswa_write_ppm": (_I, [C.c_char_p, _VP, _I, _I]),
+    "pswa_pad8": (_I, [_VP, _I, _I, _VP, C.POINTER(_I), C.POINTER(_I)]),
+    "pswa_toy_analysis": (_I, [_VP, _I, _I, _I, _VP]),
+    "pswa_toy_synthesis": (_I, [_VP, _I, _I, _I, _VP]),
     "pswa_gpu_create_band": (_I, [_I, C.POINTER(PswaCfg), _VP, _SZ, _I, _I, C.POINTER(_VP)]),
     "pswa_gpu_band_export": (_I, [_VP, _VP, _SZ, C.POINTER(_SZ)]),
     "pswa_gpu_band_link": (_I, [_VP, _VP, _SZ, _VP, _SZ]),

@@ -109,6 +109,11 @@ void zhat_to_nhwc(const int32_t* z, int c, int hw, float* out, cudaStream_t st);
 // NHWC fp32 -> rounded int32 [c][h][w] (half-to-even)
 void round_to_zhat(const float* x, int c, int hw, int32_t* z, cudaStream_t st);
 
+// ---- toy transform (toy.cu) ----------------------------
+// rgb: [Hpx][Wpx][3] u8 (extents multiples of 8); y: [192][Hpx/8][Wpx/8].
+void toy_analysis(const uint8_t* rgb, int Hpx, int Wpx, int rate, float* y, cudaStream_t st);
+void toy_synthesis(const float* y, int Hpx, int Wpx, int rate, uint8_t* rgb, cudaStream_t st);
+
 // ---- entropy coding (coder.cu) -------------------------------------------
 constexpr int kScales = 64;
 constexpr int kSyms = 257;  // v in [-127,127] + 2 escapes
