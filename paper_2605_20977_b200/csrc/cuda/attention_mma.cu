@@ -101,9 +101,14 @@ struct AttnArgs {
   int hpc;     // heads per CTA (pipelined)
 };
 
-template <int NCH>
-__global__ void __launch_bounds__(256, NCH <= 5 ? 3 : 2)
+// NP passes of up to kPassChunks 16-key chunks per (head, slot) stage; the
+// online softmax carries across passes like across slots, so the register
+// footprint is that of one pass (3 CTAs of 8 warps per SM for every shape).
+constexpr int kPassChunks = 5;
+template <int NP>
+__global__ void __launch_bounds__(256, NP == 1 ? 3 : 2)
     window_attn_t8_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap kvmap) {
+  constexpr int NCH = NP * kPassChunks;  // chunk slots held in registers (row keys)
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h0 = blockIdx.y * a.hpc;  // this CTA's heads: [h0, h0 + hpc)
@@ -224,66 +229,72 @@ __global__ void __launch_bounds__(256, NCH <= 5 ? 3 : 2)
     const uint32_t sK = sbase + buf * 2 * a.kbuf, sV = sK + a.kbuf;
     const __half* stbl = stbl0 + buf * kAttnMaxBandKeys * 8;
     if (live) {
-      // pass 1: scores and their per-query max over this slot
-      float s[NCH][4];
-      float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        if (c < nch) {
-          float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-          uint32_t fa[4];
-          ldsm_x4(sK + swz(hk[c], lane >> 4), fa);
-          mma16816(acc, fa, qb[0][0], qb[0][1]);
-          ldsm_x4(sK + swz(hk[c], (lane >> 4) + 2), fa);
-          mma16816(acc, fa, qb[1][0], qb[1][1]);
-          const int r0 = c * 16 + (lane >> 2);
-          const float2 t0 = __half22float2(*reinterpret_cast<const __half2*>(stbl + r0 * 8 + qc));
-          const float2 t1 = __half22float2(*reinterpret_cast<const __half2*>(stbl + (r0 + 8) * 8 + qc));
-          const bool k0 = (inb >> (2 * c)) & 1u, k1 = (inb >> (2 * c + 1)) & 1u;
-          s[c][0] = k0 ? fmaf(acc[0], qscale, t0.x) : -INFINITY;
-          s[c][1] = k0 ? fmaf(acc[1], qscale, t0.y) : -INFINITY;
-          s[c][2] = k1 ? fmaf(acc[2], qscale, t1.x) : -INFINITY;
-          s[c][3] = k1 ? fmaf(acc[3], qscale, t1.y) : -INFINITY;
-          mx0 = fmaxf(mx0, fmaxf(s[c][0], s[c][2]));
-          mx1 = fmaxf(mx1, fmaxf(s[c][1], s[c][3]));
+      for (int ps = 0; ps < NP; ++ps) {
+        if (ps * kPassChunks >= nch) break;
+        // pass 1: scores and their per-query max over these chunks
+        float s[kPassChunks][4];
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int ci = 0; ci < kPassChunks; ++ci) {
+          const int c = ps * kPassChunks + ci;
+          if (c < nch) {
+            float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            uint32_t fa[4];
+            ldsm_x4(sK + swz(hk[c], lane >> 4), fa);
+            mma16816(acc, fa, qb[0][0], qb[0][1]);
+            ldsm_x4(sK + swz(hk[c], (lane >> 4) + 2), fa);
+            mma16816(acc, fa, qb[1][0], qb[1][1]);
+            const int r0 = c * 16 + (lane >> 2);
+            const float2 t0 = __half22float2(*reinterpret_cast<const __half2*>(stbl + r0 * 8 + qc));
+            const float2 t1 = __half22float2(*reinterpret_cast<const __half2*>(stbl + (r0 + 8) * 8 + qc));
+            const bool k0 = (inb >> (2 * c)) & 1u, k1 = (inb >> (2 * c + 1)) & 1u;
+            s[ci][0] = k0 ? fmaf(acc[0], qscale, t0.x) : -INFINITY;
+            s[ci][1] = k0 ? fmaf(acc[1], qscale, t0.y) : -INFINITY;
+            s[ci][2] = k1 ? fmaf(acc[2], qscale, t1.x) : -INFINITY;
+            s[ci][3] = k1 ? fmaf(acc[3], qscale, t1.y) : -INFINITY;
+            mx0 = fmaxf(mx0, fmaxf(s[ci][0], s[ci][2]));
+            mx1 = fmaxf(mx1, fmaxf(s[ci][1], s[ci][3]));
+          }
         }
-      }
 #pragma unroll
-      for (int off = 4; off < 32; off <<= 1) {
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
-      }
-      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-      const float al0 = mn0 == -INFINITY ? 1.0f : ex2(m0 - mn0);  // ex2(-inf) = 0
-      const float al1 = mn1 == -INFINITY ? 1.0f : ex2(m1 - mn1);
-      m0 = mn0;
-      m1 = mn1;
-      // exp offsets: a query with no allowed key yet keeps m = -inf; use 0
-      // so that ex2(-inf - 0) = 0 instead of NaN
-      const float ms0 = mn0 == -INFINITY ? 0.0f : mn0, ms1 = mn1 == -INFINITY ? 0.0f : mn1;
-      l0 *= al0;
-      l1 *= al1;
+        for (int off = 4; off < 32; off <<= 1) {
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        }
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float al0 = mn0 == -INFINITY ? 1.0f : ex2(m0 - mn0);  // ex2(-inf) = 0
+        const float al1 = mn1 == -INFINITY ? 1.0f : ex2(m1 - mn1);
+        m0 = mn0;
+        m1 = mn1;
+        // exp offsets: a query with no allowed key yet keeps m = -inf; use 0
+        // so that ex2(-inf - 0) = 0 instead of NaN
+        const float ms0 = mn0 == -INFINITY ? 0.0f : mn0, ms1 = mn1 == -INFINITY ? 0.0f : mn1;
+        l0 *= al0;
+        l1 *= al1;
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        o[mt][0] *= al0;
-        o[mt][1] *= al1;
-        o[mt][2] *= al0;
-        o[mt][3] *= al1;
-      }
-      // pass 2: probabilities (fp16) and O^T += V^T P^T
+        for (int mt = 0; mt < 2; ++mt) {
+          o[mt][0] *= al0;
+          o[mt][1] *= al1;
+          o[mt][2] *= al0;
+          o[mt][3] *= al1;
+        }
+        // pass 2: probabilities (fp16) and O^T += V^T P^T
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        if (c < nch) {
-          const float p0 = ex2(s[c][0] - ms0), p1 = ex2(s[c][1] - ms1);
-          const float p2 = ex2(s[c][2] - ms0), p3 = ex2(s[c][3] - ms1);
-          l0 += p0 + p2;
-          l1 += p1 + p3;
-          const uint32_t b0 = movtrans(pack_h2(p0, p1)), b1 = movtrans(pack_h2(p2, p3));
+        for (int ci = 0; ci < kPassChunks; ++ci) {
+          const int c = ps * kPassChunks + ci;
+          if (c < nch) {
+            const float p0 = ex2(s[ci][0] - ms0), p1 = ex2(s[ci][1] - ms1);
+            const float p2 = ex2(s[ci][2] - ms0), p3 = ex2(s[ci][3] - ms1);
+            l0 += p0 + p2;
+            l1 += p1 + p3;
+            const uint32_t b0 = movtrans(pack_h2(p0, p1)), b1 = movtrans(pack_h2(p2, p3));
 #pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
-            uint32_t fv[4];
-            ldsm_x4_t(sV + swz(hv[c], ((lane >> 3) & 1) + 2 * mt), fv);
-            mma16816(o[mt], fv, b0, b1);
+            for (int mt = 0; mt < 2; ++mt) {
+              uint32_t fv[4];
+              ldsm_x4_t(sV + swz(hv[c], ((lane >> 3) & 1) + 2 * mt), fv);
+              mma16816(o[mt], fv, b0, b1);
+            }
           }
         }
       }
@@ -343,10 +354,10 @@ __global__ void score_table_kernel(const float* __restrict__ bias, int taps_tota
   }
 }
 
-template <int NCH>
+template <int NP>
 void launch_t8(const AttnArgs& a, const CUtensorMap& map, int halo_keys, int ntiles, int heads,
                int warps, cudaStream_t st) {
-  launch_k(window_attn_t8_kernel<NCH>, dim3(ntiles, heads / a.hpc), dim3(warps * 32),
+  launch_k(window_attn_t8_kernel<NP>, dim3(ntiles, heads / a.hpc), dim3(warps * 32),
            smem_bytes(halo_keys, a.dbuf), st, a, map);
 }
 
@@ -368,9 +379,9 @@ void build_score_tables(const float* bias, int heads, int wt, AttnShape shape, _
 }
 
 void window_attention_tiles_init(int max_smem_bytes) {
-  PSWA_CUDA(cudaFuncSetAttribute(window_attn_t8_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PSWA_CUDA(cudaFuncSetAttribute(window_attn_t8_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  max_smem_bytes));
-  PSWA_CUDA(cudaFuncSetAttribute(window_attn_t8_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PSWA_CUDA(cudaFuncSetAttribute(window_attn_t8_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  max_smem_bytes));
 }
 
@@ -387,8 +398,8 @@ void window_attention_tiles(const __half* q, int ldq, const int32_t* tiles, int 
   const int hk = halo_rows * halo_width;
   AttnArgs a{q, ldq, tiles, heads * kHD, wt, tables, wt > 0 ? wt : 1, out, ldo, shape, halo_width,
              box_buf_bytes(hk), wt > 0 ? dbuf3 : dbuf2, hpc};
-  if (shape.nbk <= 80) launch_t8<5>(a, kv_map, hk, ntiles, heads, warps_per_tile, st);
-  else launch_t8<9>(a, kv_map, hk, ntiles, heads, warps_per_tile, st);
+  if (shape.nbk <= 16 * kPassChunks) launch_t8<1>(a, kv_map, hk, ntiles, heads, warps_per_tile, st);
+  else launch_t8<2>(a, kv_map, hk, ntiles, heads, warps_per_tile, st);
   PSWA_LAUNCH_CHECK();
 }
 
