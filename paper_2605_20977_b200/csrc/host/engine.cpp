@@ -161,6 +161,16 @@ void Engine::alloc_all() {
     step_qinfo_[t] = up(qi);
     step_rows_pad_[t] = up(rp);
   }
+  {  // all steps in canonical order (teacher-forced encoder batch)
+    std::vector<int> r, rp;
+    for (int t = 0; t < D.c.s; ++t)
+      for (int v : step_rows_h_[t]) {
+        r.push_back(v);
+        rp.push_back((v / D.W + B_.lo) * D.Wp + v % D.W);
+      }
+    enc_rows_ = up(r);
+    enc_rows_pad_ = up(rp);
+  }
   {
     // 3D-stack queries: own rows of every slot, [S][HWo]; local coordinates
     // (S = T for the context transformer, T + 1 for the LRP transformer)
@@ -382,7 +392,8 @@ void Engine::alloc_all() {
   hcast_ = dalloc<__half>(HWp * D.hcp);
   s1full_ = dalloc<__half>(HWp * d);
 
-  const size_t nb = static_cast<size_t>(nmax_);
+  // batch buffers hold every own position: the encoder batches all steps
+  const size_t nb = static_cast<size_t>(std::max(nmax_, HWo));
   bx_ = dalloc<float>(nb * d);
   bxn_ = dalloc<__half>(nb * d);
   bssq_ = dalloc<float>(nb * (d / 32));
@@ -737,18 +748,46 @@ void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq
   }
 }
 
-// One S1/S2 block on the step-t batch held in bx_ (residual stream, fp32).
-void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
+// A batch of wavefront-step positions: one step (the decoder's phases) or
+// every step concatenated in canonical order (the teacher-forced encoder:
+// the same per-position kernels with one GEMM per layer instead of s; the
+// attention stays one launch per step, on that step's slice, so every query
+// sees exactly the decoder's tiles and masks and mu/sigma stay bitwise
+// equal).
+Engine::StepBatch Engine::batch_of(int t) const {
+  StepBatch b;
+  b.M = static_cast<int>(step_rows_h_[t].size());
+  b.rows = step_rows_[t];
+  b.rows_pad = step_rows_pad_[t];
+  b.parts.push_back({t, 0, b.M});
+  b.xkind = t;
+  return b;
+}
+
+Engine::StepBatch Engine::batch_all() const {
+  StepBatch b;
+  b.rows = enc_rows_;
+  b.rows_pad = enc_rows_pad_;
+  for (int t = 0; t < D_.c.s; ++t) {
+    const int n = static_cast<int>(step_rows_h_[t].size());
+    b.parts.push_back({t, b.M, n});
+    b.M += n;
+  }
+  b.xkind = kXAll;
+  return b;
+}
+
+// One S1/S2 block on the batch held in bx_ (residual stream, fp32).
+void Engine::block_step(Program& P, const Block& B, const StepBatch& bt) {
   const Dims& D = D_;
-  const int d = D.d, M = static_cast<int>(step_rows_h_[t].size());
-  const int* rows = step_rows_[t];
-  const int32_t* qinfo = step_qinfo_[t];
+  const int d = D.d, M = bt.M;
+  const int* rows = bt.rows;
   // norm1 is folded: bxn_ holds the fp16 residual stream and bssq_ its
   // sums of squares (from the previous residual GEMM or rms_prep)
-  const bool probe = &B == &s2_[0] && t == D.c.s - 1;  // bench_op probes (last step, S2 block 0)
+  const bool probe = &B == &s2_[0] && bt.parts.size() == 1 && bt.parts[0][0] == D.c.s - 1;
   if (!B.cross) {
-    // one GEMM for Q | K V: Q rows to the batch, K/V of this step's
-    // positions into the frame cache (row map)
+    // one GEMM for Q | K V: Q rows to the batch, K/V of these positions into
+    // the frame cache (row map)
     GemmEpi e = rms_in(f16_out(bq_, d), bssq_);
     e.out2 = B.kv_cache;
     e.ld_out2 = 2 * d;
@@ -756,14 +795,17 @@ void Engine::block_step(Program& P, const Block& B, int t, const char*, bool) {
     e.row_map2 = rows;
     gemm(P, bxn_, d, M, B.wqkv, d, e);
     if (probe) tag(P, "step_wq", 2.0 * M * 3.0 * d * d);
-    exchange(P, xid_of(B), t);  // band mode: step-t K/V of the boundary rows
+    exchange(P, xid_of(B), bt.xkind);  // band mode: new K/V of the boundary rows
   } else {
     gemm(P, bxn_, d, M, B.wq, d, rms_in(f16_out(bq_, d), bssq_));
   }
   const int mk = B.cross ? 0 : 1;
-  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], &shape_step_[t][mk], B.kv_cache, 0, 0,
-            mk, B.pos, batt_);
-  if (probe) tag(P, "step_attn", attn_flops(t, mk, 1));
+  for (const auto& pt : bt.parts) {
+    const int t = pt[0], off = pt[1], n = pt[2];
+    attention(P, bq_ + static_cast<size_t>(off) * d, step_qinfo_[t], n, step_tiles_[t], n_step_tiles_[t],
+              &shape_step_[t][mk], B.kv_cache, 0, 0, mk, B.pos, batt_ + static_cast<size_t>(off) * d);
+    if (probe) tag(P, "step_attn", attn_flops(t, mk, 1));
+  }
   gemm(P, batt_, d, M, B.wo, d, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + norm2 inputs
   gemm(P, bxn_, d, M, B.wgu, d, rms_in(swiglu_out(bh_, D.fp), bssq_));
   gemm(P, bh_, D.fp, M, B.wd, D.fp, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + next norm1 inputs
@@ -962,57 +1004,58 @@ void Engine::build_hyper_encode(Program& P) {
   add(P, [=, this](cudaStream_t s) { pswa_dev::round_to_zhat(fin, hc, D.zh * D.zw, zhat_, s); });
 }
 
-void Engine::build_embed(Program& P, int t) {
+void Engine::build_embed(Program& P, const StepBatch& bt) {
   const Dims& D = D_;
-  const int M = static_cast<int>(step_rows_h_[t].size());
   GemmEpi e;
   e.out = emb_cur_;
   e.ld_out = D.d;
   e.out_f32 = 1;
   e.scale = cur_rsi_;  // e = rate_scale_in * (W y_hat) + b
   e.bias = emb_b_;
-  e.row_map = step_rows_[t];
-  gemm(P, y16_, D.C, M, emb_w_, D.C, e);
+  e.row_map = bt.rows;
+  gemm(P, y16_, D.C, bt.M, emb_w_, D.C, e);
 }
 
-void Engine::build_s1(Program& P, int t, bool encoder) {
+void Engine::build_s1(Program& P, const StepBatch& bt, bool encoder) {
   const Dims& D = D_;
-  const int d = D.d, M = static_cast<int>(step_rows_h_[t].size());
-  const int* rows = step_rows_[t];
+  const int d = D.d, M = bt.M;
+  const int* rows = bt.rows;
   add(P, [=, this](cudaStream_t s) {  // gather + block 0 norm1 inputs
     pswa_dev::rms_prep(emb_cur_, d, rows, M, d, bx_, d, bxn_, d, bssq_, d / 32, s);
   });
-  for (int b = 0; b < D.c.s1_blocks; ++b) block_step(P, s1_[b], t, "s1", true);
+  for (int b = 0; b < D.c.s1_blocks; ++b) block_step(P, s1_[b], bt);
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, s1_gout_, bs1n_, d, s); });
   GemmEpi e = f16_out(acc_kv_, 2 * d);
   e.row_map = rows;
   gemm(P, bs1n_, d, M, acc_.wkv, d, e);
   if (encoder) {  // full-frame S1 for the hyper encoder (band mode: band 0 gathers it)
-    const int* rp = step_rows_pad_[t];
+    const int* rp = bt.rows_pad;
     __half* dst = band0_s1_ ? band0_s1_ : s1full_;
     add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f16(bs1n_, d, rp, M, d, dst, d, s); });
   }
-  exchange(P, kXidAcc, t);
+  exchange(P, kXidAcc, bt.xkind);
 }
 
-void Engine::build_step(Program& P, int t, int mode) {
+void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
   const Dims& D = D_;
-  const int d = D.d, M = static_cast<int>(step_rows_h_[t].size());
-  const int* rows = step_rows_[t];
-  const int32_t* qinfo = step_qinfo_[t];
+  const int d = D.d, M = bt.M;
+  const int* rows = bt.rows;
   // accumulator: A = Hq + xattn(Q = Hq, KV = S1 of strictly earlier steps)
   add(P, [=, this](cudaStream_t s) {  // residual = Hq rows, normq folded into acc.wq
     pswa_dev::rms_prep(hq_, d, rows, M, d, bx_, d, bxn_, d, bssq_, d / 32, s);
   });
   gemm(P, bxn_, d, M, acc_.wq, d, rms_in(f16_out(bq_, d), bssq_));
-  attention(P, bq_, qinfo, M, step_tiles_[t], n_step_tiles_[t], &shape_step_[t][2], acc_kv_, 0, 0, 2,
-            acc_.pos, batt_);
+  for (const auto& pt : bt.parts) {
+    const int t = pt[0], off = pt[1], n = pt[2];
+    attention(P, bq_ + static_cast<size_t>(off) * d, step_qinfo_[t], n, step_tiles_[t], n_step_tiles_[t],
+              &shape_step_[t][2], acc_kv_, 0, 0, 2, acc_.pos, batt_ + static_cast<size_t>(off) * d);
+  }
   gemm(P, batt_, d, M, acc_.wo, d, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + S2 norm1 inputs
   const bool taps = mode == 1 && want_musig_;  // debug taps in forward_params only
   if (taps)
     add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f32(bx_, d, rows, M, d, afull_, d, s); });
   // spatial module 2
-  for (int b = 0; b < D.c.s2_blocks; ++b) block_step(P, s2_[b], t, "s2", true);
+  for (int b = 0; b < D.c.s2_blocks; ++b) block_step(P, s2_[b], bt);
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, s2_gout_, bs2n_, d, s); });
   if (taps)
     add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f16(bs2n_, d, rows, M, d, s2full_, d, s); });
@@ -1024,8 +1067,6 @@ void Engine::build_step(Program& P, int t, int mode) {
   ep.ld_out = dchp;
   ep.out_f32 = 1;
   gemm(P, bs2n_, d, M, ch_proj_, d, ep);
-  uint64_t o_step = 0;
-  for (int tt = 0; tt < t; ++tt) o_step += static_cast<uint64_t>(step_rows_h_[tt].size()) * C;
   for (int g = 0; g < N; ++g) {
     float* xg = chx_ + g * sp;
     if (g >= 1)  // channel shift: slot g sees y_hat group g-1
@@ -1062,24 +1103,32 @@ void Engine::build_step(Program& P, int t, int mode) {
     e2.scale = cur_rso_ + g * Cg;
     e2.n_store = 2 * Cg;
     gemm(P, hh16_, 2 * sp, M, head_w2_[g], 2 * sp, e2);
-    const uint64_t o0 = o_step + static_cast<uint64_t>(g) * M * Cg;
     const int c0 = g * Cg;
-    if (mode == 0) {
-      const int L = D.c.lanes;
-      add(P, [=, this](cudaStream_t s) {
-        pswa_dev::lanes_decode_phase(d_main_, lanes_, L, o0, M, Cg, musig_, ms, Cg, scales_, cdf_main_,
-                                     rows, yfr_, C, c0, y16_, C, status_, s);
-      });
-    } else {
-      const bool ms_out = want_musig_;
-      add(P, [=, this](cudaStream_t s) {
-        pswa_dev::quantize_phase(musig_, ms, Cg, M, Cg, o0, rows, yfr_, C, c0, scales_, sym_v_,
-                                 sym_idx_, y16_, C, ms_out ? mu_full_ : nullptr,
-                                 ms_out ? sg_full_ : nullptr, s);
-      });
+    for (const auto& pt : bt.parts) {  // per step: the symbols of phase (t, g)
+      const int t = pt[0], off = pt[1], n = pt[2];
+      uint64_t o_step = 0;  // canonical ordinal of the first symbol of step t
+      for (int tt = 0; tt < t; ++tt) o_step += static_cast<uint64_t>(step_rows_h_[tt].size()) * C;
+      const uint64_t o0 = o_step + static_cast<uint64_t>(g) * n * Cg;
+      const float* msg = musig_ + static_cast<size_t>(off) * ms;
+      const int* rws = rows + off;
+      __half* y16 = y16_ + static_cast<size_t>(off) * C;
+      if (mode == 0) {
+        const int L = D.c.lanes;
+        add(P, [=, this](cudaStream_t s) {
+          pswa_dev::lanes_decode_phase(d_main_, lanes_, L, o0, n, Cg, msg, ms, Cg, scales_, cdf_main_,
+                                       rws, yfr_, C, c0, y16, C, status_, s);
+        });
+      } else {
+        const bool ms_out = want_musig_;
+        add(P, [=, this](cudaStream_t s) {
+          pswa_dev::quantize_phase(msg, ms, Cg, n, Cg, o0, rws, yfr_, C, c0, scales_, sym_v_,
+                                   sym_idx_, y16, C, ms_out ? mu_full_ : nullptr,
+                                   ms_out ? sg_full_ : nullptr, s);
+        });
+      }
     }
   }
-  if (mode == 0) build_embed(P, t);
+  if (mode == 0) build_embed(P, bt);
 }
 
 Program& Engine::program(const std::string& key) {
@@ -1114,8 +1163,8 @@ Program& Engine::program(const std::string& key) {
     build_ctx(P);
     if (B_.n == 1) join_side(P);
     for (int t = 0; t < D.c.s; ++t) {
-      if (t > 0) build_s1(P, t - 1, false);
-      build_step(P, t, 0);
+      if (t > 0) build_s1(P, batch_of(t - 1), false);
+      build_step(P, batch_of(t), 0);
     }
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_lane_bits(lanes_, L, bits_ + 1, s); });
     add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_to_chw(yfr_ + yoff, HW, C, ychw_, s); });
@@ -1124,13 +1173,14 @@ Program& Engine::program(const std::string& key) {
     const bool zgiven = base == "encode_z";
     add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_from_chw(ychw_, HW, C, yfr_ + yoff, s); });
     build_ctx(P);
-    for (int t = 0; t < D.c.s; ++t) {
-      const int M = static_cast<int>(step_rows_h_[t].size());
-      const int* rows = step_rows_[t];
-      add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_rows_f16(yfr_, C, rows, M, 0, C, y16_, C, C, s); });
-      build_embed(P, t);
-      build_s1(P, t, true);
-    }
+    // teacher forced: every step's latents are known, so each layer runs
+    // once over all steps (one GEMM per layer, one attention launch per step)
+    const StepBatch all = batch_all();
+    const int* arows = all.rows;
+    const int Mall = all.M;
+    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_rows_f16(yfr_, C, arows, Mall, 0, C, y16_, C, C, s); });
+    build_embed(P, all);
+    build_s1(P, all, true);
     if (!zgiven) {
       if (B_.n > 1) {
         // every band has scattered its S1 rows into band 0's full-frame
@@ -1153,7 +1203,7 @@ Program& Engine::program(const std::string& key) {
                                hsym_idx_, s);
     });
     build_hyper_decode(P);
-    for (int t = 0; t < D.c.s; ++t) build_step(P, t, 1);
+    build_step(P, all, 1);
     if (c_lrp() > 0) build_lrp(P);
     add(P, [=, this](cudaStream_t s) {
       pswa_dev::lanes_encode(hsym_v_, hsym_idx_, nz, Lz, cdf_, enc_hlanes_, enc_hcap_, enc_hlens_,
@@ -1175,12 +1225,11 @@ Program& Engine::program(const std::string& key) {
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_doubles(enc_bits_, L, bits_ + 1, s); });
   } else if (base == "push") {
     add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_from_chw(ychw_, HW, C, yfr_ + yoff, s); });
-    for (int t = 0; t < D.c.s; ++t) {
-      const int M = static_cast<int>(step_rows_h_[t].size());
-      const int* rows = step_rows_[t];
-      add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_rows_f16(yfr_, C, rows, M, 0, C, y16_, C, C, s); });
-      build_embed(P, t);
-    }
+    const StepBatch all = batch_all();  // embeddings are per position: one pass
+    const int* arows = all.rows;
+    const int Mall = all.M;
+    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_rows_f16(yfr_, C, arows, Mall, 0, C, y16_, C, C, s); });
+    build_embed(P, all);
   } else {
     throw std::invalid_argument("unknown program " + key);
   }

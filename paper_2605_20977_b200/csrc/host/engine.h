@@ -16,6 +16,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <array>
 #include <functional>
 #include <map>
 #include <string>
@@ -174,13 +175,24 @@ class Engine {
   void add(Program& P, std::function<void(cudaStream_t)> op, int launches = 1);
   void gemm(Program& P, const __half* A, int lda, int M, const PW& B, int K,
             const pswa_dev::GemmEpi& ep);
-  void block_step(Program& P, const Block& b, int t, const char* tag, bool self_mask_le);
+  struct StepBatch {  // positions of one wavefront step, or of all steps (encoder)
+    int M = 0;
+    const int* rows = nullptr;      // local raster index per batch row
+    const int* rows_pad = nullptr;  // padded global hyper-grid index per row
+    std::vector<std::array<int, 3>> parts;  // (step t, first row, rows)
+    int xkind = 0;                  // band exchange kind: t or kXAll
+  };
+  StepBatch batch_of(int t) const;
+  StepBatch batch_all() const;
+  int* enc_rows_ = nullptr;      // all steps, canonical order (batch_all)
+  int* enc_rows_pad_ = nullptr;
+  void block_step(Program& P, const Block& b, const StepBatch& bt);
   void build_ctx(Program& P);
   void build_hyper_decode(Program& P);
   void build_hyper_encode(Program& P);
-  void build_s1(Program& P, int t, bool encoder);
-  void build_step(Program& P, int t, int mode /*0 decode, 1 encode*/);
-  void build_embed(Program& P, int t);
+  void build_s1(Program& P, const StepBatch& bt, bool encoder);
+  void build_step(Program& P, const StepBatch& bt, int mode /*0 decode, 1 encode*/);
+  void build_embed(Program& P, const StepBatch& bt);
   void run(Program& P);
   void to_side(Program& P, size_t from);
   void join_side(Program& P);
