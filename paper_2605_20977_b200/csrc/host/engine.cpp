@@ -408,6 +408,8 @@ void Engine::alloc_all() {
   chn2_ = dalloc<__half>(nb * D.sp);
   chh_ = dalloc<__half>(nb * D.fgp);
   chfo_ = dalloc<__half>(nb * D.sp);
+  chx16_ = dalloc<__half>(nb * D.sp);  // zero pad columns stay zero (never written)
+  chssq_ = dalloc<float>(nb * (D.sp / 32));
   hh16_ = dalloc<__half>(nb * 2 * D.sp);
   const int ms = (2 * D.Cg + 63) / 64 * 64;
   musig_ = dalloc<float>(nb * ms);
@@ -592,7 +594,8 @@ void Engine::upload_weights(const WeightMap& w) {
     ch_g2_[b] = upload_f(fv(p + ".norm2.g"), D.dch);
     for (int g = 0; g < N; ++g) {
       const std::string q = p + ".ffn" + std::to_string(g);
-      ch_gu_[b][g] = gate_up(q + ".wg", q + ".wu", sl, D.fg, D.fgp, sp);
+      // norm2 of slot g folded (its gain slice into the weight, 1/rms in the epilogue)
+      ch_gu_[b][g] = gate_up(q + ".wg", q + ".wu", sl, D.fg, D.fgp, sp, fv(p + ".norm2.g") + g * sl);
       ch_d_[b][g] = linear(q + ".wd", D.fg, sl, sp, D.fgp);
     }
   }
@@ -622,8 +625,11 @@ void Engine::upload_weights(const WeightMap& w) {
   for (int g = 0; g < N; ++g) {
     const std::string mu = "head.mu" + std::to_string(g), sg = "head.sg" + std::to_string(g);
     std::vector<__half> h1(static_cast<size_t>(2 * sp) * sp, __float2half_rn(0.0f));
-    put_linear(h1, sp, fv(mu + ".w1"), sl, sl, 0, 0);
-    put_linear(h1, sp, fv(sg + ".w1"), sl, sl, sp, 0);
+    // the final channel norm (slot g) is folded into head 1 unless the LRP
+    // transformer needs the normalised representation itself
+    const float* gout = c_lrp() > 0 ? nullptr : fv("ch.norm_out.g") + g * sl;
+    put_linear(h1, sp, fv(mu + ".w1"), sl, sl, 0, 0, gout);
+    put_linear(h1, sp, fv(sg + ".w1"), sl, sl, sp, 0, gout);
     head_w1_[g] = PW{upload_h(h1), 2 * sp, sp};
     std::vector<float> b1(static_cast<size_t>(2 * sp), 0.0f);
     std::memcpy(b1.data(), fv(mu + ".b1"), sizeof(float) * sl);
@@ -704,6 +710,25 @@ GemmEpi swiglu_out(void* out, int ld) {
   return e;
 }
 }  // namespace
+
+// Folded RMSNorm of channel slot g (sl real columns of sp): the residual
+// epilogue writes the updated slot's fp16 copy to chx16_ [M][sp] and its
+// per-32-column sums of squares to chssq_ [M][sp/32]; the consumer reads them.
+GemmEpi Engine::ch_rms_out(GemmEpi e) const {
+  e.x16_out = chx16_;
+  e.ld_x16 = D_.sp;
+  e.ssq_out = chssq_;
+  e.ld_ssq = D_.sp / 32;
+  return e;
+}
+
+GemmEpi Engine::ch_rms_in(GemmEpi e) const {
+  e.rms_ssq = chssq_;
+  e.ld_rms = D_.sp / 32;
+  e.rms_parts = D_.slot / 32;
+  e.rms_inv_d = 1.0f / static_cast<float>(D_.slot);
+  return e;
+}
 
 GemmEpi Engine::rms_in(GemmEpi e, const float* ssq) const {
   e.rms_ssq = ssq;
@@ -1071,20 +1096,22 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
     float* xg = chx_ + g * sp;
     if (g >= 1)  // channel shift: slot g sees y_hat group g-1
       gemm(P, y16_ + (g - 1) * Cg, C, M, ch_emb_[g], D.Cgp, f32_acc(xg, dchp, sl));
+    // slot-g RMSNorms: norm1 feeds the block-lower-triangular mix over
+    // slots <= g (each slot normalised on its own, so it stays a kernel);
+    // norm2 and the final norm are folded into the following GEMMs
+    // through chx16_ / chssq_ written by the residual epilogues
     for (int b = 0; b < D.c.ch_blocks; ++b) {
       const float* g1 = ch_g1_[b] + g * sl;
-      const float* g2 = ch_g2_[b] + g * sl;
       __half* xn = chxn_[b];
       add(P, [=](cudaStream_t s) { pswa_dev::rmsnorm_rows(xg, dchp, nullptr, M, sl, sl, g1, xn + g * sp, dchp, s); });
       const PW mixg{ch_mix_[b].p + static_cast<size_t>(g) * sp * dchp, sp, dchp};
-      gemm(P, xn, dchp, M, mixg, (g + 1) * sp, f32_acc(xg, dchp, sl));
-      add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(xg, dchp, nullptr, M, sl, sl, g2, chn2_, sp, s); });
-      gemm(P, chn2_, sp, M, ch_gu_[b][g], sp, swiglu_out(chh_, D.fgp));
-      gemm(P, chh_, D.fgp, M, ch_d_[b][g], D.fgp, f32_acc(xg, dchp, sl));
+      gemm(P, xn, dchp, M, mixg, (g + 1) * sp, ch_rms_out(f32_acc(xg, dchp, sl)));
+      gemm(P, chx16_, sp, M, ch_gu_[b][g], sp, ch_rms_in(swiglu_out(chh_, D.fgp)));
+      gemm(P, chh_, D.fgp, M, ch_d_[b][g], D.fgp, ch_rms_out(f32_acc(xg, dchp, sl)));
     }
     const float* go = ch_gout_ + g * sl;
-    add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(xg, dchp, nullptr, M, sl, sl, go, chfo_, sp, s); });
-    if (c_lrp() > 0) {  // final channel representation of slot g -> LRP input
+    if (c_lrp() > 0) {  // the LRP transformer reads the normalised final representation
+      add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(xg, dchp, nullptr, M, sl, sl, go, chfo_, sp, s); });
       const int kcat = N * sp + C;
       __half* dst = lrp_cat_ + g * sp;
       add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f16(chfo_, sp, rows, M, sp, dst, kcat, s); });
@@ -1092,7 +1119,10 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
     GemmEpi e1 = f16_out(hh16_, 2 * sp);
     e1.bias = head_b1_[g];
     e1.act = kActSilu;
-    gemm(P, chfo_, sp, M, head_w1_[g], sp, e1);
+    if (c_lrp() > 0)
+      gemm(P, chfo_, sp, M, head_w1_[g], sp, e1);
+    else  // final norm folded: A = fp16 slot g, 1/rms from the last d GEMM
+      gemm(P, chx16_, sp, M, head_w1_[g], sp, ch_rms_in(e1));
     GemmEpi e2;
     e2.out = musig_;
     e2.ld_out = ms;

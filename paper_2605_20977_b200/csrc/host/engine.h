@@ -272,6 +272,10 @@ class Engine {
   std::map<std::pair<const float*, const pswa_dev::AttnShape*>, __half*> score_tables_;
   pswa_dev::AttnShape shape_step_[4][3] = {};  // [t][mask: none, <=, <]
   pswa_dev::GemmEpi rms_in(pswa_dev::GemmEpi e, const float* ssq) const;
+  pswa_dev::GemmEpi ch_rms_out(pswa_dev::GemmEpi e) const;
+  pswa_dev::GemmEpi ch_rms_in(pswa_dev::GemmEpi e) const;
+  __half* chx16_ = nullptr;  // folded channel norms: fp16 slot copy [rows][sp]
+  float* chssq_ = nullptr;   // and its sums of squares [rows][sp/32]
   float *bssq_ = nullptr, *ctx_ssq_ = nullptr;  // folded-RMSNorm sums of squares [rows][d/32]
   void attention(struct Program& P, const __half* q, const int32_t* qinfo, int Mq, const int32_t* tiles,
                  int ntiles, const pswa_dev::AttnShape* shape, const __half* kv, int slot_stride,
