@@ -449,7 +449,8 @@ def run_ours(args, rank, world, local):
         if not args.no_config4:
             dec.close()
             c4r = config4_gop_batch(torch, rank, world, GpuCodec, gen_weights, make_cfg,
-                                    synth_latent, max(3, args.steps // 2), args.warmup)
+                                    synth_latent, max(3, args.steps // 2), args.warmup,
+                                    per_gpu=int(os.environ.get("PSWA_BENCH_GOPS", 8)))
             tot = pdist.max_over_ranks(c4r["ms"], dist, device="cuda")
             okr = pdist.max_over_ranks(0.0 if c4r["bit_exact"] else 1.0, dist, device="cuda")
             n_frames = world * c4r["gops_in_flight_per_gpu"] * c4r["frames_per_gop_timed"]
