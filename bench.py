@@ -180,6 +180,14 @@ def kernel_rooflines(dec, pk):
                      "traffic": tr.get(name), "kernel": desc, "us_per_launch": us,
                      "algorithmic_flop_per_launch": flops,
                      "peak_kind": "measured burst (MEASURED_PEAKS.json bf16_tflops)"}
+        sm = tr.get(name + "_smem")
+        if sm:  # windowed attention is bound by shared memory, not the tensor pipe
+            peak_smem = 148 * 128 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e9  # GB/s
+            ach = sm["bytes"] / (us * 1e-6) / 1e9
+            out[name]["secondary"] = {
+                "bound": "smem", "achieved": ach, "peak": peak_smem, "unit": "GB/s",
+                "frac": ach / peak_smem, "smem_bytes_per_launch": sm["bytes"],
+                "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared x 128 B (profiles/traffic.json)"}
     return out
 
 
