@@ -25,7 +25,6 @@
 // masked (not padded), the learned per-offset bias is added to the scaled
 // score, softmax in fp32, a query with no allowed key outputs zeros.
 #include <cfloat>
-#include <cstdio>
 #include <cstdlib>
 
 #include "check.h"
@@ -145,10 +144,6 @@ __global__ void __launch_bounds__(256, NP == 1 ? 3 : 2)
   // one elected thread stages (head h, slot j): two 4D TMA boxes (K, V) and
   // the (head, slot offset) score-offset table, on one mbarrier
   auto stage = [&](int h, int j, int buf) {
-#ifdef PSWA_ATTN_DEBUG
-    if (threadIdx.x == 0 && blockIdx.x < 2 && blockIdx.y == 0)
-      printf("blk %d h %d j %d buf %d sraw %u sbase %u kbuf %d box %u HR %d hw %d hx0 %d hy0 %d dyn %u\n", blockIdx.x, h, j, buf, sraw, sbase, a.kbuf, box_bytes, HR, a.hw, hx0, hy0, 0u);
-#endif
     if (threadIdx.x == 0) {
       fence_proxy_async_smem();  // prior ldmatrix reads of this buffer before the overwrite
       const uint32_t kb = sbase + buf * 2 * a.kbuf;

@@ -405,7 +405,6 @@ void Engine::alloc_all() {
   y16_ = dalloc<__half>(nb * C);
   chx_ = dalloc<float>(nb * D.N * D.sp);
   for (int b = 0; b < D.c.ch_blocks; ++b) chxn_[b] = dalloc<__half>(nb * D.N * D.sp);
-  chn2_ = dalloc<__half>(nb * D.sp);
   chh_ = dalloc<__half>(nb * D.fgp);
   chfo_ = dalloc<__half>(nb * D.sp);
   chx16_ = dalloc<__half>(nb * D.sp);  // zero pad columns stay zero (never written)

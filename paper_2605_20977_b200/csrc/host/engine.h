@@ -314,7 +314,7 @@ class Engine {
   int nmax_ = 0;
   float *bx_ = nullptr, *chx_ = nullptr, *musig_ = nullptr;
   __half *bxn_ = nullptr, *bq_ = nullptr, *batt_ = nullptr, *bh_ = nullptr, *bs1n_ = nullptr,
-         *bs2n_ = nullptr, *y16_ = nullptr, *chxn_[4] = {}, *chn2_ = nullptr, *chh_ = nullptr,
+         *bs2n_ = nullptr, *y16_ = nullptr, *chxn_[4] = {}, *chh_ = nullptr,
          *chfo_ = nullptr, *hh16_ = nullptr;
   // coder
   uint8_t *d_hyper_ = nullptr, *d_main_ = nullptr;
