@@ -323,37 +323,69 @@ def config5_bands_across_ranks(torch, dist, rank, world, local, GpuCodec, BandGr
     """BASELINE config 5 on N GPUs: rank r decodes row band r of the 4K
     P-frame; halos travel as P2P stores into the neighbours' caches (CUDA IPC
     mappings) chained by device mailbox flags. Rank 0 encodes the banded
-    bitstream. Host-timed e2e per frame, max over ranks."""
+    bitstream. Host-timed e2e per frame, max over ranks. Every rank reaches
+    every collective even when a step fails locally (failures are agreed on
+    through the collectives, never by one rank leaving early)."""
     from paper_2605_20977_b200 import dist as pdist
     from paper_2605_20977_b200.codec import band_rows, split_banded
     H4, W4 = 136, 240
     cfg = make_cfg("paper", H4, W4, lanes=LANES // world, hyper_lanes=HYPER_LANES)
     blob = gen_weights(cfg, 1)
     frames = [synth_latent(cfg, 0, f) for f in range(GOP_INDEX + 1)]
+
+    def agree(ok: bool) -> bool:  # all ranks ok?
+        return pdist.max_over_ranks(0.0 if ok else 1.0, dist, device="cuda") == 0.0
+
     payload = [None]
     if rank == 0:
-        enc = BandGroupCodec(cfg, blob, [local] * world)
-        for f in frames[:GOP_INDEX]:
-            enc.push_frame(f)
-        payload = [enc.encode_frame(frames[GOP_INDEX], fidx=GOP_INDEX)[:2]]
-        enc.close()
+        try:
+            enc = BandGroupCodec(cfg, blob, [local] * world)
+            for f in frames[:GOP_INDEX]:
+                enc.push_frame(f)
+            payload = [enc.encode_frame(frames[GOP_INDEX], fidx=GOP_INDEX)[:2]]
+            enc.close()
+        except Exception as e:  # noqa: BLE001 - reported through the broadcast
+            payload = [f"encode failed: {e}"]
     dist.broadcast_object_list(payload, src=0)
+    if not isinstance(payload[0], tuple):
+        raise RuntimeError(str(payload[0]))
     hyper, main = payload[0]
-    band = GpuCodec(cfg, blob, device=local, band=rank, n_bands=world)
-    pdist.link_band(band, dist)
-    for f in frames[:GOP_INDEX]:
-        band.push_frame(f)
+    band, err = None, None
+    try:
+        band = GpuCodec(cfg, blob, device=local, band=rank, n_bands=world)
+        blob_ipc = band.band_export()
+    except Exception as e:  # noqa: BLE001
+        blob_ipc, err = None, e
+    blobs = [None] * world
+    dist.all_gather_object(blobs, blob_ipc)
+    if any(b is None for b in blobs):
+        raise RuntimeError(f"band handle creation failed on a rank ({err})")
+    ok = True
+    try:
+        up, down = pdist.neighbour_blobs(blobs, rank)
+        band.band_link(up, down)
+        for f in frames[:GOP_INDEX]:
+            band.push_frame(f)
+    except Exception as e:  # noqa: BLE001
+        ok, err = False, e
+    if not agree(ok):
+        raise RuntimeError(f"band linking failed on a rank ({err})")
     mine = split_banded(main, world)[rank]
-    ts = []
+    ts, y = [], None
     for _ in range(steps + 1):
         dist.barrier()
         t0 = time.perf_counter()
-        y, _ = band.decode_frame(hyper, mine, fidx=GOP_INDEX, advance=False)
+        try:
+            y, _ = band.decode_frame(hyper, mine, fidx=GOP_INDEX, advance=False)
+        except Exception as e:  # noqa: BLE001
+            ok, err = False, e
         ts.append(time.perf_counter() - t0)
+        if not agree(ok):
+            raise RuntimeError(f"banded decode failed on a rank ({err})")
     r0, r1 = band_rows(H4, world, rank)
-    ok = bool(np.array_equal(y[:, r0:r1], frames[GOP_INDEX][:, r0:r1]))
+    exact = bool(np.array_equal(y[:, r0:r1], frames[GOP_INDEX][:, r0:r1]))
     ms = pdist.max_over_ranks(1e3 * statistics.median(ts[1:]), dist, device="cuda")
-    okall = pdist.max_over_ranks(0.0 if ok else 1.0, dist, device="cuda") == 0.0
+    okall = agree(exact)
     band.close()
     return {"workload": "4K P-frame (240x136 latents, GOP index 4), paper scale",
             "bands": world, "e2e_ms_per_frame_max_over_ranks": ms, "bit_exact": okall,
@@ -456,11 +488,16 @@ def run_ours(args, rank, world, local):
     try:
         if not args.no_config4:
             dec.close()
-            c4r = config4_gop_batch(torch, rank, world, GpuCodec, gen_weights, make_cfg,
-                                    synth_latent, max(3, args.steps // 2), args.warmup,
-                                    per_gpu=int(os.environ.get("PSWA_BENCH_GOPS", 8)))
+            try:  # local failures are agreed on through the reductions below
+                c4r = config4_gop_batch(torch, rank, world, GpuCodec, gen_weights, make_cfg,
+                                        synth_latent, max(3, args.steps // 2), args.warmup,
+                                        per_gpu=int(os.environ.get("PSWA_BENCH_GOPS", 8)))
+            except Exception as e:  # noqa: BLE001
+                c4r = {"ms": float("inf"), "bit_exact": False, "error": str(e)}
             tot = pdist.max_over_ranks(c4r["ms"], dist, device="cuda")
             okr = pdist.max_over_ranks(0.0 if c4r["bit_exact"] else 1.0, dist, device="cuda")
+            if tot == float("inf"):
+                raise RuntimeError(c4r.get("error", "config 4 failed on a rank"))
             n_frames = world * c4r["gops_in_flight_per_gpu"] * c4r["frames_per_gop_timed"]
             c4 = {"workload": "64 independent 1080p GOPs sharded round-robin over the GPUs, "
                               "P-frames (GOP index 4), decoders in flight per GPU on their own streams",
