@@ -17,6 +17,7 @@
 #include "check.h"
 #include "kernels.h"
 #include "launch.cuh"
+#include "ptx.cuh"
 
 namespace pswa_dev {
 
@@ -90,6 +91,13 @@ __device__ __forceinline__ double sym_bits(uint32_t freq) {
   return 16.0 - log2(static_cast<double>(freq));
 }
 
+__host__ __device__ __forceinline__ uint16_t* sym_lut(uint32_t* cdf) {
+  return reinterpret_cast<uint16_t*>(cdf + kScales * (kSyms + 1) + 2 * kScales * kSyms);
+}
+__host__ __device__ __forceinline__ const uint16_t* sym_lut(const uint32_t* cdf) {
+  return reinterpret_cast<const uint16_t*>(cdf + kScales * (kSyms + 1) + 2 * kScales * kSyms);
+}
+
 __global__ void build_cdf_kernel(float* scales, uint32_t* cdf, int laplace) {
   pdl_wait();
   pdl_trigger();
@@ -129,6 +137,12 @@ __global__ void build_cdf_kernel(float* scales, uint32_t* cdf, int laplace) {
   for (int k = 0; k < kSyms; ++k) c[k + 1] = c[k] + freq[k];
   double* bt = reinterpret_cast<double*>(cdf + kScales * (kSyms + 1)) + idx * kSyms;
   for (int k = 0; k < kSyms; ++k) bt[k] = sym_bits(freq[k]);
+  uint16_t* lut = sym_lut(cdf) + idx * kLutBuckets;
+  int k = 0;
+  for (int b = 0; b < kLutBuckets; ++b) {  // largest k < kSyms with c[k] <= b * 256
+    while (k + 1 < kSyms && c[k + 1] <= static_cast<uint32_t>(b) * 256u) ++k;
+    lut[b] = static_cast<uint16_t>(k);
+  }
 }
 
 // ------------------------------------------------------------ helpers -----
@@ -210,6 +224,46 @@ __device__ __forceinline__ int dec_sym(R& rd, LaneState& s, const uint32_t* cum,
   return lo;
 }
 
+// dec_sym over a 257-symbol table with its search index: the target
+// q = floor(code / r) (a float quotient, then one exact integer correction
+// step each way: the float error is < 0.04 for q < 65536), then a binary
+// search only inside the symbols spanning q's 256-wide bucket (usually 1-2
+// candidates instead of 8 levels over the table). Same result as dec_sym.
+template <class R>
+__device__ __forceinline__ int dec_sym_lut(R& rd, LaneState& s, const uint32_t* cum,
+                                           const uint16_t* lut, int& err) {
+  const uint32_t r = static_cast<uint32_t>(s.range >> 16);  // range < 2^48
+  const uint64_t lim = static_cast<uint64_t>(r) << 16;
+  if (s.code >= lim) {
+    err = 1;
+    s.code = lim - 1;
+  }
+  uint32_t q = static_cast<uint32_t>(__fdividef(__ull2float_rz(s.code), __uint2float_rz(r)));
+  q = min(q, 65535u);
+  const uint64_t rq = static_cast<uint64_t>(r) * q;
+  if (rq > s.code)
+    --q;
+  else if (rq + r <= s.code)
+    ++q;
+  const int b = static_cast<int>(q >> 8);
+  int lo = lut[b], hi = min(static_cast<int>(lut[b + 1]) + 1, kSyms);
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (cum[mid] <= q)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const uint32_t c0 = cum[lo], c1 = cum[lo + 1];
+  s.code -= static_cast<uint64_t>(r) * c0;
+  s.range = static_cast<uint64_t>(r) * (c1 - c0);
+  while (s.range < kBot) {
+    s.code = (s.code << 8) | rd.get(s, err);
+    s.range <<= 8;
+  }
+  return lo;
+}
+
 // -log2(freq / 65536) of every (table, symbol), appended after the 64 CDF
 // tables (see build_cdf_tables): one load per decoded symbol instead of an
 // fp64 log2 on the lane's critical path.
@@ -217,12 +271,14 @@ __device__ __forceinline__ const double* bits_table(const uint32_t* cdf) {
   return reinterpret_cast<const double*>(cdf + kScales * (kSyms + 1));
 }
 
-// Decodes one value (escape + Exp-Golomb included); returns v.
+// Decodes one value (escape + Exp-Golomb included); returns v, the table
+// symbol k and the escape's extra bits (0 when k is not an escape). The
+// lane's bit count is s.bits += bits_row[k] + then esc_bits, in symbol order.
 template <class R>
-__device__ int32_t dec_value(R& rd, LaneState& s, const uint32_t* cdf_row, const double* bits_row,
-                             int& err) {
-  const int k = dec_sym(rd, s, cdf_row, kSyms, err);
-  s.bits += __ldg(bits_row + k);
+__device__ int32_t dec_value_k(R& rd, LaneState& s, const uint32_t* cdf_row, const uint16_t* lut_row,
+                               int& k, int& esc_bits, int& err) {
+  k = lut_row ? dec_sym_lut(rd, s, cdf_row, lut_row, err) : dec_sym(rd, s, cdf_row, kSyms, err);
+  esc_bits = 0;
   if (k < kEscLo) return k - 127;
   int nb = 0;
   while (dec_sym(rd, s, kBitCum, 2, err) == 0) {
@@ -233,62 +289,103 @@ __device__ int32_t dec_value(R& rd, LaneState& s, const uint32_t* cdf_row, const
   }
   uint64_t x = 1;
   for (int i = 0; i < nb; ++i) x = (x << 1) | static_cast<uint64_t>(dec_sym(rd, s, kBitCum, 2, err));
-  s.bits += 2 * nb + 1;
+  esc_bits = 2 * nb + 1;
   const long long m = static_cast<long long>(x) - 1 + 128;
   return static_cast<int32_t>(k == kEscLo ? -m : m);
 }
 
+template <class R>
+__device__ int32_t dec_value(R& rd, LaneState& s, const uint32_t* cdf_row, const double* bits_row,
+                             int& err) {
+  int k, eb;
+  const int32_t v = dec_value_k(rd, s, cdf_row, nullptr, k, eb, err);
+  s.bits += __ldg(bits_row + k);
+  if (eb) s.bits += eb;
+  return v;
+}
+
 // ------------------------------------------------------------ kernels -----
-__global__ void lanes_init_kernel(const uint8_t* __restrict__ pl, const uint32_t* __restrict__ len_p,
-                                  int L, uint32_t expect, LaneState* __restrict__ lanes, int* status) {
+// Exclusive scan of one uint64 per thread over the block (warp shuffles, then
+// the warp totals); ws is 33 shared words, ws[32] receives the block total.
+// Integer sums, so the result does not depend on the order.
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t* ws) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t inc = v;
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t u = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += u;
+  }
+  if (lane == 31) ws[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    const uint64_t w = lane < nw ? ws[lane] : 0;
+    uint64_t winc = w;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xffffffffu, winc, d);
+      if (lane >= d) winc += u;
+    }
+    if (lane < nw) ws[lane] = winc - w;
+    if (lane == 31) ws[32] = winc;
+  }
+  __syncthreads();
+  return ws[warp] + inc - v;
+}
+
+// One thread per lane, 128 lanes per block: each block first sums the
+// lengths of all lanes before it (coalesced 4 B loads; the 32 KB length
+// table is L2-resident), then scans its own 128. Spreading the lanes over
+// many SMs matters: the 6 scattered first-byte reads per lane are ~50k L2
+// requests per frame, more than one SM's load path drains quickly.
+__global__ void __launch_bounds__(128) lanes_init_kernel(const uint8_t* __restrict__ pl,
+                                                         const uint32_t* __restrict__ len_p, int L,
+                                                         uint32_t expect,
+                                                         LaneState* __restrict__ lanes, int* status) {
   pdl_wait();
   pdl_trigger();
+  __shared__ uint64_t ws[33];
   const uint32_t len = *len_p;
-  __shared__ uint64_t part[1024];
-  __shared__ int bad;
   const int t = threadIdx.x;
-  if (t == 0) bad = 0;
-  __syncthreads();
   const uint32_t hdr = 8u + 4u * static_cast<uint32_t>(L);
   if (len < hdr || rd32(pl) != static_cast<uint32_t>(L) || rd32(pl + 4) != expect) {
     if (t == 0) atomicOr(status, 1);
     return;
   }
-  const int per = (L + blockDim.x - 1) / blockDim.x;
-  const int l0 = t * per, l1 = min(L, l0 + per);
-  uint64_t acc = 0;
-  for (int l = l0; l < l1; ++l) acc += rd32(pl + 8 + 4 * l);
-  part[t] = acc;
-  __syncthreads();
-  if (t == 0) {  // exclusive scan of the partials (fixed order)
-    uint64_t run = 0;
-    for (int i = 0; i < static_cast<int>(blockDim.x); ++i) {
-      const uint64_t v = part[i];
-      part[i] = run;
-      run += v;
+  const uint32_t* lens = reinterpret_cast<const uint32_t*>(pl + 8);  // 256 B-aligned payload
+  const int l0 = blockIdx.x * blockDim.x;
+  uint64_t before = 0;
+  {
+    int i = t;
+    for (; i + 7 * 128 < l0; i += 8 * 128) {
+      uint32_t v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = lens[i + j * 128];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) before += v[j];
     }
-    if (hdr + run > len) bad = 1;
+    for (; i < l0; i += 128) before += lens[i];
   }
-  __syncthreads();
-  if (bad) {
-    if (t == 0) atomicOr(status, 1);
-    return;
-  }
-  uint64_t off = hdr + part[t];
-  for (int l = l0; l < l1; ++l) {
-    const uint32_t ln = rd32(pl + 8 + 4 * l);
-    LaneState s;
-    s.pos = static_cast<uint32_t>(off);
-    s.end = static_cast<uint32_t>(off + ln);
-    s.range = kWin;
-    s.code = 0;
-    s.bits = 0.0;
-    int err = ln < 4 ? 1 : 0;
-    for (int b = 0; b < 6; ++b) s.code = (s.code << 8) | next_byte(pl, s, err);
-    if (err) atomicOr(status, 1);
-    lanes[l] = s;
-    off += ln;
-  }
+  block_excl_scan(before, ws);
+  before = ws[32];
+  __syncthreads();  // ws is reused below
+  const int l = l0 + t;
+  const uint32_t ln = l < L ? lens[l] : 0u;
+  const uint64_t off = hdr + before + block_excl_scan(ln, ws);
+  if (l >= L) return;
+  if (off + ln > len || ln < 4) atomicOr(status, 1);  // past the payload / shorter than the flush
+  if (off + ln > len) return;
+  uint32_t byt[6];
+#pragma unroll
+  for (int b = 0; b < 6; ++b) byt[b] = static_cast<uint32_t>(b) < ln ? pl[off + b] : 0u;
+  LaneState s;
+  s.pos = static_cast<uint32_t>(off + 6);  // bytes past the lane's end are next_byte's implicit zeros
+  s.end = static_cast<uint32_t>(off + ln);
+  s.range = kWin;
+  s.code = 0;
+  s.bits = 0.0;
+#pragma unroll
+  for (int b = 0; b < 6; ++b) s.code = (s.code << 8) | byt[b];
+  lanes[l] = s;
 }
 
 __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* __restrict__ lanes,
@@ -297,18 +394,34 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
                                     const float* __restrict__ scales, const uint32_t* __restrict__ cdf,
                                     const int* __restrict__ rows, int32_t* __restrict__ yhat, int C,
                                     int c0, __half* __restrict__ yhat16, int ld16, int* status) {
-  // the 64 scale thresholds and the 64 cumulative tables (66 KB) staged in
-  // shared memory: the sigma -> table and symbol binary searches are
-  // dependent-load chains that otherwise run at L2 latency
+  // the 64 scale thresholds, the 64 cumulative tables (66 KB) and their
+  // search indexes (33 KB) staged in shared memory: the sigma -> table and
+  // symbol searches are dependent-load chains that otherwise run at L2
+  // latency (one bulk async copy each: a per-thread copy loop serialises ~30
+  // L2 round trips before the first symbol). The tables are built when the
+  // handle is created, so they may be read before pdl_wait.
   extern __shared__ uint4 s_raw[];
+  __shared__ uint64_t s_bar;
   uint32_t* s_cdf = reinterpret_cast<uint32_t*>(s_raw);
-  float* s_scales = reinterpret_cast<float*>(s_cdf + kScales * (kSyms + 1));
-  constexpr int kCdf4 = kScales * (kSyms + 1) / 4;
-  for (int i = threadIdx.x; i < kCdf4; i += blockDim.x) s_raw[i] = reinterpret_cast<const uint4*>(cdf)[i];
-  for (int i = threadIdx.x; i < kScales; i += blockDim.x) s_scales[i] = scales[i];
+  uint16_t* s_lut = reinterpret_cast<uint16_t*>(s_cdf + kScales * (kSyms + 1));
+  float* s_scales = reinterpret_cast<float*>(s_lut + kScales * kLutBuckets);
+  constexpr uint32_t kCdfBytes = kScales * (kSyms + 1) * 4, kLutBytes = kScales * kLutBuckets * 2,
+                     kScaleBytes = kScales * 4;
+  static_assert(kCdfBytes % 16 == 0 && kLutBytes % 16 == 0 && kScaleBytes % 16 == 0,
+                "bulk copies move 16 B multiples");
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+    fence_proxy_async_smem();
+    mbar_expect_tx(&s_bar, kCdfBytes + kLutBytes + kScaleBytes);
+    bulk_load(smem_u32(s_cdf), cdf, kCdfBytes, &s_bar);
+    bulk_load(smem_u32(s_lut), sym_lut(cdf), kLutBytes, &s_bar);
+    bulk_load(smem_u32(s_scales), scales, kScaleBytes, &s_bar);
+  }
+  __syncthreads();
   pdl_wait();
   pdl_trigger();
-  __syncthreads();
+  mbar_wait(&s_bar, 0);
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
   const uint64_t total = static_cast<uint64_t>(n) * per;
@@ -321,10 +434,15 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
   // the parameters (mu, table index) of a lane's next symbols do not depend
   // on the coder state: gather them in a batch (loads in flight together),
   // then run the sequential decode chain
-  constexpr int kB = 8;
+  // kB covers a lane's symbols of one full-frame phase (12 at 1080p with
+  // 8192 lanes) in one batch. The bit-cost table loads are deferred to the
+  // end of the batch (issued together, summed in symbol order) so their
+  // latency is off the sequential decode chain.
+  constexpr int kB = 16;
   const uint64_t end = o0 + total;
+  const double* bt = bits_table(cdf);
   for (uint64_t base = first; base < end; base += static_cast<uint64_t>(kB) * L) {
-    int mu_r[kB], idx[kB], dst[kB], k16[kB];
+    int mu_r[kB], idx[kB], dst[kB], k16[kB], ks[kB], eb[kB];
 #pragma unroll
     for (int q = 0; q < kB; ++q) {
       const uint64_t o = base + static_cast<uint64_t>(q) * L;
@@ -341,10 +459,20 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
 #pragma unroll
     for (int q = 0; q < kB; ++q) {
       if (idx[q] < 0) break;
-      const int32_t v = dec_value(rd, s, s_cdf + idx[q] * (kSyms + 1), bits_table(cdf) + idx[q] * kSyms, err);
+      const int32_t v = dec_value_k(rd, s, s_cdf + idx[q] * (kSyms + 1), s_lut + idx[q] * kLutBuckets,
+                                    ks[q], eb[q], err);
       const int32_t y = v + mu_r[q];
       yhat[dst[q]] = y;
       if (yhat16) yhat16[k16[q]] = __int2half_rn(y);
+    }
+    double cost[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q) cost[q] = idx[q] >= 0 ? __ldg(bt + idx[q] * kSyms + ks[q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      if (idx[q] < 0) break;
+      s.bits += cost[q];
+      if (eb[q]) s.bits += eb[q];
     }
   }
   lanes[l] = s;
@@ -508,7 +636,8 @@ void build_cdf_tables(float* scales, uint32_t* cdf, cudaStream_t st, int laplace
 
 void lanes_init(const uint8_t* payload, const uint32_t* len, int lanes, uint32_t expect_count,
                 LaneState* st_lanes, int* status, cudaStream_t st) {
-  launch_k(lanes_init_kernel, dim3(1), dim3(1024), 0, st, payload, len, lanes, expect_count, st_lanes, status);
+  launch_k(lanes_init_kernel, dim3((lanes + 127) / 128), dim3(128), 0, st, payload, len, lanes, expect_count,
+           st_lanes, status);
   PSWA_LAUNCH_CHECK();
 }
 
@@ -517,7 +646,7 @@ void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_
                         const uint32_t* cdf, const int* rows, int32_t* yhat, int C, int c0,
                         __half* yhat16, int ld16, int* status, cudaStream_t st) {
   if (n <= 0) return;
-  constexpr int smem = (kScales * (kSyms + 1) + kScales) * 4;
+  constexpr int smem = kScales * (kSyms + 1) * 4 + kScales * kLutBuckets * 2 + kScales * 4;
   static const bool attr = [] {
     PSWA_CUDA(cudaFuncSetAttribute(decode_phase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     return true;
@@ -582,28 +711,20 @@ __global__ void pack_offsets_kernel(const uint32_t* __restrict__ lens, int L, ui
                                     unsigned long long* total, uint64_t* __restrict__ offs, int* status) {
   pdl_wait();
   pdl_trigger();
-  __shared__ uint64_t part[1024];
+  __shared__ uint64_t ws[33];
   const int t = threadIdx.x;
   const int per = (L + blockDim.x - 1) / blockDim.x;
   const int l0 = t * per, l1 = min(L, l0 + per);
   uint64_t acc = 0;
   for (int l = l0; l < l1; ++l) acc += lens[l];
-  part[t] = acc;
-  __syncthreads();
+  const uint64_t excl = block_excl_scan(acc, ws);
   if (t == 0) {
-    uint64_t run = 0;
-    for (int i = 0; i < static_cast<int>(blockDim.x); ++i) {
-      const uint64_t v = part[i];
-      part[i] = run;
-      run += v;
-    }
     const uint64_t hdr = 8 + 4ull * L;
-    *total = hdr + run;
-    if (hdr + run > cap) atomicOr(status, 8);
+    *total = hdr + ws[32];
+    if (hdr + ws[32] > cap) atomicOr(status, 8);
   }
-  __syncthreads();
   const uint64_t hdr = 8 + 4ull * L;
-  uint64_t off = hdr + part[t];
+  uint64_t off = hdr + excl;
   for (int l = l0; l < l1; ++l) {
     offs[l] = off;
     off += lens[l];

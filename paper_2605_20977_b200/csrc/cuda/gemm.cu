@@ -19,6 +19,7 @@
 // symmetry contract).
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -248,6 +249,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int kblocks = K / kBK;
+  // phase stamps: compiled in only with -DPSWA_GEMM_TRACE_BUILD (make
+  // TRACE=1), so production kernels carry no trace branches
+#ifdef PSWA_GEMM_TRACE_BUILD
+  unsigned long long* const tr = ep.trace ? ep.trace + blockIdx.x * kGemmTraceSlots : nullptr;
+#else
+  constexpr unsigned long long* tr = nullptr;
+#endif
+  auto stamp = [&](int slot) {
+    if (tr) tr[slot] = clock64();
+  };
+  if (tr && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    tr[8] = g;
+    stamp(0);
+  }
   // tile schedule: CL CTAs of a cluster take adjacent M tiles of one N tile
   const int rank = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
   const int tiles_mp = (tiles_m + CL - 1) / CL, tiles_n = num_tiles / tiles_m;
@@ -275,9 +292,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) stamp(1);
   // everything above overlaps the previous kernel (PDL); inputs are read below
   pdl_wait();
   pdl_trigger();
+  if (threadIdx.x == 0) stamp(2);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -296,6 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(sb + s * Cfg::kBBytes, &tmb, &full[s], kb * kBK, n0);
         }
       }
+      stamp(10);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -309,6 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < kblocks; ++kb, ++g) {
           const int s = g % S;
           mbar_wait(&full[s], (g / S) & 1);
+          if (g == 0) stamp(3);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sa + s * Cfg::kABytes);
           const uint32_t b_base = smem_u32(sb + s * Cfg::kBBytes);
@@ -323,6 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_commit(&tfull[buf]);
       }
+      stamp(4);
     }
   } else {
     const int ew = warp - 2;
@@ -364,6 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         row_scale = 1.0f / sqrtf(ss * ep.rms_inv_d + 1e-5f);
       }
       mbar_wait(&tfull[buf], use & 1);
+      if (ew == 0 && lane == 0 && it == 0) stamp(5);
       tc_fence_after();
       const uint32_t acc = tmem + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
       auto chunk = [&](int c, float4 (&res)[8]) {
@@ -385,6 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c + 1 < c1) chunk(c + 1, resB);
       }
     }
+    if (ew == 0 && lane == 0) stamp(6);
   }
   tc_fence_before();
   if (CL > 1)
@@ -394,6 +418,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_free(tmem, 2 * BN);
+  }
+  if (tr && threadIdx.x == 0) {
+    stamp(7);
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    tr[9] = g;
   }
 }
 
@@ -511,6 +541,25 @@ void make_kv_tmap(CUtensorMap* m, const __half* kv, int ld, int W, int H, int sl
     throw CudaError("cuTensorMapEncodeTiled (kv) failed (code " + std::to_string(int(r)) + ")");
 }
 
+unsigned long long* trace_buffer() {
+  static unsigned long long* buf = [] {
+    unsigned long long* b = nullptr;
+    const size_t bytes = sizeof(unsigned long long) * kGemmTraceSlots * 1024;
+    PSWA_CUDA(cudaMalloc(&b, bytes));
+    PSWA_CUDA(cudaMemset(b, 0, bytes));
+    return b;
+  }();
+  return buf;
+}
+
+bool gemm_trace_read(unsigned long long* out, int n) {
+  if (!std::getenv("PSWA_GEMM_TRACE")) return false;
+  n = std::min(n, kGemmTraceSlots * 1024);
+  PSWA_CUDA(cudaDeviceSynchronize());
+  PSWA_CUDA(cudaMemcpy(out, trace_buffer(), sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
+  return true;
+}
+
 void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, int ldb, int N,
                int K, const GemmEpi& epi, int force_bn) {
   if (K % kBK != 0 || N % 64 != 0 || lda % 8 != 0 || ldb % 8 != 0 || M <= 0)
@@ -551,6 +600,7 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   // measured neutral-to-slower on B200 (the L2 already dedups concurrent B
   // reads; 10.56 vs 10.44 ms / frame), so opt-in via PSWA_GEMM_CLUSTER=1.
   static const bool use_cluster = std::getenv("PSWA_GEMM_CLUSTER") != nullptr;
+  if (std::getenv("PSWA_GEMM_TRACE")) p->epi.trace = trace_buffer();
   p->cluster = (use_cluster && M > kBM) ? 2 : 1;
   make_tmap(&p->ta, A, lda, M, K, kBM);
   make_tmap(&p->tb, B, ldb, N, K, bn / p->cluster);

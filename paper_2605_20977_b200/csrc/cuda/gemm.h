@@ -52,7 +52,14 @@ struct GemmEpi {
   void* out2 = nullptr;
   int ld_out2 = 0, split_n = 0;
   const int* row_map2 = nullptr;
+  // debug (PSWA_GEMM_TRACE): per-CTA clock64 stamps of the kernel phases,
+  // kGemmTraceSlots words per CTA, overwritten by every launch
+  unsigned long long* trace = nullptr;
 };
+constexpr int kGemmTraceSlots = 16;
+// Copies the last traced launch's stamps (n words) to host; false when
+// tracing is off.
+bool gemm_trace_read(unsigned long long* out, int n);
 
 struct GemmPlan {
   CUtensorMap ta;

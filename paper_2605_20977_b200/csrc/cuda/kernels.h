@@ -119,8 +119,13 @@ constexpr int kScales = 64;
 constexpr int kSyms = 257;  // v in [-127,127] + 2 escapes
 // Builds the 64 scale entries and 64 x 258 cumulative tables on the device
 // in fp64 with IEEE round-to-nearest ops only (bit-exact with the host rule),
-// followed (at cdf + 64*258, 8-byte aligned) by 64 x 257 fp64 symbol costs.
-constexpr size_t kCdfWords = static_cast<size_t>(kScales) * (kSyms + 1) + 2 * kScales * kSyms;
+// followed (at cdf + 64*258, 8-byte aligned) by 64 x 257 fp64 symbol costs
+// and 64 x 257 uint16 search-index entries (entry b of a table: the symbol
+// whose cumulative interval holds b * 256; the decoder's symbol search starts
+// from the bucket of its target).
+constexpr int kLutBuckets = 257;
+constexpr size_t kCdfWords = static_cast<size_t>(kScales) * (kSyms + 1) + 2 * kScales * kSyms +
+                             static_cast<size_t>(kScales) * kLutBuckets / 2;
 // laplace = 1: discretised Laplace with scale b = sigma instead (same 64
 // scales, same quantisation rule).
 void build_cdf_tables(float* scales, uint32_t* cdf, cudaStream_t st, int laplace = 0);

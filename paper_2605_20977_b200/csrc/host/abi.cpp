@@ -5,6 +5,7 @@
 #include <memory>
 
 #include "../cuda/check.h"
+#include "../cuda/gemm.h"
 #include "../cuda/kernels.h"
 #include "abi_util.h"
 #include "engine.h"
@@ -208,6 +209,15 @@ int pswa_gpu_bench_op(pswa_gpu* h, const char* name, int reps, double* us, doubl
 }
 
 void* pswa_gpu_stream(pswa_gpu* h) { return h->eng->stream(); }
+
+// Debug export for tools/gemm_trace.py (not part of the public header):
+// the per-CTA phase stamps of the last GEMM launch when PSWA_GEMM_TRACE is
+// set; returns 0, or 1 when tracing is off.
+extern "C" __attribute__((visibility("default"))) int pswa_debug_gemm_trace(unsigned long long* out, int n) {
+  return guard([&] {
+    if (!pswa_dev::gemm_trace_read(out, n)) throw std::invalid_argument("PSWA_GEMM_TRACE is not set");
+  });
+}
 
 // ---- sequences ----------------------------------------------------------------
 int pswa_gpu_encode_sequence(pswa_gpu* h, const int32_t* frames, int n_frames, int gop_size,
