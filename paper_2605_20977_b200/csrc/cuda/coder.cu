@@ -172,31 +172,11 @@ __device__ __forceinline__ uint32_t next_byte(const uint8_t* pl, LaneState& s, i
   return 0;
 }
 
-// Payload byte readers: direct (one global load per byte) and a 16 B
-// window (one aligned 16 B load per 16 bytes of a lane's stream: the
-// renormalisation byte reads are on the lane's sequential critical path).
+// Payload byte reader: one global load per byte (the hyperprior lanes; the
+// phase decoder uses the Rsv reservoir below).
 struct ByteDirect {
   const uint8_t* pl;
   __device__ __forceinline__ uint32_t get(LaneState& s, int& err) { return next_byte(pl, s, err); }
-};
-struct ByteWin {
-  const uint8_t* pl;
-  uint4 w;
-  uint32_t base;
-  __device__ __forceinline__ uint32_t get(LaneState& s, int& err) {
-    if (s.pos < s.end) {
-      const uint32_t b = s.pos & ~15u;
-      if (b != base) {  // the payload buffer extends >= 16 B past its end (capacity)
-        base = b;
-        w = __ldg(reinterpret_cast<const uint4*>(pl + b));
-      }
-      const uint32_t off = s.pos & 15u;
-      ++s.pos;
-      const uint32_t word = off < 8 ? (off < 4 ? w.x : w.y) : (off < 12 ? w.z : w.w);
-      return (word >> ((off & 3u) * 8u)) & 0xffu;
-    }
-    return next_byte(pl, s, err);  // implicit zero bytes / truncation
-  }
 };
 
 template <class R>
@@ -224,46 +204,6 @@ __device__ __forceinline__ int dec_sym(R& rd, LaneState& s, const uint32_t* cum,
   return lo;
 }
 
-// dec_sym over a 257-symbol table with its search index: the target
-// q = floor(code / r) (a float quotient, then one exact integer correction
-// step each way: the float error is < 0.04 for q < 65536), then a binary
-// search only inside the symbols spanning q's 256-wide bucket (usually 1-2
-// candidates instead of 8 levels over the table). Same result as dec_sym.
-template <class R>
-__device__ __forceinline__ int dec_sym_lut(R& rd, LaneState& s, const uint32_t* cum,
-                                           const uint16_t* lut, int& err) {
-  const uint32_t r = static_cast<uint32_t>(s.range >> 16);  // range < 2^48
-  const uint64_t lim = static_cast<uint64_t>(r) << 16;
-  if (s.code >= lim) {
-    err = 1;
-    s.code = lim - 1;
-  }
-  uint32_t q = static_cast<uint32_t>(__fdividef(__ull2float_rz(s.code), __uint2float_rz(r)));
-  q = min(q, 65535u);
-  const uint64_t rq = static_cast<uint64_t>(r) * q;
-  if (rq > s.code)
-    --q;
-  else if (rq + r <= s.code)
-    ++q;
-  const int b = static_cast<int>(q >> 8);
-  int lo = lut[b], hi = min(static_cast<int>(lut[b + 1]) + 1, kSyms);
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (cum[mid] <= q)
-      lo = mid;
-    else
-      hi = mid;
-  }
-  const uint32_t c0 = cum[lo], c1 = cum[lo + 1];
-  s.code -= static_cast<uint64_t>(r) * c0;
-  s.range = static_cast<uint64_t>(r) * (c1 - c0);
-  while (s.range < kBot) {
-    s.code = (s.code << 8) | rd.get(s, err);
-    s.range <<= 8;
-  }
-  return lo;
-}
-
 // -log2(freq / 65536) of every (table, symbol), appended after the 64 CDF
 // tables (see build_cdf_tables): one load per decoded symbol instead of an
 // fp64 log2 on the lane's critical path.
@@ -275,9 +215,9 @@ __device__ __forceinline__ const double* bits_table(const uint32_t* cdf) {
 // symbol k and the escape's extra bits (0 when k is not an escape). The
 // lane's bit count is s.bits += bits_row[k] + then esc_bits, in symbol order.
 template <class R>
-__device__ int32_t dec_value_k(R& rd, LaneState& s, const uint32_t* cdf_row, const uint16_t* lut_row,
-                               int& k, int& esc_bits, int& err) {
-  k = lut_row ? dec_sym_lut(rd, s, cdf_row, lut_row, err) : dec_sym(rd, s, cdf_row, kSyms, err);
+__device__ int32_t dec_value_k(R& rd, LaneState& s, const uint32_t* cdf_row, int& k, int& esc_bits,
+                               int& err) {
+  k = dec_sym(rd, s, cdf_row, kSyms, err);
   esc_bits = 0;
   if (k < kEscLo) return k - 127;
   int nb = 0;
@@ -298,7 +238,7 @@ template <class R>
 __device__ int32_t dec_value(R& rd, LaneState& s, const uint32_t* cdf_row, const double* bits_row,
                              int& err) {
   int k, eb;
-  const int32_t v = dec_value_k(rd, s, cdf_row, nullptr, k, eb, err);
+  const int32_t v = dec_value_k(rd, s, cdf_row, k, eb, err);
   s.bits += __ldg(bits_row + k);
   if (eb) s.bits += eb;
   return v;
@@ -388,8 +328,113 @@ __global__ void __launch_bounds__(128) lanes_init_kernel(const uint8_t* __restri
   lanes[l] = s;
 }
 
+// Byte reservoir of one lane for the phase decoder: the lane's next bytes
+// in a 64-bit register (cnt of them, the next one most significant), fed
+// from 16 B-aligned windows; the following window is loaded as soon as the
+// current one is entered, so its latency is hidden behind ~16 bytes of
+// decoding. Reads may run up to 32 B past the lane's end (the payload
+// buffer has that slack); bytes at or past `end` are masked to the implicit
+// zeros of next_byte (two allowed, a third is an error).
+struct Rsv {
+  const uint8_t* pl;
+  uint64_t bits;
+  uint32_t cnt, wi, wb, pos, end;
+  uint4 cur, nxt;
+  __device__ __forceinline__ static uint32_t bswap(uint32_t w) { return __byte_perm(w, 0, 0x0123); }
+  __device__ __forceinline__ uint32_t word(uint32_t i) const {
+    return i < 2 ? (i == 0 ? cur.x : cur.y) : (i == 2 ? cur.z : cur.w);
+  }
+  __device__ __forceinline__ void advance() {
+    if (wi == 4) {
+      cur = nxt;
+      wb += 16;
+      nxt = __ldg(reinterpret_cast<const uint4*>(pl + wb + 16));
+      wi = 0;
+    }
+  }
+  __device__ __forceinline__ void refill() {
+    if (cnt < 2) {
+      bits = (bits << 32) | bswap(word(wi));
+      cnt += 4;
+      ++wi;
+      advance();
+    }
+  }
+  __device__ __forceinline__ void init(const uint8_t* p, uint32_t pos0, uint32_t end0) {
+    pl = p;
+    pos = pos0;
+    end = end0;
+    wb = pos & ~15u;
+    cur = __ldg(reinterpret_cast<const uint4*>(pl + wb));
+    nxt = __ldg(reinterpret_cast<const uint4*>(pl + wb + 16));
+    wi = (pos - wb) >> 2;
+    const uint32_t skip = pos & 3u;
+    bits = bswap(word(wi)) & (0xffffffffu >> (8 * skip));
+    cnt = 4 - skip;
+    ++wi;
+    advance();
+    refill();
+  }
+  // the next nb <= 2 bytes as one big-endian value
+  __device__ __forceinline__ uint32_t take(uint32_t nb, int& err) {
+    uint32_t v = static_cast<uint32_t>(bits >> (8 * (cnt - nb))) & ((1u << (8 * nb)) - 1u);
+    if (pos + nb > end) {  // the lane's last bytes (rare)
+      for (uint32_t i = 0; i < nb; ++i)
+        if (pos + i >= end) {
+          v &= ~(0xffu << (8 * (nb - 1 - i)));
+          if (pos + i >= end + 2) err = 1;
+        }
+    }
+    cnt -= nb;
+    pos += nb;
+    refill();
+    return v;
+  }
+  __device__ __forceinline__ uint32_t get(LaneState&, int& err) { return take(1, err); }
+};
+
+// dec_sym over a 257-symbol table with its search index, same result: the
+// target q = floor(code / r) (a float quotient, then one exact integer
+// correction step each way: the float error is < 0.04 for q < 65536), a
+// binary search only inside the symbols spanning q's 256-wide bucket
+// (usually 1-2 candidates instead of 8 levels), and a branch-free
+// renormalisation: the bytes dec_sym's `while (range < kBot)` loop reads,
+// from the bit length of the new range (r >= 2^24, freq >= 1: at most 2).
+__device__ __forceinline__ int dec_sym_rsv(Rsv& rs, LaneState& s, const uint32_t* cum,
+                                           const uint16_t* lut, int& err) {
+  const uint32_t r = static_cast<uint32_t>(s.range >> 16);
+  const uint64_t lim = static_cast<uint64_t>(r) << 16;
+  if (s.code >= lim) {
+    err = 1;
+    s.code = lim - 1;
+  }
+  uint32_t q = static_cast<uint32_t>(__fdividef(__ull2float_rz(s.code), __uint2float_rz(r)));
+  q = min(q, 65535u);
+  const uint64_t rq = static_cast<uint64_t>(r) * q;
+  if (rq > s.code)
+    --q;
+  else if (rq + r <= s.code)
+    ++q;
+  const int b = static_cast<int>(q >> 8);
+  int lo = lut[b], hi = min(static_cast<int>(lut[b + 1]) + 1, kSyms);
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (cum[mid] <= q)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const uint32_t c0 = cum[lo], c1 = cum[lo + 1];
+  const uint64_t range = static_cast<uint64_t>(r) * (c1 - c0);
+  const int bl = 64 - __clzll(static_cast<long long>(range));
+  const uint32_t nb = bl > 40 ? 0u : static_cast<uint32_t>(48 - bl) >> 3;
+  s.code = ((s.code - static_cast<uint64_t>(r) * c0) << (8 * nb)) | rs.take(nb, err);
+  s.range = range << (8 * nb);
+  return lo;
+}
+
 __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* __restrict__ lanes,
-                                    int L, uint64_t o0, int n, int per,
+                                    int L, uint32_t o0_mod, int n, int per,
                                     const float* __restrict__ musig, int ldms, int sig_off,
                                     const float* __restrict__ scales, const uint32_t* __restrict__ cdf,
                                     const int* __restrict__ rows, int32_t* __restrict__ yhat, int C,
@@ -425,42 +470,85 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
   const uint64_t total = static_cast<uint64_t>(n) * per;
-  // first ordinal of lane l at or after o0
-  const uint64_t first = o0 + ((static_cast<uint64_t>(l) + L - (o0 % L)) % L);
-  if (first >= o0 + total) return;
+  // first ordinal of lane l at or after o0, relative to o0 (o0_mod = o0 % L
+  // from the host: no 64-bit division here)
+  uint32_t i_first = static_cast<uint32_t>(l) + static_cast<uint32_t>(L) - o0_mod;
+  if (i_first >= static_cast<uint32_t>(L)) i_first -= static_cast<uint32_t>(L);
+  if (i_first >= total) return;
   LaneState s = lanes[l];
   int err = 0;
-  ByteWin rd{pl, make_uint4(0, 0, 0, 0), 0xffffffffu};
+  Rsv rs;
+  rs.init(pl, s.pos, s.end);
   // the parameters (mu, table index) of a lane's next symbols do not depend
   // on the coder state: gather them in a batch (loads in flight together),
-  // then run the sequential decode chain
+  // then run the sequential decode chain.
   // kB covers a lane's symbols of one full-frame phase (12 at 1080p with
   // 8192 lanes) in one batch. The bit-cost table loads are deferred to the
   // end of the batch (issued together, summed in symbol order) so their
   // latency is off the sequential decode chain.
   constexpr int kB = 16;
-  const uint64_t end = o0 + total;
+  const uint32_t ntot = static_cast<uint32_t>(total);
+  const int Ldiv = L / per, Lmod = L - Ldiv * per;
   const double* bt = bits_table(cdf);
-  for (uint64_t base = first; base < end; base += static_cast<uint64_t>(kB) * L) {
+  for (uint32_t ib = i_first; ib < ntot; ib += static_cast<uint32_t>(kB) * L) {
     int mu_r[kB], idx[kB], dst[kB], k16[kB], ks[kB], eb[kB];
+    float mu_f[kB], sg_f[kB];
+    // all loads of the batch first (in flight together), then the table
+    // searches: interleaving them exposes one load latency per symbol.
+    // (k, j) = divmod(i, per) stepped by divmod(L, per): one division per batch
+    int k = static_cast<int>(ib) / per, j = static_cast<int>(ib) - k * per;
 #pragma unroll
     for (int q = 0; q < kB; ++q) {
-      const uint64_t o = base + static_cast<uint64_t>(q) * L;
+      const uint32_t i = ib + static_cast<uint32_t>(q) * L;
       idx[q] = -1;
-      if (o < end) {
-        const int i = static_cast<int>(o - o0);
-        const int k = i / per, j = i - k * per;
-        mu_r[q] = __float2int_rn(musig[static_cast<size_t>(k) * ldms + j]);
-        idx[q] = scale_index(s_scales, musig[static_cast<size_t>(k) * ldms + sig_off + j]);
+      if (q > 0) {
+        k += Ldiv;
+        j += Lmod;
+        if (j >= per) {
+          j -= per;
+          ++k;
+        }
+      }
+      if (i < ntot) {
+        mu_f[q] = musig[static_cast<size_t>(k) * ldms + j];
+        sg_f[q] = musig[static_cast<size_t>(k) * ldms + sig_off + j];
         dst[q] = rows[k] * C + c0 + j;
         k16[q] = k * ld16 + c0 + j;
       }
     }
 #pragma unroll
+    for (int q = 0; q < kB; ++q)
+      if (ib + static_cast<uint32_t>(q) * L < ntot) {
+        mu_r[q] = __float2int_rn(mu_f[q]);
+        idx[q] = scale_index(s_scales, sg_f[q]);
+      }
+#pragma unroll
     for (int q = 0; q < kB; ++q) {
       if (idx[q] < 0) break;
-      const int32_t v = dec_value_k(rd, s, s_cdf + idx[q] * (kSyms + 1), s_lut + idx[q] * kLutBuckets,
-                                    ks[q], eb[q], err);
+      const int k = dec_sym_rsv(rs, s, s_cdf + idx[q] * (kSyms + 1), s_lut + idx[q] * kLutBuckets, err);
+      ks[q] = k;
+      eb[q] = 0;
+      int32_t v = k - 127;
+      if (k >= kEscLo) {  // escape: Exp-Golomb magnitude (rare)
+        int nb = 0;
+        bool bad = false;
+        while (dec_sym(rs, s, kBitCum, 2, err) == 0) {
+          if (++nb > 31 || err) {
+            bad = true;
+            break;
+          }
+        }
+        if (bad) {
+          err = 1;
+          v = 0;
+        } else {
+          uint64_t x = 1;
+          for (int i = 0; i < nb; ++i) x = (x << 1) | static_cast<uint64_t>(dec_sym(rs, s, kBitCum, 2, err));
+          eb[q] = 2 * nb + 1;
+          const long long m = static_cast<long long>(x) - 1 + 128;
+          v = static_cast<int32_t>(k == kEscLo ? -m : m);
+        }
+      }
       const int32_t y = v + mu_r[q];
       yhat[dst[q]] = y;
       if (yhat16) yhat16[k16[q]] = __int2half_rn(y);
@@ -475,6 +563,7 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
       if (eb[q]) s.bits += eb[q];
     }
   }
+  s.pos = rs.pos;
   lanes[l] = s;
   if (err) atomicOr(status, 2);
 }
@@ -652,7 +741,8 @@ void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_
     return true;
   }();
   (void)attr;
-  launch_k(decode_phase_kernel, dim3(blocks(L)), dim3(128), smem, st, payload, lanes, L, o0, n, per, musig, ldms,
+  launch_k(decode_phase_kernel, dim3(blocks(L)), dim3(128), smem, st, payload, lanes, L,
+           static_cast<uint32_t>(o0 % static_cast<uint64_t>(L)), n, per, musig, ldms,
                                                   sig_off, scales, cdf, rows, yhat, C, c0, yhat16,
                                                   ld16, status);
   PSWA_LAUNCH_CHECK();

@@ -416,8 +416,9 @@ void Engine::alloc_all() {
   const size_t nsym = static_cast<size_t>(HWo) * C, nz = static_cast<size_t>(D.hc) * D.zh * D.zw;
   main_cap_ = 8 + 4ull * L + 6 * static_cast<size_t>(L) + 16 * nsym;
   hyper_cap_ = 8 + 4ull * Lz + 6 * static_cast<size_t>(Lz) + 16 * nz;
-  d_main_ = dalloc<uint8_t>(main_cap_);
-  d_hyper_ = dalloc<uint8_t>(hyper_cap_);
+  // + 64 B: the decoder's byte reservoirs read up to 32 B past a lane's end
+  d_main_ = dalloc<uint8_t>(main_cap_ + 64);
+  d_hyper_ = dalloc<uint8_t>(hyper_cap_ + 64);
   d_lens_ = dalloc<uint32_t>(2);
   lanes_ = dalloc<pswa_dev::LaneState>(L);
   hlanes_ = dalloc<pswa_dev::LaneState>(Lz);
