@@ -143,6 +143,14 @@ __global__ void build_cdf_kernel(float* scales, uint32_t* cdf, int laplace) {
     while (k + 1 < kSyms && c[k + 1] <= static_cast<uint32_t>(b) * 256u) ++k;
     lut[b] = static_cast<uint16_t>(k);
   }
+  // bit 15 of entry b: every symbol strictly between lut[b] and lut[b + 1]
+  // has frequency 1 (the distribution's tails), so the decoder finds the
+  // symbol of a target in bucket b in closed form instead of searching
+  for (int b = 0; b + 1 < kLutBuckets; ++b) {
+    bool unit = true;
+    for (int j = lut[b] + 1; j < (lut[b + 1] & 0x7fff); ++j) unit = unit && freq[j] == 1u;
+    if (unit) lut[b] |= 0x8000u;
+  }
 }
 
 // ------------------------------------------------------------ helpers -----
@@ -397,7 +405,8 @@ struct Rsv {
 // target q = floor(code / r) (a float quotient, then one exact integer
 // correction step each way: the float error is < 0.04 for q < 65536), a
 // binary search only inside the symbols spanning q's 256-wide bucket
-// (usually 1-2 candidates instead of 8 levels), and a branch-free
+// (usually 1-2 candidates instead of 8 levels; closed form inside the
+// tails' unit-frequency runs), and a branch-free
 // renormalisation: the bytes dec_sym's `while (range < kBot)` loop reads,
 // from the bit length of the new range (r >= 2^24, freq >= 1: at most 2).
 __device__ __forceinline__ int dec_sym_rsv(Rsv& rs, LaneState& s, const uint32_t* cum,
@@ -416,13 +425,20 @@ __device__ __forceinline__ int dec_sym_rsv(Rsv& rs, LaneState& s, const uint32_t
   else if (rq + r <= s.code)
     ++q;
   const int b = static_cast<int>(q >> 8);
-  int lo = lut[b], hi = min(static_cast<int>(lut[b + 1]) + 1, kSyms);
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (cum[mid] <= q)
-      lo = mid;
-    else
-      hi = mid;
+  const uint32_t e0 = lut[b], e1 = lut[b + 1];
+  int lo = static_cast<int>(e0 & 0x7fffu);
+  if (e0 & 0x8000u) {  // unit-frequency run: symbols past lo + 1 sit one per value
+    const uint32_t c1 = cum[lo + 1];
+    if (q >= c1) lo = min(lo + 1 + static_cast<int>(q - c1), static_cast<int>(e1 & 0x7fffu));
+  } else {
+    int hi = min(static_cast<int>(e1 & 0x7fffu) + 1, kSyms);
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (cum[mid] <= q)
+        lo = mid;
+      else
+        hi = mid;
+    }
   }
   const uint32_t c0 = cum[lo], c1 = cum[lo + 1];
   const uint64_t range = static_cast<uint64_t>(r) * (c1 - c0);
@@ -432,6 +448,8 @@ __device__ __forceinline__ int dec_sym_rsv(Rsv& rs, LaneState& s, const uint32_t
   s.range = range << (8 * nb);
   return lo;
 }
+
+constexpr int kDecB = 16;  // symbols per lane gathered per batch (decode_phase)
 
 __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* __restrict__ lanes,
                                     int L, uint32_t o0_mod, int n, int per,
@@ -486,48 +504,53 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
   // 8192 lanes) in one batch. The bit-cost table loads are deferred to the
   // end of the batch (issued together, summed in symbol order) so their
   // latency is off the sequential decode chain.
-  constexpr int kB = 16;
+  constexpr int kB = kDecB;
   const uint32_t ntot = static_cast<uint32_t>(total);
   const int Ldiv = L / per, Lmod = L - Ldiv * per;
   const double* bt = bits_table(cdf);
+  // per-thread parameter slots in shared memory ([q][thread]: conflict-free):
+  // the decode loop below is not unrolled, so its body exists once in the
+  // binary (a 16x unrolled body overflowed the instruction cache)
+  int4* s_par = reinterpret_cast<int4*>(s_scales + kScales);  // {table, mu, dst, dst16}
+  int* s_out = reinterpret_cast<int*>(s_par + kB * blockDim.x);  // k | escape bits << 16
+  const int tid = threadIdx.x, nth = blockDim.x;
   for (uint32_t ib = i_first; ib < ntot; ib += static_cast<uint32_t>(kB) * L) {
-    int mu_r[kB], idx[kB], dst[kB], k16[kB], ks[kB], eb[kB];
-    float mu_f[kB], sg_f[kB];
-    // all loads of the batch first (in flight together), then the table
-    // searches: interleaving them exposes one load latency per symbol.
-    // (k, j) = divmod(i, per) stepped by divmod(L, per): one division per batch
-    int k = static_cast<int>(ib) / per, j = static_cast<int>(ib) - k * per;
+    const int nq = min(kB, static_cast<int>((ntot - ib + L - 1) / static_cast<uint32_t>(L)));
+    {
+      float mu_f[kB], sg_f[kB];
+      int dst[kB], k16[kB];
+      // all loads of the batch first (in flight together), then the table
+      // searches: interleaving them exposes one load latency per symbol.
+      // (k, j) = divmod(i, per) stepped by divmod(L, per): one division per batch
+      int k = static_cast<int>(ib) / per, j = static_cast<int>(ib) - k * per;
 #pragma unroll
-    for (int q = 0; q < kB; ++q) {
-      const uint32_t i = ib + static_cast<uint32_t>(q) * L;
-      idx[q] = -1;
-      if (q > 0) {
-        k += Ldiv;
-        j += Lmod;
-        if (j >= per) {
-          j -= per;
-          ++k;
+      for (int q = 0; q < kB; ++q) {
+        if (q > 0) {
+          k += Ldiv;
+          j += Lmod;
+          if (j >= per) {
+            j -= per;
+            ++k;
+          }
+        }
+        if (q < nq) {
+          mu_f[q] = musig[static_cast<size_t>(k) * ldms + j];
+          sg_f[q] = musig[static_cast<size_t>(k) * ldms + sig_off + j];
+          dst[q] = rows[k] * C + c0 + j;
+          k16[q] = k * ld16 + c0 + j;
         }
       }
-      if (i < ntot) {
-        mu_f[q] = musig[static_cast<size_t>(k) * ldms + j];
-        sg_f[q] = musig[static_cast<size_t>(k) * ldms + sig_off + j];
-        dst[q] = rows[k] * C + c0 + j;
-        k16[q] = k * ld16 + c0 + j;
-      }
+#pragma unroll
+      for (int q = 0; q < kB; ++q)
+        if (q < nq)
+          s_par[q * nth + tid] =
+              make_int4(scale_index(s_scales, sg_f[q]), __float2int_rn(mu_f[q]), dst[q], k16[q]);
     }
-#pragma unroll
-    for (int q = 0; q < kB; ++q)
-      if (ib + static_cast<uint32_t>(q) * L < ntot) {
-        mu_r[q] = __float2int_rn(mu_f[q]);
-        idx[q] = scale_index(s_scales, sg_f[q]);
-      }
-#pragma unroll
-    for (int q = 0; q < kB; ++q) {
-      if (idx[q] < 0) break;
-      const int k = dec_sym_rsv(rs, s, s_cdf + idx[q] * (kSyms + 1), s_lut + idx[q] * kLutBuckets, err);
-      ks[q] = k;
-      eb[q] = 0;
+#pragma unroll 1
+    for (int q = 0; q < nq; ++q) {
+      const int4 pr = s_par[q * nth + tid];
+      const int k = dec_sym_rsv(rs, s, s_cdf + pr.x * (kSyms + 1), s_lut + pr.x * kLutBuckets, err);
+      int eb = 0;
       int32_t v = k - 127;
       if (k >= kEscLo) {  // escape: Exp-Golomb magnitude (rare)
         int nb = 0;
@@ -544,23 +567,34 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
         } else {
           uint64_t x = 1;
           for (int i = 0; i < nb; ++i) x = (x << 1) | static_cast<uint64_t>(dec_sym(rs, s, kBitCum, 2, err));
-          eb[q] = 2 * nb + 1;
+          eb = 2 * nb + 1;
           const long long m = static_cast<long long>(x) - 1 + 128;
           v = static_cast<int32_t>(k == kEscLo ? -m : m);
         }
       }
-      const int32_t y = v + mu_r[q];
-      yhat[dst[q]] = y;
-      if (yhat16) yhat16[k16[q]] = __int2half_rn(y);
+      s_out[q * nth + tid] = k | (eb << 16);
+      const int32_t y = v + pr.y;
+      yhat[pr.z] = y;
+      if (yhat16) yhat16[pr.w] = __int2half_rn(y);
     }
+    // bit costs: loads issued together, summed in symbol order
     double cost[kB];
-#pragma unroll
-    for (int q = 0; q < kB; ++q) cost[q] = idx[q] >= 0 ? __ldg(bt + idx[q] * kSyms + ks[q]) : 0.0;
+    int ebs[kB];
 #pragma unroll
     for (int q = 0; q < kB; ++q) {
-      if (idx[q] < 0) break;
+      cost[q] = 0.0;
+      ebs[q] = 0;
+      if (q < nq) {
+        const int o = s_out[q * nth + tid];
+        ebs[q] = o >> 16;
+        cost[q] = __ldg(bt + s_par[q * nth + tid].x * kSyms + (o & 0xffff));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      if (q >= nq) break;
       s.bits += cost[q];
-      if (eb[q]) s.bits += eb[q];
+      if (ebs[q]) s.bits += ebs[q];
     }
   }
   s.pos = rs.pos;
@@ -735,7 +769,8 @@ void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_
                         const uint32_t* cdf, const int* rows, int32_t* yhat, int C, int c0,
                         __half* yhat16, int ld16, int* status, cudaStream_t st) {
   if (n <= 0) return;
-  constexpr int smem = kScales * (kSyms + 1) * 4 + kScales * kLutBuckets * 2 + kScales * 4;
+  constexpr int smem = kScales * (kSyms + 1) * 4 + kScales * kLutBuckets * 2 + kScales * 4 +
+                       kDecB * 128 * (16 + 4);
   static const bool attr = [] {
     PSWA_CUDA(cudaFuncSetAttribute(decode_phase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     return true;

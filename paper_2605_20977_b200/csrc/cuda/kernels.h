@@ -121,8 +121,9 @@ constexpr int kSyms = 257;  // v in [-127,127] + 2 escapes
 // in fp64 with IEEE round-to-nearest ops only (bit-exact with the host rule),
 // followed (at cdf + 64*258, 8-byte aligned) by 64 x 257 fp64 symbol costs
 // and 64 x 257 uint16 search-index entries (entry b of a table: the symbol
-// whose cumulative interval holds b * 256; the decoder's symbol search starts
-// from the bucket of its target).
+// whose cumulative interval holds b * 256 in bits 0-14, bit 15 set when the
+// symbols strictly between entries b and b + 1 all have frequency 1; the
+// decoder's symbol search starts from the bucket of its target).
 constexpr int kLutBuckets = 257;
 constexpr size_t kCdfWords = static_cast<size_t>(kScales) * (kSyms + 1) + 2 * kScales * kSyms +
                              static_cast<size_t>(kScales) * kLutBuckets / 2;
