@@ -16,5 +16,7 @@ timeout 600 $NCU -k regex:window_attn -s 66 -c 1 -o gpurun_out/ncu_step_attn pyt
 # 53 = accumulator Q projection of step 0 (M=2040 N=K=512, the step_wq shape)
 timeout 600 $NCU -k regex:gemm_tc_kernel -s 8 -c 1 -o gpurun_out/ncu_ctx_ffn_gu python tools/profile_decode.py > /dev/null 2>&1
 timeout 600 $NCU -k regex:gemm_tc_kernel -s 53 -c 1 -o gpurun_out/ncu_step_wq python tools/profile_decode.py > /dev/null 2>&1
+# phase (t=1, g=1) of the entropy decoder
+timeout 600 $NCU -k regex:decode_phase -s 5 -c 1 -o gpurun_out/ncu_decode_phase python tools/profile_decode.py > /dev/null 2>&1
 python tools/ncu_traffic.py ${TAG:-r01} > gpurun_out/traffic.log 2>&1
 ls gpurun_out
