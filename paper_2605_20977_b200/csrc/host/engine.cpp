@@ -398,6 +398,9 @@ void Engine::alloc_all() {
   bxn_ = dalloc<__half>(nb * d);
   bssq_ = dalloc<float>(nb * (d / 32));
   bq_ = dalloc<__half>(nb * d);
+  qall_ = dalloc<__half>(static_cast<size_t>(HWo) * d);
+  qall16_ = dalloc<__half>(static_cast<size_t>(HWo) * d);
+  qall_ssq_ = dalloc<float>(static_cast<size_t>(HWo) * (d / 32));
   batt_ = dalloc<__half>(nb * d);
   bh_ = dalloc<__half>(nb * D.fp);
   bs1n_ = dalloc<__half>(nb * d);
@@ -1061,6 +1064,22 @@ void Engine::build_s1(Program& P, const StepBatch& bt, bool encoder) {
   exchange(P, kXidAcc, bt.xkind);
 }
 
+// The accumulator's queries depend on Hq only, not on any
+// decoded step: the decoder computes them for every position at once, in
+// batch_all order (the encoder's single-batch layout, so the rows and their
+// values are the encoder's), on the side stream next to the context
+// transformer instead of once per step on the critical path.
+void Engine::build_acc_q_all(Program& P) {
+  const int d = D_.d;
+  const StepBatch all = batch_all();
+  const int* rows = all.rows;
+  const int M = all.M;
+  add(P, [=, this](cudaStream_t s) {
+    pswa_dev::rms_prep(hq_, d, rows, M, d, nullptr, 0, qall16_, d, qall_ssq_, d / 32, s);
+  });
+  gemm(P, qall16_, d, M, acc_.wq, d, rms_in(f16_out(qall_, d), qall_ssq_));
+}
+
 void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
   const Dims& D = D_;
   const int d = D.d, M = bt.M;
@@ -1069,10 +1088,15 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
   add(P, [=, this](cudaStream_t s) {  // residual = Hq rows, normq folded into acc.wq
     pswa_dev::rms_prep(hq_, d, rows, M, d, bx_, d, bxn_, d, bssq_, d / 32, s);
   });
-  gemm(P, bxn_, d, M, acc_.wq, d, rms_in(f16_out(bq_, d), bssq_));
+  // decode: Q precomputed by build_acc_q_all (step t at its batch_all offset)
+  if (mode != 0) gemm(P, bxn_, d, M, acc_.wq, d, rms_in(f16_out(bq_, d), bssq_));
   for (const auto& pt : bt.parts) {
     const int t = pt[0], off = pt[1], n = pt[2];
-    attention(P, bq_ + static_cast<size_t>(off) * d, step_qinfo_[t], n, step_tiles_[t], n_step_tiles_[t],
+    size_t qoff = static_cast<size_t>(off);
+    if (mode == 0)
+      for (int tt = 0; tt < t; ++tt) qoff += step_rows_h_[tt].size();
+    const __half* q = (mode == 0 ? qall_ : bq_) + qoff * d;
+    attention(P, q, step_qinfo_[t], n, step_tiles_[t], n_step_tiles_[t],
               &shape_step_[t][2], acc_kv_, 0, 0, 2, acc_.pos, batt_ + static_cast<size_t>(off) * d);
   }
   gemm(P, batt_, d, M, acc_.wo, d, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + S2 norm1 inputs
@@ -1185,6 +1209,7 @@ Program& Engine::program(const std::string& key) {
     });
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_lane_bits(hlanes_, Lz, bits_, s); });
     build_hyper_decode(P);
+    build_acc_q_all(P);
     to_side(P, side_from);
     if (B_.n > 1) join_side(P);
     add(P, [=, this](cudaStream_t s) {

@@ -192,6 +192,7 @@ class Engine {
   void build_hyper_encode(Program& P);
   void build_s1(Program& P, const StepBatch& bt, bool encoder);
   void build_step(Program& P, const StepBatch& bt, int mode /*0 decode, 1 encode*/);
+  void build_acc_q_all(Program& P);
   void build_embed(Program& P, const StepBatch& bt);
   void run(Program& P);
   void to_side(Program& P, size_t from);
@@ -313,6 +314,10 @@ class Engine {
   // batch buffers
   int nmax_ = 0;
   float *bx_ = nullptr, *chx_ = nullptr, *musig_ = nullptr;
+  // decoder: accumulator queries of every step (batch_all order), computed
+  // from Hq on the side stream while the context transformer runs
+  __half *qall_ = nullptr, *qall16_ = nullptr;
+  float* qall_ssq_ = nullptr;
   __half *bxn_ = nullptr, *bq_ = nullptr, *batt_ = nullptr, *bh_ = nullptr, *bs1n_ = nullptr,
          *bs2n_ = nullptr, *y16_ = nullptr, *chxn_[4] = {}, *chh_ = nullptr,
          *chfo_ = nullptr, *hh16_ = nullptr;
