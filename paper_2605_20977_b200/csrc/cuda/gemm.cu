@@ -52,21 +52,31 @@ struct GemmCfg {
 };
 
 __device__ __forceinline__ float silu_f(float v) { return __fdividef(v, 1.0f + __expf(-v)); }
-__device__ __forceinline__ float softplus_f(float v) {
-  if (v > 30.0f) return v;
-  if (v < -30.0f) return __expf(v);
-  return log1pf(__expf(v));
-}
 
 // Elementwise part of the epilogue for 32 accumulator columns [n0, n0+32).
 template <int EPI>
 __device__ __forceinline__ void epi_values(const GemmEpi& ep, int n0, float (&v)[32]) {
   if (EPI == kEpiHead) {
+    // mu = (v + b) * scale; sigma = 0.11 + softplus(v + b) with softplus(x)
+    // = x above 30, exp(x) below -30, log1p(exp(x)) between; evaluated
+    // branch-free with the column parameters loaded up front (per-element
+    // branches and loads made this epilogue ~11k cycles per tile)
+    float b[32], sc[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const int n = n0 + j;
-      const float b = ep.bias ? ep.bias[n] : 0.0f;
-      v[j] = n < ep.split ? (v[j] + b) * (ep.scale ? ep.scale[n] : 1.0f) : 0.11f + softplus_f(v[j] + b);
+      b[j] = ep.bias ? ep.bias[n0 + j] : 0.0f;
+      sc[j] = ep.scale ? ep.scale[n0 + j] : 1.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float x = v[j] + b[j];
+      if (n0 + j < ep.split) {
+        v[j] = x * sc[j];
+      } else {
+        const float e = __expf(x);
+        const float l = log1pf(e);
+        v[j] = 0.11f + (x > 30.0f ? x : (x < -30.0f ? e : l));
+      }
     }
     return;
   }
@@ -159,7 +169,7 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
   const bool full = oc0 + ncols <= ep.n_store;
   if (EPI == kEpiF32 || EPI == kEpiHead) {
     float* dst = static_cast<float*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0;
-    if (EPI == kEpiF32 && full) {
+    if ((EPI == kEpiF32 || EPI == kEpiHead) && full) {  // (head: no residual / norm outputs)
       float4* d4 = reinterpret_cast<float4*>(dst);
       float ss = 0.0f;
       uint32_t hp[16];
@@ -557,6 +567,7 @@ bool gemm_trace_read(unsigned long long* out, int n) {
   n = std::min(n, kGemmTraceSlots * 1024);
   PSWA_CUDA(cudaDeviceSynchronize());
   PSWA_CUDA(cudaMemcpy(out, trace_buffer(), sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
+  PSWA_CUDA(cudaMemset(trace_buffer(), 0, sizeof(unsigned long long) * kGemmTraceSlots * 1024));
   return true;
 }
 

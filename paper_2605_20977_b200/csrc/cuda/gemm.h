@@ -57,8 +57,8 @@ struct GemmEpi {
   unsigned long long* trace = nullptr;
 };
 constexpr int kGemmTraceSlots = 16;
-// Copies the last traced launch's stamps (n words) to host; false when
-// tracing is off.
+// Copies the stamps written since the previous call (n words) to host and
+// clears them; false when tracing is off.
 bool gemm_trace_read(unsigned long long* out, int n);
 
 struct GemmPlan {

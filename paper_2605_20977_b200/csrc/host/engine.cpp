@@ -1157,6 +1157,7 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
     e2.scale = cur_rso_ + g * Cg;
     e2.n_store = 2 * Cg;
     gemm(P, hh16_, 2 * sp, M, head_w2_[g], 2 * sp, e2);
+    if (mode == 0 && g == 0 && bt.parts[0][0] == 0) tag(P, "ch_head2", 2.0 * M * (2.0 * Cg) * (2.0 * sp));
     const int c0 = g * Cg;
     for (const auto& pt : bt.parts) {  // per step: the symbols of phase (t, g)
       const int t = pt[0], off = pt[1], n = pt[2];

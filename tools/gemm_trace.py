@@ -37,8 +37,7 @@ names = {1: "setup", 2: "pdl_wait", 10: "tma_issued", 3: "first_stage", 4: "mma_
          5: "acc_ready", 6: "epi_done", 7: "exit"}
 for op in sys.argv[1:] or ["step_wq", "ctx_ffn_gu"]:
     buf = np.zeros(SLOTS * 1024, np.uint64)
-    lib().pswa_debug_gemm_trace(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), buf.size)
-    buf[:] = 0
+    lib().pswa_debug_gemm_trace(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), buf.size)  # clears
     us, _ = dec.bench_op(op, 5)
     lib().pswa_debug_gemm_trace(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), buf.size)
     t = buf.reshape(1024, SLOTS).astype(np.int64)
