@@ -835,8 +835,11 @@ void Engine::block_step(Program& P, const Block& B, const StepBatch& bt) {
     if (probe) tag(P, "step_attn", attn_flops(t, mk, 1));
   }
   gemm(P, batt_, d, M, B.wo, d, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + norm2 inputs
+  if (probe) tag(P, "step_wo", 2.0 * M * d * d);
   gemm(P, bxn_, d, M, B.wgu, d, rms_in(swiglu_out(bh_, D.fp), bssq_));
+  if (probe) tag(P, "step_gu", 2.0 * M * 2.0 * D.f * d);
   gemm(P, bh_, D.fp, M, B.wd, D.fp, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + next norm1 inputs
+  if (probe) tag(P, "step_wd", 2.0 * M * D.f * d);
 }
 
 // Blocks of time-causal 3D SWA over S slots of own rows held in ctx_x_
@@ -1129,9 +1132,13 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
       __half* xn = chxn_[b];
       add(P, [=](cudaStream_t s) { pswa_dev::rmsnorm_rows(xg, dchp, nullptr, M, sl, sl, g1, xn + g * sp, dchp, s); });
       const PW mixg{ch_mix_[b].p + static_cast<size_t>(g) * sp * dchp, sp, dchp};
+      const bool pr = mode == 0 && g == 1 && b == 0 && bt.parts[0][0] == 0;
       gemm(P, xn, dchp, M, mixg, (g + 1) * sp, ch_rms_out(f32_acc(xg, dchp, sl)));
+      if (pr) tag(P, "ch_mix", 2.0 * M * sl * (g + 1) * sl);
       gemm(P, chx16_, sp, M, ch_gu_[b][g], sp, ch_rms_in(swiglu_out(chh_, D.fgp)));
+      if (pr) tag(P, "ch_gu", 2.0 * M * 2.0 * D.fg * sl);
       gemm(P, chh_, D.fgp, M, ch_d_[b][g], D.fgp, ch_rms_out(f32_acc(xg, dchp, sl)));
+      if (pr) tag(P, "ch_d", 2.0 * M * D.fg * sl);
     }
     const float* go = ch_gout_ + g * sl;
     if (c_lrp() > 0) {  // the LRP transformer reads the normalised final representation
@@ -1147,6 +1154,7 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
       gemm(P, chfo_, sp, M, head_w1_[g], sp, e1);
     else  // final norm folded: A = fp16 slot g, 1/rms from the last d GEMM
       gemm(P, chx16_, sp, M, head_w1_[g], sp, ch_rms_in(e1));
+    if (mode == 0 && g == 0 && bt.parts[0][0] == 0) tag(P, "ch_head1", 2.0 * M * (2.0 * sl) * sl);
     GemmEpi e2;
     e2.out = musig_;
     e2.ld_out = ms;

@@ -1,6 +1,4 @@
-for g in 8 16; do
-PSWA_BENCH_GOPS=$g timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu --no-config5 --no-lrp > gpurun_out/bench_g$g.json 2> gpurun_out/bench_g$g.err
-python -c "
-import json; d=json.load(open('gpurun_out/bench_g$g.json'))
-print($g, d['ms_per_frame'], d['config4_gop_batch'])"
-done
+# scratch GPU call (edited per experiment)
+mkdir -p gpurun_out
+make -C paper_2605_20977_b200 clean > /dev/null; make -C paper_2605_20977_b200 -j16 TRACE=1 > /dev/null 2>&1; echo build rc=$?
+timeout 300 python tools/gemm_trace.py step_wq step_wo step_gu step_wd ch_mix ch_gu ch_d ch_head1 ch_head2 2>&1 | grep -v "^ *\(setup\|tma_issued\)"
