@@ -609,7 +609,8 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   }
   // CTA pairs sharing B through TMA multicast: correct and available, but
   // measured neutral-to-slower on B200 (the L2 already dedups concurrent B
-  // reads; 10.56 vs 10.44 ms / frame), so opt-in via PSWA_GEMM_CLUSTER=1.
+  // reads; 10.56 vs 10.44 ms / frame; on the M = 2040 step GEMMs alone
+  // 7.80 vs 7.59 ms / frame), so opt-in via PSWA_GEMM_CLUSTER=1.
   static const bool use_cluster = std::getenv("PSWA_GEMM_CLUSTER") != nullptr;
   if (std::getenv("PSWA_GEMM_TRACE")) p->epi.trace = trace_buffer();
   p->cluster = (use_cluster && M > kBM) ? 2 : 1;
