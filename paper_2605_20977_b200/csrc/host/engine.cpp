@@ -194,7 +194,9 @@ void Engine::alloc_all() {
       auto ctx_tiles = [&](int slot_from, int row_base, int S) {
         std::vector<int> v;
         const int yend = own0 + B_.nown;
-        for (int j = slot_from; j < S; ++j)
+        // newest slot first: a slot-j tile walks min(j + 1, wt) key slots, so
+        // the heaviest tiles are dispatched first and the launch tail is light
+        for (int j = S - 1; j >= slot_from; --j)
           for (int y0 = own0; y0 < yend; y0 += 4)
             for (int x0 = 0; x0 < D.W; x0 += 16) {
               std::vector<int> t(TI, -1);

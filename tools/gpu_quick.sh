@@ -1,4 +1,8 @@
 # scratch GPU call (edited per experiment)
 mkdir -p gpurun_out
-make -C paper_2605_20977_b200 clean > /dev/null; make -C paper_2605_20977_b200 -j16 TRACE=1 > /dev/null 2>&1; echo build rc=$?
-timeout 300 python tools/gemm_trace.py step_wq step_wo step_gu step_wd ch_mix ch_gu ch_d ch_head1 ch_head2 2>&1 | grep -v "^ *\(setup\|tma_issued\)"
+B="python bench.py --steps 20 --warmup 3 --no-cpu --no-config4 --no-config5 --no-lrp"
+P="import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['e2e']['ms_per_frame'], d['decoded_bit_exact'])"
+timeout 600 $B 2>/dev/null | python -c "$P"
+timeout 300 python tools/probe_ops.py 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 600 $B 2>/dev/null | python -c "$P"
