@@ -111,8 +111,10 @@ __global__ void __launch_bounds__(256, NP == 1 ? 3 : 2)
   constexpr int NCH = NP * kPassChunks;  // chunk slots held in registers (row keys)
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h0 = blockIdx.y * a.hpc;  // this CTA's heads: [h0, h0 + hpc)
-  const int32_t* T = a.tiles + blockIdx.x * kAttnTileInts;
+  // grid x = head group (fastest in dispatch order), y = tile: a tile's head
+  // groups launch together, so tile order (heaviest first) is dispatch order
+  const int h0 = blockIdx.x * a.hpc;  // this CTA's heads: [h0, h0 + hpc)
+  const int32_t* T = a.tiles + blockIdx.y * kAttnTileInts;
   const int hy0 = T[0], hx0 = T[1], HR = T[2], sl = T[3], nw = T[4];
   const int nslots = a.wt > 0 ? min(sl + 1, a.wt) : 1;
   const int j0 = sl - nslots + 1;
@@ -353,7 +355,7 @@ __global__ void score_table_kernel(const float* __restrict__ bias, int taps_tota
 template <int NP>
 void launch_t8(const AttnArgs& a, const CUtensorMap& map, int halo_keys, int ntiles, int heads,
                int warps, cudaStream_t st) {
-  launch_k(window_attn_t8_kernel<NP>, dim3(ntiles, heads / a.hpc), dim3(warps * 32),
+  launch_k(window_attn_t8_kernel<NP>, dim3(heads / a.hpc, ntiles), dim3(warps * 32),
            smem_bytes(halo_keys, a.dbuf), st, a, map);
 }
 
