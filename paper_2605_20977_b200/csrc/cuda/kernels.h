@@ -32,6 +32,9 @@ void fill_context_slots(const float* const* ring, const int* slot_src, const flo
                         int HW, int d, float* x, cudaStream_t st);
 // frame [HW][C] int32 -> [C][HW] int32
 void yhat_to_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st);
+// channels [c0, c0 + nc) only: dst[c][p] = src[p][c]
+void yhat_to_chw_cols(const int32_t* src, int HW, int C, int c0, int nc, int32_t* dst,
+                      cudaStream_t st);
 void yhat_from_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st);
 void scatter_rows_f32(const float* src, int lds, const int* rows, int M, int n, float* dst,
                       int ldd, cudaStream_t st);

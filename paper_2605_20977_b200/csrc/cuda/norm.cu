@@ -158,20 +158,21 @@ __global__ void fill_slots_kernel(const float* const* __restrict__ ring, const i
   }
 }
 
-__global__ void transpose_i32_kernel(const int32_t* __restrict__ src, int rows, int cols,
-                                     int32_t* __restrict__ dst) {
+// dst[c * ldd + r] = src[r * lds + c] for r < rows, c < cols
+__global__ void transpose_i32_kernel(const int32_t* __restrict__ src, int rows, int cols, int lds,
+                                     int32_t* __restrict__ dst, int ldd) {
   pdl_wait();
   pdl_trigger();
   __shared__ int32_t tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   for (int j = threadIdx.y; j < 32; j += 8) {
     const int r = by + j, c = bx + threadIdx.x;
-    if (r < rows && c < cols) tile[j][threadIdx.x] = src[static_cast<size_t>(r) * cols + c];
+    if (r < rows && c < cols) tile[j][threadIdx.x] = src[static_cast<size_t>(r) * lds + c];
   }
   __syncthreads();
   for (int j = threadIdx.y; j < 32; j += 8) {
     const int c = bx + j, r = by + threadIdx.x;
-    if (r < rows && c < cols) dst[static_cast<size_t>(c) * rows + r] = tile[threadIdx.x][j];
+    if (r < rows && c < cols) dst[static_cast<size_t>(c) * ldd + r] = tile[threadIdx.x][j];
   }
 }
 
@@ -313,14 +314,20 @@ void rms_prep(const float* x, int ldx, const int* src_rows, int M, int d, float*
 }
 
 void yhat_to_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st) {
-  dim3 grid((C + 31) / 32, (HW + 31) / 32);
-  launch_k(transpose_i32_kernel, dim3(grid), dim3(32, 8), 0, st, src, HW, C, dst);
+  yhat_to_chw_cols(src, HW, C, 0, C, dst, st);
+}
+
+void yhat_to_chw_cols(const int32_t* src, int HW, int C, int c0, int nc, int32_t* dst,
+                      cudaStream_t st) {
+  dim3 grid((nc + 31) / 32, (HW + 31) / 32);
+  launch_k(transpose_i32_kernel, dim3(grid), dim3(32, 8), 0, st, src + c0, HW, nc, C,
+           dst + static_cast<size_t>(c0) * HW, HW);
   PSWA_LAUNCH_CHECK();
 }
 
 void yhat_from_chw(const int32_t* src, int HW, int C, int32_t* dst, cudaStream_t st) {
   dim3 grid((HW + 31) / 32, (C + 31) / 32);
-  launch_k(transpose_i32_kernel, dim3(grid), dim3(32, 8), 0, st, src, C, HW, dst);
+  launch_k(transpose_i32_kernel, dim3(grid), dim3(32, 8), 0, st, src, C, HW, HW, dst, C);
   PSWA_LAUNCH_CHECK();
 }
 

@@ -99,6 +99,10 @@ Engine::Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len, in
   PSWA_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
   PSWA_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   PSWA_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  PSWA_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+  for (auto& e : ev_copy_) PSWA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  PSWA_CUDA(cudaEventCreateWithFlags(&ev_copy_done_, cudaEventDisableTiming));
+  PSWA_CUDA(cudaEventCreateWithFlags(&ev_main_in_, cudaEventDisableTiming));
   const WeightMap w = parse_psww(cfg, blob, len);
   build_tables();
   alloc_all();
@@ -123,6 +127,11 @@ Engine::~Engine() {
   for (void* p : allocs_) cudaFree(p);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
+  for (auto& e : ev_copy_)
+    if (e) cudaEventDestroy(e);
+  if (ev_copy_done_) cudaEventDestroy(ev_copy_done_);
+  if (ev_main_in_) cudaEventDestroy(ev_main_in_);
+  if (copy_) cudaStreamDestroy(copy_);
   if (side_) cudaStreamDestroy(side_);
   if (st_) cudaStreamDestroy(st_);
 }
@@ -1192,6 +1201,13 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
         });
       }
     }
+    if (mode == 0 && host_copy_ && bt.parts.size() == 1 && bt.parts[0][0] == D.c.s - 1) {
+      // channel group g of the last step decoded: its CHW planes are final
+      const int HWo = HWo_;
+      add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_to_chw_cols(yfr_, HWo, C, c0, Cg, ychw_, s); });
+      P.cuts.push_back(Cut{P.ops.size(), false});
+      P.copy_group.push_back(g);
+    }
   }
   if (mode == 0) build_embed(P, bt);
 }
@@ -1206,6 +1222,8 @@ Program& Engine::program(const std::string& key) {
   const size_t yoff = static_cast<size_t>(B_.own0) * D.W * C;  // own rows in yfr_
   const std::string base = key.substr(0, key.find('+'));  // "+ms": mu/sigma outputs
   if (base == "decode") {
+    // "+h" (single band): per-group ŷ transpositions and cuts for the host copies
+    host_copy_ = key == "decode+h" && B_.n == 1;
     // the hyperprior branch (z_hat lanes -> hyper decoder -> Hq) does not
     // depend on the context transformer: it runs on a side stream of the
     // same graph and joins before the first Hq consumer (band mode: before
@@ -1223,17 +1241,23 @@ Program& Engine::program(const std::string& key) {
     build_acc_q_all(P);
     to_side(P, side_from);
     if (B_.n > 1) join_side(P);
+    build_ctx(P);
+    if (B_.n == 1) join_side(P);
+    if (host_copy_) {  // the main payload's H2D copy runs beside the context transformer
+      P.cuts.push_back(Cut{P.ops.size(), false});
+      P.copy_group.push_back(kCutMainIn);
+    }
     add(P, [=, this](cudaStream_t s) {
       pswa_dev::lanes_init(d_main_, d_lens_ + 1, L, static_cast<uint32_t>(HW) * C, lanes_, status_, s);
     });
-    build_ctx(P);
-    if (B_.n == 1) join_side(P);
     for (int t = 0; t < D.c.s; ++t) {
       if (t > 0) build_s1(P, batch_of(t - 1), false);
       build_step(P, batch_of(t), 0);
     }
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_lane_bits(lanes_, L, bits_ + 1, s); });
-    add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_to_chw(yfr_ + yoff, HW, C, ychw_, s); });
+    if (!host_copy_)
+      add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_to_chw(yfr_ + yoff, HW, C, ychw_, s); });
+    host_copy_ = false;
     if (c_lrp() > 0) build_lrp(P);
   } else if (base == "encode" || base == "encode_z") {
     const bool zgiven = base == "encode_z";
@@ -1334,6 +1358,23 @@ void Engine::run(Program& P) {
   if (B_.n > 1 && !ipc_) throw std::logic_error("in-process band engines are run by their BandGroup");
   last_launches_ = P.launches;
   launch_segment(P, 0);
+}
+
+void Engine::run_host_copy(Program& P, int32_t* yhat_out) {
+  last_launches_ = P.launches;
+  const size_t plane = static_cast<size_t>(HWo_) * D_.Cg;  // one channel group, int32
+  for (int k = 0; k < segments(P); ++k) {
+    launch_segment(P, k);
+    const int g = k < static_cast<int>(P.copy_group.size()) ? P.copy_group[k] : -1;
+    if (g == kCutMainIn) PSWA_CUDA(cudaStreamWaitEvent(st_, ev_main_in_, 0));
+    if (g < 0) continue;
+    PSWA_CUDA(cudaEventRecord(ev_copy_[g], st_));
+    PSWA_CUDA(cudaStreamWaitEvent(copy_, ev_copy_[g], 0));
+    PSWA_CUDA(cudaMemcpyAsync(yhat_out + g * plane, ychw_ + g * plane, plane * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, copy_));
+  }
+  PSWA_CUDA(cudaEventRecord(ev_copy_done_, copy_));
+  PSWA_CUDA(cudaStreamWaitEvent(st_, ev_copy_done_, 0));
 }
 
 // ------------------------------------------------------------ probes ------
@@ -1685,13 +1726,20 @@ FrameResult Engine::encode(const int32_t* yhat_chw, int rate, int fidx, const in
 }
 
 void Engine::prep_decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
-                         int rate, int fidx, bool device) {
+                         int rate, int fidx, bool device, bool defer_main) {
   if (hyper_len > hyper_cap_ || main_len > main_cap_)
     throw pswa_abi::TruncatedError("payload larger than the decoder's capacity");
   set_frame_params(rate, fidx);
   const cudaMemcpyKind in_kind = device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   PSWA_CUDA(cudaMemcpyAsync(d_hyper_, hyper, hyper_len, in_kind, st_));
-  PSWA_CUDA(cudaMemcpyAsync(d_main_, main_pl, main_len, in_kind, st_));
+  if (defer_main) {  // on copy_, awaited by the program's kCutMainIn cut
+    PSWA_CUDA(cudaEventRecord(ev_main_in_, st_));  // d_main_ free: earlier work on st_ done
+    PSWA_CUDA(cudaStreamWaitEvent(copy_, ev_main_in_, 0));
+    PSWA_CUDA(cudaMemcpyAsync(d_main_, main_pl, main_len, in_kind, copy_));
+    PSWA_CUDA(cudaEventRecord(ev_main_in_, copy_));
+  } else {
+    PSWA_CUDA(cudaMemcpyAsync(d_main_, main_pl, main_len, in_kind, st_));
+  }
   lens_h_[0] = static_cast<uint32_t>(hyper_len);
   lens_h_[1] = static_cast<uint32_t>(main_len);
   PSWA_CUDA(cudaMemcpyAsync(d_lens_, lens_h_, sizeof(lens_h_), cudaMemcpyHostToDevice, st_));
@@ -1702,12 +1750,15 @@ FrameResult Engine::finish_decode(bool advance, int32_t* yhat_out, bool device) 
   FrameResult r;
   const size_t row = static_cast<size_t>(HWo_) * sizeof(int32_t);
   const cudaMemcpyKind k = device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  if (B_.n == 1)
+  if (!yhat_out) {
+    // already copied (run_host_copy)
+  } else if (B_.n == 1) {
     PSWA_CUDA(cudaMemcpyAsync(yhat_out, ychw_, row * D.C, k, st_));
-  else
+  } else {
     PSWA_CUDA(cudaMemcpy2DAsync(yhat_out + static_cast<size_t>(B_.r0) * D.W,
                                 static_cast<size_t>(D.HW) * sizeof(int32_t), ychw_, row, row, D.C,
                                 k, st_));
+  }
   PSWA_CUDA(cudaMemcpyAsync(r.bits, bits_, sizeof(r.bits), cudaMemcpyDeviceToHost, st_));
   PSWA_CUDA(cudaMemcpyAsync(&r.status, status_, sizeof(int), cudaMemcpyDeviceToHost, st_));
   PSWA_CUDA(cudaStreamSynchronize(st_));
@@ -1741,6 +1792,19 @@ FrameResult Engine::finish_async() {
 
 FrameResult Engine::decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
                            int rate, int fidx, bool advance, int32_t* yhat_out, bool device) {
+  // pinned host output: the copies of finished channel groups overlap the
+  // last groups' decoding (a pageable destination makes each copy blocking,
+  // so it keeps the single copy at the end)
+  cudaPointerAttributes pa{};
+  const bool pinned = !device && cudaPointerGetAttributes(&pa, yhat_out) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost;
+  if (!device) (void)cudaGetLastError();  // pageable pointers may set an error on older drivers
+  if (pinned && B_.n == 1 && D_.N <= 8) {
+    Program& P = program("decode+h");
+    prep_decode(hyper, hyper_len, main_pl, main_len, rate, fidx, device, true);
+    run_host_copy(P, yhat_out);
+    return finish_decode(advance, nullptr, device);
+  }
   prep_decode(hyper, hyper_len, main_pl, main_len, rate, fidx, device);
   run(program("decode"));
   return finish_decode(advance, yhat_out, device);

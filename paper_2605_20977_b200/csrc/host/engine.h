@@ -75,9 +75,14 @@ struct Cut {
   size_t at;
   bool global;
 };
+constexpr int kCutMainIn = -2;
 struct Program {
   std::vector<std::function<void(cudaStream_t)>> ops;
   std::vector<Cut> cuts;
+  // host-output decode (single band): cut k ends channel group copy_group[k]
+  // of the last step (its CHW planes are final); kCutMainIn: the segment
+  // after this cut reads the main payload (its H2D copy overlaps the first)
+  std::vector<int> copy_group;
   int launches = 0;
   std::vector<cudaGraphExec_t> execs;  // one graph per segment
 };
@@ -134,7 +139,7 @@ class Engine {
   // Split-phase frame API: prep_* stage inputs on the stream, the group runs
   // the program's segments on every band, finish_* collects the outputs.
   void prep_decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
-                   int rate, int fidx, bool device);
+                   int rate, int fidx, bool device, bool defer_main = false);
   FrameResult finish_decode(bool advance, int32_t* yhat_out, bool device);
   // Asynchronous device-resident decode (no host sync; ring not advanced):
   // several handles on their own streams overlap on one GPU (GOP batches,
@@ -195,6 +200,12 @@ class Engine {
   void build_acc_q_all(Program& P);
   void build_embed(Program& P, const StepBatch& bt);
   void run(Program& P);
+  // decode program "decode+h": every segment in order, each finished channel
+  // group's ŷ planes copied to the host on copy_ while later groups decode
+  void run_host_copy(Program& P, int32_t* yhat_out);
+  bool host_copy_ = false;  // set while the "+h" program is being built
+  cudaStream_t copy_ = nullptr;
+  cudaEvent_t ev_copy_[8] = {}, ev_copy_done_ = nullptr, ev_main_in_ = nullptr;
   void to_side(Program& P, size_t from);
   void join_side(Program& P);
   cudaStream_t side_ = nullptr;
