@@ -101,8 +101,8 @@ class GpuCodec:
     def encode_frame(self, yhat: np.ndarray, rate: int = 0, fidx: int = 0):
         y = np.ascontiguousarray(yhat, np.int32)
         cap = 20 * y.size + (1 << 20)
-        hb = np.zeros(cap, np.uint8)
-        mb = np.zeros(cap, np.uint8)
+        hb = np.empty(cap, np.uint8)
+        mb = np.empty(cap, np.uint8)
         hl, ml = C.c_size_t(), C.c_size_t()
         bits = np.zeros(2, np.float64)
         check(lib().pswa_gpu_encode_frame(self.h, _ptr(y), rate, fidx, _ptr(hb), cap, C.byref(hl),
@@ -125,7 +125,7 @@ class GpuCodec:
                      advance: bool = True):
         hb = np.frombuffer(hyper, np.uint8)
         mb = np.frombuffer(main, np.uint8)
-        y = np.zeros(self.shape, np.int32)
+        y = np.empty(self.shape, np.int32)
         bits = np.zeros(2, np.float64)
         check(lib().pswa_gpu_decode_frame(self.h, _ptr(hb), len(hyper), _ptr(mb), len(main), rate,
                                           fidx, int(advance), _ptr(y),
@@ -147,7 +147,7 @@ class GpuCodec:
         f = np.ascontiguousarray(frames, np.int32)
         n = C.c_size_t()
         cap = 20 * f.size + (1 << 20) * max(1, f.shape[0])
-        buf = np.zeros(cap, np.uint8)
+        buf = np.empty(cap, np.uint8)
         check(lib().pswa_gpu_encode_sequence(self.h, _ptr(f), f.shape[0], gop, rate, _ptr(buf), cap,
                                              C.byref(n)))
         return bytes(buf[:n.value])
@@ -272,8 +272,8 @@ class BandGroupCodec:
         y = np.ascontiguousarray(yhat, np.int32)
         z = None if zhat is None else np.ascontiguousarray(zhat, np.int32)
         cap = 20 * y.size + (1 << 20)
-        hb = np.zeros(cap, np.uint8)
-        mb = np.zeros(cap, np.uint8)
+        hb = np.empty(cap, np.uint8)
+        mb = np.empty(cap, np.uint8)
         hl, ml = C.c_size_t(), C.c_size_t()
         bits = np.zeros(2, np.float64)
         check(lib().pswa_group_encode_frame(self.h, _ptr(y), None if z is None else _ptr(z), rate,
@@ -290,7 +290,7 @@ class BandGroupCodec:
                      advance: bool = True):
         hb = np.frombuffer(hyper, np.uint8)
         mb = np.frombuffer(main, np.uint8)
-        y = np.zeros(self.shape, np.int32)
+        y = np.empty(self.shape, np.int32)
         bits = np.zeros(2, np.float64)
         check(lib().pswa_group_decode_frame(self.h, _ptr(hb), len(hyper), _ptr(mb), len(main),
                                             rate, fidx, int(advance), _ptr(y),

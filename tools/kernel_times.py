@@ -1,7 +1,8 @@
 """Warm, in-graph per-kernel GPU times (run with PSWA_NO_PDL=1: with PDL a
 kernel's duration includes its wait on the predecessor) of the bench decode (CUPTI via the
 torch profiler): N decodes of the 1080p paper-scale P-frame, aggregated by
-kernel. Unlike an ncu launch list these are not serialised or cold-cache."""
+kernel. Unlike an ncu launch list these are not serialised or cold-cache.
+PK=encode profiles the teacher-forced encode of the same frame instead."""
 import collections
 import os
 import sys
@@ -30,9 +31,20 @@ for _ in range(3):
     y, _ = dec.decode_frame(hyper, main, fidx=4, advance=False)
 assert np.array_equal(y, frames[4])
 torch.cuda.synchronize()
+MODE = os.environ.get("PK", "decode")
+if MODE == "encode":
+    enc = GpuCodec(cfg, blob)
+    for f in frames[:4]:
+        enc.push_frame(f)
+    for _ in range(2):
+        enc.encode_frame(frames[4], fidx=4)
+    torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(N):
-        dec.decode_frame(hyper, main, fidx=4, advance=False)
+        if MODE == "encode":
+            enc.encode_frame(frames[4], fidx=4)
+        else:
+            dec.decode_frame(hyper, main, fidx=4, advance=False)
     torch.cuda.synchronize()
 agg = collections.defaultdict(lambda: [0, 0.0])
 for ev in prof.events():
@@ -47,7 +59,7 @@ for ev in prof.events():
     agg[name][0] += 1
     agg[name][1] += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
 tot = sum(v[1] for v in agg.values()) / N
-lines = [f"warm in-graph kernel time per frame: {tot/1e3:.3f} ms (sum of kernel durations)"]
+lines = [f"warm in-graph kernel time per frame ({MODE}): {tot/1e3:.3f} ms (sum of kernel durations)"]
 for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     lines.append(f"{t/N/1e3:8.3f} ms {100*t/N/tot:5.1f}%  n={n//N:4d}  avg={t/n:7.1f} us  {k}")
 print("\n".join(lines))
