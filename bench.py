@@ -508,7 +508,7 @@ def run_ours(args, rank, world, local):
             try:  # local failures are agreed on through the reductions below
                 c4r = config4_gop_batch(torch, rank, world, GpuCodec, gen_weights, make_cfg,
                                         synth_latent, max(3, args.steps // 2), args.warmup,
-                                        per_gpu=int(os.environ.get("PSWA_BENCH_GOPS", 8)))
+                                        per_gpu=int(os.environ.get("PSWA_BENCH_GOPS", 4)))
             except Exception as e:  # noqa: BLE001
                 c4r = {"ms": float("inf"), "bit_exact": False, "error": str(e)}
             tot = pdist.max_over_ranks(c4r["ms"], dist, device="cuda")

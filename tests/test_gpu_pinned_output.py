@@ -14,9 +14,10 @@ from paper_2605_20977_b200.codec import GpuCodec, gen_weights, make_cfg, synth_l
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("preset,H,W", [("desk", 12, 20), ("paper", 16, 16)])
-def test_pinned_output_matches(preset, H, W):
-    cfg = make_cfg(preset, H, W, lanes=16, hyper_lanes=4)
+@pytest.mark.parametrize("preset,H,W,lrp", [("desk", 12, 20, 0), ("paper", 16, 16, 0),
+                                             ("desk", 12, 20, 2)])
+def test_pinned_output_matches(preset, H, W, lrp):
+    cfg = make_cfg(preset, H, W, lanes=16, hyper_lanes=4, lrp_blocks=lrp)
     blob = gen_weights(cfg, 1)
     frames = [synth_latent(cfg, 0, f) for f in range(3)]
     enc = GpuCodec(cfg, blob)
@@ -35,3 +36,5 @@ def test_pinned_output_matches(preset, H, W):
         y_pin = out.numpy().reshape(cfg.latent_ch, H, W)
         y_page, _ = pageable.decode_frame(hyper, main, fidx=i)
         assert np.array_equal(y_pin, frames[i]) and np.array_equal(y_page, frames[i])
+        if lrp:  # the LRP stage after the overlapped copies sees the same y_hat
+            assert np.array_equal(pinned.last_eps(), pageable.last_eps())
