@@ -760,7 +760,14 @@ void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq
                        __half* out, int kv_slots) {
   const Dims& D = D_;
   const int d = D.d, Hl = B_.Hl;  // key grid bounds: the band's local grid
-  if (mma_attn_) {
+  if (mma_attn_ && shape->nbk == 0) {
+    // the mask allows no key (the accumulator at step 0): the
+    // kernel would stage halos only to write zeros; a memset writes the same
+    // +0 halves
+    add(P, [=](cudaStream_t s) {
+      PSWA_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(Mq) * d * sizeof(__half), s));
+    }, 0);
+  } else if (mma_attn_) {
     const pswa_dev::AttnShape sh = *shape;
     const int hr = wt > 0 ? kCtxHaloRows : kStepHaloRows, hw = wt > 0 ? kCtxHaloW : kStepHaloW;
     CUtensorMap map;  // halo boxes of this K/V buffer: 32 channels x hw x hr x 1 slot
