@@ -482,21 +482,29 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
     bulk_load(smem_u32(s_scales), scales, kScaleBytes, &s_bar);
   }
   __syncthreads();
-  pdl_wait();
-  pdl_trigger();
-  mbar_wait(&s_bar, 0);
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= L) return;
   const uint64_t total = static_cast<uint64_t>(n) * per;
   // first ordinal of lane l at or after o0, relative to o0 (o0_mod = o0 % L
   // from the host: no 64-bit division here)
   uint32_t i_first = static_cast<uint32_t>(l) + static_cast<uint32_t>(L) - o0_mod;
   if (i_first >= static_cast<uint32_t>(L)) i_first -= static_cast<uint32_t>(L);
-  if (i_first >= total) return;
-  LaneState s = lanes[l];
-  int err = 0;
+  const bool active = l < L && i_first < total;
+  // The lane state and payload bytes are read before the PDL wait: this grid
+  // starts once the head GEMM before it has passed its own wait, so every
+  // earlier kernel (the previous phase, which wrote the lane states, and the
+  // lane init) has completed. Only mu/sigma come from the immediate
+  // predecessor.
+  LaneState s;
   Rsv rs;
-  rs.init(pl, s.pos, s.end);
+  if (active) {
+    s = lanes[l];
+    rs.init(pl, s.pos, s.end);
+  }
+  pdl_wait();
+  pdl_trigger();
+  mbar_wait(&s_bar, 0);
+  if (!active) return;
+  int err = 0;
   // the parameters (mu, table index) of a lane's next symbols do not depend
   // on the coder state: gather them in a batch (loads in flight together),
   // then run the sequential decode chain.
