@@ -303,6 +303,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) stamp(1);
+  // B is always a packed weight matrix (constant for the whole program): the
+  // first tile's B stages are requested before the PDL wait, so they land
+  // while the previous kernel drains; A (an activation) follows the wait
+  int npre = 0;
+  if (CL == 1 && warp == 0 && lane == 0 && unit0 < n_units) {
+    const int n0 = (unit0 % tiles_n) * BN;
+    npre = min(S, kblocks);
+    for (int kb = 0; kb < npre; ++kb) {
+      mbar_expect_tx(&full[kb], Cfg::kStageBytes);
+      tma_load_2d(sb + kb * Cfg::kBBytes, &tmb, &full[kb], kb * kBK, n0);
+    }
+  }
   // everything above overlaps the previous kernel (PDL); inputs are read below
   pdl_wait();
   pdl_trigger();
@@ -315,6 +327,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = ((u / tiles_n) * CL + rank) * kBM, n0 = (u % tiles_n) * BN;
         for (int kb = 0; kb < kblocks; ++kb, ++g) {
           const int s = g % S, round = g / S;
+          if (g < npre) {  // B already requested (and the stage's bytes expected)
+            tma_load_2d(sa + s * Cfg::kABytes, &tma, &full[s], kb * kBK, m0);
+            continue;
+          }
           if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
           mbar_expect_tx(&full[s], Cfg::kStageBytes);
           tma_load_2d(sa + s * Cfg::kABytes, &tma, &full[s], kb * kBK, m0);
