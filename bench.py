@@ -169,7 +169,7 @@ PROBES = {  # production launches replayed by pswa_gpu_bench_op (warm, real oper
     "ctx_attn": "window_attn_mma_kernel, context block 0: 3D 4-slot 7x7 window, 32640 queries x 16 heads",
     "ctx_ffn_gu": "gemm_tc_kernel<256> context FFN gate|up (SwiGLU epilogue), M=32640 N=2736 K=512",
     "step_attn": "window_attn_mma_kernel, S2 block 0 self attention, step 3 batch (2040 queries)",
-    "step_wq": "gemm_tc_kernel<128> S2 block 0 fused Q|K|V projection, step 3 batch, M=2040 N=1536 K=512",
+    "step_wq": "gemm_tc_kernel<256> S2 block 0 fused Q|K|V projection, step 3 batch, M=2040 N=1536 K=512",
 }
 
 

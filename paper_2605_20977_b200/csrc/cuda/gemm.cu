@@ -593,10 +593,13 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
     throw std::invalid_argument("gemm_plan: unsupported shape (K%64, N%64, ld%8)");
   int bn = force_bn;
   if (bn == 0) {
-    // largest tile that still gives every SM work; small-M step GEMMs end
-    // up on BN=64 (more CTAs), the 4-slot context GEMMs on BN=256
+    // BN=256 once its tiles cover half the SMs (one wave of wide tiles beats
+    // ~2 waves of BN=128 for the M = 2040 Q|K|V and gate|up GEMMs: 7.26 vs
+    // 7.39 ms / frame; thresholds of 48-96 tiles measured alike), else
+    // BN=128 when its tiles fill the SMs, else BN=64 (the N = 512 step
+    // GEMMs: BN=128 there measured 7.47+ ms)
     const int mt = (M + kBM - 1) / kBM, sms = sm_count();
-    if (N % 256 == 0 && mt * (N / 256) >= 2 * sms)
+    if (N % 256 == 0 && mt * (N / 256) >= sms / 2)
       bn = 256;
     else if (N % 128 == 0 && mt * (N / 128) >= sms)
       bn = 128;
