@@ -471,7 +471,7 @@ def run_ours(args, rank, world, local):
 
     def step_host():
         rc = lib().pswa_gpu_decode_frame(dec.h, h_hyper.data_ptr(), len(hyper), h_main.data_ptr(),
-                                         len(main), 0, GOP_INDEX, 0, h_out.data_ptr(),
+                                         len(main), 0, GOP_INDEX, 0, h_out.data_ptr(), None, None,
                                          hb.ctypes.data_as(C.POINTER(C.c_double)))
         assert rc == 0
 

@@ -20,18 +20,21 @@ int main(int argc, char** argv) {
   std::vector<uint8_t> psww(n);
   pswa::throw_on(pswa_gen_weights(&cfg, 1, psww.data(), n, &n));
   pswa::GpuCodec enc(0, cfg, psww), dec(0, cfg, psww);
+  enc.set_stats(true);
   for (int f = 0; f < frames; ++f) {
     std::vector<int32_t> y(enc.latent_count());
     pswa::throw_on(pswa_synth_latent(&cfg, 0, f, y.data()));
-    pswa::FrameBits eb, db;
-    const pswa::Payloads p = pswa::encode_frame(enc, y, 0, f, &eb);
-    const std::vector<int32_t> yd = pswa::decode_frame_wavefront(dec, p, 0, f, 1, &db);
-    if (yd != y) {
+    const pswa::EncodedFrame e = pswa::encode_frame(enc, y, 0, f, true);
+    const pswa::DecodedFrame d = pswa::decode_frame_wavefront(dec, e.payloads, 0, f, 1);
+    if (d.yhat != y) {
       std::printf("frame %d: MISMATCH\n", f);
       return 1;
     }
-    std::printf("frame %d ok: %zu+%zu bytes, %.0f bits (enc %.0f)\n", f, p.hyper.size(),
-                p.main.size(), db.hyper + db.main, eb.hyper + eb.main);
+    double sum = 0.0;  // BitStats: per-position, per-group bits add up to the main estimate
+    for (double v : e.stats.per_position_group) sum += v;
+    std::printf("frame %d ok: %zu+%zu bytes, %.0f bits (enc %.0f, BitStats sum %.0f)\n", f,
+                e.payloads.hyper.size(), e.payloads.main.size(), d.bits.hyper + d.bits.main,
+                e.stats.totals.hyper + e.stats.totals.main, sum);
   }
   return 0;
 }

@@ -100,9 +100,15 @@ int pswa_gpu_encode_frame(pswa_gpu* h, const int32_t* yhat, int rate_idx, int fr
                           uint8_t* hyper_out, size_t hyper_cap, size_t* hyper_len,
                           uint8_t* main_out, size_t main_cap, size_t* main_len,
                           double* bits_out /* [2] = {hyper, main}, nullable */);
+/* mu_out / sigma_out (nullable, [C][H][W]): the entropy parameters the
+ * decoder itself computed for every symbol (the wavefront
+ * decoder evaluates (mu, sigma) per phase); bitwise equal to the encoder's and
+ * to pswa_gpu_forward_params on the same frame. Requesting them runs the
+ * decode program variant with per-symbol taps (also fills BitStats). */
 int pswa_gpu_decode_frame(pswa_gpu* h, const uint8_t* hyper, size_t hyper_len,
                           const uint8_t* main_payload, size_t main_len, int rate_idx,
                           int frame_idx_in_gop, int advance_state, int32_t* yhat_out,
+                          float* mu_out /* nullable */, float* sigma_out /* nullable */,
                           double* bits_out /* [2], nullable */);
 /* Teacher-forced entropy parameters for a known frame (parity probe).
  * zhat: [hyper_ch][H/4][W/4]; mu/sigma: [C][H][W]. */
@@ -113,6 +119,14 @@ int pswa_gpu_forward_params(pswa_gpu* h, const int32_t* yhat, const int32_t* zha
  * decoded or encoded by this handle (computed in the same frame program
  * when cfg.lrp_blocks > 0); the reconstruction input is y_hat + eps. */
 int pswa_gpu_last_eps(pswa_gpu* h, float* eps_out);
+/* BitStats. With stats on, every frame call (encode,
+ * decode, forward_params) also computes per-position, per-group estimated
+ * bits; pswa_gpu_last_bitstats returns those of the last such call as
+ * [N][H][W] doubles (group g of position (y, x) at g*H*W + y*W + x; their sum
+ * is the frame's main estimate, bits_out[1]). Calls with stats off leave no
+ * BitStats (PSWA_E_ARG). Requesting mu/sigma implies stats for that call. */
+int pswa_gpu_set_stats(pswa_gpu* h, int on);
+int pswa_gpu_last_bitstats(pswa_gpu* h, double* bits_nhw);
 /* Returns the z_hat the encoder produced for the last encode_frame call. */
 int pswa_gpu_last_zhat(pswa_gpu* h, int32_t* zhat_out);
 /* Append a decoded / known frame to the temporal ring. */
@@ -242,6 +256,19 @@ int pswa_gpu_op_window_attn(const void* q, int ld_q, const int32_t* qinfo, int M
 int pswa_gpu_op_build_cdf(uint32_t* cdf_out /* host [64*258] */, float* scales_out /* [64] */);
 /* laplace = 1: the Laplace tables of the prior = 1 parameter head. */
 int pswa_gpu_op_build_cdf_family(uint32_t* cdf_out, float* scales_out, int laplace);
+/* encode_symbols / decode_symbols on explicit symbols, host
+ * buffers, through the production lane kernels: value v[i] (escapes up to
+ * |v| < 2^31 - 128) under table idx[i] in [0, 64) of the Gaussian (laplace = 0)
+ * or Laplace family; ordinal i in lane i % lanes; payload in the lane format
+ * of DESIGN.md §3 (lanes = 1 is the SPEC's single stream). *len gets the
+ * payload size (out may be NULL to query it); bits_out (nullable) the
+ * estimate_bits of the symbols. Decoding a corrupt or
+ * truncated payload returns PSWA_E_TRUNCATED. */
+int pswa_gpu_op_encode_symbols(const int32_t* v, const int32_t* idx, size_t n, int lanes,
+                               int laplace, uint8_t* out, size_t cap, size_t* len,
+                               double* bits_out);
+int pswa_gpu_op_decode_symbols(const uint8_t* payload, size_t len, const int32_t* idx, size_t n,
+                               int laplace, int32_t* v_out, double* bits_out);
 
 #ifdef __cplusplus
 }

@@ -44,7 +44,9 @@ _SIGS = {
     "pswa_gpu_reset_gop": (_I, [_VP]),
     "pswa_gpu_encode_frame": (_I, [_VP, _VP, _I, _I, _VP, _SZ, C.POINTER(_SZ), _VP, _SZ,
                                    C.POINTER(_SZ), _D]),
-    "pswa_gpu_decode_frame": (_I, [_VP, _VP, _SZ, _VP, _SZ, _I, _I, _I, _VP, _D]),
+    "pswa_gpu_decode_frame": (_I, [_VP, _VP, _SZ, _VP, _SZ, _I, _I, _I, _VP, _VP, _VP, _D]),
+    "pswa_gpu_set_stats": (_I, [_VP, _I]),
+    "pswa_gpu_last_bitstats": (_I, [_VP, _VP]),
     "pswa_gpu_forward_params": (_I, [_VP, _VP, _VP, _I, _I, _VP, _VP, _D]),
     "pswa_gpu_last_zhat": (_I, [_VP, _VP]),
     "pswa_gpu_last_eps": (_I, [_VP, _VP]),
@@ -63,6 +65,8 @@ _SIGS = {
                                      _I, _I, _VP, _VP, _I, _VP]),
     "pswa_gpu_op_build_cdf": (_I, [_VP, _VP]),
     "pswa_gpu_op_build_cdf_family": (_I, [_VP, _VP, _I]),
+    "pswa_gpu_op_encode_symbols": (_I, [_VP, _VP, _SZ, _I, _I, _VP, _SZ, C.POINTER(_SZ), _D]),
+    "pswa_gpu_op_decode_symbols": (_I, [_VP, _SZ, _VP, _SZ, _I, _VP, _D]),
     "pswa_band_rows": (_I, [_I, _I, _I, C.POINTER(_I), C.POINTER(_I)]),
     "pswa_group_create": (_I, [_VP, _I, C.POINTER(PswaCfg), _VP, _SZ, C.POINTER(_VP)]),
     "pswa_group_destroy": (None, [_VP]),

@@ -122,15 +122,32 @@ class GpuCodec:
         return e
 
     def decode_frame(self, hyper: bytes, main: bytes, rate: int = 0, fidx: int = 0,
-                     advance: bool = True):
+                     advance: bool = True, params: bool = False):
+        """-> (y_hat, bits[2]); with params=True -> (y_hat, bits, mu, sigma): the
+        entropy parameters the decoder computed itself ([C][H][W] each)."""
         hb = np.frombuffer(hyper, np.uint8)
         mb = np.frombuffer(main, np.uint8)
         y = np.empty(self.shape, np.int32)
         bits = np.zeros(2, np.float64)
+        mu = np.empty(self.shape, np.float32) if params else None
+        sg = np.empty(self.shape, np.float32) if params else None
         check(lib().pswa_gpu_decode_frame(self.h, _ptr(hb), len(hyper), _ptr(mb), len(main), rate,
                                           fidx, int(advance), _ptr(y),
+                                          None if mu is None else _ptr(mu),
+                                          None if sg is None else _ptr(sg),
                                           bits.ctypes.data_as(C.POINTER(C.c_double))))
-        return y, bits
+        return (y, bits, mu, sg) if params else (y, bits)
+
+    def set_stats(self, on: bool = True):
+        """BitStats for every later frame call."""
+        check(lib().pswa_gpu_set_stats(self.h, int(on)))
+
+    def last_bitstats(self) -> np.ndarray:
+        """Per-position, per-group estimated bits [N][H][W] of the last frame
+        call made with stats on (or with mu/sigma requested)."""
+        out = np.zeros((self.cfg.n_groups, self.cfg.height, self.cfg.width), np.float64)
+        check(lib().pswa_gpu_last_bitstats(self.h, _ptr(out)))
+        return out
 
     def forward_params(self, yhat: np.ndarray, zhat: np.ndarray, rate: int = 0, fidx: int = 0):
         y = np.ascontiguousarray(yhat, np.int32)

@@ -13,6 +13,7 @@
 // This file is compiled with -fmad=false: the fp64 table builder must round
 // every add/mul exactly like the host restatement (det_math.cpp:49-130).
 #include <cfloat>
+#include <cstdint>
 
 #include "check.h"
 #include "kernels.h"
@@ -456,7 +457,8 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
                                     const float* __restrict__ musig, int ldms, int sig_off,
                                     const float* __restrict__ scales, const uint32_t* __restrict__ cdf,
                                     const int* __restrict__ rows, int32_t* __restrict__ yhat, int C,
-                                    int c0, __half* __restrict__ yhat16, int ld16, int* status) {
+                                    int c0, __half* __restrict__ yhat16, int ld16, int* status,
+                                    PhaseTaps taps) {
   // the 64 scale thresholds, the 64 cumulative tables (66 KB) and their
   // search indexes (33 KB) staged in shared memory: the sigma -> table and
   // symbol searches are dependent-load chains that otherwise run at L2
@@ -548,6 +550,14 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
           k16[q] = k * ld16 + c0 + j;
         }
       }
+      if (taps.mu) {  // the decoder's own entropy parameters (parity / BitStats taps)
+#pragma unroll
+        for (int q = 0; q < kB; ++q)
+          if (q < nq) {
+            taps.mu[dst[q]] = mu_f[q];
+            taps.sigma[dst[q]] = sg_f[q];
+          }
+      }
 #pragma unroll
       for (int q = 0; q < kB; ++q)
         if (q < nq)
@@ -582,9 +592,16 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
       }
       s_out[q * nth + tid] = k | (eb << 16);
       const int32_t y = v + pr.y;
+      // a y_hat the encoder cannot have produced (|y_hat| > kYhatMax) marks
+      // the stream corrupt
+      if (y > taps.ymax || y < -taps.ymax) err = 1;
       yhat[pr.z] = y;
       if (yhat16) yhat16[pr.w] = __int2half_rn(y);
+      // a lane that ran past its end stops here: no further reads past the
+      // payload (the frame fails with status 2)
+      if (err) break;
     }
+    if (err) break;
     // bit costs: loads issued together, summed in symbol order
     double cost[kB];
     int ebs[kB];
@@ -603,6 +620,11 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
       if (q >= nq) break;
       s.bits += cost[q];
       if (ebs[q]) s.bits += ebs[q];
+    }
+    if (taps.bits) {
+#pragma unroll
+      for (int q = 0; q < kB; ++q)
+        if (q < nq) taps.bits[s_par[q * nth + tid].z] = cost[q] + static_cast<double>(ebs[q]);
     }
   }
   s.pos = rs.pos;
@@ -632,13 +654,20 @@ __global__ void decode_hyper_kernel(const uint8_t* __restrict__ pl, LaneState* _
   if (err) atomicOr(status, 2);
 }
 
+// Escape bits of a coded value (Exp-Golomb(0) of |v| - 128, 0 in range).
+__device__ __forceinline__ int escape_bits(int64_t v) {
+  if (v >= -127 && v <= 127) return 0;
+  const uint64_t x = static_cast<uint64_t>(v < 0 ? -v : v) - 128 + 1;
+  return 2 * (63 - __clzll(static_cast<long long>(x))) + 1;
+}
+
 __global__ void quantize_phase_kernel(const float* __restrict__ musig, int ldms, int sig_off, int n,
                                       int per, uint64_t o0, const int* __restrict__ rows,
                                       const int32_t* __restrict__ yhat, int C, int c0,
-                                      const float* __restrict__ scales, int32_t* __restrict__ sym_v,
-                                      uint8_t* __restrict__ sym_idx, __half* __restrict__ yhat16,
-                                      int ld16, float* __restrict__ mu_out,
-                                      float* __restrict__ sigma_out) {
+                                      const float* __restrict__ scales, const uint32_t* __restrict__ cdf,
+                                      int32_t* __restrict__ sym_v, uint8_t* __restrict__ sym_idx,
+                                      __half* __restrict__ yhat16, int ld16, PhaseTaps taps,
+                                      int* status) {
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -648,13 +677,39 @@ __global__ void quantize_phase_kernel(const float* __restrict__ musig, int ldms,
   const float sg = musig[static_cast<size_t>(k) * ldms + sig_off + j];
   const size_t e = static_cast<size_t>(rows[k]) * C + c0 + j;
   const int32_t y = yhat[e];
-  sym_v[o0 + i] = y - __float2int_rn(mu);
-  sym_idx[o0 + i] = static_cast<uint8_t>(scale_index(scales, sg));
+  // the coded value must stay in the escape code's 32-bit range (a mean
+  // that is not finite, from a y_hat outside the supported range, lands here)
+  const int64_t v = static_cast<int64_t>(y) - static_cast<int64_t>(__float2ll_rn(mu));
+  if (y > kYhatMax || y < -kYhatMax || !(fabsf(mu) < 1.0e9f) || v > INT32_MAX - 128 ||
+      v < -(INT32_MAX - 128))
+    atomicOr(status, 16);
+  const int idx = scale_index(scales, sg);
+  sym_v[o0 + i] = static_cast<int32_t>(v);
+  sym_idx[o0 + i] = static_cast<uint8_t>(idx);
   if (yhat16) yhat16[static_cast<size_t>(k) * ld16 + c0 + j] = __int2half_rn(y);
-  if (mu_out) {
-    mu_out[e] = mu;
-    sigma_out[e] = sg;
+  if (taps.mu) {
+    taps.mu[e] = mu;
+    taps.sigma[e] = sg;
   }
+  if (taps.bits) {
+    const int ks = v < -127 ? kEscLo : (v > 127 ? kEscHi : static_cast<int>(v) + 127);
+    taps.bits[e] = bits_table(cdf)[idx * kSyms + ks] + static_cast<double>(escape_bits(v));
+  }
+}
+
+// One thread per (group, position): the group's Cg symbol costs in channel
+// order (a fixed order: BitStats are bitwise identical on both sides).
+__global__ void bitstats_kernel(const double* __restrict__ sym_bits, int C, int row0, int npos,
+                                int N, int Cg, double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N * npos) return;
+  const int g = i / npos, p = i - g * npos;
+  const double* b = sym_bits + static_cast<size_t>(row0 + p) * C + g * Cg;
+  double acc = 0.0;
+  for (int c = 0; c < Cg; ++c) acc += b[c];
+  out[i] = acc;
 }
 
 __global__ void quantize_hyper_kernel(const int32_t* __restrict__ zhat, int n, int per_ch,
@@ -775,7 +830,7 @@ void lanes_init(const uint8_t* payload, const uint32_t* len, int lanes, uint32_t
 void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_t o0, int n,
                         int per, const float* musig, int ldms, int sig_off, const float* scales,
                         const uint32_t* cdf, const int* rows, int32_t* yhat, int C, int c0,
-                        __half* yhat16, int ld16, int* status, cudaStream_t st) {
+                        __half* yhat16, int ld16, int* status, cudaStream_t st, PhaseTaps taps) {
   if (n <= 0) return;
   constexpr int smem = kScales * (kSyms + 1) * 4 + kScales * kLutBuckets * 2 + kScales * 4 +
                        kDecB * 128 * (16 + 4);
@@ -787,7 +842,7 @@ void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_
   launch_k(decode_phase_kernel, dim3(blocks(L)), dim3(128), smem, st, payload, lanes, L,
            static_cast<uint32_t>(o0 % static_cast<uint64_t>(L)), n, per, musig, ldms,
                                                   sig_off, scales, cdf, rows, yhat, C, c0, yhat16,
-                                                  ld16, status);
+                                                  ld16, status, taps);
   PSWA_LAUNCH_CHECK();
 }
 
@@ -801,11 +856,20 @@ void lanes_decode_hyper(const uint8_t* payload, LaneState* lanes, int L, int n, 
 
 void quantize_phase(const float* musig, int ldms, int sig_off, int n, int per, uint64_t o0,
                     const int* rows, const int32_t* yhat, int C, int c0, const float* scales,
-                    int32_t* sym_v, uint8_t* sym_idx, __half* yhat16, int ld16, float* mu_out,
-                    float* sigma_out, cudaStream_t st) {
+                    const uint32_t* cdf, int32_t* sym_v, uint8_t* sym_idx, __half* yhat16, int ld16,
+                    PhaseTaps taps, int* status, cudaStream_t st) {
   if (n <= 0) return;
-  launch_k(quantize_phase_kernel, dim3(blocks(static_cast<long>(n) * per, 256)), dim3(256), 0, st, musig, ldms, sig_off, n, per, o0, rows, yhat, C, c0, scales, sym_v, sym_idx, yhat16, ld16,
-      mu_out, sigma_out);
+  launch_k(quantize_phase_kernel, dim3(blocks(static_cast<long>(n) * per, 256)), dim3(256), 0, st,
+           musig, ldms, sig_off, n, per, o0, rows, yhat, C, c0, scales, cdf, sym_v, sym_idx, yhat16,
+           ld16, taps, status);
+  PSWA_LAUNCH_CHECK();
+}
+
+void bitstats_reduce(const double* sym_bits, int C, int row0, int npos, int N, int Cg, double* out,
+                     cudaStream_t st) {
+  if (npos <= 0) return;
+  launch_k(bitstats_kernel, dim3(blocks(static_cast<long>(N) * npos, 256)), dim3(256), 0, st,
+           sym_bits, C, row0, npos, N, Cg, out);
   PSWA_LAUNCH_CHECK();
 }
 

@@ -119,6 +119,10 @@ void toy_synthesis(const float* y, int Hpx, int Wpx, int rate, uint8_t* rgb, cud
 
 // ---- entropy coding (coder.cu) -------------------------------------------
 constexpr int kScales = 64;
+// Largest |y_hat| the codec accepts: the networks read y_hat as fp16 (exact
+// integers up to 2^11). The encoder rejects larger values (status 16 ->
+// PSWA_E_ARG); the decoder treats them as a corrupt stream.
+constexpr int kYhatMax = 2048;
 constexpr int kSyms = 257;  // v in [-127,127] + 2 escapes
 // Builds the 64 scale entries and 64 x 258 cumulative tables on the device
 // in fp64 with IEEE round-to-nearest ops only (bit-exact with the host rule),
@@ -140,6 +144,16 @@ struct LaneState {
   double bits;           // estimated bits of this lane's symbols
 };
 
+// Optional per-symbol outputs of a phase (BitStats and the decoder's entropy
+// parameters), all indexed like y_hat
+// ([rows[k]][c0 + j]); null pointers disable them.
+struct PhaseTaps {
+  float* mu = nullptr;
+  float* sigma = nullptr;
+  double* bits = nullptr;  // -log2(freq / 2^16) + escape bits of the symbol
+  int ymax = kYhatMax;     // decoded |y_hat| above this marks the stream corrupt
+};
+
 // Parses a lane payload header in device memory and initialises lane states.
 // status[0] |= 1 on malformed payload.
 void lanes_init(const uint8_t* payload, const uint32_t* len, int lanes, uint32_t expect_count,
@@ -151,7 +165,8 @@ void lanes_init(const uint8_t* payload, const uint32_t* len, int lanes, uint32_t
 void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_t o0, int n,
                         int per, const float* musig, int ldms, int sig_off, const float* scales,
                         const uint32_t* cdf, const int* rows, int32_t* yhat, int C, int c0,
-                        __half* yhat16, int ld16, int* status, cudaStream_t st);
+                        __half* yhat16, int ld16, int* status, cudaStream_t st,
+                        PhaseTaps taps = {});
 // Hyper payload: ordinal i -> channel i / per_ch; mean/scale from the prior
 // bank entry; writes z_hat [c][h][w].
 void lanes_decode_hyper(const uint8_t* payload, LaneState* lanes, int L, int n, int per_ch,
@@ -159,10 +174,15 @@ void lanes_decode_hyper(const uint8_t* payload, LaneState* lanes, int L, int n, 
                         const uint32_t* cdf, int32_t* zhat, int* status, cudaStream_t st);
 // Encoder side of one phase: v = y_hat - rint(mu), idx = scale_index(sigma)
 // into sym_v / sym_idx at ordinals [o0, ...); also fills yhat16 from y_hat.
+// taps.bits needs cdf (its symbol-cost table).
 void quantize_phase(const float* musig, int ldms, int sig_off, int n, int per, uint64_t o0,
                     const int* rows, const int32_t* yhat, int C, int c0, const float* scales,
-                    int32_t* sym_v, uint8_t* sym_idx, __half* yhat16, int ld16,
-                    float* mu_out, float* sigma_out, cudaStream_t st);
+                    const uint32_t* cdf, int32_t* sym_v, uint8_t* sym_idx, __half* yhat16, int ld16,
+                    PhaseTaps taps, int* status, cudaStream_t st);
+// BitStats: out[g][i] = sum over the Cg channels of group g
+// (ascending) of sym_bits[(row0 + i)][g*Cg + c], i in [0, npos).
+void bitstats_reduce(const double* sym_bits, int C, int row0, int npos, int N, int Cg, double* out,
+                     cudaStream_t st);
 void quantize_hyper(const int32_t* zhat, int n, int per_ch, const float* loc, const float* scale,
                     const float* scales, int32_t* sym_v, uint8_t* sym_idx, cudaStream_t st);
 // Encodes n symbols into L lanes: lane l writes at out + l*cap; lens[l]

@@ -79,7 +79,15 @@ int pswa_gpu_create(int device, const pswa_cfg* cfg, const void* blob, size_t le
   });
 }
 
-void pswa_gpu_destroy(pswa_gpu* h) { delete h; }
+void pswa_gpu_destroy(pswa_gpu* h) {
+  if (!h) return;
+  try {
+    pswa_dev::DeviceScope ds(h->eng->device());
+    delete h;
+  } catch (...) {
+    delete h;
+  }
+}
 
 int pswa_gpu_create_band(int device, const pswa_cfg* cfg, const void* blob, size_t len, int band_idx,
                          int n_bands, pswa_gpu** out) {
@@ -93,7 +101,7 @@ int pswa_gpu_create_band(int device, const pswa_cfg* cfg, const void* blob, size
 
 int pswa_gpu_band_export(pswa_gpu* h, void* out, size_t cap, size_t* len) {
   return guard([&] {
-    PSWA_CUDA(cudaSetDevice(h->eng->device()));
+    pswa_dev::DeviceScope ds(h->eng->device());
     const auto b = h->eng->ipc_export();
     *len = b.size();
     if (out) {
@@ -105,24 +113,31 @@ int pswa_gpu_band_export(pswa_gpu* h, void* out, size_t cap, size_t* len) {
 
 int pswa_gpu_band_link(pswa_gpu* h, const void* up, size_t up_len, const void* down, size_t down_len) {
   return guard([&] {
-    PSWA_CUDA(cudaSetDevice(h->eng->device()));
+    pswa_dev::DeviceScope ds(h->eng->device());
     h->eng->link_ipc(static_cast<const uint8_t*>(up), up_len, static_cast<const uint8_t*>(down),
                      down_len);
   });
 }
 
 int pswa_gpu_reset_gop(pswa_gpu* h) {
-  return guard([&] { h->eng->reset_gop(); });
+  return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
+    h->eng->reset_gop();
+  });
 }
 
 int pswa_gpu_push_frame(pswa_gpu* h, const int32_t* yhat, int rate_idx) {
-  return guard([&] { h->eng->push_frame(yhat, rate_idx); });
+  return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
+    h->eng->push_frame(yhat, rate_idx);
+  });
 }
 
 int pswa_gpu_encode_frame(pswa_gpu* h, const int32_t* yhat, int rate_idx, int frame_idx_in_gop,
                           uint8_t* hyper_out, size_t hyper_cap, size_t* hyper_len,
                           uint8_t* main_out, size_t main_cap, size_t* main_len, double* bits_out) {
   return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
     const auto r = h->eng->encode(yhat, rate_idx, frame_idx_in_gop, nullptr, nullptr, nullptr,
                                   hyper_out, hyper_cap, main_out, main_cap, /*advance=*/true);
     *hyper_len = r.hyper_len;
@@ -137,10 +152,12 @@ int pswa_gpu_encode_frame(pswa_gpu* h, const int32_t* yhat, int rate_idx, int fr
 int pswa_gpu_decode_frame(pswa_gpu* h, const uint8_t* hyper, size_t hyper_len,
                           const uint8_t* main_payload, size_t main_len, int rate_idx,
                           int frame_idx_in_gop, int advance_state, int32_t* yhat_out,
-                          double* bits_out) {
+                          float* mu_out, float* sigma_out, double* bits_out) {
   return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
     const auto r = h->eng->decode(hyper, hyper_len, main_payload, main_len, rate_idx,
-                                  frame_idx_in_gop, advance_state != 0, yhat_out, false);
+                                  frame_idx_in_gop, advance_state != 0, yhat_out, false, mu_out,
+                                  sigma_out);
     if (bits_out) {
       bits_out[0] = r.bits[0];
       bits_out[1] = r.bits[1];
@@ -152,6 +169,7 @@ int pswa_gpu_decode_frame_device(pswa_gpu* h, const void* d_hyper, size_t hyper_
                                  const void* d_main, size_t main_len, int rate_idx,
                                  int frame_idx_in_gop, int advance_state, void* d_yhat_out) {
   return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
     h->eng->decode(d_hyper, hyper_len, d_main, main_len, rate_idx, frame_idx_in_gop,
                    advance_state != 0, static_cast<int32_t*>(d_yhat_out), true);
   });
@@ -161,6 +179,7 @@ int pswa_gpu_decode_frame_async(pswa_gpu* h, const void* d_hyper, size_t hyper_l
                                 const void* d_main, size_t main_len, int rate_idx,
                                 int frame_idx_in_gop, void* d_yhat_out) {
   return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
     h->eng->decode_async(d_hyper, hyper_len, d_main, main_len, rate_idx, frame_idx_in_gop,
                          static_cast<int32_t*>(d_yhat_out));
   });
@@ -168,6 +187,7 @@ int pswa_gpu_decode_frame_async(pswa_gpu* h, const void* d_hyper, size_t hyper_l
 
 int pswa_gpu_finish(pswa_gpu* h, double* bits_out) {
   return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
     const auto r = h->eng->finish_async();
     if (bits_out) {
       bits_out[0] = r.bits[0];
@@ -180,6 +200,7 @@ int pswa_gpu_forward_params(pswa_gpu* h, const int32_t* yhat, const int32_t* zha
                             int frame_idx_in_gop, float* mu_out, float* sigma_out,
                             double* bits_out) {
   return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
     if (!mu_out || !sigma_out) throw std::invalid_argument("mu_out / sigma_out required");
     const auto r = h->eng->encode(yhat, rate_idx, frame_idx_in_gop, zhat, mu_out, sigma_out,
                                   nullptr, 0, nullptr, 0, /*advance=*/false);
@@ -190,22 +211,45 @@ int pswa_gpu_forward_params(pswa_gpu* h, const int32_t* yhat, const int32_t* zha
   });
 }
 
+int pswa_gpu_set_stats(pswa_gpu* h, int on) {
+  return guard([&] { h->eng->set_stats(on != 0); });
+}
+
+int pswa_gpu_last_bitstats(pswa_gpu* h, double* out) {
+  return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
+    h->eng->last_bitstats(out);
+  });
+}
+
 int pswa_gpu_last_eps(pswa_gpu* h, float* eps_out) {
-  return guard([&] { h->eng->last_eps(eps_out); });
+  return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
+    h->eng->last_eps(eps_out);
+  });
 }
 
 int pswa_gpu_last_zhat(pswa_gpu* h, int32_t* zhat_out) {
-  return guard([&] { h->eng->last_zhat(zhat_out); });
+  return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
+    h->eng->last_zhat(zhat_out);
+  });
 }
 
 int pswa_gpu_debug_fetch(pswa_gpu* h, const char* name, void* out, size_t cap, size_t* bytes) {
-  return guard([&] { *bytes = h->eng->debug_fetch(name, out, cap); });
+  return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
+    *bytes = h->eng->debug_fetch(name, out, cap);
+  });
 }
 
 int pswa_gpu_last_launch_count(pswa_gpu* h) { return h->eng->last_launches(); }
 
 int pswa_gpu_bench_op(pswa_gpu* h, const char* name, int reps, double* us, double* flops) {
-  return guard([&] { *us = h->eng->bench_op(name, reps, flops); });
+  return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
+    *us = h->eng->bench_op(name, reps, flops);
+  });
 }
 
 void* pswa_gpu_stream(pswa_gpu* h) { return h->eng->stream(); }
@@ -223,6 +267,7 @@ extern "C" __attribute__((visibility("default"))) int pswa_debug_gemm_trace(unsi
 int pswa_gpu_encode_sequence(pswa_gpu* h, const int32_t* frames, int n_frames, int gop_size,
                              int rate_idx, uint8_t* out, size_t cap, size_t* len) {
   return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
     if (n_frames < 0 || gop_size < 1) throw std::invalid_argument("n_frames / gop_size");
     const pswa_cfg& c = h->cfg;
     pswa_host::ContainerHeader hd;
@@ -258,6 +303,7 @@ int pswa_gpu_encode_sequence(pswa_gpu* h, const int32_t* frames, int n_frames, i
 int pswa_gpu_decode_sequence(pswa_gpu* h, const uint8_t* cont, size_t len, int32_t* frames_out,
                              int max_frames, int* frame_status, double* bits_out, int* n_frames) {
   return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
     std::vector<pswa_host::FrameRef> fr;
     const auto hd = pswa_host::parse_container(cont, len, &fr);
     const pswa_cfg& c = h->cfg;
@@ -324,11 +370,17 @@ int pswa_group_create(const int* devices, int n_bands, const pswa_cfg* cfg, cons
 void pswa_group_destroy(pswa_group* g) { delete g; }
 
 int pswa_group_reset_gop(pswa_group* g) {
-  return guard([&] { g->grp->reset_gop(); });
+  return guard([&] {
+    pswa_dev::DeviceScope ds(g->grp->band(0).device());
+    g->grp->reset_gop();
+  });
 }
 
 int pswa_group_push_frame(pswa_group* g, const int32_t* yhat, int rate_idx) {
-  return guard([&] { g->grp->push_frame(yhat, rate_idx); });
+  return guard([&] {
+    pswa_dev::DeviceScope ds(g->grp->band(0).device());
+    g->grp->push_frame(yhat, rate_idx);
+  });
 }
 
 int pswa_group_encode_frame(pswa_group* g, const int32_t* yhat, const int32_t* zhat, int rate_idx,
@@ -336,6 +388,7 @@ int pswa_group_encode_frame(pswa_group* g, const int32_t* yhat, const int32_t* z
                             size_t* hyper_len, uint8_t* main_out, size_t main_cap, size_t* main_len,
                             double* bits_out) {
   return guard([&] {
+    pswa_dev::DeviceScope ds(g->grp->band(0).device());
     const auto r = g->grp->encode(yhat, rate_idx, frame_idx_in_gop, zhat, nullptr, nullptr,
                                   hyper_out, hyper_cap, main_out, main_cap, /*advance=*/true);
     *hyper_len = r.hyper_len;
@@ -352,6 +405,7 @@ int pswa_group_decode_frame(pswa_group* g, const uint8_t* hyper, size_t hyper_le
                             int frame_idx_in_gop, int advance_state, int32_t* yhat_out,
                             double* bits_out) {
   return guard([&] {
+    pswa_dev::DeviceScope ds(g->grp->band(0).device());
     const auto r = g->grp->decode(hyper, hyper_len, main_payload, main_len, rate_idx,
                                   frame_idx_in_gop, advance_state != 0, yhat_out);
     if (bits_out) {
@@ -365,6 +419,7 @@ int pswa_group_forward_params(pswa_group* g, const int32_t* yhat, const int32_t*
                               int frame_idx_in_gop, float* mu_out, float* sigma_out,
                               double* bits_out) {
   return guard([&] {
+    pswa_dev::DeviceScope ds(g->grp->band(0).device());
     if (!mu_out || !sigma_out || !zhat) throw std::invalid_argument("zhat / mu_out / sigma_out required");
     const auto r = g->grp->encode(yhat, rate_idx, frame_idx_in_gop, zhat, mu_out, sigma_out, nullptr,
                                   0, nullptr, 0, /*advance=*/false);
@@ -376,7 +431,10 @@ int pswa_group_forward_params(pswa_group* g, const int32_t* yhat, const int32_t*
 }
 
 int pswa_group_last_zhat(pswa_group* g, int32_t* zhat_out) {
-  return guard([&] { g->grp->band(0).last_zhat(zhat_out); });
+  return guard([&] {
+    pswa_dev::DeviceScope ds(g->grp->band(0).device());
+    g->grp->band(0).last_zhat(zhat_out);
+  });
 }
 
 int pswa_group_last_launch_count(pswa_group* g) { return g->grp->last_launches(); }

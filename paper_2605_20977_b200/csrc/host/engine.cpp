@@ -452,6 +452,8 @@ void Engine::alloc_all() {
   enc_hbits_ = dalloc<double>(Lz);
   pack_total_ = dalloc<unsigned long long>(2);
   pack_offs_ = dalloc<uint64_t>(std::max(L, Lz));
+  symbits_ = dalloc<double>(static_cast<size_t>(HWl) * C);
+  bitstats_ = dalloc<double>(static_cast<size_t>(D.N) * HWo);
   mu_full_ = dalloc<float>(static_cast<size_t>(HWl) * C);
   sg_full_ = dalloc<float>(static_cast<size_t>(HWl) * C);
   afull_ = dalloc<float>(static_cast<size_t>(HWl) * d);
@@ -1193,18 +1195,17 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
       const float* msg = musig_ + static_cast<size_t>(off) * ms;
       const int* rws = rows + off;
       __half* y16 = y16_ + static_cast<size_t>(off) * C;
+      const pswa_dev::PhaseTaps taps = phase_taps();
       if (mode == 0) {
         const int L = D.c.lanes;
         add(P, [=, this](cudaStream_t s) {
           pswa_dev::lanes_decode_phase(d_main_, lanes_, L, o0, n, Cg, msg, ms, Cg, scales_, cdf_main_,
-                                       rws, yfr_, C, c0, y16, C, status_, s);
+                                       rws, yfr_, C, c0, y16, C, status_, s, taps);
         });
       } else {
-        const bool ms_out = want_musig_;
         add(P, [=, this](cudaStream_t s) {
-          pswa_dev::quantize_phase(msg, ms, Cg, n, Cg, o0, rws, yfr_, C, c0, scales_, sym_v_,
-                                   sym_idx_, y16, C, ms_out ? mu_full_ : nullptr,
-                                   ms_out ? sg_full_ : nullptr, s);
+          pswa_dev::quantize_phase(msg, ms, Cg, n, Cg, o0, rws, yfr_, C, c0, scales_, cdf_main_, sym_v_,
+                                   sym_idx_, y16, C, taps, status_, s);
         });
       }
     }
@@ -1227,10 +1228,12 @@ Program& Engine::program(const std::string& key) {
   const int HW = HWo_, C = D.C, L = D.c.lanes, Lz = D.c.hyper_lanes;  // HW: own positions
   const int nz = D.hc * D.zh * D.zw;
   const size_t yoff = static_cast<size_t>(B_.own0) * D.W * C;  // own rows in yfr_
-  const std::string base = key.substr(0, key.find('+'));  // "+ms": mu/sigma outputs
+  const std::string base = key.substr(0, key.find('+'));
+  // "+ms": mu/sigma and per-symbol bit taps (BitStats) in every phase
+  taps_ = key.find("+ms") != std::string::npos;
   if (base == "decode") {
     // "+h" (single band): per-group ŷ transpositions and cuts for the host copies
-    host_copy_ = key == "decode+h" && B_.n == 1;
+    host_copy_ = key.find("+h") != std::string::npos && B_.n == 1;
     // the hyperprior branch (z_hat lanes -> hyper decoder -> Hq) does not
     // depend on the context transformer: it runs on a side stream of the
     // same graph and joins before the first Hq consumer (band mode: before
@@ -1262,6 +1265,12 @@ Program& Engine::program(const std::string& key) {
       build_step(P, batch_of(t), 0);
     }
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_lane_bits(lanes_, L, bits_ + 1, s); });
+    if (taps_) {
+      const int row0 = B_.own0 * D.W;
+      add(P, [=, this](cudaStream_t s) {
+        pswa_dev::bitstats_reduce(symbits_, C, row0, HW, D.N, D.Cg, bitstats_, s);
+      });
+    }
     if (!host_copy_)
       add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_to_chw(yfr_ + yoff, HW, C, ychw_, s); });
     host_copy_ = false;
@@ -1320,6 +1329,12 @@ Program& Engine::program(const std::string& key) {
     }, 2);
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_doubles(enc_hbits_, Lz, bits_, s); });
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_doubles(enc_bits_, L, bits_ + 1, s); });
+    if (taps_) {
+      const int row0 = B_.own0 * D.W;
+      add(P, [=, this](cudaStream_t s) {
+        pswa_dev::bitstats_reduce(symbits_, C, row0, HW, D.N, D.Cg, bitstats_, s);
+      });
+    }
   } else if (base == "push") {
     add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_from_chw(ychw_, HW, C, yfr_ + yoff, s); });
     const StepBatch all = batch_all();  // embeddings are per position: one pass
@@ -1330,6 +1345,7 @@ Program& Engine::program(const std::string& key) {
   } else {
     throw std::invalid_argument("unknown program " + key);
   }
+  taps_ = false;
   return P;
 }
 
@@ -1675,13 +1691,15 @@ void Engine::prep_encode(const int32_t* yhat_chw, int rate, int fidx, const int3
 FrameResult Engine::finish_encode(float* mu_out, float* sigma_out, uint8_t* hyper_out,
                                   size_t hyper_cap, uint8_t* main_out, size_t main_cap,
                                   bool advance) {
-  const Dims& D = D_;
   FrameResult r;
   unsigned long long tot[2];
   PSWA_CUDA(cudaMemcpyAsync(tot, pack_total_, sizeof(tot), cudaMemcpyDeviceToHost, st_));
   PSWA_CUDA(cudaMemcpyAsync(r.bits, bits_, sizeof(r.bits), cudaMemcpyDeviceToHost, st_));
   PSWA_CUDA(cudaMemcpyAsync(&r.status, status_, sizeof(int), cudaMemcpyDeviceToHost, st_));
   PSWA_CUDA(cudaStreamSynchronize(st_));
+  if (r.status & 16)
+    throw std::invalid_argument("encode: y_hat outside the supported range (|y_hat| <= " +
+                                std::to_string(pswa_dev::kYhatMax) + ")");
   if (r.status) throw pswa_abi::LaneError("encoder status " + std::to_string(r.status));
   r.hyper_len = tot[0];
   r.main_len = tot[1];
@@ -1693,22 +1711,42 @@ FrameResult Engine::finish_encode(float* mu_out, float* sigma_out, uint8_t* hype
     if (main_cap < r.main_len) throw std::invalid_argument("main output buffer too small");
     PSWA_CUDA(cudaMemcpyAsync(main_out, d_main_, r.main_len, cudaMemcpyDeviceToHost, st_));
   }
-  if (mu_out) {  // [HWl][C] device -> own rows of the [C][H][W] host frame
-    const size_t n = static_cast<size_t>(HWl_) * D.C;
-    std::vector<float> a(n), b(n);
-    PSWA_CUDA(cudaMemcpyAsync(a.data(), mu_full_, sizeof(float) * n, cudaMemcpyDeviceToHost, st_));
-    PSWA_CUDA(cudaMemcpyAsync(b.data(), sg_full_, sizeof(float) * n, cudaMemcpyDeviceToHost, st_));
-    PSWA_CUDA(cudaStreamSynchronize(st_));
-    const size_t o = static_cast<size_t>(B_.own0) * D.W, g = static_cast<size_t>(B_.r0) * D.W;
-    for (int p = 0; p < HWo_; ++p)
-      for (int c = 0; c < D.C; ++c) {
-        mu_out[static_cast<size_t>(c) * D.HW + g + p] = a[(o + p) * D.C + c];
-        sigma_out[static_cast<size_t>(c) * D.HW + g + p] = b[(o + p) * D.C + c];
-      }
-  }
+  fetch_musig(mu_out, sigma_out);
+  have_stats_ = want_musig_ || stats_on_;
   if (advance) advance_ring();
   PSWA_CUDA(cudaStreamSynchronize(st_));
   return r;
+}
+
+// [HWl][C] device taps -> own rows of [C][H][W] host frames (nullable)
+void Engine::fetch_musig(float* mu_out, float* sigma_out) {
+  if (!mu_out && !sigma_out) return;
+  const Dims& D = D_;
+  const size_t n = static_cast<size_t>(HWl_) * D.C;
+  std::vector<float> a(n), b(n);
+  PSWA_CUDA(cudaMemcpyAsync(a.data(), mu_full_, sizeof(float) * n, cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaMemcpyAsync(b.data(), sg_full_, sizeof(float) * n, cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+  const size_t o = static_cast<size_t>(B_.own0) * D.W, g = static_cast<size_t>(B_.r0) * D.W;
+  for (int p = 0; p < HWo_; ++p)
+    for (int c = 0; c < D.C; ++c) {
+      if (mu_out) mu_out[static_cast<size_t>(c) * D.HW + g + p] = a[(o + p) * D.C + c];
+      if (sigma_out) sigma_out[static_cast<size_t>(c) * D.HW + g + p] = b[(o + p) * D.C + c];
+    }
+}
+
+void Engine::last_bitstats(double* out) {
+  if (!have_stats_)
+    throw std::invalid_argument("last_bitstats: the last frame call ran without stats "
+                                "(pswa_gpu_set_stats, or request mu/sigma)");
+  const Dims& D = D_;
+  std::vector<double> v(static_cast<size_t>(D.N) * HWo_);
+  PSWA_CUDA(cudaMemcpyAsync(v.data(), bitstats_, sizeof(double) * v.size(), cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaStreamSynchronize(st_));
+  const size_t g0 = static_cast<size_t>(B_.r0) * D.W;
+  for (int g = 0; g < D.N; ++g)
+    std::memcpy(out + static_cast<size_t>(g) * D.HW + g0, v.data() + static_cast<size_t>(g) * HWo_,
+                sizeof(double) * HWo_);
 }
 
 void Engine::fetch_payloads(uint8_t* hyper_out, size_t hyper_cap, const FrameResult& r,
@@ -1726,9 +1764,9 @@ FrameResult Engine::encode(const int32_t* yhat_chw, int rate, int fidx, const in
                            uint8_t* main_out, size_t main_cap, bool advance) {
   prep_encode(yhat_chw, rate, fidx, zhat_in);
   want_musig_ = mu_out != nullptr;
-  // the mu/sigma output pointers are baked into the captured graph, so the
-  // two variants are separate programs
-  run(program(encode_key(zhat_in != nullptr, want_musig_)));
+  // the taps (mu/sigma/bit outputs) are baked into the captured graph, so
+  // the two variants are separate programs
+  run(program(encode_key(zhat_in != nullptr, want_musig_ || stats_on_)));
   return finish_encode(mu_out, sigma_out, hyper_out, hyper_cap, main_out, main_cap, advance);
 }
 
@@ -1752,7 +1790,8 @@ void Engine::prep_decode(const void* hyper, size_t hyper_len, const void* main_p
   PSWA_CUDA(cudaMemcpyAsync(d_lens_, lens_h_, sizeof(lens_h_), cudaMemcpyHostToDevice, st_));
 }
 
-FrameResult Engine::finish_decode(bool advance, int32_t* yhat_out, bool device) {
+FrameResult Engine::finish_decode(bool advance, int32_t* yhat_out, bool device, float* mu_out,
+                                  float* sigma_out) {
   const Dims& D = D_;
   FrameResult r;
   const size_t row = static_cast<size_t>(HWo_) * sizeof(int32_t);
@@ -1771,6 +1810,7 @@ FrameResult Engine::finish_decode(bool advance, int32_t* yhat_out, bool device) 
   PSWA_CUDA(cudaStreamSynchronize(st_));
   if (r.status) throw pswa_abi::TruncatedError("corrupt or truncated payload (status " +
                                                std::to_string(r.status) + ")");
+  fetch_musig(mu_out, sigma_out);
   if (advance) {
     advance_ring();
     PSWA_CUDA(cudaStreamSynchronize(st_));
@@ -1782,7 +1822,8 @@ void Engine::decode_async(const void* d_hyper, size_t hyper_len, const void* d_m
                           size_t main_len, int rate, int fidx, int32_t* d_yhat_out) {
   if (B_.n > 1) throw std::invalid_argument("decode_async: not for band handles");
   prep_decode(d_hyper, hyper_len, d_main, main_len, rate, fidx, true);
-  run(program("decode"));
+  run(program(decode_key(false, stats_on_)));
+  have_stats_ = stats_on_;
   PSWA_CUDA(cudaMemcpyAsync(d_yhat_out, ychw_, sizeof(int32_t) * HWo_ * D_.C,
                             cudaMemcpyDeviceToDevice, st_));
 }
@@ -1798,7 +1839,10 @@ FrameResult Engine::finish_async() {
 }
 
 FrameResult Engine::decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
-                           int rate, int fidx, bool advance, int32_t* yhat_out, bool device) {
+                           int rate, int fidx, bool advance, int32_t* yhat_out, bool device,
+                           float* mu_out, float* sigma_out) {
+  const bool taps = mu_out || sigma_out || stats_on_;
+  have_stats_ = false;
   // pinned host output: the copies of finished channel groups overlap the
   // last groups' decoding (a pageable destination makes each copy blocking,
   // so it keeps the single copy at the end)
@@ -1807,14 +1851,18 @@ FrameResult Engine::decode(const void* hyper, size_t hyper_len, const void* main
                       pa.type == cudaMemoryTypeHost;
   if (!device) (void)cudaGetLastError();  // pageable pointers may set an error on older drivers
   if (pinned && B_.n == 1 && D_.N <= 8) {
-    Program& P = program("decode+h");
+    Program& P = program(decode_key(true, taps));
     prep_decode(hyper, hyper_len, main_pl, main_len, rate, fidx, device, true);
     run_host_copy(P, yhat_out);
-    return finish_decode(advance, nullptr, device);
+    const FrameResult r = finish_decode(advance, nullptr, device, mu_out, sigma_out);
+    have_stats_ = taps;
+    return r;
   }
   prep_decode(hyper, hyper_len, main_pl, main_len, rate, fidx, device);
-  run(program("decode"));
-  return finish_decode(advance, yhat_out, device);
+  run(program(decode_key(false, taps)));
+  const FrameResult r = finish_decode(advance, yhat_out, device, mu_out, sigma_out);
+  have_stats_ = taps;
+  return r;
 }
 
 

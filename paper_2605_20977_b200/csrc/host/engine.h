@@ -118,9 +118,19 @@ class Engine {
                      float* mu_out, float* sigma_out, uint8_t* hyper_out, size_t hyper_cap,
                      uint8_t* main_out, size_t main_cap, bool advance);
   // Decoder. Payloads and output either on the host (copies inside the call)
-  // or already in device memory (device == true).
+  // or already in device memory (device == true). mu/sigma (nullable, host
+  // [C][H][W]) receive the decoder's own entropy parameters; requesting them
+  // (or enabling stats) runs the "+ms" variant of the decode program, which
+  // also produces BitStats.
   FrameResult decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
-                     int rate, int fidx, bool advance, int32_t* yhat_out, bool device);
+                     int rate, int fidx, bool advance, int32_t* yhat_out, bool device,
+                     float* mu_out = nullptr, float* sigma_out = nullptr);
+  // BitStats of every later frame call: per-position,
+  // per-group estimated bits, read with last_bitstats().
+  void set_stats(bool on) { stats_on_ = on; }
+  // [N][H][W] (own rows of the full frame) of the last frame decoded or
+  // encoded with stats on.
+  void last_bitstats(double* out_nhw);
   void last_zhat(int32_t* out_host);
   // LRP output eps [C][H][W] of the last decoded / encoded frame (lrp_blocks > 0).
   void last_eps(float* out_chw);
@@ -140,7 +150,13 @@ class Engine {
   // the program's segments on every band, finish_* collects the outputs.
   void prep_decode(const void* hyper, size_t hyper_len, const void* main_pl, size_t main_len,
                    int rate, int fidx, bool device, bool defer_main = false);
-  FrameResult finish_decode(bool advance, int32_t* yhat_out, bool device);
+  FrameResult finish_decode(bool advance, int32_t* yhat_out, bool device, float* mu_out = nullptr,
+                            float* sigma_out = nullptr);
+  // decode program key: "+h" host-copy variant, "+ms" taps variant
+  std::string decode_key(bool host_copy, bool taps) const {
+    return std::string("decode") + (host_copy ? "+h" : "") + (taps ? "+ms" : "");
+  }
+  bool stats_on() const { return stats_on_; }
   // Asynchronous device-resident decode (no host sync; ring not advanced):
   // several handles on their own streams overlap on one GPU (GOP batches,
   // BASELINE config 4). finish_async() syncs and checks the status.
@@ -204,6 +220,16 @@ class Engine {
   // group's ŷ planes copied to the host on copy_ while later groups decode
   void run_host_copy(Program& P, int32_t* yhat_out);
   bool host_copy_ = false;  // set while the "+h" program is being built
+  bool taps_ = false;       // set while a "+ms" program is being built
+  pswa_dev::PhaseTaps phase_taps() const {
+    pswa_dev::PhaseTaps t;
+    if (taps_) t = {mu_full_, sg_full_, symbits_};
+    return t;
+  }
+  void fetch_musig(float* mu_out, float* sigma_out);
+  bool stats_on_ = false, have_stats_ = false;
+  double* symbits_ = nullptr;   // [HWl][C] per-symbol bits ("+ms" programs)
+  double* bitstats_ = nullptr;  // [N][HWo]
   cudaStream_t copy_ = nullptr;
   cudaEvent_t ev_copy_[8] = {}, ev_copy_done_ = nullptr, ev_main_in_ = nullptr;
   void to_side(Program& P, size_t from);

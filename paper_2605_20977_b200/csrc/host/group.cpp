@@ -82,7 +82,11 @@ BandGroup::~BandGroup() {
 void BandGroup::run(const std::string& key) {
   const int n = size();
   std::vector<Program*> P(n);
-  for (int b = 0; b < n; ++b) P[b] = &bands_[b]->program(key);
+  for (int b = 0; b < n; ++b) {
+    // building a program allocates tables and launches on the band's stream
+    PSWA_CUDA(cudaSetDevice(bands_[b]->device()));
+    P[b] = &bands_[b]->program(key);
+  }
   const int S = bands_[0]->segments(*P[0]);
   last_launches_ = 0;
   for (int b = 0; b < n; ++b) {
@@ -104,7 +108,7 @@ void BandGroup::run(const std::string& key) {
     }
 }
 
-void BandGroup::reset_gop() {
+void BandGroup::reset_gop() {  // host-side ring indices only
   for (auto& e : bands_) e->reset_gop();
 }
 

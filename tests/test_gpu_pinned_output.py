@@ -30,7 +30,7 @@ def test_pinned_output_matches(preset, H, W, lrp):
         hb = np.frombuffer(hyper, np.uint8)
         mb = np.frombuffer(main, np.uint8)
         rc = lib().pswa_gpu_decode_frame(pinned.h, hb.ctypes.data, len(hyper), mb.ctypes.data,
-                                         len(main), 0, i, 1, out.data_ptr(),
+                                         len(main), 0, i, 1, out.data_ptr(), None, None,
                                          bits.ctypes.data_as(C.POINTER(C.c_double)))
         assert rc == 0
         y_pin = out.numpy().reshape(cfg.latent_ch, H, W)
