@@ -86,6 +86,17 @@ int pswa_gen_weights(const pswa_cfg* cfg, uint64_t seed, void* buf, size_t cap, 
 /* Synthetic latent frame: y_hat[C][H][W] int32 for frame
  * `frame_idx` of GOP `gop`. */
 int pswa_synth_latent(const pswa_cfg* cfg, int gop, int frame_idx, int32_t* yhat_out);
+/* Frames 0..n_frames-1 of GOP `gop` in one pass: out[n_frames][C][H][W]. */
+int pswa_synth_gop(const pswa_cfg* cfg, int gop, int n_frames, int32_t* out);
+
+/* validate_schedule (proj/include/pswa/wavefront.h:54-66)
+ * for plain-C callers: *ok = 1 when the (s, window, N) schedule is decodable
+ * -- accumulator edges strictly backward, spatial-self edges never forward,
+ * the canonical decode order a topological order of the symbol dependency
+ * graph derived from the network's dataflow -- else 0 with the first
+ * violation (nullable buffer of cap bytes). Host only. */
+int pswa_validate_schedule(int h, int w, int s, int wh, int ww, int n_groups, int* ok,
+                           int* sequential_steps, char* first_violation, size_t cap);
 
 /* ---- handle lifecycle --------------------------------------------------- */
 int pswa_gpu_create(int device, const pswa_cfg* cfg, const void* psww_blob, size_t blob_len,
@@ -156,6 +167,15 @@ int pswa_gpu_last_launch_count(pswa_gpu* h);
  * algorithmic FLOPs (mask-allowed keys only) feed bench.py's roofline. */
 int pswa_gpu_bench_op(pswa_gpu* h, const char* name, int reps, double* us_per_launch,
                       double* flops_per_launch);
+/* Every probe of the handle's programs: one "name flops bytes launches" line
+ * each (algorithmic FLOPs / HBM bytes per replay; probes are tagged when a
+ * program is built, so decode a frame first). pswa_gpu_bench_probe replays
+ * one like pswa_gpu_bench_op and also returns its bytes. tools/
+ * profile_probes.py captures the same replays under ncu, so bench.py's
+ * per-kernel rooflines and profiles/ describe the same launches. */
+int pswa_gpu_probe_list(pswa_gpu* h, char* out, size_t cap, size_t* len);
+int pswa_gpu_bench_probe(pswa_gpu* h, const char* name, int reps, double* us_per_replay,
+                         double* flops, double* bytes);
 /* Stream the handle runs on (cudaStream_t as void*). */
 void* pswa_gpu_stream(pswa_gpu* h);
 

@@ -1,6 +1,8 @@
 // ORACLE — test infrastructure only: C entry points for tests/ (ctypes) and
 // bench.py's cpu_baseline leg. Config is passed as the 22 ints of pswa_cfg.
+#include <cmath>
 #include <cstring>
+#include <vector>
 #include <exception>
 #include <stdexcept>
 #include <string>
@@ -272,3 +274,42 @@ int oracle_decode(void* h, int mode, const uint8_t* hyper, size_t hlen, const ui
 }
 
 }  // extern "C"
+
+// ---- synthetic latents ------------------------------------------
+// Independent restatement of the bench input generator, so the reference arm
+// of bench.py builds its inputs without the product library:
+//   y[c,p] ~ Laplace(0, b_g), b_g = 8 / 2^g for channel group g (inverse CDF
+//   with det::log on a 24-bit uniform in (0,1)); P-frames add Laplace(0, b_g/4)
+//   to the previous frame; frame seed 1000 + 100 gop + frame; y_hat =
+//   round-half-even(y); 1 in 10^4 positions forced to +-300.
+// Writes frames [0, n_frames) of GOP `gop`: out[f][C][H][W].
+extern "C" int oracle_synth_gop(const int* cfg, int gop, int n_frames, int32_t* out) {
+  return guard([&] {
+    const Config c = to_cfg(cfg);
+    const int C = c.C, HW = c.H * c.W, Cg = C / c.N;
+    std::vector<float> y(static_cast<size_t>(C) * HW, 0.0f);
+    auto lap = [](Rng& r, double b) {
+      const double u = (static_cast<double>(r.u64() >> 40) + 0.5) / 16777216.0;
+      return u < 0.5 ? b * det::log(2.0 * u) : -b * det::log(2.0 * (1.0 - u));
+    };
+    for (int f = 0; f < n_frames; ++f) {
+      const uint64_t seed = 1000ull + 100ull * static_cast<uint64_t>(gop) + static_cast<uint64_t>(f);
+      Rng r(seed);
+      for (int ch = 0; ch < C; ++ch) {
+        const int g = ch / Cg;
+        const double b = 8.0 / static_cast<double>(1 << (g < 30 ? g : 30));
+        float* row = y.data() + static_cast<size_t>(ch) * HW;
+        for (int p = 0; p < HW; ++p)
+          row[p] = f == 0 ? static_cast<float>(lap(r, b)) : row[p] + static_cast<float>(lap(r, b / 4.0));
+      }
+      int32_t* o = out + static_cast<size_t>(f) * C * HW;
+      for (size_t i = 0; i < y.size(); ++i) o[i] = static_cast<int32_t>(std::nearbyint(y[i]));
+      Rng e(seed ^ 0x5EEDE5CA9Eull);
+      for (int p = 0; p < HW; ++p)
+        if (e.u64() % 10000 == 0) {
+          const int ch = static_cast<int>(e.u64() % static_cast<uint64_t>(C));
+          o[static_cast<size_t>(ch) * HW + p] = (e.u64() & 1) ? 300 : -300;
+        }
+    }
+  });
+}

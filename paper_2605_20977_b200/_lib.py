@@ -39,6 +39,7 @@ _SIGS = {
     "pswa_cfg_preset": (None, [C.POINTER(PswaCfg), _I, _I, _I]),
     "pswa_gen_weights": (_I, [C.POINTER(PswaCfg), C.c_uint64, _VP, _SZ, C.POINTER(_SZ)]),
     "pswa_synth_latent": (_I, [C.POINTER(PswaCfg), _I, _I, _VP]),
+    "pswa_synth_gop": (_I, [C.POINTER(PswaCfg), _I, _I, _VP]),
     "pswa_gpu_create": (_I, [_I, C.POINTER(PswaCfg), _VP, _SZ, C.POINTER(_VP)]),
     "pswa_gpu_destroy": (None, [_VP]),
     "pswa_gpu_reset_gop": (_I, [_VP]),
@@ -56,6 +57,8 @@ _SIGS = {
     "pswa_gpu_last_launch_count": (_I, [_VP]),
     "pswa_gpu_stream": (_VP, [_VP]),
     "pswa_gpu_bench_op": (_I, [_VP, C.c_char_p, _I, _D, _D]),
+    "pswa_gpu_bench_probe": (_I, [_VP, C.c_char_p, _I, _D, _D, _D]),
+    "pswa_gpu_probe_list": (_I, [_VP, C.c_char_p, _SZ, C.POINTER(_SZ)]),
     "pswa_gpu_decode_frame_async": (_I, [_VP, _VP, _SZ, _VP, _SZ, _I, _I, _VP]),
     "pswa_gpu_finish": (_I, [_VP, _D]),
     "pswa_gpu_op_gemm_f16": (_I, [_VP, _I, _I, _VP, _I, _I, _I, _VP, _I, _I, _I, _VP, _VP, _I,
@@ -67,6 +70,14 @@ _SIGS = {
     "pswa_gpu_op_build_cdf_family": (_I, [_VP, _VP, _I]),
     "pswa_gpu_op_encode_symbols": (_I, [_VP, _VP, _SZ, _I, _I, _VP, _SZ, C.POINTER(_SZ), _D]),
     "pswa_gpu_op_decode_symbols": (_I, [_VP, _SZ, _VP, _SZ, _I, _VP, _D]),
+    "pswa_validate_schedule": (_I, [_I, _I, _I, _I, _I, _I, C.POINTER(_I), C.POINTER(_I), C.c_char_p, _SZ]),
+    "pswa_tensor_matmul": (_I, [_VP, _VP, _VP, _I, _I, _I]),
+    "pswa_tensor_softmax_rows": (_I, [_VP, _VP, _I, _I]),
+    "pswa_tensor_rmsnorm": (_I, [_VP, _VP, _I, _VP]),
+    "pswa_tensor_swiglu_ffn": (_I, [_VP, _VP, _VP, _VP, _I, _I, _VP]),
+    "pswa_tensor_conv2d": (_I, [_VP, _I, _I, _I, _VP, _I, _I, _I, _I, _I, _VP]),
+    "pswa_tensor_upsample2": (_I, [_VP, _I, _I, _I, _VP]),
+    "pswa_tensor_ffn_hidden_dim": (_I, [_I]),
     "pswa_band_rows": (_I, [_I, _I, _I, C.POINTER(_I), C.POINTER(_I)]),
     "pswa_group_create": (_I, [_VP, _I, C.POINTER(PswaCfg), _VP, _SZ, C.POINTER(_VP)]),
     "pswa_group_destroy": (None, [_VP]),

@@ -44,6 +44,13 @@ def synth_latent(cfg: PswaCfg, gop: int, frame: int) -> np.ndarray:
     return y
 
 
+def synth_gop(cfg: PswaCfg, gop: int, n_frames: int) -> np.ndarray:
+    """Frames 0..n_frames-1 of GOP `gop`, [F][C][H][W] int32, in one pass."""
+    y = np.zeros((n_frames, cfg.latent_ch, cfg.height, cfg.width), np.int32)
+    check(lib().pswa_synth_gop(C.byref(cfg), gop, n_frames, y.ctypes.data_as(_P)))
+    return y
+
+
 def _ptr(a: np.ndarray):
     return a.ctypes.data_as(_P)
 
@@ -214,6 +221,25 @@ class GpuCodec:
         us, fl = C.c_double(), C.c_double()
         check(lib().pswa_gpu_bench_op(self.h, name.encode(), reps, C.byref(us), C.byref(fl)))
         return us.value, fl.value
+
+    def probes(self) -> dict:
+        """{name: (flops, bytes, launches)} of every bench probe."""
+        n = C.c_size_t()
+        check(lib().pswa_gpu_probe_list(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(lib().pswa_gpu_probe_list(self.h, buf, n.value, C.byref(n)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, fl, by, nl = line.split()
+            out[name] = (float(fl), float(by), int(nl))
+        return out
+
+    def bench_probe(self, name: str, reps: int = 50) -> tuple[float, float, float]:
+        """(us per replay, FLOPs, HBM bytes) of one probe."""
+        us, fl, by = C.c_double(), C.c_double(), C.c_double()
+        check(lib().pswa_gpu_bench_probe(self.h, name.encode(), reps, C.byref(us), C.byref(fl),
+                                         C.byref(by)))
+        return us.value, fl.value, by.value
 
     def stream(self) -> int:
         return lib().pswa_gpu_stream(self.h)

@@ -19,6 +19,7 @@
 #include "kernels.h"
 #include "launch.cuh"
 #include "ptx.cuh"
+#include "det_device.cuh"
 
 namespace pswa_dev {
 
@@ -28,65 +29,6 @@ constexpr uint64_t kWin = (uint64_t{1} << 48) - 1;
 constexpr uint64_t kBot = uint64_t{1} << 40;
 constexpr int kEscLo = 255, kEscHi = 256;
 __device__ const uint32_t kBitCum[3] = {0, 32768, 65536};
-
-// ------------------------------------------------- fp64 det math (device) --
-__device__ double d_pow2i(int k) {
-  if (k > 1023) return __longlong_as_double(0x7FF0000000000000LL);
-  if (k < -1074) return 0.0;
-  if (k >= -1022) return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
-  return __longlong_as_double(1LL << (k + 1074));
-}
-__device__ double d_exp(double x) {
-  if (x != x) return x;
-  if (x > 709.782712893384) return __longlong_as_double(0x7FF0000000000000LL);
-  if (x < -745.1332191019412) return 0.0;
-  const double t = x * 1.44269504088896338700e+00;
-  const int n = static_cast<int>(t >= 0.0 ? t + 0.5 : t - 0.5);
-  const double nd = n;
-  const double r = (x - nd * 6.93147180369123816490e-01) - nd * 1.90821492927058770002e-10;
-  const double c[11] = {1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0,
-                        1.0 / 3628800.0,    1.0 / 362880.0,    1.0 / 40320.0,
-                        1.0 / 5040.0,       1.0 / 720.0,       1.0 / 120.0,
-                        1.0 / 24.0,         1.0 / 6.0};
-  double p = c[0];
-#pragma unroll
-  for (int i = 1; i < 11; ++i) p = p * r + c[i];
-  const double rr = r * r;
-  return (1.0 + r + 0.5 * rr + rr * r * p) * d_pow2i(n);
-}
-__device__ double d_log(double x) {
-  long long b = __double_as_longlong(x);
-  int e = 0;
-  if (b < (1LL << 52)) {
-    x *= 18014398509481984.0;  // 2^54
-    e = -54;
-    b = __double_as_longlong(x);
-  }
-  e += static_cast<int>((b >> 52) & 0x7FF) - 1023;
-  double m = __longlong_as_double((b & ((1LL << 52) - 1)) | (1023LL << 52));
-  if (m > 1.4142135623730951) {
-    m *= 0.5;
-    e += 1;
-  }
-  const double f = m - 1.0, s = f / (2.0 + f), z = s * s, w = z * z;
-  const double t1 = w * (3.999999999940941908e-01 +
-                         w * (2.222219843214978396e-01 + w * 1.531383769920937332e-01));
-  const double t2 = z * (6.666666666666735130e-01 +
-                         w * (2.857142874366239149e-01 +
-                              w * (1.818357216161805012e-01 + w * 1.479819860511658591e-01)));
-  const double hf = 0.5 * f * f, R = t2 + t1, ed = e;
-  return ed * 6.93147180369123816490e-01 -
-         ((hf - (s * (hf + R) + ed * 1.90821492927058770002e-10)) - f);
-}
-__device__ double d_erf(double x) {
-  const double a = x < 0.0 ? -x : x;
-  const double t = 1.0 / (1.0 + 0.3275911 * a);
-  const double poly =
-      t * (0.254829592 +
-           t * (-0.284496736 + t * (1.421413741 + t * (-1.453152027 + t * 1.061405429))));
-  const double y = 1.0 - poly * d_exp(-a * a);
-  return x < 0.0 ? -y : y;
-}
 
 __device__ __forceinline__ double sym_bits(uint32_t freq) {
   return 16.0 - log2(static_cast<double>(freq));
@@ -321,8 +263,17 @@ __global__ void __launch_bounds__(128) lanes_init_kernel(const uint8_t* __restri
   const uint32_t ln = l < L ? lens[l] : 0u;
   const uint64_t off = hdr + before + block_excl_scan(ln, ws);
   if (l >= L) return;
-  if (off + ln > len || ln < 4) atomicOr(status, 1);  // past the payload / shorter than the flush
-  if (off + ln > len) return;
+  if (off + ln > len || ln < 4) {  // past the payload / shorter than the flush
+    atomicOr(status, 1);
+    // a dead lane the decoders can run over without leaving the payload
+    LaneState s;
+    s.pos = s.end = static_cast<uint32_t>(off < len ? off : len);
+    s.range = kWin;
+    s.code = 0;
+    s.bits = 0.0;
+    lanes[l] = s;
+    return;
+  }
   uint32_t byt[6];
 #pragma unroll
   for (int b = 0; b < 6; ++b) byt[b] = static_cast<uint32_t>(b) < ln ? pl[off + b] : 0u;
@@ -505,7 +456,8 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
   pdl_wait();
   pdl_trigger();
   mbar_wait(&s_bar, 0);
-  if (!active) return;
+  // a malformed lane header (lanes_init) already failed the frame: decode nothing
+  if (!active || (*reinterpret_cast<volatile int*>(status) & 1)) return;
   int err = 0;
   // the parameters (mu, table index) of a lane's next symbols do not depend
   // on the coder state: gather them in a batch (loads in flight together),
@@ -640,10 +592,10 @@ __global__ void decode_hyper_kernel(const uint8_t* __restrict__ pl, LaneState* _
   pdl_wait();
   pdl_trigger();
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= L) return;
+  if (l >= L || (*status & 1)) return;
   LaneState s = lanes[l];
   int err = 0;
-  for (int i = l; i < n; i += L) {
+  for (int i = l; i < n && !err; i += L) {
     const int ch = i / per_ch;
     const int idx = scale_index(scales, scale[ch]);
     ByteDirect rd{pl};

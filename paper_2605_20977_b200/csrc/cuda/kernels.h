@@ -199,4 +199,14 @@ void lanes_pack(const uint8_t* enc, uint32_t cap, const uint32_t* lens, int L, u
                 uint8_t* payload, uint64_t payload_cap, unsigned long long* total, uint64_t* offs,
                 int* status, cudaStream_t st);
 
+// ---- the reference's fp32 operator API, bit-exact (tensor_ops.cu) --------
+void matmul_exact(const float* a, const float* b, float* c, int m, int k, int p, cudaStream_t st);
+void softmax_rows_exact(const float* x, float* y, int m, int k, cudaStream_t st);
+void rmsnorm_exact(const float* x, const float* g, int d, float* out, int rows, cudaStream_t st);
+void swiglu_exact(const float* x, const float* wg, const float* wu, const float* wd, int d, int f,
+                  float* h_scratch, float* out, cudaStream_t st);
+void conv2d_exact(const float* x, int c, int h, int w, const float* k, int o, int kh, int kw, int stride,
+                  int pad, float* y, cudaStream_t st);
+void upsample2_chw(const float* x, int c, int h, int w, float* y, cudaStream_t st);
+
 }  // namespace pswa_dev

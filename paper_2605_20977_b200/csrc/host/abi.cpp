@@ -68,6 +68,14 @@ int pswa_synth_latent(const pswa_cfg* cfg, int gop, int frame_idx, int32_t* out)
   });
 }
 
+int pswa_synth_gop(const pswa_cfg* cfg, int gop, int n_frames, int32_t* out) {
+  return guard([&] {
+    pswa_host::validate_cfg(*cfg);
+    if (n_frames < 0) throw std::invalid_argument("n_frames < 0");
+    pswa_host::synth_gop(*cfg, gop, n_frames, out);
+  });
+}
+
 int pswa_gpu_create(int device, const pswa_cfg* cfg, const void* blob, size_t len, pswa_gpu** out) {
   *out = nullptr;
   return guard([&] {
@@ -249,6 +257,25 @@ int pswa_gpu_bench_op(pswa_gpu* h, const char* name, int reps, double* us, doubl
   return guard([&] {
     pswa_dev::DeviceScope ds(h->eng->device());
     *us = h->eng->bench_op(name, reps, flops);
+  });
+}
+
+int pswa_gpu_bench_probe(pswa_gpu* h, const char* name, int reps, double* us, double* flops,
+                         double* bytes) {
+  return guard([&] {
+    pswa_dev::DeviceScope ds(h->eng->device());
+    *us = h->eng->bench_op(name, reps, flops, bytes);
+  });
+}
+
+int pswa_gpu_probe_list(pswa_gpu* h, char* out, size_t cap, size_t* len) {
+  return guard([&] {
+    const std::string s = h->eng->probe_list();
+    *len = s.size() + 1;
+    if (out) {
+      if (cap < s.size() + 1) throw std::invalid_argument("probe_list: buffer too small");
+      std::memcpy(out, s.c_str(), s.size() + 1);
+    }
   });
 }
 

@@ -10,6 +10,7 @@
 
 #include "../cuda/check.h"
 #include "abi_util.h"
+#include "pswa/wavefront.h"
 
 namespace pswa_host {
 
@@ -108,6 +109,14 @@ Engine::Engine(int device, const pswa_cfg& cfg, const void* blob, size_t len, in
   alloc_all();
   upload_weights(w);
   pswa_dev::build_cdf_tables(scales_, cdf_, st_);  // Gaussian (hyperprior, and main when prior = 0)
+  {  // probe: the table build into scratch buffers (64 x 258 cumulative + costs + search index)
+    float* ps = dalloc<float>(pswa_dev::kScales);
+    uint32_t* pc = dalloc<uint32_t>(pswa_dev::kCdfWords);
+    Probe pr;
+    pr.op = [ps, pc](cudaStream_t s) { pswa_dev::build_cdf_tables(ps, pc, s); };
+    pr.bytes = pswa_dev::kCdfWords * 4.0;
+    probes_["cdf_build"] = pr;
+  }
   if (D_.c.prior == 1) {
     float* tmp_scales = dalloc<float>(pswa_dev::kScales);
     cdf_main_ = dalloc<uint32_t>(pswa_dev::kCdfWords);
@@ -294,8 +303,12 @@ void Engine::alloc_all() {
               const int dy = kr - qr, dx = kc - qc;
               row[i] = -1;
               if (dy < -3 || dy > 3 || dx < -3 || dx > 3) continue;
-              const int ks = ((kr - 3 + kc - 3) % 4 + 4) % 4;  // band origin = block origin - 3
-              if (t >= 0 && ((mk == 1 && ks > t) || (mk == 2 && ks >= t))) continue;
+              // band origin = block origin - 3 and block origins are 0 mod 4:
+              // band (r, c) has the step of (r + 1, c + 1)
+              if (t >= 0 && mk > 0 &&
+                  !pswa::mask_allows(mk == 1 ? pswa::MaskKind::kSpatialSelf : pswa::MaskKind::kAccumulator,
+                                     pswa::Pos{qr + 1, qc + 1}, pswa::Pos{kr + 1, kc + 1}, 4))
+                continue;
               row[i] = static_cast<int8_t>((dy + 3) * 7 + dx + 3);
               any = true;
             }
@@ -887,6 +900,7 @@ void Engine::run_stack3d(Program& P, const Block* blocks, int nblocks, int S, co
       e.split_n = d;
       e.row_map2 = ctx_kv_map_;
       gemm(P, ctx_xn_, d, n, B.wqkv, d, e);
+      if (b == 0 && probe) tag(P, std::string(probe) + "_wqkv", 2.0 * n * 3.0 * d * d);
       if (exchange_kv) exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
     } else {  // last block: K/V of every slot, queries of the last slot only
       GemmEpi ekv = rms_in(f16_out(kv, 2 * d), ctx_ssq_);
@@ -913,14 +927,17 @@ void Engine::build_ctx(Program& P) {
   add(P, [=, this](cudaStream_t s) {
     pswa_dev::fill_context_slots(ring_ptrs_, slot_src_, pad_, T, HWo, d, ctx_x_, s);
   });
+  tag(P, "fill_slots", 0.0, 2.0 * n * d * 4.0);  // ring rows in, T slots out (fp32)
   // block 0 norm1 inputs; later norms come out of the residual GEMMs
   add(P, [=, this](cudaStream_t s) {
     pswa_dev::rms_prep(ctx_x_, d, nullptr, n, d, nullptr, 0, ctx_xn_, d, ctx_ssq_, d / 32, s);
   });
+  tag(P, "rms_prep", 0.0, n * (d * (4.0 + 2.0) + (d / 32) * 4.0));  // fp32 in, fp16 + ssq out
   run_stack3d(P, ctx_, D.c.ctx_blocks, T, tiles_ctx_, true, "ctx");
   const float* last = ctx_x_ + static_cast<size_t>(T - 1) * HWo * d;
   __half* c16 = ctx16_ + static_cast<size_t>(B_.own0) * D.W * d;
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(last, d, nullptr, HWo, d, d, ctx_gout_, c16, d, s); });
+  tag(P, "rmsnorm", 0.0, static_cast<double>(HWo) * d * (4.0 + 2.0));
   exchange(P, kXidCtx16, kXAll);  // band mode: normed context of the boundary rows
   // cross-attention K/V of every cross block, once per frame (K7), over the
   // whole local grid (own rows + the halo received above)
@@ -987,6 +1004,7 @@ void Engine::build_hyper_decode(Program& P) {
     w *= 2;
     const int oh = h, ow = w;
     add(P, [=, this](cudaStream_t s) { pswa_dev::im2col3x3(out, oh, ow, hc, 1, 0, hcol_, D.kconv, s); });
+    if (j == 1) tag(P, "im2col", 0.0, static_cast<double>(oh) * ow * (hc * 4.0 + D.kconv * 2.0));
     GemmEpi e1;
     e1.out = hh_;
     e1.ld_out = hc;
@@ -995,6 +1013,7 @@ void Engine::build_hyper_decode(Program& P) {
     e1.act = kActSilu;
     e1.n_store = hc;
     gemm(P, hcol_, D.kconv, oh * ow, hd_c_[j][0], D.kconv, e1);
+    if (j == 1) tag(P, "hd_conv", 2.0 * oh * ow * hc * 9.0 * hc);
     add(P, [=, this](cudaStream_t s) { pswa_dev::im2col3x3(hh_, oh, ow, hc, 1, 0, hcol_, D.kconv, s); });
     GemmEpi e2 = f32_acc(out, hc, hc);  // RB-up: out = up2(x) + conv(silu(conv(up2(x))))
     e2.bias = hd_b_[j][1];
@@ -1013,6 +1032,7 @@ void Engine::build_hyper_decode(Program& P) {
   e.bias_first = 1;
   e.row_map = crop_rows_;  // crop the padded hyper grid to the latent grid
   gemm(P, hcast_, D.hcp, np, hd_out_, D.hcp, e);
+  tag(P, "hq_out", 2.0 * np * D.d * hc);
 }
 
 void Engine::build_hyper_encode(Program& P) {
@@ -1065,6 +1085,7 @@ void Engine::build_embed(Program& P, const StepBatch& bt) {
   e.bias = emb_b_;
   e.row_map = bt.rows;
   gemm(P, y16_, D.C, bt.M, emb_w_, D.C, e);
+  if (bt.parts.size() == 1 && bt.parts[0][0] == D.c.s - 1) tag(P, "embed", 2.0 * bt.M * D.d * D.C);
 }
 
 void Engine::build_s1(Program& P, const StepBatch& bt, bool encoder) {
@@ -1101,6 +1122,7 @@ void Engine::build_acc_q_all(Program& P) {
     pswa_dev::rms_prep(hq_, d, rows, M, d, nullptr, 0, qall16_, d, qall_ssq_, d / 32, s);
   });
   gemm(P, qall16_, d, M, acc_.wq, d, rms_in(f16_out(qall_, d), qall_ssq_));
+  tag(P, "acc_q", 2.0 * M * d * d);
 }
 
 void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
@@ -1139,6 +1161,7 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
   ep.ld_out = dchp;
   ep.out_f32 = 1;
   gemm(P, bs2n_, d, M, ch_proj_, d, ep);
+  if (mode == 0 && bt.parts[0][0] == 0) tag(P, "ch_proj", 2.0 * M * (D.N * sl) * d);
   for (int g = 0; g < N; ++g) {
     float* xg = chx_ + g * sp;
     if (g >= 1)  // channel shift: slot g sees y_hat group g-1
@@ -1246,6 +1269,8 @@ Program& Engine::program(const std::string& key) {
       pswa_dev::lanes_decode_hyper(d_hyper_, hlanes_, Lz, nz, D.zh * D.zw, cur_loc_, cur_scale_,
                                    scales_, cdf_, zhat_, status_, s);
     });
+    // replayable as a pair only (the decode consumes the lanes the init sets up)
+    tag(P, "decode_hyper", 0.0, 0.0, 2);
     add(P, [=, this](cudaStream_t s) { pswa_dev::sum_lane_bits(hlanes_, Lz, bits_, s); });
     build_hyper_decode(P);
     build_acc_q_all(P);
@@ -1260,6 +1285,7 @@ Program& Engine::program(const std::string& key) {
     add(P, [=, this](cudaStream_t s) {
       pswa_dev::lanes_init(d_main_, d_lens_ + 1, L, static_cast<uint32_t>(HW) * C, lanes_, status_, s);
     });
+    tag(P, "lanes_init", 0.0, L * (4.0 + 6.0 + sizeof(pswa_dev::LaneState)));
     for (int t = 0; t < D.c.s; ++t) {
       if (t > 0) build_s1(P, batch_of(t - 1), false);
       build_step(P, batch_of(t), 0);
@@ -1401,8 +1427,24 @@ void Engine::run_host_copy(Program& P, int32_t* yhat_out) {
 }
 
 // ------------------------------------------------------------ probes ------
-void Engine::tag(Program& P, const std::string& name, double flops) {
-  probes_[name] = {P.ops.back(), flops};
+void Engine::tag(Program& P, const std::string& name, double flops, double bytes, int nops) {
+  std::vector<std::function<void(cudaStream_t)>> ops(P.ops.end() - nops, P.ops.end());
+  Probe pr;
+  pr.op = nops == 1 ? ops[0] : [ops](cudaStream_t s) {
+    for (auto& o : ops) o(s);
+  };
+  pr.flops = flops;
+  pr.bytes = bytes;
+  pr.launches = nops;
+  probes_[name] = std::move(pr);
+}
+
+std::string Engine::probe_list() const {
+  std::string out;
+  for (const auto& [name, p] : probes_)
+    out += name + " " + std::to_string(p.flops) + " " + std::to_string(p.bytes) + " " +
+           std::to_string(p.launches) + "\n";
+  return out;
 }
 
 // Algorithmic attention FLOPs of one launch: 4 * d per (query, allowed key)
@@ -1430,11 +1472,18 @@ double Engine::attn_flops(int t, int mask, int slots) const {
   return 4.0 * D.d * keys;
 }
 
-double Engine::bench_op(const std::string& name, int reps, double* flops) {
+double Engine::bench_op(const std::string& name, int reps, double* flops, double* bytes) {
   auto it = probes_.find(name);
   if (it == probes_.end())
     throw std::invalid_argument("bench_op: unknown probe (run a decode first): " + name);
-  auto& op = it->second.first;
+  auto& op = it->second.op;
+  if (reps <= 0) {  // one bare replay (profilers capture exactly this launch)
+    op(st_);
+    PSWA_CUDA(cudaStreamSynchronize(st_));
+    if (flops) *flops = it->second.flops;
+    if (bytes) *bytes = it->second.bytes;
+    return 0.0;
+  }
   for (int i = 0; i < 3; ++i) op(st_);
   cudaEvent_t a, b;
   PSWA_CUDA(cudaEventCreate(&a));
@@ -1447,8 +1496,9 @@ double Engine::bench_op(const std::string& name, int reps, double* flops) {
   PSWA_CUDA(cudaEventElapsedTime(&ms, a, b));
   cudaEventDestroy(a);
   cudaEventDestroy(b);
-  if (flops) *flops = it->second.second;
-  return 1e3 * ms / reps;  // us per launch
+  if (flops) *flops = it->second.flops;
+  if (bytes) *bytes = it->second.bytes;
+  return 1e3 * ms / reps;  // us per replay
 }
 
 // ------------------------------------------------------------ band mode ---

@@ -180,7 +180,9 @@ class Engine {
   // "ctx_attn" (context block 0 attention), "ctx_ffn_gu" (its SwiGLU gate|up
   // GEMM), "step_attn" / "step_wq" (S2 block 0, last step). Returns us per
   // launch; *flops = the algorithmic FLOPs of one launch.
-  double bench_op(const std::string& name, int reps, double* flops);
+  double bench_op(const std::string& name, int reps, double* flops, double* bytes = nullptr);
+  // "name flops bytes launches" per line, every probe of the last-built programs
+  std::string probe_list() const;
   // Debug taps (filled by forward_params): ctx, emb, hq, s1 (padded grid),
   // a, s2. Returns the byte size; copies when out != nullptr.
   size_t debug_fetch(const std::string& name, void* out, size_t cap);
@@ -236,9 +238,16 @@ class Engine {
   void join_side(Program& P);
   cudaStream_t side_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
-  void tag(Program& P, const std::string& name, double flops);
+  // Registers the last op of P (or the last `nops` ops) as bench probe
+  // `name` with its algorithmic FLOPs and HBM bytes per replay.
+  void tag(Program& P, const std::string& name, double flops, double bytes = 0.0, int nops = 1);
+  struct Probe {
+    std::function<void(cudaStream_t)> op;
+    double flops = 0.0, bytes = 0.0;
+    int launches = 1;
+  };
   double attn_flops(int t, int mask, int slots) const;  // t < 0: 3D over `slots` slots
-  std::map<std::string, std::pair<std::function<void(cudaStream_t)>, double>> probes_;
+  std::map<std::string, Probe> probes_;
   void set_frame_params(int rate, int fidx);
   void advance_ring();
   // band mode: push the halo rows of exchange buffer `id` (kind: step t in

@@ -302,14 +302,16 @@ WeightMap parse_psww(const pswa_cfg& c, const void* blob, size_t n) {
   return m;
 }
 
-void synth_latent(const pswa_cfg& c, int gop, int frame_idx, int32_t* yhat) {
+// Frames [f_from, f_to] of GOP `gop` (the y random walk is regenerated from
+// frame 0); frame f lands at out[(f - f_from) * C * HW].
+static void synth_frames(const pswa_cfg& c, int gop, int f_from, int f_to, int32_t* out) {
   const int C = c.latent_ch, HW = c.height * c.width, Cg = C / c.n_groups;
   std::vector<float> y(static_cast<size_t>(C) * HW, 0.0f);
   auto laplace = [](pswa::Rng& r, double b) {
     const double u = (static_cast<double>(r.next_u64() >> 40) + 0.5) * 0x1p-24;  // (0,1)
     return u < 0.5 ? b * pswa::det::log(2.0 * u) : -b * pswa::det::log(2.0 * (1.0 - u));
   };
-  for (int f = 0; f <= frame_idx; ++f) {
+  for (int f = 0; f <= f_to; ++f) {
     pswa::Rng r(1000ull + 100ull * static_cast<uint64_t>(gop) + static_cast<uint64_t>(f));
     for (int ch = 0; ch < C; ++ch) {
       const double b = 8.0 / static_cast<double>(1 << (ch / Cg < 30 ? ch / Cg : 30));
@@ -318,15 +320,24 @@ void synth_latent(const pswa_cfg& c, int gop, int frame_idx, int32_t* yhat) {
         v = f == 0 ? static_cast<float>(laplace(r, b)) : v + static_cast<float>(laplace(r, b / 4.0));
       }
     }
+    if (f < f_from) continue;
+    int32_t* yhat = out + static_cast<size_t>(f - f_from) * C * HW;
+    for (size_t i = 0; i < y.size(); ++i) yhat[i] = static_cast<int32_t>(std::nearbyint(y[i]));
+    pswa::Rng e((1000ull + 100ull * static_cast<uint64_t>(gop) + static_cast<uint64_t>(f)) ^ 0x5EEDE5CA9Eull);
+    for (int p = 0; p < HW; ++p)
+      if (e.next_u64() % 10000 == 0) {
+        const int ch = static_cast<int>(e.next_u64() % static_cast<uint64_t>(C));
+        yhat[static_cast<size_t>(ch) * HW + p] = (e.next_u64() & 1) ? 300 : -300;
+      }
   }
-  for (size_t i = 0; i < y.size(); ++i) yhat[i] = static_cast<int32_t>(std::nearbyint(y[i]));
-  pswa::Rng e((1000ull + 100ull * static_cast<uint64_t>(gop) + static_cast<uint64_t>(frame_idx)) ^
-              0x5EEDE5CA9Eull);
-  for (int p = 0; p < HW; ++p)
-    if (e.next_u64() % 10000 == 0) {
-      const int ch = static_cast<int>(e.next_u64() % static_cast<uint64_t>(C));
-      yhat[static_cast<size_t>(ch) * HW + p] = (e.next_u64() & 1) ? 300 : -300;
-    }
+}
+
+void synth_latent(const pswa_cfg& c, int gop, int frame_idx, int32_t* yhat) {
+  synth_frames(c, gop, frame_idx, frame_idx, yhat);
+}
+
+void synth_gop(const pswa_cfg& c, int gop, int n_frames, int32_t* out) {
+  if (n_frames > 0) synth_frames(c, gop, 0, n_frames - 1, out);
 }
 
 }  // namespace pswa_host

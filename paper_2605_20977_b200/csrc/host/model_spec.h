@@ -53,5 +53,7 @@ WeightMap parse_psww(const pswa_cfg& c, const void* blob, size_t n);
 // b_g = 8 / 2^g, drifting by Laplace(0, b_g/4) per P-frame, 1 in 10^4
 // positions forced to +-300 (escape path), y_hat = round-half-even(y).
 void synth_latent(const pswa_cfg& c, int gop, int frame_idx, int32_t* yhat_chw);
+// frames 0..n_frames-1 of GOP `gop` in one pass: out[f][C][H][W]
+void synth_gop(const pswa_cfg& c, int gop, int n_frames, int32_t* out);
 
 }  // namespace pswa_host

@@ -208,6 +208,14 @@ class OracleModel:
         return y, bits, ph.value
 
 
+def synth_gop(cfg: dict, gop: int, n_frames: int) -> np.ndarray:
+    """The oracle's restatement of the synthetic latent generator (SURVEY
+    §8(d)): frames 0..n_frames-1 of GOP `gop`, [F][C][H][W] int32."""
+    y = np.zeros((n_frames, cfg["latent_ch"], cfg["height"], cfg["width"]), np.int32)
+    assert oracle().oracle_synth_gop(cfg_array(cfg), gop, n_frames, ptr(y)) == 0
+    return y
+
+
 def encode_lanes(v: np.ndarray, idx: np.ndarray, lanes: int) -> bytes:
     v = np.ascontiguousarray(v, np.int32)
     idx = np.ascontiguousarray(idx, np.int32)

