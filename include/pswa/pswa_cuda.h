@@ -148,12 +148,14 @@ int pswa_gpu_decode_frame_device(pswa_gpu* h, const void* d_hyper, size_t hyper_
                                  const void* d_main, size_t main_len, int rate_idx,
                                  int frame_idx_in_gop, int advance_state, void* d_yhat_out);
 /* Asynchronous variant: enqueues the decode on the handle's stream and
- * returns; pswa_gpu_finish() waits and reports the status and bits. Handles
- * on separate streams then overlap on one GPU (independent GOPs, BASELINE
- * config 4). The temporal ring is not advanced. */
+ * returns; handles on separate streams overlap on one GPU (independent GOPs,
+ * BASELINE config 4). With advance_state the temporal ring takes the frame on
+ * the stream, so a GOP is queued frame after frame (call reset_gop at GOP
+ * starts). pswa_gpu_finish() waits, reports PSWA_E_TRUNCATED if ANY frame
+ * queued since the previous finish failed, and the last frame's bits. */
 int pswa_gpu_decode_frame_async(pswa_gpu* h, const void* d_hyper, size_t hyper_len,
                                 const void* d_main, size_t main_len, int rate_idx,
-                                int frame_idx_in_gop, void* d_yhat_out);
+                                int frame_idx_in_gop, int advance_state, void* d_yhat_out);
 int pswa_gpu_finish(pswa_gpu* h, double* bits_out /* [2], nullable */);
 /* Intermediate activations of the last forward_params call, for parity
  * triage: "ctx", "emb", "hq", "a" (fp32 / fp16 [H*W][d]) and "s1" (fp16, padded

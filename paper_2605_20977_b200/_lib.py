@@ -59,7 +59,7 @@ _SIGS = {
     "pswa_gpu_bench_op": (_I, [_VP, C.c_char_p, _I, _D, _D]),
     "pswa_gpu_bench_probe": (_I, [_VP, C.c_char_p, _I, _D, _D, _D]),
     "pswa_gpu_probe_list": (_I, [_VP, C.c_char_p, _SZ, C.POINTER(_SZ)]),
-    "pswa_gpu_decode_frame_async": (_I, [_VP, _VP, _SZ, _VP, _SZ, _I, _I, _VP]),
+    "pswa_gpu_decode_frame_async": (_I, [_VP, _VP, _SZ, _VP, _SZ, _I, _I, _I, _VP]),
     "pswa_gpu_finish": (_I, [_VP, _D]),
     "pswa_gpu_op_gemm_f16": (_I, [_VP, _I, _I, _VP, _I, _I, _I, _VP, _I, _I, _I, _VP, _VP, _I,
                                   _I, _VP]),

@@ -196,9 +196,9 @@ class GpuCodec:
                                                  rate, fidx, int(advance), d_out))
 
     def decode_async(self, d_hyper: int, hyper_len: int, d_main: int, main_len: int, rate: int,
-                     fidx: int, d_out: int):
+                     fidx: int, d_out: int, advance: bool = False):
         check(lib().pswa_gpu_decode_frame_async(self.h, d_hyper, hyper_len, d_main, main_len,
-                                                rate, fidx, d_out))
+                                                rate, fidx, int(advance), d_out))
 
     def finish(self):
         bits = np.zeros(2, np.float64)

@@ -840,6 +840,19 @@ void lanes_encode(const int32_t* sym_v, const uint8_t* sym_idx, uint64_t n, int 
   PSWA_LAUNCH_CHECK();
 }
 
+namespace {
+__global__ void accumulate_status_kernel(const int* status, int* sticky) {
+  pdl_wait();
+  pdl_trigger();
+  if (*status) atomicOr(sticky, *status);
+}
+}  // namespace
+
+void accumulate_status(const int* status, int* sticky, cudaStream_t st) {
+  launch_k(accumulate_status_kernel, dim3(1), dim3(1), 0, st, status, sticky);
+  PSWA_LAUNCH_CHECK();
+}
+
 void sum_lane_bits(const LaneState* lanes, int L, double* out, cudaStream_t st) {
   launch_k(sum_bits_kernel, dim3(1), dim3(256), 0, st, &lanes[0].bits, static_cast<int>(sizeof(LaneState) / 8), L,
                                      out);

@@ -65,7 +65,8 @@ __device__ __forceinline__ void epi_values(const GemmEpi& ep, int n0, float (&v)
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       b[j] = ep.bias ? ep.bias[n0 + j] : 0.0f;
-      sc[j] = ep.scale ? ep.scale[n0 + j] : 1.0f;
+      // the rate scales cover the mu columns only (sigma columns read none)
+      sc[j] = (ep.scale && n0 + j < ep.split) ? ep.scale[n0 + j] : 1.0f;
     }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
@@ -453,6 +454,287 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------ GEMM chain --
+// See gemm.h (gemm_chain_*). One persistent CTA per SM, BN = 128, the warp
+// roles of gemm_tc_kernel; the tile sequence is the concatenation of the jobs'
+// tiles (each N-fastest) handed out by an atomic counter through a 4-deep
+// smem queue shared by the producer, the MMA warp and the epilogue warps.
+constexpr int kChBN = 128;
+constexpr int kChStages = 6;
+constexpr int kChQ = 4;
+struct ChainJobDev {
+  CUtensorMap ta, tb;
+  GemmEpi ep;
+  int M, K, tiles_m, tiles_n, kind, first;
+};
+struct ChainArgs {
+  ChainJobDev job[kChainMaxJobs];
+  int njobs, total, ctr_stride;
+  unsigned* ctr;  // [kChainMaxJobs][ctr_stride] row-block completions, then tile counter, done
+};
+constexpr int kChABytes = kBM * kBK * 2, kChBBytes = kChBN * kBK * 2;
+constexpr int kChStageBytes = kChABytes + kChBBytes;
+constexpr int kChSmem = kChStages * kChStageBytes + 1024 + 512;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// job index of global tile t
+__device__ __forceinline__ int chain_job_of(const ChainArgs& a, int t) {
+  int j = 0;
+#pragma unroll
+  for (int k = 1; k < kChainMaxJobs; ++k)
+    if (k < a.njobs && t >= a.job[k].first) j = k;
+  return j;
+}
+
+// Spin until every tile of row block mb of job j - 1 has been stored.
+__device__ __forceinline__ void chain_wait_dep(const ChainArgs& a, int j, int mb) {
+  if (j == 0) return;
+  const unsigned* c = a.ctr + (j - 1) * a.ctr_stride + mb;
+  const unsigned need = static_cast<unsigned>(a.job[j - 1].tiles_n);
+  while (ld_acquire_u32(c) < need) {
+  }
+}
+
+template <int EPI>
+__device__ __forceinline__ void chain_epi_tile(const GemmEpi& ep, int M, int m0, int n0, int q, int half,
+                                               int lane, uint32_t acc, uint64_t* tempty_buf) {
+  const int c0 = half * (kChBN / 64), c1 = (half + 1) * (kChBN / 64);
+  const int m = m0 + q * 32 + lane;
+  const bool side2 = ep.out2 != nullptr && n0 >= ep.split_n;
+  const int* rmap = side2 ? ep.row_map2 : ep.row_map;
+  const int orow = m < M ? (rmap ? rmap[m] : m) : -1;
+  float4 resA[8], resB[8];
+  const bool acc_res = EPI == kEpiF32 && ep.accumulate;
+  if (acc_res) {
+    prefetch_residual(ep, orow, n0 + c0 * 32, resA);
+    if (c0 + 1 < c1) prefetch_residual(ep, orow, n0 + (c0 + 1) * 32, resB);
+  }
+  float row_scale = 1.0f;
+  if (ep.rms_ssq && m < M) {
+    const float* sp = ep.rms_ssq + static_cast<size_t>(m) * ep.ld_rms;
+    float ss = 0.0f;
+    if ((ep.rms_parts & 3) == 0 && (ep.ld_rms & 3) == 0) {
+      for (int k = 0; k < ep.rms_parts; k += 4) {
+        const float4 q4 = *reinterpret_cast<const float4*>(sp + k);
+        ss += q4.x;
+        ss += q4.y;
+        ss += q4.z;
+        ss += q4.w;
+      }
+    } else {
+      for (int k = 0; k < ep.rms_parts; ++k) ss += sp[k];
+    }
+    row_scale = 1.0f / sqrtf(ss * ep.rms_inv_d + 1e-5f);
+  }
+  auto chunk = [&](int c, float4 (&res)[8]) {
+    uint32_t raw[32];
+    tmem_ld_32x32(acc + c * 32, raw);
+    tc_wait_ld();
+    if (c + 1 == c1) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_buf);
+    }
+    epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res, row_scale, side2);
+    if (acc_res && c + 2 < c1) prefetch_residual(ep, orow, n0 + (c + 2) * 32, res);
+  };
+#pragma unroll 1
+  for (int c = c0; c < c1; c += 2) {
+    chunk(c, resA);
+    if (c + 1 < c1) chunk(c + 1, resB);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_constant__ ChainArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kChStages * kChABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kChStages * kChStageBytes);
+  uint64_t* empty = full + kChStages;
+  uint64_t* tfull = empty + kChStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* qfull = tempty + 2;
+  uint64_t* qempty = qfull + kChQ;
+  int* tq = reinterpret_cast<int*>(qempty + kChQ);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + kChQ);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned* tile_ctr = a.ctr + kChainMaxJobs * a.ctr_stride;
+  unsigned* done_ctr = tile_ctr + 1;
+
+  if (warp == 0 && lane == 0) {
+    for (int j = 0; j < a.njobs; ++j) {
+      tma_prefetch(&a.job[j].ta);
+      tma_prefetch(&a.job[j].tb);
+    }
+    for (int s = 0; s < kChStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpiWarps);
+    }
+    for (int i = 0; i < kChQ; ++i) {
+      mbar_init(&qfull[i], 1);
+      mbar_init(&qempty[i], 1 + kEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * kChBN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // the tile counter is reset by the previous launch of this op at its very
+  // end: it may only be touched after the PDL wait (back-to-back replays of
+  // one chain op, e.g. pswa_gpu_bench_probe, would otherwise steal tiles)
+  pdl_wait();
+  pdl_trigger();
+  int t_first = -1, npre = 0;
+  if (warp == 0 && lane == 0) {
+    t_first = static_cast<int>(atomicAdd(tile_ctr, 1u));
+    if (t_first < a.total) {
+      const ChainJobDev& J = a.job[chain_job_of(a, t_first)];
+      const int u = t_first - J.first;
+      npre = min(kChStages, J.K / kBK);
+      for (int kb = 0; kb < npre; ++kb) {
+        mbar_expect_tx(&full[kb], kChStageBytes);
+        tma_load_2d(sb + kb * kChBBytes, &J.tb, &full[kb], kb * kBK, (u % J.tiles_n) * kChBN);
+      }
+    }
+  }
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0;
+      for (int i = 0;; ++i) {
+        const int slot = i % kChQ;
+        if (i >= kChQ) mbar_wait(&qempty[slot], ((i / kChQ) - 1) & 1);
+        const int t = i == 0 ? t_first : static_cast<int>(atomicAdd(tile_ctr, 1u));
+        const bool valid = t < a.total;
+        tq[slot] = valid ? t : -1;
+        mbar_arrive(&qfull[slot]);
+        if (!valid) break;
+        const int j = chain_job_of(a, t);
+        const ChainJobDev& J = a.job[j];
+        const int u = t - J.first, m0 = (u / J.tiles_n) * kBM, n0 = (u % J.tiles_n) * kChBN;
+        const int kblocks = J.K / kBK;
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          const int s = g % kChStages, round = g / kChStages;
+          if (g < npre) {  // first tile: B already requested
+            if (kb == 0) {
+              chain_wait_dep(a, j, m0 / kBM);
+              fence_proxy_async_global();
+            }
+            tma_load_2d(sa + s * kChABytes, &J.ta, &full[s], kb * kBK, m0);
+            continue;
+          }
+          if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+          mbar_expect_tx(&full[s], kChStageBytes);
+          tma_load_2d(sb + s * kChBBytes, &J.tb, &full[s], kb * kBK, n0);
+          if (kb == 0) {  // weights first, then wait for the rows this tile reads
+            chain_wait_dep(a, j, m0 / kBM);
+            fence_proxy_async_global();
+          }
+          tma_load_2d(sa + s * kChABytes, &J.ta, &full[s], kb * kBK, m0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_f16_f32(kBM, kChBN);
+      int g = 0;
+      for (int i = 0;; ++i) {
+        const int slot = i % kChQ;
+        mbar_wait(&qfull[slot], (i / kChQ) & 1);
+        const int t = tq[slot];
+        mbar_arrive(&qempty[slot]);
+        if (t < 0) break;
+        const ChainJobDev& J = a.job[chain_job_of(a, t)];
+        const int buf = i & 1, use = i >> 1;
+        if (use > 0) mbar_wait(&tempty[buf], (use - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * kChBN;
+        const int kblocks = J.K / kBK;
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          const int s = g % kChStages;
+          mbar_wait(&full[s], (g / kChStages) & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sa + s * kChABytes);
+          const uint32_t b_base = smem_u32(sb + s * kChBBytes);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            tc_mma_f16(acc, umma_desc_k_sw128(a_base + kk * 32), umma_desc_k_sw128(b_base + kk * 32), idesc,
+                       (kb | kk) != 0 ? 1u : 0u);
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    const int ew = warp - 2, q = warp & 3, half = ew >> 2;
+    for (int i = 0;; ++i) {
+      const int slot = i % kChQ;
+      mbar_wait(&qfull[slot], (i / kChQ) & 1);
+      const int t = tq[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty[slot]);
+      if (t < 0) break;
+      const int j = chain_job_of(a, t);
+      const ChainJobDev& J = a.job[j];
+      const int u = t - J.first, m0 = (u / J.tiles_n) * kBM, n0 = (u % J.tiles_n) * kChBN;
+      const int buf = i & 1, use = i >> 1;
+      // the epilogue reads the previous job's outputs too (residual rows, the
+      // folded norm's sums of squares): same dependency as the A operand
+      chain_wait_dep(a, j, m0 / kBM);  // every lane acquires before its own reads
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const uint32_t acc = tmem + buf * kChBN + (static_cast<uint32_t>(q * 32) << 16);
+      switch (J.kind) {
+        case kEpiF16: chain_epi_tile<kEpiF16>(J.ep, J.M, m0, n0, q, half, lane, acc, &tempty[buf]); break;
+        case kEpiF32: chain_epi_tile<kEpiF32>(J.ep, J.M, m0, n0, q, half, lane, acc, &tempty[buf]); break;
+        case kEpiSwiGLU: chain_epi_tile<kEpiSwiGLU>(J.ep, J.M, m0, n0, q, half, lane, acc, &tempty[buf]); break;
+        default: chain_epi_tile<kEpiHead>(J.ep, J.M, m0, n0, q, half, lane, acc, &tempty[buf]); break;
+      }
+      // every epilogue warp's stores of this tile, then one release increment
+      named_bar_sync(1, 32 * kEpiWarps);
+      if (ew == 0 && lane == 0) {
+        __threadfence();
+        atomicAdd(a.ctr + j * a.ctr_stride + m0 / kBM, 1u);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free(tmem, 2 * kChBN);
+  }
+  if (threadIdx.x == 0) {  // the last CTA out resets the counters for the next replay
+    __threadfence();
+    if (atomicAdd(done_ctr, 1u) == gridDim.x - 1) {
+      for (int k = 0; k < kChainMaxJobs * a.ctr_stride; ++k) a.ctr[k] = 0u;
+      *tile_ctr = 0u;
+      *done_ctr = 0u;
+      __threadfence();
+    }
+  }
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -639,6 +921,51 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   if (bn == 64) prep<64>(kind);
   if (bn == 128) prep<128>(kind);
   if (bn == 256) prep<256>(kind);
+}
+
+int gemm_chain_counter_words(int M) { return kChainMaxJobs * ((M + kBM - 1) / kBM) + 2; }
+
+void gemm_chain_add(GemmChainPlan* c, const __half* A, int lda, int M, const __half* B, int ldb, int N,
+                    int K, const GemmEpi& epi) {
+  if (c->njobs >= kChainMaxJobs) throw std::invalid_argument("gemm_chain_add: too many jobs");
+  if (N % kChBN != 0) throw std::invalid_argument("gemm_chain_add: N % 128 != 0");
+  if (c->njobs > 0 && c->job[0].M != M) throw std::invalid_argument("gemm_chain_add: M differs");
+  if (epi.act == kActTanhHalf) throw std::invalid_argument("gemm_chain_add: unsupported activation");
+  gemm_plan(&c->job[c->njobs], A, lda, M, B, ldb, N, K, epi, kChBN);
+  c->ctr_stride = (M + kBM - 1) / kBM;
+  ++c->njobs;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    PSWA_CUDA(cudaFuncSetAttribute(gemm_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kChSmem));
+  });
+}
+
+void gemm_chain_run(const GemmChainPlan& c, cudaStream_t stream) {
+  if (c.njobs == 0) return;
+  if (!c.counters) throw std::invalid_argument("gemm_chain_run: no counters");
+  ChainArgs a{};
+  int first = 0;
+  for (int j = 0; j < c.njobs; ++j) {
+    const GemmPlan& p = c.job[j];
+    ChainJobDev& d = a.job[j];
+    d.ta = p.ta;
+    d.tb = p.tb;
+    d.ep = p.epi;
+    d.M = p.M;
+    d.K = p.K;
+    d.tiles_m = (p.M + kBM - 1) / kBM;
+    d.tiles_n = p.N / kChBN;
+    d.kind = epi_kind(p.epi);
+    d.first = first;
+    first += d.tiles_m * d.tiles_n;
+  }
+  a.njobs = c.njobs;
+  a.total = first;
+  a.ctr_stride = c.ctr_stride;
+  a.ctr = c.counters;
+  const int grid = first < sm_count() ? first : sm_count();
+  launch_k(gemm_chain_kernel, dim3(grid), dim3(kThreads), kChSmem, stream, a);
+  PSWA_LAUNCH_CHECK();
 }
 
 void gemm_run(const GemmPlan& p, cudaStream_t stream) {

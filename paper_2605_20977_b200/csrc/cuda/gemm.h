@@ -75,6 +75,30 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
                int K, const GemmEpi& epi, int force_bn = 0);
 void gemm_run(const GemmPlan& p, cudaStream_t stream);
 
+// A chain of dependent GEMMs in ONE persistent launch (the S1/S2 block
+// tail: out-projection + residual -> SwiGLU gate|up -> down + residual -> the
+// next block's Q|K|V). Job j+1 reads rows of job j's outputs: its 128-row
+// block m starts as soon as every tile of block m of job j is stored
+// (per-block completion counters in global memory, acquire/release), so the
+// jobs overlap as a wavefront over the row blocks instead of draining the GPU
+// between launches. Tiles are handed out by an atomic counter in chain order,
+// so a tile only ever waits on tiles already taken by running CTAs (no
+// deadlock whatever else shares the GPU). Every job uses BN = 128; per-output
+// reduction order is that of gemm_run (ascending 64-wide K blocks), so the
+// results are bitwise those of the separate launches.
+constexpr int kChainMaxJobs = 4;
+struct GemmChainPlan {
+  int njobs = 0;
+  GemmPlan job[kChainMaxJobs];
+  unsigned* counters = nullptr;  // device, >= gemm_chain_counter_words(), zeroed once
+  int ctr_stride = 0;            // row blocks per job slot
+};
+int gemm_chain_counter_words(int M);
+// Adds a job (same M as the chain's first job); B K-major [N][ldb], N % 128 == 0.
+void gemm_chain_add(GemmChainPlan* c, const __half* A, int lda, int M, const __half* B, int ldb, int N,
+                    int K, const GemmEpi& epi);
+void gemm_chain_run(const GemmChainPlan& c, cudaStream_t stream);
+
 // TMA map of a frame K/V cache [slots][H][W][ld] fp16 for the attention halo
 // loads: box = 32 channels (one head) x box_w x box_h x 1 slot, SWIZZLE_64B.
 void make_kv_tmap(CUtensorMap* m, const __half* kv, int ld, int W, int H, int slots,

@@ -185,11 +185,11 @@ int pswa_gpu_decode_frame_device(pswa_gpu* h, const void* d_hyper, size_t hyper_
 
 int pswa_gpu_decode_frame_async(pswa_gpu* h, const void* d_hyper, size_t hyper_len,
                                 const void* d_main, size_t main_len, int rate_idx,
-                                int frame_idx_in_gop, void* d_yhat_out) {
+                                int frame_idx_in_gop, int advance_state, void* d_yhat_out) {
   return guard([&] {
     pswa_dev::DeviceScope ds(h->eng->device());
     h->eng->decode_async(d_hyper, hyper_len, d_main, main_len, rate_idx, frame_idx_in_gop,
-                         static_cast<int32_t*>(d_yhat_out));
+                         static_cast<int32_t*>(d_yhat_out), advance_state != 0);
   });
 }
 

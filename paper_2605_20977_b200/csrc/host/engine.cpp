@@ -243,6 +243,21 @@ void Engine::alloc_all() {
         tl.n_last = static_cast<int>(last.size()) / TI;
         tl.all = up(all);
         tl.last = up(last);
+        if (S == 4 && D.c.win_t >= 4) {  // slot-sharing launch (window_attention_ctx_slots)
+          // one tile per (spatial tile, group of QS query slots), the group
+          // with the most key slots first (heaviest tiles lead the launch)
+          const int qs = pswa_dev::ctx_slot_group();
+          const auto base = ctx_tiles(0, 0, 1);
+          std::vector<int> sl;
+          for (int qb = S - qs; qb >= 0; qb -= qs)
+            for (size_t t0 = 0; t0 < base.size(); t0 += TI) {
+              std::vector<int> t(base.begin() + t0, base.begin() + t0 + TI);
+              t[3] = qb;
+              sl.insert(sl.end(), t.begin(), t.end());
+            }
+          tl.n_slots = static_cast<int>(sl.size()) / TI;
+          tl.slots = up(sl);
+        }
       };
       make(T, tiles_ctx_);
       if (D.c.lrp_blocks > 0) make(T + 1, tiles_lrp_);
@@ -450,6 +465,7 @@ void Engine::alloc_all() {
   lanes_ = dalloc<pswa_dev::LaneState>(L);
   hlanes_ = dalloc<pswa_dev::LaneState>(Lz);
   status_ = dalloc<int>(1);
+  sticky_status_ = dalloc<int>(1);
   bits_ = dalloc<double>(2);
   sym_v_ = dalloc<int32_t>(nsym);
   sym_idx_ = dalloc<uint8_t>(nsym);
@@ -677,14 +693,42 @@ void Engine::upload_weights(const WeightMap& w) {
 
 // ----------------------------------------------------- program builders ---
 void Engine::add(Program& P, std::function<void(cudaStream_t)> op, int launches) {
+  flush_chain(P);
   P.ops.push_back(std::move(op));
   P.launches += launches;
+}
+
+void Engine::flush_chain(Program& P) {
+  const int n = chain_.plan.njobs;
+  if (n == 0) return;
+  OpenChain c = std::move(chain_);
+  chain_ = OpenChain{};
+  if (n == 1) {  // a lone GEMM keeps its own tile-width choice
+    const int M = static_cast<int>(reinterpret_cast<intptr_t>(c.jobs[0][2]));
+    const bool was = chaining_;
+    chaining_ = false;
+    gemm(P, static_cast<const __half*>(c.jobs[0][0]), c.lda[0], M, c.B[0], c.K[0], c.epi[0]);
+    chaining_ = was;
+    if (!c.tag.empty()) tag(P, c.tag, c.flops);
+    return;
+  }
+  pswa_dev::GemmChainPlan plan = c.plan;
+  plan.counters = dalloc<unsigned>(pswa_dev::gemm_chain_counter_words(plan.job[0].M));
+  P.ops.push_back([plan](cudaStream_t s) { pswa_dev::gemm_chain_run(plan, s); });
+  P.launches += 1;
+  if (!c.tag.empty()) {  // the whole launch is the probe: FLOPs of its (padded) GEMMs
+    double fl = 0.0;
+    for (int j = 0; j < n; ++j) fl += 2.0 * plan.job[j].M * plan.job[j].N * plan.job[j].K;
+    const std::string base = c.tag.substr(0, c.tag.find('_'));
+    tag(P, base + "_chain", fl);
+  }
 }
 
 // Moves ops [from, end) onto the side stream: a fork (event record on the
 // main stream, wait on the side stream) precedes them; join_side() later
 // makes the main stream wait for the side stream. Both are capturable.
 void Engine::to_side(Program& P, size_t from) {
+  flush_chain(P);
   std::vector<std::function<void(cudaStream_t)>> moved(P.ops.begin() + from, P.ops.end());
   P.ops.resize(from);
   P.ops.push_back([this](cudaStream_t s) {
@@ -695,6 +739,7 @@ void Engine::to_side(Program& P, size_t from) {
 }
 
 void Engine::join_side(Program& P) {
+  flush_chain(P);
   P.ops.push_back([this](cudaStream_t s) {
     PSWA_CUDA(cudaEventRecord(ev_join_, side_));
     PSWA_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
@@ -702,6 +747,19 @@ void Engine::join_side(Program& P) {
 }
 
 void Engine::gemm(Program& P, const __half* A, int lda, int M, const PW& B, int K, const GemmEpi& ep) {
+  if (chaining_ && B.N % 128 == 0 && ep.act != pswa_dev::kActTanhHalf) {
+    if (chain_.plan.njobs == pswa_dev::kChainMaxJobs ||
+        (chain_.plan.njobs > 0 && chain_.plan.job[0].M != M))
+      flush_chain(P);
+    pswa_dev::gemm_chain_add(&chain_.plan, A, lda, M, B.p, B.K, B.N, K, ep);
+    chain_.jobs.push_back({A, B.p, reinterpret_cast<const void*>(static_cast<intptr_t>(M)), nullptr});
+    chain_.lda.push_back(lda);
+    chain_.K.push_back(K);
+    chain_.B.push_back(B);
+    chain_.epi.push_back(ep);
+    return;
+  }
+  flush_chain(P);
   pswa_dev::GemmPlan plan;
   pswa_dev::gemm_plan(&plan, A, lda, M, B.p, B.K, B.N, K, ep);
   add(P, [plan](cudaStream_t s) { pswa_dev::gemm_run(plan, s); });
@@ -739,6 +797,17 @@ GemmEpi swiglu_out(void* out, int ld) {
   return e;
 }
 }  // namespace
+
+// Opt-in (PSWA_CHAIN=1): correct and bitwise equal to the separate launches
+// (tests pass either way), but measured slower on B200 -- one S2 block tail +
+// next Q|K|V as one chain took 47.6 us against 35.6 us for the four tuned
+// launches (BN 256 for the wide gate|up and Q|K|V GEMMs halves their
+// activation re-reads; PDL already hides the launch gaps), 8.21 vs 7.26 ms
+// per frame.
+bool Engine::chain_enabled() {
+  static const bool on = std::getenv("PSWA_CHAIN") != nullptr;
+  return on;
+}
 
 // Folded RMSNorm of channel slot g (sl real columns of sp): the residual
 // epilogue writes the updated slot's fp16 copy to chx16_ [M][sp] and its
@@ -807,6 +876,29 @@ void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq
                                  D.c.win_h, D.c.win_w, wt, mask, D.c.s, bias, out, d, s);
     });
   }
+}
+
+// Context layer over all 4 query slots at once: every key-slot halo is
+// staged once per head and its fragments feed each query slot that reaches it.
+void Engine::attention_ctx_slots(Program& P, const __half* q, const Tiles3d& tl, const __half* kv,
+                                 int S, const float* bias, __half* out) {
+  const Dims& D = D_;
+  const int d = D.d, wt = D.c.win_t;
+  const pswa_dev::AttnShape sh = shape_ctx_;
+  CUtensorMap map;
+  pswa_dev::make_kv_tmap(&map, kv, 2 * d, D.W, B_.Hl, S, HWl_, kCtxHaloW, kCtxHaloRows);
+  __half*& tab = score_tables_[{bias, &shape_ctx_}];
+  if (!tab) {
+    tab = dalloc<__half>(static_cast<size_t>(D.heads) * wt * sh.nbk * 8);
+    pswa_dev::build_score_tables(bias, D.heads, wt, sh, tab, st_);
+  }
+  const __half* tables = tab;
+  const int32_t* tiles = tl.slots;
+  const int ntiles = tl.n_slots, qstride = HWo_;
+  add(P, [=](cudaStream_t s) {
+    pswa_dev::window_attention_ctx_slots(q, d, qstride, tiles, ntiles, kCtxHaloRows, kCtxHaloW, sh, map,
+                                         D.heads, wt, tables, out, d, s);
+  });
 }
 
 // A batch of wavefront-step positions: one step (the decoder's phases) or
@@ -909,8 +1001,16 @@ void Engine::run_stack3d(Program& P, const Block* blocks, int nblocks, int S, co
       if (exchange_kv) exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
       gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, rms_in(f16_out(ctx_q_, d), ssq_q));
     }
-    attention(P, ctx_q_, tl.qinfo + q0, nq, last ? tl.last : tl.all, last ? tl.n_last : tl.n_all,
-              &shape_ctx_, kv, HWl_, D.c.win_t, 0, pos, ctx_att_, S);
+    // slot-sharing context attention: opt-in (PSWA_CTX_SLOTS=1). Measured
+    // slower on B200 than the per-slot launch (129 / 197 us per layer with 2
+    // / 4 query slots per warp vs 118 us): the fragment reuse does not pay
+    // for the lower occupancy and the per-slot bookkeeping
+    static const bool ctx_slots = std::getenv("PSWA_CTX_SLOTS") != nullptr;
+    if (!last && tl.n_slots > 0 && S == 4 && mma_attn_ && ctx_slots)
+      attention_ctx_slots(P, ctx_q_, tl, kv, S, pos, ctx_att_);
+    else
+      attention(P, ctx_q_, tl.qinfo + q0, nq, last ? tl.last : tl.all, last ? tl.n_last : tl.n_all,
+                &shape_ctx_, kv, HWl_, D.c.win_t, 0, pos, ctx_att_, S);
     if (b == 0 && probe) tag(P, std::string(probe) + "_attn", attn_flops(-1, 0, S));
     float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
     __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;
@@ -1095,7 +1195,10 @@ void Engine::build_s1(Program& P, const StepBatch& bt, bool encoder) {
   add(P, [=, this](cudaStream_t s) {  // gather + block 0 norm1 inputs
     pswa_dev::rms_prep(emb_cur_, d, rows, M, d, bx_, d, bxn_, d, bssq_, d / 32, s);
   });
+  chaining_ = chain_enabled() && !encoder;
   for (int b = 0; b < D.c.s1_blocks; ++b) block_step(P, s1_[b], bt);
+  flush_chain(P);
+  chaining_ = false;
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, s1_gout_, bs1n_, d, s); });
   GemmEpi e = f16_out(acc_kv_, 2 * d);
   e.row_map = rows;
@@ -1148,8 +1251,12 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
   const bool taps = mode == 1 && want_musig_;  // debug taps in forward_params only
   if (taps)
     add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f32(bx_, d, rows, M, d, afull_, d, s); });
-  // spatial module 2
+  // spatial module 2 (decoder: each block's GEMM tail and the next block's
+  // projection run as one chained launch)
+  chaining_ = chain_enabled() && mode == 0;
   for (int b = 0; b < D.c.s2_blocks; ++b) block_step(P, s2_[b], bt);
+  flush_chain(P);
+  chaining_ = false;
   add(P, [=, this](cudaStream_t s) { pswa_dev::rmsnorm_rows(bx_, d, nullptr, M, d, d, s2_gout_, bs2n_, d, s); });
   if (taps)
     add(P, [=, this](cudaStream_t s) { pswa_dev::scatter_rows_f16(bs2n_, d, rows, M, d, s2full_, d, s); });
@@ -1233,6 +1340,7 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
       }
     }
     if (mode == 0 && host_copy_ && bt.parts.size() == 1 && bt.parts[0][0] == D.c.s - 1) {
+      flush_chain(P);
       // channel group g of the last step decoded: its CHW planes are final
       const int HWo = HWo_;
       add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_to_chw_cols(yfr_, HWo, C, c0, Cg, ychw_, s); });
@@ -1371,6 +1479,7 @@ Program& Engine::program(const std::string& key) {
   } else {
     throw std::invalid_argument("unknown program " + key);
   }
+  flush_chain(P);
   taps_ = false;
   return P;
 }
@@ -1428,6 +1537,11 @@ void Engine::run_host_copy(Program& P, int32_t* yhat_out) {
 
 // ------------------------------------------------------------ probes ------
 void Engine::tag(Program& P, const std::string& name, double flops, double bytes, int nops) {
+  if (chain_.plan.njobs > 0) {  // a GEMM inside an open chain: the chain launch is the probe
+    if (chain_.tag.empty()) chain_.tag = name;
+    chain_.flops += flops;
+    return;
+  }
   std::vector<std::function<void(cudaStream_t)>> ops(P.ops.end() - nops, P.ops.end());
   Probe pr;
   pr.op = nops == 1 ? ops[0] : [ops](cudaStream_t s) {
@@ -1503,6 +1617,7 @@ double Engine::bench_op(const std::string& name, int reps, double* flops, double
 
 // ------------------------------------------------------------ band mode ---
 void Engine::cut(Program& P, bool global) {
+  flush_chain(P);
   if (B_.n > 1) P.cuts.push_back(Cut{P.ops.size(), global});
 }
 
@@ -1869,22 +1984,25 @@ FrameResult Engine::finish_decode(bool advance, int32_t* yhat_out, bool device, 
 }
 
 void Engine::decode_async(const void* d_hyper, size_t hyper_len, const void* d_main,
-                          size_t main_len, int rate, int fidx, int32_t* d_yhat_out) {
+                          size_t main_len, int rate, int fidx, int32_t* d_yhat_out, bool advance) {
   if (B_.n > 1) throw std::invalid_argument("decode_async: not for band handles");
   prep_decode(d_hyper, hyper_len, d_main, main_len, rate, fidx, true);
   run(program(decode_key(false, stats_on_)));
   have_stats_ = stats_on_;
+  pswa_dev::accumulate_status(status_, sticky_status_, st_);
   PSWA_CUDA(cudaMemcpyAsync(d_yhat_out, ychw_, sizeof(int32_t) * HWo_ * D_.C,
                             cudaMemcpyDeviceToDevice, st_));
+  if (advance) advance_ring();  // stream-ordered copy + host ring indices
 }
 
 FrameResult Engine::finish_async() {
   FrameResult r;
   PSWA_CUDA(cudaMemcpyAsync(r.bits, bits_, sizeof(r.bits), cudaMemcpyDeviceToHost, st_));
-  PSWA_CUDA(cudaMemcpyAsync(&r.status, status_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaMemcpyAsync(&r.status, sticky_status_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  PSWA_CUDA(cudaMemsetAsync(sticky_status_, 0, sizeof(int), st_));
   PSWA_CUDA(cudaStreamSynchronize(st_));
-  if (r.status) throw pswa_abi::TruncatedError("corrupt or truncated payload (status " +
-                                               std::to_string(r.status) + ")");
+  if (r.status) throw pswa_abi::TruncatedError("corrupt or truncated payload in a frame since the "
+                                               "last finish (status " + std::to_string(r.status) + ")");
   return r;
 }
 

@@ -160,8 +160,12 @@ class Engine {
   // Asynchronous device-resident decode (no host sync; ring not advanced):
   // several handles on their own streams overlap on one GPU (GOP batches,
   // BASELINE config 4). finish_async() syncs and checks the status.
+  // advance: the ring takes the frame (on the stream, no host sync), so a
+  // whole GOP can be queued frame after frame. Statuses accumulate until
+  // finish_async(), which reports any failure since the previous finish and
+  // the last frame's bits.
   void decode_async(const void* d_hyper, size_t hyper_len, const void* d_main, size_t main_len,
-                    int rate, int fidx, int32_t* d_yhat_out);
+                    int rate, int fidx, int32_t* d_yhat_out, bool advance = false);
   FrameResult finish_async();
   void prep_encode(const int32_t* yhat_chw_host, int rate, int fidx, const int32_t* zhat_in);
   FrameResult finish_encode(float* mu_out, float* sigma_out, uint8_t* hyper_out, size_t hyper_cap,
@@ -196,6 +200,23 @@ class Engine {
   T* dalloc(size_t n);
   // ---- program building blocks
   void add(Program& P, std::function<void(cudaStream_t)> op, int launches = 1);
+  // GEMM chains (gemm.h gemm_chain_*): while chaining_ is set, consecutive
+  // gemm() calls are collected (each reads the previous one's identity-row
+  // outputs: the S1/S2 block tail out-proj -> gate|up -> down -> next Q|K|V)
+  // and emitted as one persistent launch when any other op is added, at 4
+  // jobs, or by flush_chain(). A chain of one job stays a plain GEMM.
+  bool chaining_ = false;
+  struct OpenChain {
+    pswa_dev::GemmChainPlan plan;
+    std::vector<std::array<const void*, 4>> jobs;  // A, B, M (as pointer-size int), K for re-planning
+    std::vector<int> lda, K;
+    std::vector<PW> B;
+    std::vector<pswa_dev::GemmEpi> epi;
+    std::string tag;
+    double flops = 0.0;
+  } chain_;
+  void flush_chain(Program& P);
+  static bool chain_enabled();
   void gemm(Program& P, const __half* A, int lda, int M, const PW& B, int K,
             const pswa_dev::GemmEpi& ep);
   struct StepBatch {  // positions of one wavefront step, or of all steps (encoder)
@@ -330,7 +351,11 @@ class Engine {
   struct Tiles3d {  // attention work of a 3D stack: all slots / last slot only
     const int32_t *all = nullptr, *last = nullptr, *qinfo = nullptr;
     int n_all = 0, n_last = 0;
+    const int32_t* slots = nullptr;  // slot-0 rows, every query slot per warp (T = 4)
+    int n_slots = 0;
   };
+  void attention_ctx_slots(Program& P, const __half* q, const Tiles3d& tl, const __half* kv,
+                           int S, const float* bias, __half* out);
   Tiles3d tiles_ctx_, tiles_lrp_;
   void run_stack3d(Program& P, const Block* blocks, int nblocks, int S, const Tiles3d& tl,
                    bool exchange_kv, const char* probe);
@@ -374,6 +399,7 @@ class Engine {
   uint32_t lens_h_[2] = {0, 0};  // host staging of d_lens_ (stable address for async copies)
   pswa_dev::LaneState *lanes_ = nullptr, *hlanes_ = nullptr;
   int* status_ = nullptr;
+  int* sticky_status_ = nullptr;  // async frames: statuses OR-ed until finish_async
   double* bits_ = nullptr;  // [2]
   int32_t *sym_v_ = nullptr, *hsym_v_ = nullptr;
   uint8_t *sym_idx_ = nullptr, *hsym_idx_ = nullptr;

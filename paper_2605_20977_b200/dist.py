@@ -59,6 +59,17 @@ def max_over_ranks(value: float, dist=None, device=None) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(value: float, dist=None, device=None) -> float:
+    """Sum of a per-rank scalar (work counts of the whole job)."""
+    if dist is None:
+        return float(value)
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64,
+                     device=device if device is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def barrier(dist=None):
     if dist is not None:
         dist.barrier()

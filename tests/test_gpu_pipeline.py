@@ -257,3 +257,40 @@ def test_laplace_head_roundtrip_and_rate(paper, H, W):
     bits_o = om.encode(y, rate=0, fidx=0, zhat=z)[2]
     compare_params(f"laplace_{'paper' if paper else 'desk'}_{H}x{W}", mu_g, sg_g, mu_o, sg_o,
                    bits_g, bits_o)
+
+
+@pytest.mark.parametrize("big", [2049, 70000, 1 << 30])
+def test_out_of_range_yhat_is_rejected(big):
+    """|y_hat| above kYhatMax = 2048 (the networks read y_hat as fp16, exact
+    to 2^11): the GPU encoder refuses the frame (PSWA_E_ARG), and a stream the
+    fp32 oracle coded with such a value decodes to PSWA_E_TRUNCATED (corrupt
+    for this codec) -- never NaN parameters or a silent mismatch."""
+    c, blob, om, g = setup(False, 16, 16)
+    rng = np.random.default_rng(big % 97)
+    y = laplace_yhat(rng, 192, 16, 16)
+    y[7, 3, 5] = big
+    with pytest.raises(PswaError) as e:
+        g.encode_frame(y, rate=0, fidx=0)
+    assert e.value.code == 1
+    hyper, main, _, _ = om.encode(y, rate=0, fidx=0)
+    g.reset_gop()
+    with pytest.raises(PswaError) as e:
+        g.decode_frame(hyper, main, rate=0, fidx=0)
+    assert e.value.code == 2
+
+
+def test_yhat_at_the_limit_roundtrips():
+    c, blob, om, g = setup(False, 16, 16)
+    rng = np.random.default_rng(5)
+    y = laplace_yhat(rng, 192, 16, 16)
+    y[7, 3, 5], y[150, 9, 2] = 2048, -2048
+    hyper, main, _ = g.encode_frame(y, rate=0, fidx=0)
+    z = g.last_zhat()
+    g.reset_gop()
+    yd, _ = g.decode_frame(hyper, main, rate=0, fidx=0)
+    assert np.array_equal(yd, y)
+    g.reset_gop()
+    mu_g, sg_g, bits_g = g.forward_params(y, z, rate=0, fidx=0)
+    mu_o, sg_o, _ = om.forward(y, rate=0, zhat=z)
+    bits_o = om.encode(y, rate=0, fidx=0, zhat=z)[2]
+    compare_params("yhat_limit_2048", mu_g, sg_g, mu_o, sg_o, bits_g, bits_o)
