@@ -506,10 +506,13 @@ __device__ __forceinline__ void chain_wait_dep(const ChainArgs& a, int j, int mb
   }
 }
 
-template <int EPI>
-__device__ __forceinline__ void chain_epi_tile(const GemmEpi& ep, int M, int m0, int n0, int q, int half,
-                                               int lane, uint32_t acc, uint64_t* tempty_buf) {
-  const int c0 = half * (kChBN / 64), c1 = (half + 1) * (kChBN / 64);
+// Epilogue of one 128-row x BN accumulator tile by one warp (lane quarter q,
+// column half `half`); the accumulator is handed back by an arrive on the
+// (possibly remote: CTA-pair leader) barrier at cluster address tempty_addr.
+template <int BN, int EPI>
+__device__ __forceinline__ void epi_tile(const GemmEpi& ep, int M, int m0, int n0, int q, int half,
+                                         int lane, uint32_t acc, uint32_t tempty_addr) {
+  const int c0 = half * (BN / 64), c1 = (half + 1) * (BN / 64);
   const int m = m0 + q * 32 + lane;
   const bool side2 = ep.out2 != nullptr && n0 >= ep.split_n;
   const int* rmap = side2 ? ep.row_map2 : ep.row_map;
@@ -544,7 +547,7 @@ __device__ __forceinline__ void chain_epi_tile(const GemmEpi& ep, int M, int m0,
     if (c + 1 == c1) {
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_buf);
+      if (lane == 0) mbar_arrive_cluster(tempty_addr);
     }
     epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res, row_scale, side2);
     if (acc_res && c + 2 < c1) prefetch_residual(ep, orow, n0 + (c + 2) * 32, res);
@@ -704,11 +707,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const uint32_t acc = tmem + buf * kChBN + (static_cast<uint32_t>(q * 32) << 16);
+      const uint32_t te = smem_u32(&tempty[buf]);
       switch (J.kind) {
-        case kEpiF16: chain_epi_tile<kEpiF16>(J.ep, J.M, m0, n0, q, half, lane, acc, &tempty[buf]); break;
-        case kEpiF32: chain_epi_tile<kEpiF32>(J.ep, J.M, m0, n0, q, half, lane, acc, &tempty[buf]); break;
-        case kEpiSwiGLU: chain_epi_tile<kEpiSwiGLU>(J.ep, J.M, m0, n0, q, half, lane, acc, &tempty[buf]); break;
-        default: chain_epi_tile<kEpiHead>(J.ep, J.M, m0, n0, q, half, lane, acc, &tempty[buf]); break;
+        case kEpiF16: epi_tile<kChBN, kEpiF16>(J.ep, J.M, m0, n0, q, half, lane, acc, te); break;
+        case kEpiF32: epi_tile<kChBN, kEpiF32>(J.ep, J.M, m0, n0, q, half, lane, acc, te); break;
+        case kEpiSwiGLU: epi_tile<kChBN, kEpiSwiGLU>(J.ep, J.M, m0, n0, q, half, lane, acc, te); break;
+        default: epi_tile<kChBN, kEpiHead>(J.ep, J.M, m0, n0, q, half, lane, acc, te); break;
       }
       // every epilogue warp's stores of this tile, then one release increment
       named_bar_sync(1, 32 * kEpiWarps);
@@ -732,6 +736,122 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
       *done_ctr = 0u;
       __threadfence();
     }
+  }
+}
+
+// --------------------------------------------------- CTA-pair GEMM (2SM) --
+// For the large-M context GEMMs (M = 32640): a cluster of 2 CTAs computes a
+// 256 x 256 tile with tcgen05.mma.cta_group::2 issued by the pair leader.
+// Each CTA stages only its own 128 rows of A and its own 128 rows (N half)
+// of B per K block, 32 KB instead of the 48 KB a single-SM 128 x 256 tile
+// needs for the same MMA work: the per-SM operand stream, which bounds the
+// single-SM kernel (~74% MMA-paced), drops below the MMA time. Each CTA's
+// TMEM holds its own 128 rows x 256 columns; the epilogue is the single-SM
+// one. Same K order (ascending 64-wide blocks): bitwise equal results.
+constexpr int kPBN = 256;
+constexpr int kPStages = 6;
+constexpr int kPABytes = kBM * kBK * 2, kPBBytes = (kPBN / 2) * kBK * 2;
+constexpr int kPStageBytes = kPABytes + kPBBytes;
+constexpr int kPSmem = kPStages * kPStageBytes + 1024 + 256;
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, int M,
+                     int K, int tiles_mp, int tiles_n, const __grid_constant__ GemmEpi ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kPStages * kPABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPStages * kPStageBytes);
+  uint64_t* empty = full + kPStages;
+  uint64_t* tfull = empty + kPStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int kblocks = K / kBK;
+  const int n_units = tiles_mp * tiles_n;
+  const int unit0 = blockIdx.x / 2, unit_step = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tma);
+    tma_prefetch(&tmb);
+    for (int s = 0; s < kPStages; ++s) {
+      mbar_init(&full[s], 1);   // leader: one arrive.expect_tx for both CTAs' bytes
+      mbar_init(&empty[s], 1);  // the leader's multicast commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);              // multicast commit
+      mbar_init(&tempty[b], 2 * kEpiWarps);  // leader: both CTAs' epilogue warps
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 2 * kPBN);
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0;
+      for (int u = unit0; u < n_units; u += unit_step) {
+        const int m0 = (u / tiles_n) * 2 * kBM + rank * kBM, n0 = (u % tiles_n) * kPBN + rank * (kPBN / 2);
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          const int s = g % kPStages, round = g / kPStages;
+          if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+          const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+          if (leader) mbar_expect_tx(&full[s], 2 * kPStageBytes);
+          tma_load_2d_pair(sa + s * kPABytes, &tma, fb, kb * kBK, m0);
+          tma_load_2d_pair(sb + s * kPBBytes, &tmb, fb, kb * kBK, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = umma_idesc_f16_f32(2 * kBM, kPBN);
+      int g = 0, it = 0;
+      for (int u = unit0; u < n_units; u += unit_step, ++it) {
+        const int buf = it & 1, use = it >> 1;
+        if (use > 0) mbar_wait(&tempty[buf], (use - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * kPBN;
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          const int s = g % kPStages;
+          mbar_wait(&full[s], (g / kPStages) & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sa + s * kPABytes);
+          const uint32_t b_base = smem_u32(sb + s * kPBBytes);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            tc_mma_f16_pair(acc, umma_desc_k_sw128(a_base + kk * 32), umma_desc_k_sw128(b_base + kk * 32), idesc,
+                            (kb | kk) != 0 ? 1u : 0u);
+          tc_commit_pair(&empty[s]);
+        }
+        tc_commit_pair(&tfull[buf]);
+      }
+    }
+  } else {
+    const int ew = warp - 2, q = warp & 3, half = ew >> 2;
+    int it = 0;
+    for (int u = unit0; u < n_units; u += unit_step, ++it) {
+      const int buf = it & 1, use = it >> 1;
+      const int m0 = (u / tiles_n) * 2 * kBM + rank * kBM, n0 = (u % tiles_n) * kPBN;
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const uint32_t acc = tmem + buf * kPBN + (static_cast<uint32_t>(q * 32) << 16);
+      epi_tile<kPBN, EPI>(ep, M, m0, n0, q, half, lane, acc, mapa_shared(smem_u32(&tempty[buf]), 0));
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // no commit / remote arrive can still target this CTA
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free_pair(tmem, 2 * kPBN);
   }
 }
 
@@ -873,7 +993,9 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
                int K, const GemmEpi& epi, int force_bn) {
   if (K % kBK != 0 || N % 64 != 0 || lda % 8 != 0 || ldb % 8 != 0 || M <= 0)
     throw std::invalid_argument("gemm_plan: unsupported shape (K%64, N%64, ld%8)");
-  int bn = force_bn;
+  // force_bn = -1: the CTA-pair kernel (256 x 256 tiles, N % 256 == 0)
+  const bool force_pair = force_bn < 0;
+  int bn = force_pair ? 0 : force_bn;
   if (bn == 0) {
     // BN=256 once its tiles cover half the SMs (one wave of wide tiles beats
     // ~2 waves of BN=128 for the M = 2040 Q|K|V and gate|up GEMMs: 7.26 vs
@@ -915,8 +1037,33 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   static const bool use_cluster = std::getenv("PSWA_GEMM_CLUSTER") != nullptr;
   if (std::getenv("PSWA_GEMM_TRACE")) p->epi.trace = trace_buffer();
   p->cluster = (use_cluster && M > kBM) ? 2 : 1;
+  // CTA-pair tiles (cta_group::2) for the large context GEMMs: correct and
+  // bitwise equal to the single-SM kernel (test_pair_gemm_bitwise_equals_
+  // single_sm) but measured no faster on B200 -- the context SwiGLU GEMM took
+  // 90 vs 84.5 us and the frame 7.38 vs 7.25 ms: these tiles are paced by the
+  // epilogue (TMEM reads, SiLU, stores), not the per-SM operand stream the
+  // pair halves. Opt-in: PSWA_GEMM_PAIR=1, or force_bn = -1 per call.
+  static const bool use_pair = std::getenv("PSWA_GEMM_PAIR") != nullptr;
+  const int pair_units = ((M + 2 * kBM - 1) / (2 * kBM)) * (N / kPBN);
+  p->pair = N % kPBN == 0 &&
+            (force_pair || (use_pair && force_bn == 0 && M >= 16384 && pair_units >= sm_count()));
+  if (p->pair) {
+    bn = kPBN;
+    p->BN = bn;
+    p->cluster = 1;
+  }
   make_tmap(&p->ta, A, lda, M, K, kBM);
-  make_tmap(&p->tb, B, ldb, N, K, bn / p->cluster);
+  make_tmap(&p->tb, B, ldb, N, K, p->pair ? kPBN / 2 : bn / p->cluster);
+  if (p->pair) {
+    static std::once_flag once_pair;
+    std::call_once(once_pair, [] {
+      PSWA_CUDA(cudaFuncSetAttribute(gemm_pair_kernel<kEpiF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
+      PSWA_CUDA(cudaFuncSetAttribute(gemm_pair_kernel<kEpiF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
+      PSWA_CUDA(cudaFuncSetAttribute(gemm_pair_kernel<kEpiSwiGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
+      PSWA_CUDA(cudaFuncSetAttribute(gemm_pair_kernel<kEpiHead>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
+    });
+    return;
+  }
   const int kind = epi_kind(epi);
   if (bn == 64) prep<64>(kind);
   if (bn == 128) prep<128>(kind);
@@ -970,6 +1117,18 @@ void gemm_chain_run(const GemmChainPlan& c, cudaStream_t stream) {
 
 void gemm_run(const GemmPlan& p, cudaStream_t stream) {
   const int kind = epi_kind(p.epi);
+  if (p.pair) {
+    const int tiles_mp = (p.M + 2 * kBM - 1) / (2 * kBM), tiles_n = p.N / kPBN;
+    const int units = tiles_mp * tiles_n, clusters = std::min(units, sm_count() / 2);
+    switch (kind) {
+      case kEpiF16: launch_kc(gemm_pair_kernel<kEpiF16>, dim3(2 * clusters), dim3(kThreads), kPSmem, stream, 2u, p.ta, p.tb, p.M, p.K, tiles_mp, tiles_n, p.epi); break;
+      case kEpiF32: launch_kc(gemm_pair_kernel<kEpiF32>, dim3(2 * clusters), dim3(kThreads), kPSmem, stream, 2u, p.ta, p.tb, p.M, p.K, tiles_mp, tiles_n, p.epi); break;
+      case kEpiSwiGLU: launch_kc(gemm_pair_kernel<kEpiSwiGLU>, dim3(2 * clusters), dim3(kThreads), kPSmem, stream, 2u, p.ta, p.tb, p.M, p.K, tiles_mp, tiles_n, p.epi); break;
+      default: launch_kc(gemm_pair_kernel<kEpiHead>, dim3(2 * clusters), dim3(kThreads), kPSmem, stream, 2u, p.ta, p.tb, p.M, p.K, tiles_mp, tiles_n, p.epi); break;
+    }
+    PSWA_LAUNCH_CHECK();
+    return;
+  }
   switch (p.BN) {
     case 64: launch<64>(p, kind, stream); break;
     case 128: launch<128>(p, kind, stream); break;

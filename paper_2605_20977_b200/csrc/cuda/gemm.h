@@ -66,6 +66,7 @@ struct GemmPlan {
   CUtensorMap tb;
   int M = 0, N = 0, K = 0, BN = 0;
   int cluster = 1;  // 2: CTA pairs multicasting the shared B tile
+  bool pair = false;  // cta_group::2 256 x 256 tiles (large M, N % 256 == 0)
   GemmEpi epi;
 };
 

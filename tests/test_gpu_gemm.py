@@ -92,3 +92,15 @@ def test_gemm_head_epilogue():
     acc = a.float() @ b.float().t() + bias
     ref = torch.cat([acc[:, :64] * scale[:64], 0.11 + torch.nn.functional.softplus(acc[:, 64:])], 1)
     assert torch.allclose(c, ref, atol=1e-3, rtol=1e-3)
+
+
+@pytest.mark.parametrize("M,N,K,acc", [(32640, 2816, 512, 0), (16500, 512, 1408, 1), (32640, 1536, 512, 0)])
+def test_pair_gemm_bitwise_equals_single_sm(M, N, K, acc):
+    """The CTA-pair (tcgen05 cta_group::2) kernel (force_bn = -1; opt-in for
+    the large context GEMMs) gives bitwise the single-SM kernel's results
+    (same K order), so the encoder/decoder symmetry does not depend on it."""
+    c_pair, ref = _run(M, N, K, accumulate=acc, force_bn=-1)
+    c_one, _ = _run(M, N, K, accumulate=acc, force_bn=256)
+    assert torch.equal(c_pair, c_one)
+    err = (c_pair - ref).abs().max().item()
+    assert err <= 1e-3 * max(1.0, ref.abs().max().item()), err
