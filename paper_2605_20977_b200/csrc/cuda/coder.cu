@@ -97,16 +97,20 @@ __global__ void build_cdf_kernel(float* scales, uint32_t* cdf, int laplace) {
 }
 
 // ------------------------------------------------------------ helpers -----
+// Smallest i with scales[i] >= sigma (63 when none, NaN included): a log2
+// estimate of i (the scales are log-spaced, 0.146 octaves apart) corrected
+// against the table itself, so the result is exactly the binary search's
+// (the correction loops run 0-1 steps) with 2 dependent table reads instead
+// of 6.
 __device__ __forceinline__ int scale_index(const float* scales, float sigma) {
-  int lo = 0, hi = kScales;  // first i with scales[i] >= sigma
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (scales[mid] >= sigma)
-      hi = mid;
-    else
-      lo = mid + 1;
-  }
-  return lo < kScales ? lo : kScales - 1;
+  if (!(sigma <= scales[kScales - 1])) return kScales - 1;
+  constexpr float kLog2Lo = -3.184424571f;                  // log2(0.11)
+  constexpr float kPerOctave = 63.0f / 9.184424571f;        // 63 / log2(64 / 0.11)
+  int i = __float2int_ru((__log2f(sigma) - kLog2Lo) * kPerOctave);
+  i = min(max(i, 0), kScales - 1);
+  while (i > 0 && scales[i - 1] >= sigma) --i;
+  while (i < kScales - 1 && scales[i] < sigma) ++i;
+  return i;
 }
 
 __device__ __forceinline__ uint32_t rd32(const uint8_t* p) {
@@ -475,6 +479,7 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
   // binary (a 16x unrolled body overflowed the instruction cache)
   int4* s_par = reinterpret_cast<int4*>(s_scales + kScales);  // {table, mu, dst, dst16}
   int* s_out = reinterpret_cast<int*>(s_par + kB * blockDim.x);  // k | escape bits << 16
+  double* s_cost = reinterpret_cast<double*>(s_out + kB * blockDim.x);  // [q][thread] symbol costs
   const int tid = threadIdx.x, nth = blockDim.x;
   for (uint32_t ib = i_first; ib < ntot; ib += static_cast<uint32_t>(kB) * L) {
     const int nq = min(kB, static_cast<int>((ntot - ib + L - 1) / static_cast<uint32_t>(L)));
@@ -543,6 +548,9 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
         }
       }
       s_out[q * nth + tid] = k | (eb << 16);
+      // this symbol's cost (fp64, global) fetched into smem while the chain
+      // continues; summed after the chain in symbol order
+      cp_async_8(smem_u32(s_cost + q * nth + tid), bt + pr.x * kSyms + k);
       const int32_t y = v + pr.y;
       // a y_hat the encoder cannot have produced (|y_hat| > kYhatMax) marks
       // the stream corrupt
@@ -554,7 +562,8 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
       if (err) break;
     }
     if (err) break;
-    // bit costs: loads issued together, summed in symbol order
+    // bit costs: copied during the chain, summed in symbol order
+    cp_async_wait_all();
     double cost[kB];
     int ebs[kB];
 #pragma unroll
@@ -562,9 +571,8 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
       cost[q] = 0.0;
       ebs[q] = 0;
       if (q < nq) {
-        const int o = s_out[q * nth + tid];
-        ebs[q] = o >> 16;
-        cost[q] = __ldg(bt + s_par[q * nth + tid].x * kSyms + (o & 0xffff));
+        ebs[q] = s_out[q * nth + tid] >> 16;
+        cost[q] = s_cost[q * nth + tid];
       }
     }
 #pragma unroll
@@ -579,6 +587,7 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
         if (q < nq) taps.bits[s_par[q * nth + tid].z] = cost[q] + static_cast<double>(ebs[q]);
     }
   }
+  cp_async_wait_all();  // (an erroring lane left the batch with copies in flight)
   s.pos = rs.pos;
   lanes[l] = s;
   if (err) atomicOr(status, 2);
@@ -785,7 +794,7 @@ void lanes_decode_phase(const uint8_t* payload, LaneState* lanes, int L, uint64_
                         __half* yhat16, int ld16, int* status, cudaStream_t st, PhaseTaps taps) {
   if (n <= 0) return;
   constexpr int smem = kScales * (kSyms + 1) * 4 + kScales * kLutBuckets * 2 + kScales * 4 +
-                       kDecB * 128 * (16 + 4);
+                       kDecB * 128 * (16 + 4 + 8);
   static const bool attr = [] {
     PSWA_CUDA(cudaFuncSetAttribute(decode_phase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     return true;

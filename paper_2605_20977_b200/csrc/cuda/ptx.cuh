@@ -92,6 +92,14 @@ __device__ __forceinline__ void bulk_load(uint32_t smem_dst, const void* src, ui
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// 8-byte asynchronous global -> shared copy (LDGSTS), completed by
+// cp_async_wait_all() of the issuing thread.
+__device__ __forceinline__ void cp_async_8(uint32_t smem_dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
 // Orders this thread's prior generic-proxy smem accesses before later
 // async-proxy (TMA) writes to the same buffer.
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -39,7 +39,9 @@ def _worker(rank, world, port, q):
     ms = 10.0 + 5.0 * info.rank  # per-rank "timed region"
     worst = pdist.max_over_ranks(ms, d)
     gops = pdist.gops_for_rank(64, info.rank, info.world)
-    q.put((info.rank, worst, gops))
+    # config 4 accounting: frames of this rank's GOPs (32 each), summed
+    total = pdist.sum_over_ranks(32.0 * len(gops), d)
+    q.put((info.rank, worst, gops, total))
     pdist.barrier(d)
     d.destroy_process_group()
 
@@ -56,6 +58,7 @@ def test_two_rank_gloo_max_and_shards():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert [r[1] for r in res] == [15.0, 15.0]  # every rank reports the slowest
+    assert [r[3] for r in res] == [64 * 32.0, 64 * 32.0]  # job-wide frame count
     assert sorted(res[0][2] + res[1][2]) == list(range(64))
     assert not set(res[0][2]) & set(res[1][2])
 
