@@ -746,7 +746,8 @@ void Engine::join_side(Program& P) {
   });
 }
 
-void Engine::gemm(Program& P, const __half* A, int lda, int M, const PW& B, int K, const GemmEpi& ep) {
+void Engine::gemm(Program& P, const __half* A, int lda, int M, const PW& B, int K, const GemmEpi& ep,
+                  double alg_flops) {
   if (chaining_ && B.N % 128 == 0 && ep.act != pswa_dev::kActTanhHalf) {
     if (chain_.plan.njobs == pswa_dev::kChainMaxJobs ||
         (chain_.plan.njobs > 0 && chain_.plan.job[0].M != M))
@@ -762,7 +763,12 @@ void Engine::gemm(Program& P, const __half* A, int lda, int M, const PW& B, int 
   flush_chain(P);
   pswa_dev::GemmPlan plan;
   pswa_dev::gemm_plan(&plan, A, lda, M, B.p, B.K, B.N, K, ep);
-  add(P, [plan](cudaStream_t s) { pswa_dev::gemm_run(plan, s); });
+  auto op = [plan](cudaStream_t s) { pswa_dev::gemm_run(plan, s); };
+  add(P, op);
+  if (log_gemms_) {
+    gemm_log_.push_back(op);
+    gemm_log_flops_ += alg_flops >= 0.0 ? alg_flops : 2.0 * M * B.N * K;
+  }
 }
 
 namespace {
@@ -961,9 +967,10 @@ void Engine::block_step(Program& P, const Block& B, const StepBatch& bt) {
   }
   gemm(P, batt_, d, M, B.wo, d, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + norm2 inputs
   if (probe) tag(P, "step_wo", 2.0 * M * d * d);
-  gemm(P, bxn_, d, M, B.wgu, d, rms_in(swiglu_out(bh_, D.fp), bssq_));
+  gemm(P, bxn_, d, M, B.wgu, d, rms_in(swiglu_out(bh_, D.fp), bssq_), 2.0 * M * 2.0 * D.f * d);
   if (probe) tag(P, "step_gu", 2.0 * M * 2.0 * D.f * d);
-  gemm(P, bh_, D.fp, M, B.wd, D.fp, rms_out(f32_acc(bx_, d), bxn_, bssq_));  // + next norm1 inputs
+  gemm(P, bh_, D.fp, M, B.wd, D.fp, rms_out(f32_acc(bx_, d), bxn_, bssq_),  // + next norm1 inputs
+       2.0 * M * d * D.f);
   if (probe) tag(P, "step_wd", 2.0 * M * D.f * d);
 }
 
@@ -1015,9 +1022,9 @@ void Engine::run_stack3d(Program& P, const Block* blocks, int nblocks, int S, co
     float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
     __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;
     gemm(P, ctx_att_, d, nq, B.wo, d, rms_out(f32_acc(xq, d), xnq, ssq_q));
-    gemm(P, xnq, d, nq, B.wgu, d, rms_in(swiglu_out(ctx_h_, D.fp), ssq_q));
+    gemm(P, xnq, d, nq, B.wgu, d, rms_in(swiglu_out(ctx_h_, D.fp), ssq_q), 2.0 * nq * 2.0 * D.f * d);
     if (b == 0 && probe) tag(P, std::string(probe) + "_ffn_gu", 2.0 * nq * (2.0 * D.f) * d);
-    gemm(P, ctx_h_, D.fp, nq, B.wd, D.fp, rms_out(f32_acc(xq, d), xnq, ssq_q));
+    gemm(P, ctx_h_, D.fp, nq, B.wd, D.fp, rms_out(f32_acc(xq, d), xnq, ssq_q), 2.0 * nq * d * D.f);
   }
 }
 
@@ -1272,7 +1279,7 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
   for (int g = 0; g < N; ++g) {
     float* xg = chx_ + g * sp;
     if (g >= 1)  // channel shift: slot g sees y_hat group g-1
-      gemm(P, y16_ + (g - 1) * Cg, C, M, ch_emb_[g], D.Cgp, f32_acc(xg, dchp, sl));
+      gemm(P, y16_ + (g - 1) * Cg, C, M, ch_emb_[g], D.Cgp, f32_acc(xg, dchp, sl), 2.0 * M * sl * Cg);
     // slot-g RMSNorms: norm1 feeds the block-lower-triangular mix over
     // slots <= g (each slot normalised on its own, so it stays a kernel);
     // norm2 and the final norm are folded into the following GEMMs
@@ -1285,9 +1292,9 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
       const bool pr = mode == 0 && g == 1 && b == 0 && bt.parts[0][0] == 0;
       gemm(P, xn, dchp, M, mixg, (g + 1) * sp, ch_rms_out(f32_acc(xg, dchp, sl)));
       if (pr) tag(P, "ch_mix", 2.0 * M * sl * (g + 1) * sl);
-      gemm(P, chx16_, sp, M, ch_gu_[b][g], sp, ch_rms_in(swiglu_out(chh_, D.fgp)));
+      gemm(P, chx16_, sp, M, ch_gu_[b][g], sp, ch_rms_in(swiglu_out(chh_, D.fgp)), 2.0 * M * 2.0 * D.fg * sl);
       if (pr) tag(P, "ch_gu", 2.0 * M * 2.0 * D.fg * sl);
-      gemm(P, chh_, D.fgp, M, ch_d_[b][g], D.fgp, ch_rms_out(f32_acc(xg, dchp, sl)));
+      gemm(P, chh_, D.fgp, M, ch_d_[b][g], D.fgp, ch_rms_out(f32_acc(xg, dchp, sl)), 2.0 * M * sl * D.fg);
       if (pr) tag(P, "ch_d", 2.0 * M * D.fg * sl);
     }
     const float* go = ch_gout_ + g * sl;
@@ -1314,7 +1321,7 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
     e2.bias = head_b2_[g];
     e2.scale = cur_rso_ + g * Cg;
     e2.n_store = 2 * Cg;
-    gemm(P, hh16_, 2 * sp, M, head_w2_[g], 2 * sp, e2);
+    gemm(P, hh16_, 2 * sp, M, head_w2_[g], 2 * sp, e2, 2.0 * M * (2.0 * Cg) * sl);
     if (mode == 0 && g == 0 && bt.parts[0][0] == 0) tag(P, "ch_head2", 2.0 * M * (2.0 * Cg) * (2.0 * sp));
     const int c0 = g * Cg;
     for (const auto& pt : bt.parts) {  // per step: the symbols of phase (t, g)
@@ -1363,6 +1370,9 @@ Program& Engine::program(const std::string& key) {
   // "+ms": mu/sigma and per-symbol bit taps (BitStats) in every phase
   taps_ = key.find("+ms") != std::string::npos;
   if (base == "decode") {
+    log_gemms_ = true;
+    gemm_log_.clear();
+    gemm_log_flops_ = 0.0;
     // "+h" (single band): per-group ŷ transpositions and cuts for the host copies
     host_copy_ = key.find("+h") != std::string::npos && B_.n == 1;
     // the hyperprior branch (z_hat lanes -> hyper decoder -> Hq) does not
@@ -1409,6 +1419,18 @@ Program& Engine::program(const std::string& key) {
       add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_to_chw(yfr_ + yoff, HW, C, ychw_, s); });
     host_copy_ = false;
     if (c_lrp() > 0) build_lrp(P);
+    flush_chain(P);
+    log_gemms_ = false;
+    {  // every GEMM launch of the frame, replayed in program order
+      Probe pr;
+      auto ops = gemm_log_;
+      pr.op = [ops](cudaStream_t s) {
+        for (auto& o : ops) o(s);
+      };
+      pr.flops = gemm_log_flops_;
+      pr.launches = static_cast<int>(ops.size());
+      probes_["gemm_all"] = std::move(pr);
+    }
   } else if (base == "encode" || base == "encode_z") {
     const bool zgiven = base == "encode_z";
     add(P, [=, this](cudaStream_t s) { pswa_dev::yhat_from_chw(ychw_, HW, C, yfr_ + yoff, s); });

@@ -217,8 +217,15 @@ class Engine {
   } chain_;
   void flush_chain(Program& P);
   static bool chain_enabled();
+  // alg_flops: the layer's algorithmic FLOPs when the packed operands are
+  // padded (default 2 M N K of the padded GEMM)
   void gemm(Program& P, const __half* A, int lda, int M, const PW& B, int K,
-            const pswa_dev::GemmEpi& ep);
+            const pswa_dev::GemmEpi& ep, double alg_flops = -1.0);
+  // every GEMM launch of the decode program being built, for the whole-class
+  // probe "gemm_all" (the dominant kernel: ~2/3 of the frame's launch time)
+  bool log_gemms_ = false;
+  std::vector<std::function<void(cudaStream_t)>> gemm_log_;
+  double gemm_log_flops_ = 0.0;
   struct StepBatch {  // positions of one wavefront step, or of all steps (encoder)
     int M = 0;
     const int* rows = nullptr;      // local raster index per batch row

@@ -35,7 +35,9 @@ for _ in range(2):
     y, _ = dec.decode_frame(hyper, main, fidx=4, advance=False)
 assert np.array_equal(y, frames[4])
 probes = dec.probes()
-names = sys.argv[1:] or sorted(probes)
+# gemm_all replays ~380 launches: too many for --set full (its members are
+# captured as the individual GEMM probes)
+names = sys.argv[1:] or sorted(n for n in probes if n != "gemm_all")
 order = []
 for name in names:
     dec.bench_probe(name, 3)  # warm
