@@ -476,11 +476,16 @@ constexpr int kChABytes = kBM * kBK * 2, kChBBytes = kChBN * kBK * 2;
 constexpr int kChStageBytes = kChABytes + kChBBytes;
 constexpr int kChSmem = kChStages * kChStageBytes + 1024 + 512;
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+// Spin loads are relaxed: an ld.acquire.gpu per iteration compiles to an L1
+// invalidate (CCTL.IVALL) each time -- it was the chain kernel's top stall
+// and it evicted the epilogue's cached rows. One acq_rel fence after the
+// value is seen gives the acquire.
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -497,13 +502,15 @@ __device__ __forceinline__ int chain_job_of(const ChainArgs& a, int t) {
   return j;
 }
 
-// Spin until every tile of row block mb of job j - 1 has been stored.
+// Spin (one thread) until every tile of row block mb of job j - 1 has been
+// stored, then acquire.
 __device__ __forceinline__ void chain_wait_dep(const ChainArgs& a, int j, int mb) {
   if (j == 0) return;
   const unsigned* c = a.ctr + (j - 1) * a.ctr_stride + mb;
   const unsigned need = static_cast<unsigned>(a.job[j - 1].tiles_n);
-  while (ld_acquire_u32(c) < need) {
+  while (ld_relaxed_u32(c) < need) {
   }
+  fence_acq_rel_gpu();
 }
 
 // Epilogue of one 128-row x BN accumulator tile by one warp (lane quarter q,
@@ -703,7 +710,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_chain_kernel(const __grid_co
       const int buf = i & 1, use = i >> 1;
       // the epilogue reads the previous job's outputs too (residual rows, the
       // folded norm's sums of squares): same dependency as the A operand
-      chain_wait_dep(a, j, m0 / kBM);  // every lane acquires before its own reads
+      // one lane acquires; the warp barrier orders the other lanes' reads after it
+      if (lane == 0) chain_wait_dep(a, j, m0 / kBM);
+      __syncwarp();
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const uint32_t acc = tmem + buf * kChBN + (static_cast<uint32_t>(q * 32) << 16);

@@ -1276,6 +1276,8 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
   ep.out_f32 = 1;
   gemm(P, bs2n_, d, M, ch_proj_, d, ep);
   if (mode == 0 && bt.parts[0][0] == 0) tag(P, "ch_proj", 2.0 * M * (D.N * sl) * d);
+  static const bool ch_chain = std::getenv("PSWA_CH_CHAIN") != nullptr;
+  chaining_ = ch_chain && mode == 0;
   for (int g = 0; g < N; ++g) {
     float* xg = chx_ + g * sp;
     if (g >= 1)  // channel shift: slot g sees y_hat group g-1
@@ -1355,6 +1357,8 @@ void Engine::build_step(Program& P, const StepBatch& bt, int mode) {
       P.copy_group.push_back(g);
     }
   }
+  flush_chain(P);
+  chaining_ = false;
   if (mode == 0) build_embed(P, bt);
 }
 
