@@ -325,250 +325,6 @@ __global__ void __launch_bounds__(256, NP == 1 ? 3 : 2)
   }
 }
 
-// Context layers over all T = 4 query slots at once (the context
-// transformer's blocks 0..L-2, A4): the queries of every
-// slot at one spatial position see the same 7x7 key band in each key slot
-// they reach (wt = 5 >= T: slot j sees key slots 0..j). A warp therefore owns
-// its 8 spatial queries in all 4 query slots; a CTA walks (head, key slot)
-// stages, and each K / V fragment read from shared memory feeds the MMAs of
-// every query slot at or after the key slot (4, 3, 2, 1 for key slots 0..3:
-// 2.5x reuse on average), and each key-slot halo is staged once per head
-// instead of once per (head, query slot). Scores of one pass (kCtxPC chunks
-// of 16 keys) are kept for all query slots; the online softmax carries
-// across passes and key slots per query slot, so results equal the per-slot
-// kernel's up to fp32 summation order.
-constexpr int kQS = 4;  // context slots T (query slots of a tile: QS of them from slot T[3])
-constexpr int kCtxPC = 3;
-template <int QS>
-__global__ void __launch_bounds__(256, QS == 4 ? 1 : 2)
-    window_attn_ctx4_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap kvmap, int qstride) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h0 = blockIdx.x * a.hpc;
-  const int32_t* T = a.tiles + blockIdx.y * kAttnTileInts;
-  const int hy0 = T[0], hx0 = T[1], HR = T[2], qbase = T[3], nw = T[4];
-  const int nks = qbase + QS;              // key slots 0..nks-1 reach this tile's query slots
-  const int nstages = a.hpc * nks;         // (head, key slot) stages
-  const uint32_t sraw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
-  const uint32_t sbase = (sraw + 1023u) & ~1023u;
-  uint8_t* smem = smem_raw + (sbase - sraw);
-  // [2 bufs][QS tables][kAttnMaxBandKeys][8] fp16 score offsets, barriers, band keys
-  __half* stbl0 = reinterpret_cast<__half*>(smem + 2 * 2 * a.kbuf);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stbl0 + 2 * QS * kAttnMaxBandKeys * 8);
-  int16_t* sbk = reinterpret_cast<int16_t*>(bars + 2);
-  const int nbk = a.shape.nbk;
-  const uint32_t box_bytes = static_cast<uint32_t>(HR * a.hw * 64);
-  const uint32_t tbl_bytes = static_cast<uint32_t>(nbk * 8 * 2);
-  const CUtensorMap* kvm = &kvmap;
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-    tma_prefetch(kvm);
-  }
-  for (int i = threadIdx.x; i < nbk; i += blockDim.x) sbk[i] = a.shape.bkey[i];
-  pdl_wait();
-  pdl_trigger();
-  __syncthreads();
-
-  // stage (head h, key slot jk): K and V halo boxes of slot jk, and the score
-  // tables of the query slots qbase + q >= jk (slot offset jk - (qbase + q) + wt - 1)
-  auto stage = [&](int h, int jk, int buf) {
-    if (threadIdx.x == 0) {
-      fence_proxy_async_smem();
-      const uint32_t kb = sbase + buf * 2 * a.kbuf;
-      const int q0 = jk > qbase ? jk - qbase : 0;
-      mbar_expect_tx(&bars[buf], 2 * box_bytes + (QS - q0) * tbl_bytes);
-      tma_load_4d(kb, kvm, &bars[buf], h * kHD, hx0, hy0, jk);
-      tma_load_4d(kb + a.kbuf, kvm, &bars[buf], a.d + h * kHD, hx0, hy0, jk);
-      for (int q = q0; q < QS; ++q)
-        bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(stbl0 + (buf * QS + q) * kAttnMaxBandKeys * 8)),
-                  a.tables + (static_cast<size_t>(h) * a.nsl + (jk - qbase - q + a.wt - 1)) * nbk * 8,
-                  tbl_bytes, &bars[buf]);
-    }
-  };
-  uint32_t phase = 0;
-  stage(h0, 0, 0);
-
-  const int32_t* Wd = T + 8 + warp * 10;
-  const int br = warp < nw ? Wd[0] : 0, bc = warp < nw ? Wd[1] : 0;
-  const int qrow = warp < nw ? Wd[2 + (lane >> 2)] : -1;  // slot-0 row; slot q adds q * qstride
-  const bool live = __any_sync(0xffffffffu, qrow >= 0);
-  const int nch = nbk / 16;
-  constexpr int NCH = 2 * kCtxPC;
-  auto halo_key = [&](int bk) {
-    const int v = sbk[bk];
-    return (br + (v >> 8)) * a.hw + bc + (v & 255);
-  };
-  int hk[NCH], hv[NCH];
-  uint32_t inb = 0;
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    hk[c] = hv[c] = 0;
-    if (c < nch) {
-      hk[c] = halo_key(c * 16 + (lane & 7) + ((lane >> 3) & 1) * 8);
-      hv[c] = halo_key(c * 16 + (lane & 7) + ((lane >> 4) & 1) * 8);
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const int v = sbk[c * 16 + (lane >> 2) + 8 * rr];
-        const int ky = hy0 + br + (v >> 8), kx = hx0 + bc + (v & 255);
-        if (ky >= 0 && ky < a.shape.H && kx >= 0 && kx < a.shape.W) inb |= 1u << (2 * c + rr);
-      }
-    }
-  }
-  const int qc = (lane & 3) * 2;
-  const float qscale = 0.17677669529663687f * kLog2e;
-  uint32_t qb[QS][2][2];
-  float o[QS][2][4];
-  float m0[QS], m1[QS], l0[QS], l1[QS];
-
-  int hi = 0, jk = 0;
-  for (int st = 0; st < nstages; ++st) {
-    const int h = h0 + hi;
-    const int buf = st & 1;
-    if (st + 1 < nstages) stage(jk + 1 == nks ? h + 1 : h, jk + 1 == nks ? 0 : jk + 1, buf ^ 1);
-    const int qlo = jk - qbase;  // query slots q >= qlo reach key slot jk
-    if (jk == 0) {  // new head: Q fragments of all query slots, fresh softmax states
-#pragma unroll
-      for (int q = 0; q < QS; ++q) {
-        const __half* qp = a.q + static_cast<size_t>(qrow < 0 ? 0 : qrow + (qbase + q) * qstride) * a.ldq +
-                           h * kHD + qc;
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-          qb[q][ks][0] = qrow >= 0 ? *reinterpret_cast<const uint32_t*>(qp + ks * 16) : 0u;
-          qb[q][ks][1] = qrow >= 0 ? *reinterpret_cast<const uint32_t*>(qp + ks * 16 + 8) : 0u;
-        }
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) o[q][i][e] = 0.0f;
-        m0[q] = m1[q] = -INFINITY;
-        l0[q] = l1[q] = 0.0f;
-      }
-    }
-    mbar_wait(&bars[buf], (phase >> buf) & 1u);
-    phase ^= 1u << buf;
-    const uint32_t sK = sbase + buf * 2 * a.kbuf, sV = sK + a.kbuf;
-    if (live) {
-#pragma unroll
-      for (int ps = 0; ps < 2; ++ps) {
-        if (ps * kCtxPC >= nch) break;
-        float s[QS][kCtxPC][4];
-        float mx0[QS], mx1[QS];
-#pragma unroll
-        for (int q = 0; q < QS; ++q) mx0[q] = mx1[q] = -INFINITY;
-#pragma unroll
-        for (int ci = 0; ci < kCtxPC; ++ci) {
-          const int c = ps * kCtxPC + ci;
-          if (c < nch) {
-            uint32_t fa0[4], fa1[4];
-            ldsm_x4(sK + swz(hk[c], lane >> 4), fa0);
-            ldsm_x4(sK + swz(hk[c], (lane >> 4) + 2), fa1);
-            const int r0 = c * 16 + (lane >> 2);
-            const bool k0 = (inb >> (2 * c)) & 1u, k1 = (inb >> (2 * c + 1)) & 1u;
-#pragma unroll
-            for (int q = 0; q < QS; ++q) {
-              if (q < qlo) continue;  // query slot qbase + q does not reach key slot jk
-              float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-              mma16816(acc, fa0, qb[q][0][0], qb[q][0][1]);
-              mma16816(acc, fa1, qb[q][1][0], qb[q][1][1]);
-              const __half* tb = stbl0 + (buf * QS + q) * kAttnMaxBandKeys * 8;
-              const float2 t0 = __half22float2(*reinterpret_cast<const __half2*>(tb + r0 * 8 + qc));
-              const float2 t1 = __half22float2(*reinterpret_cast<const __half2*>(tb + (r0 + 8) * 8 + qc));
-              s[q][ci][0] = k0 ? fmaf(acc[0], qscale, t0.x) : -INFINITY;
-              s[q][ci][1] = k0 ? fmaf(acc[1], qscale, t0.y) : -INFINITY;
-              s[q][ci][2] = k1 ? fmaf(acc[2], qscale, t1.x) : -INFINITY;
-              s[q][ci][3] = k1 ? fmaf(acc[3], qscale, t1.y) : -INFINITY;
-              mx0[q] = fmaxf(mx0[q], fmaxf(s[q][ci][0], s[q][ci][2]));
-              mx1[q] = fmaxf(mx1[q], fmaxf(s[q][ci][1], s[q][ci][3]));
-            }
-          }
-        }
-        float ms0[QS], ms1[QS];
-#pragma unroll
-        for (int q = 0; q < QS; ++q) {
-          ms0[q] = ms1[q] = 0.0f;
-          if (q < qlo) continue;
-#pragma unroll
-          for (int off = 4; off < 32; off <<= 1) {
-            mx0[q] = fmaxf(mx0[q], __shfl_xor_sync(0xffffffffu, mx0[q], off));
-            mx1[q] = fmaxf(mx1[q], __shfl_xor_sync(0xffffffffu, mx1[q], off));
-          }
-          const float mn0 = fmaxf(m0[q], mx0[q]), mn1 = fmaxf(m1[q], mx1[q]);
-          const float al0 = mn0 == -INFINITY ? 1.0f : ex2(m0[q] - mn0);
-          const float al1 = mn1 == -INFINITY ? 1.0f : ex2(m1[q] - mn1);
-          m0[q] = mn0;
-          m1[q] = mn1;
-          ms0[q] = mn0 == -INFINITY ? 0.0f : mn0;
-          ms1[q] = mn1 == -INFINITY ? 0.0f : mn1;
-          l0[q] *= al0;
-          l1[q] *= al1;
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
-            o[q][mt][0] *= al0;
-            o[q][mt][1] *= al1;
-            o[q][mt][2] *= al0;
-            o[q][mt][3] *= al1;
-          }
-        }
-#pragma unroll
-        for (int ci = 0; ci < kCtxPC; ++ci) {
-          const int c = ps * kCtxPC + ci;
-          if (c < nch) {
-            uint32_t b0[QS], b1[QS];
-#pragma unroll
-            for (int q = 0; q < QS; ++q) {
-              b0[q] = b1[q] = 0u;
-              if (q < qlo) continue;
-              const float p0 = ex2(s[q][ci][0] - ms0[q]), p1 = ex2(s[q][ci][1] - ms1[q]);
-              const float p2 = ex2(s[q][ci][2] - ms0[q]), p3 = ex2(s[q][ci][3] - ms1[q]);
-              l0[q] += p0 + p2;
-              l1[q] += p1 + p3;
-              b0[q] = movtrans(pack_h2(p0, p1));
-              b1[q] = movtrans(pack_h2(p2, p3));
-            }
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-              uint32_t fv[4];
-              ldsm_x4_t(sV + swz(hv[c], ((lane >> 3) & 1) + 2 * mt), fv);
-#pragma unroll
-              for (int q = 0; q < QS; ++q)
-                if (q >= qlo) mma16816(o[q][mt], fv, b0[q], b1[q]);
-            }
-          }
-        }
-      }
-      if (jk == nks - 1) {  // every key slot seen: normalise and store all query slots
-#pragma unroll
-        for (int q = 0; q < QS; ++q) {
-          float t0 = l0[q], t1 = l1[q];
-#pragma unroll
-          for (int off = 4; off < 32; off <<= 1) {
-            t0 += __shfl_xor_sync(0xffffffffu, t0, off);
-            t1 += __shfl_xor_sync(0xffffffffu, t1, off);
-          }
-          const float inv0 = t0 > 0.0f ? 1.0f / t0 : 0.0f;
-          const float inv1 = t1 > 0.0f ? 1.0f / t1 : 0.0f;
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int hb = 0; hb < 2; ++hb) {
-              const uint32_t v = movtrans(pack_h2(o[q][mt][2 * hb] * inv0, o[q][mt][2 * hb + 1] * inv1));
-              if (qrow >= 0)
-                *reinterpret_cast<uint32_t*>(a.out + static_cast<size_t>(qrow + (qbase + q) * qstride) * a.ldo +
-                                             h * kHD + mt * 16 + hb * 8 + (lane & 3) * 2) = v;
-            }
-        }
-      }
-    }
-    __syncthreads();
-    if (++jk == nks) {
-      jk = 0;
-      ++hi;
-    }
-  }
-}
-
 // Per-shape launch policy: heads per CTA (their halos pipelined through
 // two buffers) and double buffering. PSWA_ATTN_HPC / PSWA_ATTN_DBUF override
 // for experiments. Context: 4 heads per CTA, double-buffered (measured with
@@ -605,46 +361,7 @@ void launch_t8(const AttnArgs& a, const CUtensorMap& map, int halo_keys, int nti
            smem_bytes(halo_keys, a.dbuf), st, a, map);
 }
 
-int smem_bytes_ctx4(int halo_keys, int qs) {
-  return 1024 + 4 * box_buf_bytes(halo_keys) + 2 * qs * kAttnMaxBandKeys * 8 * 2 + 16 +
-         kAttnMaxBandKeys * 2;
-}
-
 }  // namespace
-
-int ctx_slot_group() {
-  static const int g = env_int("PSWA_ATTN_CTX_QS", 2) == 4 ? 4 : 2;
-  return g;
-}
-
-void window_attention_ctx_slots(const __half* q, int ldq, int q_slot_stride, const int32_t* tiles,
-                                int ntiles, int halo_rows, int halo_width, AttnShape shape,
-                                const CUtensorMap& kv_map, int heads, int wt, const __half* tables,
-                                __half* out, int ldo, cudaStream_t st) {
-  if (ntiles <= 0) return;
-  if (shape.nbk % 16 || shape.nbk > 16 * 2 * kCtxPC || wt < kQS)
-    throw std::invalid_argument("context slot attention shape");
-  static const int hpc_env = env_int("PSWA_ATTN_CTX_HPC", 4);
-  int hpc = hpc_env;
-  while (heads % hpc) --hpc;
-  const int hk = halo_rows * halo_width;
-  const int qs = ctx_slot_group();
-  const int smem = smem_bytes_ctx4(hk, qs);
-  static bool attr = false;
-  if (!attr) {
-    PSWA_CUDA(cudaFuncSetAttribute(window_attn_ctx4_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   smem_bytes_ctx4(hk, 4)));
-    PSWA_CUDA(cudaFuncSetAttribute(window_attn_ctx4_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   smem_bytes_ctx4(hk, 2)));
-    attr = true;
-  }
-  AttnArgs a{q, ldq, tiles, heads * kHD, wt, tables, wt, out, ldo, shape, halo_width, box_buf_bytes(hk), 1, hpc};
-  if (qs == 4)
-    launch_k(window_attn_ctx4_kernel<4>, dim3(heads / hpc, ntiles), dim3(256), smem, st, a, kv_map, q_slot_stride);
-  else
-    launch_k(window_attn_ctx4_kernel<2>, dim3(heads / hpc, ntiles), dim3(256), smem, st, a, kv_map, q_slot_stride);
-  PSWA_LAUNCH_CHECK();
-}
 
 bool window_attention_tiles_supported(int hd, int win_h, int win_w) {
   return hd == kHD && win_h == 7 && win_w == 7;

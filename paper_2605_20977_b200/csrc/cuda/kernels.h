@@ -92,15 +92,6 @@ void window_attention_tiles_init(int max_smem_bytes);
 // bias enters the fp32 score as its fp16 rounding, < 1e-3 relative).
 void build_score_tables(const float* bias, int heads, int wt, AttnShape shape, __half* out,
                         cudaStream_t st);
-// The context layers' all-slot launch: tiles as above with the slot-0 query
-// rows; a tile covers query slots [T[3], T[3] + ctx_slot_group()) (slot q
-// adds q * q_slot_stride), every warp all of them, each key-slot halo and
-// fragment shared by the query slots that reach it (attention_mma.cu).
-int ctx_slot_group();
-void window_attention_ctx_slots(const __half* q, int ldq, int q_slot_stride, const int32_t* tiles,
-                                int ntiles, int halo_rows, int halo_width, AttnShape shape,
-                                const CUtensorMap& kv_map, int heads, int wt, const __half* tables,
-                                __half* out, int ldo, cudaStream_t st);
 // kv_map: make_kv_tmap() of the K/V cache (gemm.h); halos are staged by TMA.
 void window_attention_tiles(const __half* q, int ldq, const int32_t* tiles, int ntiles,
                             int warps_per_tile, int halo_rows, int halo_width, AttnShape shape,

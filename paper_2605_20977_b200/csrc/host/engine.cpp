@@ -243,21 +243,6 @@ void Engine::alloc_all() {
         tl.n_last = static_cast<int>(last.size()) / TI;
         tl.all = up(all);
         tl.last = up(last);
-        if (S == 4 && D.c.win_t >= 4) {  // slot-sharing launch (window_attention_ctx_slots)
-          // one tile per (spatial tile, group of QS query slots), the group
-          // with the most key slots first (heaviest tiles lead the launch)
-          const int qs = pswa_dev::ctx_slot_group();
-          const auto base = ctx_tiles(0, 0, 1);
-          std::vector<int> sl;
-          for (int qb = S - qs; qb >= 0; qb -= qs)
-            for (size_t t0 = 0; t0 < base.size(); t0 += TI) {
-              std::vector<int> t(base.begin() + t0, base.begin() + t0 + TI);
-              t[3] = qb;
-              sl.insert(sl.end(), t.begin(), t.end());
-            }
-          tl.n_slots = static_cast<int>(sl.size()) / TI;
-          tl.slots = up(sl);
-        }
       };
       make(T, tiles_ctx_);
       if (D.c.lrp_blocks > 0) make(T + 1, tiles_lrp_);
@@ -884,29 +869,6 @@ void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq
   }
 }
 
-// Context layer over all 4 query slots at once: every key-slot halo is
-// staged once per head and its fragments feed each query slot that reaches it.
-void Engine::attention_ctx_slots(Program& P, const __half* q, const Tiles3d& tl, const __half* kv,
-                                 int S, const float* bias, __half* out) {
-  const Dims& D = D_;
-  const int d = D.d, wt = D.c.win_t;
-  const pswa_dev::AttnShape sh = shape_ctx_;
-  CUtensorMap map;
-  pswa_dev::make_kv_tmap(&map, kv, 2 * d, D.W, B_.Hl, S, HWl_, kCtxHaloW, kCtxHaloRows);
-  __half*& tab = score_tables_[{bias, &shape_ctx_}];
-  if (!tab) {
-    tab = dalloc<__half>(static_cast<size_t>(D.heads) * wt * sh.nbk * 8);
-    pswa_dev::build_score_tables(bias, D.heads, wt, sh, tab, st_);
-  }
-  const __half* tables = tab;
-  const int32_t* tiles = tl.slots;
-  const int ntiles = tl.n_slots, qstride = HWo_;
-  add(P, [=](cudaStream_t s) {
-    pswa_dev::window_attention_ctx_slots(q, d, qstride, tiles, ntiles, kCtxHaloRows, kCtxHaloW, sh, map,
-                                         D.heads, wt, tables, out, d, s);
-  });
-}
-
 // A batch of wavefront-step positions: one step (the decoder's phases) or
 // every step concatenated in canonical order (the teacher-forced encoder:
 // the same per-position kernels with one GEMM per layer instead of s; the
@@ -1008,16 +970,8 @@ void Engine::run_stack3d(Program& P, const Block* blocks, int nblocks, int S, co
       if (exchange_kv) exchange(P, b % 2 ? kXidCtx1 : kXidCtx0, kXCtx);
       gemm(P, ctx_xn_ + static_cast<size_t>(q0) * d, d, nq, B.wq, d, rms_in(f16_out(ctx_q_, d), ssq_q));
     }
-    // slot-sharing context attention: opt-in (PSWA_CTX_SLOTS=1). Measured
-    // slower on B200 than the per-slot launch (129 / 197 us per layer with 2
-    // / 4 query slots per warp vs 118 us): the fragment reuse does not pay
-    // for the lower occupancy and the per-slot bookkeeping
-    static const bool ctx_slots = std::getenv("PSWA_CTX_SLOTS") != nullptr;
-    if (!last && tl.n_slots > 0 && S == 4 && mma_attn_ && ctx_slots)
-      attention_ctx_slots(P, ctx_q_, tl, kv, S, pos, ctx_att_);
-    else
-      attention(P, ctx_q_, tl.qinfo + q0, nq, last ? tl.last : tl.all, last ? tl.n_last : tl.n_all,
-                &shape_ctx_, kv, HWl_, D.c.win_t, 0, pos, ctx_att_, S);
+    attention(P, ctx_q_, tl.qinfo + q0, nq, last ? tl.last : tl.all, last ? tl.n_last : tl.n_all,
+              &shape_ctx_, kv, HWl_, D.c.win_t, 0, pos, ctx_att_, S);
     if (b == 0 && probe) tag(P, std::string(probe) + "_attn", attn_flops(-1, 0, S));
     float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
     __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;

@@ -358,11 +358,7 @@ class Engine {
   struct Tiles3d {  // attention work of a 3D stack: all slots / last slot only
     const int32_t *all = nullptr, *last = nullptr, *qinfo = nullptr;
     int n_all = 0, n_last = 0;
-    const int32_t* slots = nullptr;  // slot-0 rows, every query slot per warp (T = 4)
-    int n_slots = 0;
   };
-  void attention_ctx_slots(Program& P, const __half* q, const Tiles3d& tl, const __half* kv,
-                           int S, const float* bias, __half* out);
   Tiles3d tiles_ctx_, tiles_lrp_;
   void run_stack3d(Program& P, const Block* blocks, int nblocks, int S, const Tiles3d& tl,
                    bool exchange_kv, const char* probe);
