@@ -148,16 +148,19 @@ ScheduleReport validate_schedule_with(int h, int w, int s, int wh, int ww, int n
 // ---- C ABI ------------------------------------------------------------------
 #include <cstring>
 
+#include "abi_util.h"
 #include "pswa/pswa_cuda.h"
 
 extern "C" int pswa_validate_schedule(int h, int w, int s, int wh, int ww, int n_groups, int* ok,
                                       int* sequential_steps, char* first_violation, size_t cap) {
-  const pswa::ScheduleReport r = pswa::validate_schedule(h, w, s, wh, ww, n_groups);
-  *ok = r.ok ? 1 : 0;
-  *sequential_steps = r.sequential_steps;
-  if (first_violation && cap) {
-    std::strncpy(first_violation, r.first_violation.c_str(), cap - 1);
-    first_violation[cap - 1] = '\0';
-  }
-  return PSWA_OK;
+  return pswa_abi::guard([&] {
+    if (static_cast<long>(h) * w > (1L << 24)) throw std::invalid_argument("validate_schedule: grid too large");
+    const pswa::ScheduleReport r = pswa::validate_schedule(h, w, s, wh, ww, n_groups);
+    *ok = r.ok ? 1 : 0;
+    *sequential_steps = r.sequential_steps;
+    if (first_violation && cap) {
+      std::strncpy(first_violation, r.first_violation.c_str(), cap - 1);
+      first_violation[cap - 1] = '\0';
+    }
+  });
 }
