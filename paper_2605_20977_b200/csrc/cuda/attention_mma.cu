@@ -106,7 +106,7 @@ struct AttnArgs {
 // (80 registers, 68 B of spills) measured slower (15.7 -> 18.5 us).
 constexpr int kPassChunks = 5;
 template <int NP>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, NP == 1 ? 3 : 2)
     window_attn_t8_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap kvmap) {
   constexpr int NCH = NP * kPassChunks;  // chunk slots held in registers (row keys)
   extern __shared__ __align__(128) uint8_t smem_raw[];
