@@ -117,3 +117,58 @@ def test_headline_decoder_params(paper, fidx):
     record(tag + "_decoder", mu_bitwise_vs_forward_params=True,
            payload_bits=payload_bits, estimate_bits=float(bits_d[1]),
            framing_overhead_bits=float(overhead), lanes=LANES)
+
+
+def test_headline_lrp_eps_1080p():
+    """The LRP transformer at the headline grid with the paper's 4 blocks
+    (SURVEY §8(f)2): decoder eps == encoder eps bitwise, within 0.01 of the
+    oracle on >= 99.9% of elements, (-0.5, 0.5) everywhere."""
+    oracle().oracle_set_threads(os.cpu_count() or 1)
+    c = preset(True, H, W, lanes=LANES, hyper_lanes=HYPER_LANES, lrp_blocks=4)
+    cfg = cfg_from_dict(c)
+    blob = gen_weights(c, 1)
+    frames = [synth_latent(cfg, 1, f) for f in range(5)]
+    enc, dec = GpuCodec(cfg, blob), GpuCodec(cfg, blob)
+    for f in frames[:4]:
+        enc.push_frame(f)
+        dec.push_frame(f)
+    hyper, main, _ = enc.encode_frame(frames[4], fidx=4)
+    eps_e, z = enc.last_eps(), enc.last_zhat()
+    yd, _ = dec.decode_frame(hyper, main, fidx=4)
+    eps_d = dec.last_eps()
+    assert np.array_equal(yd, frames[4])
+    assert np.array_equal(eps_e.view(np.uint32), eps_d.view(np.uint32))
+    assert (np.abs(eps_d) < 0.5).all()
+    eps_o = OracleModel(c, blob).lrp(frames[4], z, past=frames[:4])
+    err = np.abs(eps_d - eps_o)
+    record("headline_lrp_paper_68x120_f4", eps_max_abs=float(err.max()), eps_mean_abs=float(err.mean()),
+           frac_within_0p01=float((err <= 0.01).mean()))
+    assert (err <= 0.01).mean() >= 0.999 and err.max() <= 0.05
+
+
+def test_headline_laplace_head_1080p():
+    """The Laplace parameter head (prior = 1, north_star item 3) at the
+    headline grid: bit-exact round trip, decoder mu/sigma bitwise equal to the
+    encoder program's, within the stated tolerance of the oracle, rate within
+    1e-3 (estimate_bits of the oracle's own parameters under its Laplace
+    tables)."""
+    oracle().oracle_set_threads(os.cpu_count() or 1)
+    c = preset(True, H, W, lanes=LANES, hyper_lanes=HYPER_LANES, prior=1)
+    cfg = cfg_from_dict(c)
+    blob = gen_weights(c, 1)
+    y = synth_latent(cfg, 3, 0)
+    enc = GpuCodec(cfg, blob)
+    hyper, main, bits_e = enc.encode_frame(y, fidx=0)
+    z = enc.last_zhat()
+    dec = GpuCodec(cfg, blob)
+    yd, bits_d, mu_d, sg_d = dec.decode_frame(hyper, main, fidx=0, params=True)
+    assert np.array_equal(yd, y) and bits_d[1] == bits_e[1]
+    fp = GpuCodec(cfg, blob)
+    mu_f, sg_f, _ = fp.forward_params(y, z, fidx=0)
+    assert np.array_equal(mu_d.view(np.uint32), mu_f.view(np.uint32))
+    om = OracleModel(c, blob)
+    mu_o, sg_o, _ = om.forward(y, zhat=z)
+    v_o, idx_o = oracle_symbol_bits(y, mu_o, sg_o)
+    main_o = oracle_bits(v_o, idx_o + 64)  # the oracle's Laplace tables follow the Gaussian 64
+    compare_params("headline_laplace_paper_68x120_f0", mu_d, sg_d, mu_o, sg_o, bits_d,
+                   [bits_d[0], main_o])
