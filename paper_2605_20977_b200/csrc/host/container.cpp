@@ -1,6 +1,8 @@
 // Sequence container reader / writer (see container.h, FORMAT.md).
 #include "container.h"
 
+#include <string>
+
 #include <cstring>
 #include <stdexcept>
 
@@ -53,7 +55,9 @@ ContainerHeader parse_container(const uint8_t* p, size_t len, std::vector<FrameR
   if (len < kContainerHeader || std::memcmp(p, "PSWA", 4) != 0)
     throw pswa_abi::TruncatedError("container: not a PSWA stream");
   if (get(p + 4, 2) != kContainerVersion || get(p + 6, 2) != kContainerHeader)
-    throw std::invalid_argument("container: unsupported version");
+    throw std::invalid_argument("container: unsupported version " + std::to_string(get(p + 4, 2)) +
+                                " (this decoder reads version " + std::to_string(kContainerVersion) +
+                                "; other versions were coded under other model numerics)");
   ContainerHeader h;
   uint32_t* f[7] = {&h.w_px, &h.h_px, &h.frames, &h.gop, &h.rate, &h.s, &h.N};
   for (int i = 0; i < 7; ++i) *f[i] = static_cast<uint32_t>(get(p + 8 + 4 * i, 4));

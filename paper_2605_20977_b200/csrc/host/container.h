@@ -12,7 +12,11 @@
 
 namespace pswa_host {
 
-constexpr uint16_t kContainerVersion = 1;
+// 2: numerics revision 2 of the device entropy model (SiLU via tanh.approx,
+// softplus via __expf/__logf in the GEMM epilogues). A symbol decodes only
+// under the exact mu/sigma that coded it, so streams of another numerics
+// revision are refused instead of decoding to wrong latents.
+constexpr uint16_t kContainerVersion = 2;
 constexpr size_t kContainerHeader = 64;
 
 struct ContainerHeader {
