@@ -44,11 +44,14 @@ struct GemmCfg {
   // as deep as shared memory allows (<= 227 KB with the epilogue staging):
   // the small-M step GEMMs are latency bound, so all K blocks in flight helps
   static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
-  static_assert(kStages * (kBM * kBK * 2 + BN * kBK * 2) + 1280 <= 227 * 1024, "smem");
+  static_assert(kStages * (kBM * kBK * 2 + BN * kBK * 2) + 1280 + kEpiWarps * 4096 <= 227 * 1024, "smem");
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  // + one 32 x 128 B store stage per epilogue warp (warp_store_rows) for the
+  // fp32-output kinds only: the others keep the smaller carve-out (more L1)
+  static constexpr int smem_for(int epi) { return kSmem + ((epi == 1 || epi == 3) ? kEpiWarps * 4096 : 0); }
 };
 
 __device__ __forceinline__ float tanh_approx(float x) {
@@ -170,22 +173,103 @@ __device__ __forceinline__ void prefetch_residual(const GemmEpi& ep, int orow, i
   }
 }
 
+// Coalesced store of one row segment per lane (the TMEM layout: lane = row)
+// through this warp's swizzled 32 x 128 B smem stage: the lanes first write
+// their NCH 16 B chunks (chunk c of row r at position c ^ (r & 7)), then store
+// whole row segments -- NCH lanes per row, 32 / NCH rows per instruction --
+// so a warp instruction writes 4 full 128 B lines (NCH = 8) instead of 32
+// scattered 32 B sectors. `dst` (nullable: row skipped) is this lane's row.
+template <int NCH>
+__device__ __forceinline__ void warp_store_rows(uint32_t stg, const uint4 (&d)[NCH], void* dst, int lane) {
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 128 + ((c ^ (lane & 7)) << 4)),
+                 "r"(d[c].x), "r"(d[c].y), "r"(d[c].z), "r"(d[c].w)
+                 : "memory");
+  __syncwarp();
+  constexpr int kRows = 32 / NCH;  // rows per instruction
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const int row = k * kRows + lane / NCH, ch = lane % NCH;
+    const unsigned long long base = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), row);
+    uint4 val;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(val.x), "=r"(val.y), "=r"(val.z), "=r"(val.w)
+                 : "r"(stg + row * 128 + ((ch ^ (row & 7)) << 4))
+                 : "memory");
+    if (base) reinterpret_cast<uint4*>(base)[ch] = val;
+  }
+  __syncwarp();
+}
+
 // Drain one accumulator row segment: lane = TMEM lane = output row, columns
 // n0..n0+31; fused op, then straight 16 B stores from registers (each lane
 // writes whole 32 B sectors of its own row).
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
                                           const uint32_t (&raw)[32], const float4 (&res)[8],
-                                          float row_scale, bool side2) {
+                                          float row_scale, bool side2, uint32_t stg = 0) {
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]) * row_scale;
   epi_values<EPI>(ep, n0, v);
-  if (orow < 0) return;
   const int ncols = EPI == kEpiSwiGLU ? 16 : 32;
   const int oc0 = EPI == kEpiSwiGLU ? (n0 >> 1) : n0;
-  if (oc0 >= ep.n_store) return;
+  if (oc0 >= ep.n_store) return;  // (warp-uniform)
   const bool full = oc0 + ncols <= ep.n_store;
+  // warp-cooperative coalesced stores (every lane takes part, rows < 0
+  // skipped) for the fp32 outputs (residual stream + its fp16 copy, heads):
+  // measured 6.7 -> 6.4 us (out-proj), 7.5 -> 7.2 us (channel down); the
+  // fp16 / SwiGLU outputs (32 / 64 B per row) measured faster row-per-lane
+  if ((EPI == kEpiF32 || EPI == kEpiHead) && stg && full && ep.v8) {
+    if (EPI == kEpiF32 || EPI == kEpiHead) {
+      float ss = 0.0f;
+      uint4 ov[8], hp[4];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        if (EPI == kEpiF32 && ep.accumulate) {
+          o.x += res[q].x;
+          o.y += res[q].y;
+          o.z += res[q].z;
+          o.w += res[q].w;
+        }
+        ov[q] = make_uint4(__float_as_uint(o.x), __float_as_uint(o.y), __float_as_uint(o.z), __float_as_uint(o.w));
+        ss = fmaf(o.x, o.x, ss);
+        ss = fmaf(o.y, o.y, ss);
+        ss = fmaf(o.z, o.z, ss);
+        ss = fmaf(o.w, o.w, ss);
+        __half2 h0 = __floats2half2_rn(o.x, o.y), h1 = __floats2half2_rn(o.z, o.w);
+        (q & 1 ? hp[q >> 1].z : hp[q >> 1].x) = *reinterpret_cast<uint32_t*>(&h0);
+        (q & 1 ? hp[q >> 1].w : hp[q >> 1].y) = *reinterpret_cast<uint32_t*>(&h1);
+      }
+      warp_store_rows<8>(stg, ov, orow >= 0 ? static_cast<float*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0 : nullptr,
+                         threadIdx.x & 31);
+      if (EPI == kEpiF32 && ep.x16_out)
+        warp_store_rows<4>(stg, hp, orow >= 0 ? ep.x16_out + static_cast<size_t>(orow) * ep.ld_x16 + oc0 : nullptr,
+                           threadIdx.x & 31);
+      if (EPI == kEpiF32 && ep.ssq_out && orow >= 0) ep.ssq_out[static_cast<size_t>(orow) * ep.ld_ssq + (oc0 >> 5)] = ss;
+    } else {
+      constexpr int NCH = EPI == kEpiSwiGLU ? 2 : 4;  // 16 / 32 fp16 per row
+      uint4 hp[NCH];
+#pragma unroll
+      for (int q = 0; q < NCH; ++q) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __half2 h2 = __floats2half2_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+          w[e] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        hp[q] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      __half* dst = orow < 0 ? nullptr
+                    : side2  ? static_cast<__half*>(ep.out2) + static_cast<size_t>(orow) * ep.ld_out2 + oc0 - ep.split_n
+                             : static_cast<__half*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0;
+      warp_store_rows<NCH>(stg, hp, dst, threadIdx.x & 31);
+    }
+    return;
+  }
+  if (orow < 0) return;
   if (EPI == kEpiF32 || EPI == kEpiHead) {
     float* dst = static_cast<float*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0;
     if ((EPI == kEpiF32 || EPI == kEpiHead) && full) {  // (head: no residual / norm outputs)
@@ -274,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* stg_base = smem + S * Cfg::kStageBytes + 1024;  // [kEpiWarps][32][128 B]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -393,6 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int ew = warp - 2;
+    const bool no_coalesce = !ep.coalesce;
     const int q = warp & 3;                // TMEM lane quarter this warp may access
     const int half = ew >> 2;              // column half of the tile
     int it = 0;
@@ -430,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         row_scale = 1.0f / sqrtf(ss * ep.rms_inv_d + 1e-5f);
       }
+      if (ew == 0 && lane == 0 && it == 0) stamp(13);  // epilogue inputs (residual, row scale) issued
       mbar_wait(&tfull[buf], use & 1);
       if (ew == 0 && lane == 0 && it == 0) stamp(5);
       tc_fence_after();
@@ -438,13 +525,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t raw[32];
         tmem_ld_32x32(acc + c * 32, raw);
         tc_wait_ld();
+        if (ew == 0 && lane == 0 && it == 0 && c == c0) stamp(11);
         if (c + 1 == c1) {
           // accumulator fully read: hand it back to the MMA warp early
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);
         }
-        epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res, row_scale, side2);
+        epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res, row_scale, side2,
+                       (no_coalesce || (EPI != kEpiF32 && EPI != kEpiHead)) ? 0u
+                                                                            : smem_u32(stg_base + ew * 4096));
+        if (ew == 0 && lane == 0 && it == 0 && c == c0) stamp(12);
         if (acc_res && c + 2 < c1) prefetch_residual(ep, orow, n0 + (c + 2) * 32, res);
       };
 #pragma unroll 1
@@ -929,9 +1020,9 @@ void set_attr() {
   static std::once_flag once;
   std::call_once(once, [] {
     PSWA_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, 1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kSmem));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::smem_for(EPI)));
     PSWA_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, 2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kSmem));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::smem_for(EPI)));
   });
 }
 
@@ -955,7 +1046,7 @@ template <int BN, int EPI>
 void launch_epi(const GemmPlan& p, cudaStream_t st) {
   const int tiles_m = (p.M + kBM - 1) / kBM;
   const int tiles = tiles_m * (p.N / BN);
-  const int smem = GemmCfg<BN>::kSmem;
+  const int smem = GemmCfg<BN>::smem_for(EPI);
   if (p.cluster == 2) {
     const int units = (tiles_m + 1) / 2 * (p.N / BN);
     const int clusters = units < sm_count() / 2 ? units : sm_count() / 2;
@@ -1057,6 +1148,9 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
                     ? 1
                     : 0;
   }
+  // coalesced epilogue stores through the per-warp smem stage (gemm_tc_kernel)
+  static const bool no_coalesce = std::getenv("PSWA_GEMM_NO_COALESCE") != nullptr;
+  p->epi.coalesce = no_coalesce ? 0 : 1;
   // CTA pairs sharing B through TMA multicast: correct and available, but
   // measured neutral-to-slower on B200 (the L2 already dedups concurrent B
   // reads; 10.56 vs 10.44 ms / frame; on the M = 2040 step GEMMs alone

@@ -47,6 +47,7 @@ struct GemmEpi {
   int ld_rms = 0, rms_parts = 0;
   float rms_inv_d = 0.0f;
   int v8 = 0;  // set by gemm_plan: every output row segment is 32 B aligned (256-bit ld/st)
+  int coalesce = 0;  // set by gemm_plan: stores go through the per-warp smem stage
   // Second fp16 output (fused projections sharing A, e.g. Q | K V): output
   // columns >= split_n go to out2[row_map2[m]][n - split_n] (split_n % BN == 0).
   void* out2 = nullptr;

@@ -34,7 +34,8 @@ y, _ = dec.decode_frame(hyper, main, fidx=4, advance=False)
 assert np.array_equal(y, frames[4])
 SLOTS = 16
 names = {1: "setup", 2: "pdl_wait", 10: "tma_issued", 3: "first_stage", 4: "mma_done",
-         5: "acc_ready", 6: "epi_done", 7: "exit"}
+         13: "epi_inputs", 5: "acc_ready", 11: "chunk0_ld", 12: "chunk0_done", 6: "epi_done",
+         7: "exit"}
 for op in sys.argv[1:] or ["step_wq", "ctx_ffn_gu"]:
     buf = np.zeros(SLOTS * 1024, np.uint64)
     lib().pswa_debug_gemm_trace(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), buf.size)  # clears
@@ -45,7 +46,7 @@ for op in sys.argv[1:] or ["step_wq", "ctx_ffn_gu"]:
     g0 = ctas[:, 8].min()
     print(f"{op}: {len(ctas)} CTAs, bench {us:.2f} us/launch; start spread "
           f"{(ctas[:, 8].max() - g0) / 1e3:.2f} us, last exit {(ctas[:, 9].max() - g0) / 1e3:.2f} us")
-    for k in (1, 2, 10, 3, 4, 5, 6, 7):
+    for k in (1, 2, 10, 3, 4, 13, 5, 11, 12, 6, 7):
         d = ctas[:, k] - ctas[:, 0]
         d = d[ctas[:, k] != 0]
         if len(d):
