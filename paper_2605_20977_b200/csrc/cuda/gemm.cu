@@ -218,10 +218,8 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
   if (oc0 >= ep.n_store) return;  // (warp-uniform)
   const bool full = oc0 + ncols <= ep.n_store;
   // warp-cooperative coalesced stores (every lane takes part, rows < 0
-  // skipped) for the fp32 outputs (residual stream + its fp16 copy, heads):
-  // measured 6.7 -> 6.4 us (out-proj), 7.5 -> 7.2 us (channel down); the
-  // fp16 / SwiGLU outputs (32 / 64 B per row) measured faster row-per-lane
-  if ((EPI == kEpiF32 || EPI == kEpiHead) && stg && full && ep.v8) {
+  // skipped): measured 6.7 -> 6.4 us (out-proj), 7.5 -> 7.2 us (channel down)
+  if (stg && full && ep.v8) {
     if (EPI == kEpiF32 || EPI == kEpiHead) {
       float ss = 0.0f;
       uint4 ov[8], hp[4];
@@ -358,7 +356,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* stg_base = smem + S * Cfg::kStageBytes + 1024;  // [kEpiWarps][32][128 B]
+  // per-warp 32 x 128 B store stages (warp_store_rows): a CTA with a single
+  // tile reuses its A stage ring (all MMAs have read it when the accumulator
+  // is ready); persistent multi-tile CTAs of the fp32-output kinds use the
+  // region allocated after the barriers; the others store row-per-lane
+  const bool single_tile = CL == 1 && num_tiles <= static_cast<int>(gridDim.x);
+  uint8_t* stg_base = single_tile ? sa
+                      : (EPI == kEpiF32 || EPI == kEpiHead) ? smem + S * Cfg::kStageBytes + 1024 : nullptr;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -533,8 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(&tempty[buf]);
         }
         epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res, row_scale, side2,
-                       (no_coalesce || (EPI != kEpiF32 && EPI != kEpiHead)) ? 0u
-                                                                            : smem_u32(stg_base + ew * 4096));
+                       (no_coalesce || !stg_base) ? 0u : smem_u32(stg_base + ew * 4096));
         if (ew == 0 && lane == 0 && it == 0 && c == c0) stamp(12);
         if (acc_res && c + 2 < c1) prefetch_residual(ep, orow, n0 + (c + 2) * 32, res);
       };
