@@ -72,19 +72,49 @@ __device__ __forceinline__ float silu_f(float v) {
 }
 
 // Elementwise part of the epilogue for 32 accumulator columns [n0, n0+32).
+// Head column parameters of columns [n0, n0 + 32): bias (0 past n_store)
+// and rate scale (1 on the sigma columns, which read none).
+__device__ __forceinline__ void head_params(const GemmEpi& ep, int n0, float4 (&b)[8], float4 (&s)[8]) {
+  float bv[32], sv[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    bv[j] = (ep.bias && n0 + j < ep.n_store) ? ep.bias[n0 + j] : 0.0f;
+    sv[j] = (ep.scale && n0 + j < ep.split) ? ep.scale[n0 + j] : 1.0f;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    b[q] = make_float4(bv[4 * q], bv[4 * q + 1], bv[4 * q + 2], bv[4 * q + 3]);
+    s[q] = make_float4(sv[4 * q], sv[4 * q + 1], sv[4 * q + 2], sv[4 * q + 3]);
+  }
+}
+__device__ __forceinline__ float f4_at(const float4* a, int j) {
+  const float4 x = a[j >> 2];
+  return (j & 3) == 0 ? x.x : (j & 3) == 1 ? x.y : (j & 3) == 2 ? x.z : x.w;
+}
+
 template <int EPI>
-__device__ __forceinline__ void epi_values(const GemmEpi& ep, int n0, float (&v)[32]) {
+__device__ __forceinline__ void epi_values(const GemmEpi& ep, int n0, float (&v)[32],
+                                           const float4* hb = nullptr, const float4* hs = nullptr) {
   if (EPI == kEpiHead) {
     // mu = (v + b) * scale; sigma = 0.11 + softplus(v + b) with softplus(x)
     // = x above 30, exp(x) below -30, log1p(exp(x)) between; evaluated
     // branch-free with the column parameters loaded up front (per-element
-    // branches and loads made this epilogue ~11k cycles per tile)
+    // branches and loads made this epilogue ~11k cycles per tile), or
+    // before the accumulator wait (hb / hs: head_params)
     float b[32], sc[32];
+    if (hb) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      b[j] = ep.bias ? ep.bias[n0 + j] : 0.0f;
-      // the rate scales cover the mu columns only (sigma columns read none)
-      sc[j] = (ep.scale && n0 + j < ep.split) ? ep.scale[n0 + j] : 1.0f;
+      for (int j = 0; j < 32; ++j) {
+        b[j] = f4_at(hb, j);
+        sc[j] = f4_at(hs, j);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        b[j] = ep.bias ? ep.bias[n0 + j] : 0.0f;
+        // the rate scales cover the mu columns only (sigma columns read none)
+        sc[j] = (ep.scale && n0 + j < ep.split) ? ep.scale[n0 + j] : 1.0f;
+      }
     }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
@@ -208,11 +238,12 @@ __device__ __forceinline__ void warp_store_rows(uint32_t stg, const uint4 (&d)[N
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
                                           const uint32_t (&raw)[32], const float4 (&res)[8],
-                                          float row_scale, bool side2, uint32_t stg = 0) {
+                                          float row_scale, bool side2, uint32_t stg = 0,
+                                          const float4* hb = nullptr, const float4* hs = nullptr) {
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]) * row_scale;
-  epi_values<EPI>(ep, n0, v);
+  epi_values<EPI>(ep, n0, v, hb, hs);
   const int ncols = EPI == kEpiSwiGLU ? 16 : 32;
   const int oc0 = EPI == kEpiSwiGLU ? (n0 >> 1) : n0;
   if (oc0 >= ep.n_store) return;  // (warp-uniform)
@@ -503,6 +534,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         prefetch_residual(ep, orow, n0 + c0 * 32, resA);
         if (c0 + 1 < c1) prefetch_residual(ep, orow, n0 + (c0 + 1) * 32, resB);
       }
+      // head with one chunk per warp: its bias / rate scales (resA / resB)
+      // are loaded ahead of the accumulator wait as well
+      const bool head_pre = EPI == kEpiHead && c1 - c0 == 1;
+      if (head_pre) head_params(ep, n0 + c0 * 32, resA, resB);
       float row_scale = 1.0f;  // folded RMSNorm of A's row m
       if (ep.rms_ssq && m < M) {
         const float* sp = ep.rms_ssq + static_cast<size_t>(m) * ep.ld_rms;
@@ -537,7 +572,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(&tempty[buf]);
         }
         epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res, row_scale, side2,
-                       (no_coalesce || !stg_base) ? 0u : smem_u32(stg_base + ew * 4096));
+                       (no_coalesce || !stg_base) ? 0u : smem_u32(stg_base + ew * 4096),
+                       head_pre ? resA : nullptr, head_pre ? resB : nullptr);
         if (ew == 0 && lane == 0 && it == 0 && c == c0) stamp(12);
         if (acc_res && c + 2 < c1) prefetch_residual(ep, orow, n0 + (c + 2) * 32, res);
       };
