@@ -309,12 +309,21 @@ struct Rsv {
     return i < 2 ? (i == 0 ? cur.x : cur.y) : (i == 2 ? cur.z : cur.w);
   }
   __device__ __forceinline__ void advance() {
-    if (wi == 4) {
+    const uint32_t enter = wi == 4;
+    if (enter) {
       cur = nxt;
       wb += 16;
-      nxt = __ldg(reinterpret_cast<const uint4*>(pl + wb + 16));
       wi = 0;
     }
+    // the next window, loaded in place by an unconditional (predicated)
+    // instruction with tied operands: as a plain conditional load the
+    // compiler landed it in other registers and copied them at the loop back
+    // edge, which turned every window prefetch into a full-latency stall of
+    // the decode chain
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.u32 p, %5, 0;\n @p ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];\n}"
+        : "+r"(nxt.x), "+r"(nxt.y), "+r"(nxt.z), "+r"(nxt.w)
+        : "l"(pl + wb + 16), "r"(enter));
   }
   __device__ __forceinline__ void refill() {
     if (cnt < 2) {
@@ -446,16 +455,49 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
   uint32_t i_first = static_cast<uint32_t>(l) + static_cast<uint32_t>(L) - o0_mod;
   if (i_first >= static_cast<uint32_t>(L)) i_first -= static_cast<uint32_t>(L);
   const bool active = l < L && i_first < total;
-  // The lane state and payload bytes are read before the PDL wait: this grid
-  // starts once the head GEMM before it has passed its own wait, so every
-  // earlier kernel (the previous phase, which wrote the lane states, and the
-  // lane init) has completed. Only mu/sigma come from the immediate
-  // predecessor.
+  // per-thread parameter slots in shared memory ([q][thread]: conflict-free):
+  // the decode loop below is not unrolled, so its body exists once in the
+  // binary (a 16x unrolled body overflowed the instruction cache)
+  constexpr int kB = kDecB;
+  const uint32_t ntot = static_cast<uint32_t>(total);
+  const int Ldiv = L / per, Lmod = L - Ldiv * per;
+  const double* bt = bits_table(cdf);
+  int4* s_par = reinterpret_cast<int4*>(s_scales + kScales);  // {table | mu offset, mu, dst, dst16}
+  int* s_out = reinterpret_cast<int*>(s_par + kB * blockDim.x);  // k | escape bits << 16
+  double* s_cost = reinterpret_cast<double*>(s_out + kB * blockDim.x);  // [q][thread] symbol costs
+  const int tid = threadIdx.x, nth = blockDim.x;
+  auto batch_size = [&](uint32_t ib) {
+    return min(kB, static_cast<int>((ntot - ib + L - 1) / static_cast<uint32_t>(L)));
+  };
+  // index part of a batch's parameters (symbol i -> (k, j) = divmod(i, per),
+  // stepped by divmod(L, per): one division per batch): the mu/sigma offset
+  // and the y_hat destinations, from the constant row table only
+  auto batch_index = [&](uint32_t ib, int nq) {
+    int k = static_cast<int>(ib) / per, j = static_cast<int>(ib) - k * per;
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      if (q > 0) {
+        k += Ldiv;
+        j += Lmod;
+        if (j >= per) {
+          j -= per;
+          ++k;
+        }
+      }
+      if (q < nq) s_par[q * nth + tid] = make_int4(k * ldms + j, 0, rows[k] * C + c0 + j, k * ld16 + c0 + j);
+    }
+  };
+  // The lane state, payload bytes and the first batch's indexes are read
+  // before the PDL wait: this grid starts once the head GEMM before it has
+  // passed its own wait, so every earlier kernel (the previous phase, which
+  // wrote the lane states, and the lane init) has completed. Only mu/sigma
+  // come from the immediate predecessor.
   LaneState s;
   Rsv rs;
   if (active) {
     s = lanes[l];
     rs.init(pl, s.pos, s.end);
+    batch_index(i_first, batch_size(i_first));
   }
   pdl_wait();
   pdl_trigger();
@@ -470,56 +512,35 @@ __global__ void decode_phase_kernel(const uint8_t* __restrict__ pl, LaneState* _
   // 8192 lanes) in one batch. The bit-cost table loads are deferred to the
   // end of the batch (issued together, summed in symbol order) so their
   // latency is off the sequential decode chain.
-  constexpr int kB = kDecB;
-  const uint32_t ntot = static_cast<uint32_t>(total);
-  const int Ldiv = L / per, Lmod = L - Ldiv * per;
-  const double* bt = bits_table(cdf);
-  // per-thread parameter slots in shared memory ([q][thread]: conflict-free):
-  // the decode loop below is not unrolled, so its body exists once in the
-  // binary (a 16x unrolled body overflowed the instruction cache)
-  int4* s_par = reinterpret_cast<int4*>(s_scales + kScales);  // {table, mu, dst, dst16}
-  int* s_out = reinterpret_cast<int*>(s_par + kB * blockDim.x);  // k | escape bits << 16
-  double* s_cost = reinterpret_cast<double*>(s_out + kB * blockDim.x);  // [q][thread] symbol costs
-  const int tid = threadIdx.x, nth = blockDim.x;
   for (uint32_t ib = i_first; ib < ntot; ib += static_cast<uint32_t>(kB) * L) {
-    const int nq = min(kB, static_cast<int>((ntot - ib + L - 1) / static_cast<uint32_t>(L)));
+    const int nq = batch_size(ib);
+    if (ib != i_first) batch_index(ib, nq);
     {
       float mu_f[kB], sg_f[kB];
-      int dst[kB], k16[kB];
       // all loads of the batch first (in flight together), then the table
-      // searches: interleaving them exposes one load latency per symbol.
-      // (k, j) = divmod(i, per) stepped by divmod(L, per): one division per batch
-      int k = static_cast<int>(ib) / per, j = static_cast<int>(ib) - k * per;
+      // searches: interleaving them exposes one load latency per symbol
 #pragma unroll
       for (int q = 0; q < kB; ++q) {
-        if (q > 0) {
-          k += Ldiv;
-          j += Lmod;
-          if (j >= per) {
-            j -= per;
-            ++k;
-          }
-        }
         if (q < nq) {
-          mu_f[q] = musig[static_cast<size_t>(k) * ldms + j];
-          sg_f[q] = musig[static_cast<size_t>(k) * ldms + sig_off + j];
-          dst[q] = rows[k] * C + c0 + j;
-          k16[q] = k * ld16 + c0 + j;
+          const int off = s_par[q * nth + tid].x;
+          mu_f[q] = musig[off];
+          sg_f[q] = musig[off + sig_off];
         }
       }
       if (taps.mu) {  // the decoder's own entropy parameters (parity / BitStats taps)
 #pragma unroll
         for (int q = 0; q < kB; ++q)
           if (q < nq) {
-            taps.mu[dst[q]] = mu_f[q];
-            taps.sigma[dst[q]] = sg_f[q];
+            const int dst = s_par[q * nth + tid].z;
+            taps.mu[dst] = mu_f[q];
+            taps.sigma[dst] = sg_f[q];
           }
       }
 #pragma unroll
       for (int q = 0; q < kB; ++q)
         if (q < nq)
-          s_par[q * nth + tid] =
-              make_int4(scale_index(s_scales, sg_f[q]), __float2int_rn(mu_f[q]), dst[q], k16[q]);
+          *reinterpret_cast<int2*>(&s_par[q * nth + tid]) =
+              make_int2(scale_index(s_scales, sg_f[q]), __float2int_rn(mu_f[q]));
     }
 #pragma unroll 1
     for (int q = 0; q < nq; ++q) {
