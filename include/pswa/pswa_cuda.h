@@ -261,7 +261,10 @@ int pswa_gpu_band_link(pswa_gpu* h, const void* up_blob, size_t up_len, const vo
                        size_t down_len);
 
 /* ---- operator-level entry points (device pointers, on `stream`) -------- */
-/* C[M,N] = A[M,K] . B[N,K]^T, fp16 in, fp32 accumulate; out fp16 or fp32. */
+/* C[M,N] = A[M,K] . B[N,K]^T, fp16 in, fp32 accumulate; out fp16 or fp32.
+ * force_bn: 0 automatic tile width; 64 / 128 / 256 forced; -1 CTA-pair
+ * (cta_group::2) 256 x 256 tiles; -2 split-K CTA pairs (128 x 128 tiles, K
+ * halves reduced through distributed shared memory). */
 int pswa_gpu_op_gemm_f16(const void* A, int lda, int M, const void* B, int ldb, int N, int K,
                          void* C, int ldc, int out_f32, int accumulate, const float* bias,
                          const float* scale, int act, int force_bn, void* stream);

@@ -371,6 +371,10 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
   }
 }
 
+#ifdef PSWA_GEMM_TRACE_BUILD
+__device__ int g_gemm_exp = 0;
+#endif
+
 template <int BN, int EPI, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
@@ -408,6 +412,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto stamp = [&](int slot) {
     if (tr) tr[slot] = clock64();
   };
+  // timing experiments of the trace build (gemm_set_experiment): 1 = no
+  // MMAs, 2 = no operand loads after the first pipeline round
+#ifdef PSWA_GEMM_TRACE_BUILD
+  const int exp_flags = g_gemm_exp;
+#else
+  constexpr int exp_flags = 0;
+#endif
+  const bool exp_no_mma = exp_flags & 1, exp_no_tma = exp_flags & 2;
   if (tr && threadIdx.x == 0) {
     unsigned long long g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -471,6 +483,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+          if (exp_no_tma) {  // timing experiment: stale operands
+            mbar_arrive(&full[s]);
+            continue;
+          }
           mbar_expect_tx(&full[s], Cfg::kStageBytes);
           tma_load_2d(sa + s * Cfg::kABytes, &tma, &full[s], kb * kBK, m0);
           if (CL > 1)
@@ -498,10 +514,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t a_base = smem_u32(sa + s * Cfg::kABytes);
           const uint32_t b_base = smem_u32(sb + s * Cfg::kBBytes);
+          if (!exp_no_mma) {
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk)
-            tc_mma_f16(acc, umma_desc_k_sw128(a_base + kk * 32), umma_desc_k_sw128(b_base + kk * 32),
-                       idesc, (kb | kk) != 0 ? 1u : 0u);
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              tc_mma_f16(acc, umma_desc_k_sw128(a_base + kk * 32), umma_desc_k_sw128(b_base + kk * 32),
+                         idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
           if (CL > 1)
             tc_commit_mc(&empty[s], static_cast<uint16_t>((1u << CL) - 1));
           else
@@ -1012,6 +1030,171 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------- split-K pairs --
+// The M = 2040 step GEMMs are paced per SM by the tensor pipe's per-
+// instruction floor (a K = 16 tcgen05.mma costs ~92 cycles for any N <= 128,
+// tools/umma_probe.cu) and by the operand stream into shared memory, not by
+// the chip. A cluster of two CTAs therefore splits one 128 x 128 output tile
+// along K: rank r accumulates k-blocks [r h, min(KB, (r + 1) h)), h =
+// ceil(KB / 2), in its own TMEM (half the MMAs and half the operand bytes of
+// a CTA each). Rank r owns output columns [64 r, 64 r + 64): it sends its
+// partial sums of the other 64 columns into the peer's receive buffer
+// (st.shared::cluster, 16 B per lane, chunk-swizzled rows), and after one
+// cluster barrier adds the peer's partial of its own columns and runs the
+// usual epilogue (8 warps, one 32 x 32 chunk each). Every output is
+// fl(P0 + P1) with P_r the ascending sum over rank r's k-blocks: a function
+// of K alone (fp32 addition commutes), so results are bitwise identical for
+// any M and schedule; the engine requests it per layer (GemmEpi::split_k),
+// so an encoder and a decoder program agree.
+constexpr int kSBN = 128;
+constexpr int kSStages = 5;
+constexpr int kSABytes = kBM * kBK * 2, kSBBytes = kSBN * kBK * 2;
+constexpr int kSStageBytes = kSABytes + kSBBytes;
+constexpr int kSRecvBytes = kBM * 64 * 4;  // the peer's partials of this CTA's 64 columns
+constexpr int kSSmem = kSStages * kSStageBytes + kSRecvBytes + 1024 + 256;
+
+// receive buffer: [128 rows][64 fp32] (256 B rows), 16 B piece j of column
+// half `hsel` of row r at hsel * 128 + ((j ^ (r & 7)) << 4): the 32 lanes
+// (one row each) of a warp write / read conflict-free
+__device__ __forceinline__ uint32_t recv_off(int row, int hsel, int j) {
+  return static_cast<uint32_t>(row * 256 + hsel * 128 + ((j ^ (row & 7)) << 4));
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_splitk_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, int M,
+                       int K, int tiles_n, const __grid_constant__ GemmEpi ep) {
+  constexpr int S = kSStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + S * kSABytes;
+  uint8_t* recv = smem + S * kSStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(recv + kSRecvBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
+  const int tile = blockIdx.x >> 1;
+  const int m0 = (tile / tiles_n) * kBM, n0 = (tile % tiles_n) * kSBN;
+  const int KB = K / kBK, h = (KB + 1) / 2;
+  const int kb0 = static_cast<int>(rank) * h, nkb = min(KB, kb0 + h) - kb0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tma);
+    tma_prefetch(&tmb);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kSBN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // weights (B) of the first stages requested before the PDL wait
+  int npre = 0;
+  if (warp == 0 && lane == 0) {
+    npre = min(S, nkb);
+    for (int i = 0; i < npre; ++i) {
+      mbar_expect_tx(&full[i], kSStageBytes);
+      tma_load_2d(sb + i * kSBBytes, &tmb, &full[i], (kb0 + i) * kBK, n0);
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % S, round = i / S, kb = kb0 + i;
+        if (i < npre) {
+          tma_load_2d(sa + s * kSABytes, &tma, &full[s], kb * kBK, m0);
+          continue;
+        }
+        if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+        mbar_expect_tx(&full[s], kSStageBytes);
+        tma_load_2d(sa + s * kSABytes, &tma, &full[s], kb * kBK, m0);
+        tma_load_2d(sb + s * kSBBytes, &tmb, &full[s], kb * kBK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_f16_f32(kBM, kSBN);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % S;
+        mbar_wait(&full[s], (i / S) & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(sa + s * kSABytes);
+        const uint32_t b_base = smem_u32(sb + s * kSBBytes);
+#pragma unroll
+        for (int kk = 0; kk < kBK / 16; ++kk)
+          tc_mma_f16(tmem, umma_desc_k_sw128(a_base + kk * 32), umma_desc_k_sw128(b_base + kk * 32), idesc,
+                     (i | kk) != 0 ? 1u : 0u);
+        tc_commit(&empty[s]);
+      }
+      tc_commit(tfull);
+    }
+  }
+  const int ew = warp - 2, q = warp & 3, hsel = ew >> 2;
+  const int row = q * 32 + lane, m = m0 + row;
+  const int orow = m < M ? (ep.row_map ? ep.row_map[m] : m) : -1;
+  const int c_own = 2 * static_cast<int>(rank) + hsel, c_exp = 2 * static_cast<int>(peer) + hsel;
+  uint32_t own[32];
+  float4 res[8];
+  float row_scale = 1.0f;
+  if (warp >= 2) {
+    if (EPI == kEpiF32 && ep.accumulate) prefetch_residual(ep, orow, n0 + c_own * 32, res);
+    if (ep.rms_ssq && m < M) {
+      const float* sp = ep.rms_ssq + static_cast<size_t>(m) * ep.ld_rms;
+      float ss = 0.0f;
+      for (int k = 0; k < ep.rms_parts; ++k) ss += sp[k];
+      row_scale = 1.0f / sqrtf(ss * ep.rms_inv_d + 1e-5f);
+    }
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const uint32_t acc = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    uint32_t xp[32];
+    tmem_ld_32x32(acc + c_exp * 32, xp);
+    tmem_ld_32x32(acc + c_own * 32, own);
+    tc_wait_ld();
+    const uint32_t rbase = mapa_shared(smem_u32(recv), peer);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      st_cluster_v4(rbase + recv_off(row, hsel, j), make_uint4(xp[4 * j], xp[4 * j + 1], xp[4 * j + 2], xp[4 * j + 3]));
+  }
+  // the peer's partials of this CTA's columns have landed (release / acquire)
+  cluster_sync();
+  if (warp >= 2) {
+    const uint32_t rl = smem_u32(recv);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint4 v;
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                   : "r"(rl + recv_off(row, hsel, j)));
+      own[4 * j] = __float_as_uint(__uint_as_float(own[4 * j]) + __uint_as_float(v.x));
+      own[4 * j + 1] = __float_as_uint(__uint_as_float(own[4 * j + 1]) + __uint_as_float(v.y));
+      own[4 * j + 2] = __float_as_uint(__uint_as_float(own[4 * j + 2]) + __uint_as_float(v.z));
+      own[4 * j + 3] = __float_as_uint(__uint_as_float(own[4 * j + 3]) + __uint_as_float(v.w));
+    }
+    // coalesced stores staged in the (now idle) A ring, 4 KB per warp
+    epi_chunk<EPI>(ep, orow, n0 + c_own * 32, own, res, row_scale, false,
+                   ep.coalesce ? smem_u32(sa + ew * 4096) : 0u);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free(tmem, kSBN);
+  }
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -1098,6 +1281,13 @@ void launch_epi(const GemmPlan& p, cudaStream_t st) {
   }
 }
 
+template <int EPI>
+void launch_splitk(const GemmPlan& p, cudaStream_t st) {
+  const int tiles_n = p.N / kSBN, tiles = ((p.M + kBM - 1) / kBM) * tiles_n;
+  launch_kc(gemm_splitk_kernel<EPI>, dim3(2 * tiles), dim3(kThreads), kSSmem, st, 2u, p.ta, p.tb, p.M, p.K,
+            tiles_n, p.epi);
+}
+
 template <int BN>
 void launch(const GemmPlan& p, int kind, cudaStream_t st) {
   switch (kind) {
@@ -1135,6 +1325,15 @@ unsigned long long* trace_buffer() {
     return b;
   }();
   return buf;
+}
+
+void gemm_set_experiment(int flags) {
+#ifdef PSWA_GEMM_TRACE_BUILD
+  PSWA_CUDA(cudaDeviceSynchronize());
+  PSWA_CUDA(cudaMemcpyToSymbol(g_gemm_exp, &flags, sizeof(int)));
+#else
+  (void)flags;
+#endif
 }
 
 bool gemm_trace_read(unsigned long long* out, int n) {
@@ -1212,8 +1411,26 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
     p->BN = bn;
     p->cluster = 1;
   }
+  // split-K CTA pairs (gemm_splitk_kernel), on request: fp32 / fp16 outputs
+  static const bool no_splitk = std::getenv("PSWA_GEMM_NO_SPLITK") != nullptr;
+  const int kind0 = epi_kind(epi);
+  p->splitk = !p->pair && !no_splitk && epi.split_k && force_bn == 0 && epi.out2 == nullptr &&
+              (kind0 == kEpiF32 || kind0 == kEpiF16) && N % kSBN == 0 && K / kBK >= 2;
+  if (p->splitk) {
+    bn = kSBN;
+    p->BN = bn;
+    p->cluster = 1;
+  }
   make_tmap(&p->ta, A, lda, M, K, kBM);
   make_tmap(&p->tb, B, ldb, N, K, p->pair ? kPBN / 2 : bn / p->cluster);
+  if (p->splitk) {
+    static std::once_flag once_sk;
+    std::call_once(once_sk, [] {
+      PSWA_CUDA(cudaFuncSetAttribute(gemm_splitk_kernel<kEpiF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem));
+      PSWA_CUDA(cudaFuncSetAttribute(gemm_splitk_kernel<kEpiF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem));
+    });
+    return;
+  }
   if (p->pair) {
     static std::once_flag once_pair;
     std::call_once(once_pair, [] {
@@ -1286,6 +1503,14 @@ void gemm_run(const GemmPlan& p, cudaStream_t stream) {
       case kEpiSwiGLU: launch_kc(gemm_pair_kernel<kEpiSwiGLU>, dim3(2 * clusters), dim3(kThreads), kPSmem, stream, 2u, p.ta, p.tb, p.M, p.K, tiles_mp, tiles_n, p.epi); break;
       default: launch_kc(gemm_pair_kernel<kEpiHead>, dim3(2 * clusters), dim3(kThreads), kPSmem, stream, 2u, p.ta, p.tb, p.M, p.K, tiles_mp, tiles_n, p.epi); break;
     }
+    PSWA_LAUNCH_CHECK();
+    return;
+  }
+  if (p.splitk) {
+    if (kind == kEpiF32)
+      launch_splitk<kEpiF32>(p, stream);
+    else
+      launch_splitk<kEpiF16>(p, stream);
     PSWA_LAUNCH_CHECK();
     return;
   }

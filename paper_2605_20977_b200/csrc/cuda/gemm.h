@@ -48,6 +48,10 @@ struct GemmEpi {
   float rms_inv_d = 0.0f;
   int v8 = 0;  // set by gemm_plan: every output row segment is 32 B aligned (256-bit ld/st)
   int coalesce = 0;  // set by gemm_plan: stores go through the per-warp smem stage
+  // request: split K over a CTA pair (fp32 / fp16 outputs, N % 128 == 0):
+  // every output is fl(P0 + P1) of the two halves' ascending sums, the same
+  // for any M -- a layer must request it in every program that runs it
+  int split_k = 0;
   // Second fp16 output (fused projections sharing A, e.g. Q | K V): output
   // columns >= split_n go to out2[row_map2[m]][n - split_n] (split_n % BN == 0).
   void* out2 = nullptr;
@@ -61,6 +65,10 @@ constexpr int kGemmTraceSlots = 16;
 // Copies the stamps written since the previous call (n words) to host and
 // clears them; false when tracing is off.
 bool gemm_trace_read(unsigned long long* out, int n);
+// Trace builds only: timing experiments of gemm_tc_kernel (1 = skip the
+// MMAs, 2 = skip operand loads after the first pipeline round); results
+// are garbage while set. No-op in production builds.
+void gemm_set_experiment(int flags);
 
 struct GemmPlan {
   CUtensorMap ta;
@@ -68,6 +76,7 @@ struct GemmPlan {
   int M = 0, N = 0, K = 0, BN = 0;
   int cluster = 1;  // 2: CTA pairs multicasting the shared B tile
   bool pair = false;  // cta_group::2 256 x 256 tiles (large M, N % 256 == 0)
+  bool splitk = false;  // split-K CTA pairs, 128 x 128 tiles (GemmEpi::split_k)
   GemmEpi epi;
 };
 

@@ -290,6 +290,12 @@ extern "C" __attribute__((visibility("default"))) int pswa_debug_gemm_trace(unsi
   });
 }
 
+// Debug export for tools/gemm_trace.py: GEMM timing experiments (trace
+// builds only; see pswa_dev::gemm_set_experiment).
+extern "C" __attribute__((visibility("default"))) int pswa_debug_gemm_experiment(int flags) {
+  return guard([&] { pswa_dev::gemm_set_experiment(flags); });
+}
+
 // ---- sequences ----------------------------------------------------------------
 int pswa_gpu_encode_sequence(pswa_gpu* h, const int32_t* frames, int n_frames, int gop_size,
                              int rate_idx, uint8_t* out, size_t cap, size_t* len) {

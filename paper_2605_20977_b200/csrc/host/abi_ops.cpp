@@ -37,6 +37,10 @@ extern "C" int pswa_gpu_op_gemm_f16(const void* A, int lda, int M, const void* B
     ep.scale = scale;
     ep.act = act;
     if (act == pswa_dev::kActHead) ep.split = N / 2;
+    if (force_bn == -2) {  // split-K CTA pairs
+      ep.split_k = 1;
+      force_bn = 0;
+    }
     pswa_dev::GemmPlan p;
     pswa_dev::gemm_plan(&p, static_cast<const __half*>(A), lda, M,
                         static_cast<const __half*>(B), ldb, N, K, ep, force_bn);

@@ -12,11 +12,12 @@
 
 namespace pswa_host {
 
-// 2: numerics revision 2 of the device entropy model (SiLU via tanh.approx,
-// softplus via __expf/__logf in the GEMM epilogues). A symbol decodes only
-// under the exact mu/sigma that coded it, so streams of another numerics
-// revision are refused instead of decoding to wrong latents.
-constexpr uint16_t kContainerVersion = 2;
+// Numerics revision of the device entropy model: 2 = SiLU via tanh.approx,
+// softplus via __expf/__logf in the GEMM epilogues; 3 = the spatial blocks'
+// down projections reduce K as two halves (split-K CTA pairs). A symbol
+// decodes only under the exact mu/sigma that coded it, so streams of another
+// numerics revision are refused instead of decoding to wrong latents.
+constexpr uint16_t kContainerVersion = 3;
 constexpr size_t kContainerHeader = 64;
 
 struct ContainerHeader {

@@ -32,6 +32,9 @@ for f in frames[:4]:
     dec.push_frame(f)
 y, _ = dec.decode_frame(hyper, main, fidx=4, advance=False)
 assert np.array_equal(y, frames[4])
+# GEMM_EXP=1: replays without MMAs, 2: without operand loads (timing only)
+EXP = int(os.environ.get("GEMM_EXP", "0"))
+lib().pswa_debug_gemm_experiment(EXP)
 SLOTS = 16
 names = {1: "setup", 2: "pdl_wait", 10: "tma_issued", 3: "first_stage", 4: "mma_done",
          13: "epi_inputs", 5: "acc_ready", 11: "chunk0_ld", 12: "chunk0_done", 6: "epi_done",

@@ -100,6 +100,93 @@ __global__ void probe2_kernel(const __grid_constant__ CUtensorMap map0, const __
   if (w == 0) out[blockIdx.x] = clock64() - t0;
 }
 
+
+// Variant 3: issuers = (warps x lanes-per-warp); lane stride 16 inside a warp.
+// Records the cycles the issuing thread spends inside the TMA issue and
+// inside the waits.
+__global__ void probe3_kernel(const __grid_constant__ CUtensorMap map0, int box_rows, int row_blocks, int kbs,
+                              int nbox, int inflight, int warps, int lanes, uint32_t box_bytes,
+                              unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bars[kSlots];
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSlots; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    tma_prefetch(&map0);
+  }
+  __syncthreads();
+  if (w >= warps || (ln % 16) != 0 || ln / 16 >= lanes) return;
+  const int id = w * lanes + ln / 16, nis = warps * lanes;
+  const int per = inflight / nis, nb = nbox / nis;
+  unsigned long long t_issue = 0, t_wait = 0, t_exp = 0;
+  auto issue = [&](int b) {
+    const int s = id * per + b % per;
+    const int g = b * nis + id;
+    const int rb = (blockIdx.x * 7 + g) % row_blocks, kb = g % kbs;
+    const unsigned long long a = clock64();
+    mbar_expect_tx(&bars[s], box_bytes);
+    const unsigned long long a2 = clock64();
+    tma_load_2d(smem + static_cast<size_t>(s) * box_bytes, &map0, &bars[s], kb * 64, rb * box_rows);
+    const unsigned long long a3 = clock64();
+    t_issue += a3 - a2;
+    t_exp += a2 - a;
+  };
+  const unsigned long long t0 = clock64();
+  int issued = 0;
+  for (; issued < per && issued < nb; ++issued) issue(issued);
+  for (int b = 0; b < nb; ++b) {
+    const int s = id * per + b % per;
+    const unsigned long long a = clock64();
+    mbar_wait(&bars[s], (b / per) & 1);
+    t_wait += clock64() - a;
+    if (issued < nb) issue(issued++);
+  }
+  if (id == 0) {
+    out[3 * blockIdx.x] = clock64() - t0;
+    out[3 * blockIdx.x + 1] = t_issue;
+    out[3 * blockIdx.x + 2] = t_wait;
+    if (blockIdx.x == 0) out[1000] = t_exp;
+  }
+}
+
+
+// Variant 4: burst of nb boxes (16 KB, precomputed coordinates) issued back
+// to back by `issuers` warps, then all waited for: the TMA unit's own
+// throughput without issue-loop latency. Repeated `reps` times.
+__global__ void probe4_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant__ CUtensorMap map1,
+                              int nb, int issuers, int reps, int mixed, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bars[kSlots];
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSlots; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    tma_prefetch(&map0);
+    tma_prefetch(&map1);
+  }
+  __syncthreads();
+  const int rb = blockIdx.x % 16;
+  unsigned long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    if (ln == 0 && w < issuers) {
+      for (int b = w; b < nb; b += issuers) {
+        // mixed: even boxes 16 KB (A-like, map0), odd boxes 8 KB (B-like, map1)
+        const bool small = mixed && (b & 1);
+        const uint32_t bytes = small ? 8192u : 16384u;
+        mbar_expect_tx(&bars[b], bytes);
+        tma_load_2d(smem + b * 16384, small ? &map1 : &map0, &bars[b], (r * nb + b) % 24 * 64, rb * 128);
+      }
+    }
+    if (threadIdx.x == 0)
+      for (int b = 0; b < nb; ++b) mbar_wait(&bars[b], r & 1);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = clock64() - t0;
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -114,7 +201,7 @@ int main() {
   cudaMalloc(&A, static_cast<size_t>(R) * K * 2);
   cudaMemset(A, 0, static_cast<size_t>(R) * K * 2);
   unsigned long long* out;
-  cudaMalloc(&out, 1024 * 8);
+  cudaMalloc(&out, 2048 * 8);
   cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   struct Cfg { int dims, rows, kbpb; };
   const Cfg cfgs[] = {{2, 64, 1}, {2, 128, 1}, {2, 256, 1}, {3, 64, 2}, {3, 128, 2}, {3, 128, 4}, {3, 64, 4}};
@@ -198,6 +285,65 @@ int main() {
         const double cyc = double(h[ctas / 2]) / nbox;
         std::printf("%s, %d CTAs: %.1f cycles per 16 KB box, %.1f B/clk\n", v.name, ctas, cyc, 16384 / cyc);
       }
+  }
+
+  {
+    auto mk = [&](CUtensorMap* m, __half* base, int rows) {
+      cuuint64_t d[2] = {(cuuint64_t)K, (cuuint64_t)R};
+      cuuint64_t st[1] = {(cuuint64_t)K * 2};
+      cuuint32_t box[2] = {64, (cuuint32_t)rows}, es[2] = {1, 1};
+      enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base, d, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    };
+    CUtensorMap mA;
+    mk(&mA, A, 128);
+    cudaFuncSetAttribute(probe3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    struct V { int warps, lanes, inflight; };
+    const V vs[] = {{1, 1, 8}, {1, 1, 1}, {1, 1, 2}, {1, 2, 8}, {2, 1, 8}, {4, 1, 8}, {8, 1, 8}};
+    for (const V& v : vs)
+      for (int ctas : {1, 128}) {
+        const int nbox = 64;
+        for (int rep = 0; rep < 2; ++rep)
+          probe3_kernel<<<ctas, 256, v.inflight * 16384 + 1024>>>(mA, 128, R / 128, K / 64, nbox, v.inflight,
+                                                                  v.warps, v.lanes, 16384, out);
+        cudaDeviceSynchronize();
+        std::vector<unsigned long long> h(3 * ctas);
+        cudaMemcpy(h.data(), out, 3 * ctas * 8, cudaMemcpyDeviceToHost);
+        unsigned long long te = 0;
+        cudaMemcpy(&te, out + 1000, 8, cudaMemcpyDeviceToHost);
+        std::printf("warps %d x lanes %d, inflight %d, %3d CTAs: %.1f cycles per box (CTA 0 issuer 0 per box: expect_tx %.1f, tma %.1f, wait %.1f)\n",
+                    v.warps, v.lanes, v.inflight, ctas, double(h[0]) / nbox, double(te) * v.warps * v.lanes / nbox,
+                    double(h[1]) * v.warps * v.lanes / nbox, double(h[2]) * v.warps * v.lanes / nbox);
+      }
+  }
+
+  {
+    auto mk = [&](CUtensorMap* m, __half* base, int rows) {
+      cuuint64_t d[2] = {(cuuint64_t)K, (cuuint64_t)R};
+      cuuint64_t st[1] = {(cuuint64_t)K * 2};
+      cuuint32_t box[2] = {64, (cuuint32_t)rows}, es[2] = {1, 1};
+      enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base, d, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    };
+    CUtensorMap m128, m64;
+    mk(&m128, A, 128);
+    mk(&m64, A, 64);
+    cudaFuncSetAttribute(probe4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int mixed : {0, 1})
+      for (int issuers : {1, 2, 4})
+        for (int ctas : {1, 128}) {
+          const int nb = 8, reps = 32;
+          for (int rep = 0; rep < 2; ++rep)
+            probe4_kernel<<<ctas, 128, 8 * 16384 + 1024>>>(m128, m64, nb, issuers, reps, mixed, out);
+          cudaDeviceSynchronize();
+          std::vector<unsigned long long> h(ctas);
+          cudaMemcpy(h.data(), out, ctas * 8, cudaMemcpyDeviceToHost);
+          std::sort(h.begin(), h.end());
+          const double per_burst = double(h[ctas / 2]) / reps;
+          const double bytes = mixed ? 4 * 16384.0 + 4 * 8192.0 : 8 * 16384.0;
+          std::printf("burst of 8 boxes (%s), %d issuers, %3d CTAs: %.0f cycles per burst, %.1f B/clk per SM\n",
+                      mixed ? "16K/8K alternating" : "16K", issuers, ctas, per_burst, bytes / per_burst);
+        }
   }
   return 0;
 }
