@@ -1,6 +1,7 @@
 // ORACLE — test infrastructure only.
 // Discretised-Gaussian CDF tables and the multi-lane range coder
 // (lane format DESIGN.md "Bitstream").
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -161,12 +162,21 @@ std::vector<uint8_t> encode_lanes(const std::vector<CodedSym>& syms, int lanes) 
       for (int i = nb; i >= 0; --i) e.bit(static_cast<int>((x >> i) & 1));
     }
   }
+  // header: lanes, symbol count, width of the length entries (2 when every
+  // lane is shorter than 64 KiB, else 4), then the lane lengths
+  size_t longest = 0;
+  for (auto& e : L) {
+    e.finish();
+    longest = std::max(longest, e.out.size());
+  }
+  const uint32_t w = longest < 65536 ? 2u : 4u;
   std::vector<uint8_t> out;
   put32le(out, static_cast<uint32_t>(lanes));
   put32le(out, static_cast<uint32_t>(syms.size()));
+  put32le(out, w);
   for (auto& e : L) {
-    e.finish();
-    put32le(out, static_cast<uint32_t>(e.out.size()));
+    const uint32_t n = static_cast<uint32_t>(e.out.size());
+    for (uint32_t b = 0; b < w; ++b) out.push_back(static_cast<uint8_t>(n >> (8 * b)));
   }
   for (auto& e : L) out.insert(out.end(), e.out.begin(), e.out.end());
   return out;
@@ -191,14 +201,16 @@ uint32_t next_byte(LaneDecoder::Lane& l, bool& err) {
 bool LaneDecoder::init(const uint8_t* data, size_t n) {
   error = false;
   lanes.clear();
-  if (n < 8) return !(error = true);
+  if (n < 12) return !(error = true);
   const uint32_t L = get32le(data);
   count = get32le(data + 4);
-  if (L == 0 || n < 8 + 4ull * L) return !(error = true);
-  size_t off = 8 + 4ull * L;
+  const uint32_t w = get32le(data + 8);
+  if (L == 0 || (w != 2 && w != 4) || n < 12 + static_cast<uint64_t>(w) * L) return !(error = true);
+  size_t off = 12 + static_cast<size_t>(w) * L;
   lanes.resize(L);
   for (uint32_t i = 0; i < L; ++i) {
-    const uint32_t len = get32le(data + 8 + 4ull * i);
+    const uint8_t* lp = data + 12 + static_cast<size_t>(w) * i;
+    const uint32_t len = w == 2 ? static_cast<uint32_t>(lp[0] | (lp[1] << 8)) : get32le(lp);
     if (len < 4 || off + len > n) return !(error = true);
     Lane& l = lanes[i];
     l.p = data + off;

@@ -1,8 +1,9 @@
 // Entropy coding on the device: quantised discretised-
 // Gaussian CDF tables, and the multi-lane 64-bit-state range coder.
 //
-// Lane format: [u32 L][u32 count][u32 len_0..L-1]
-// [lane 0 bytes]...; symbol ordinal o (canonical order: step, group, raster
+// Lane format (FORMAT.md §2): [u32 L][u32 count][u32 w][len_0..L-1, w bytes
+// each: 2 when every lane is shorter than 64 KiB, else 4][lane 0 bytes]...;
+// symbol ordinal o (canonical order: step, group, raster
 // position, channel) lives in lane o % L. Each lane is an independent range
 // coder with a 48-bit window (range in [2^40, 2^48)), big-endian byte
 // renormalisation, carry into written bytes and a 4-byte flush; the decoder
@@ -228,8 +229,8 @@ __device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t* ws) {
 }
 
 // One thread per lane, 128 lanes per block: each block first sums the
-// lengths of all lanes before it (coalesced 4 B loads; the 32 KB length
-// table is L2-resident), then scans its own 128. Spreading the lanes over
+// lengths of all lanes before it (coalesced 2 / 4 B loads; the length table
+// is L2-resident), then scans its own 128. Spreading the lanes over
 // many SMs matters: the 6 scattered first-byte reads per lane are ~50k L2
 // requests per frame, more than one SM's load path drains quickly.
 __global__ void __launch_bounds__(128) lanes_init_kernel(const uint8_t* __restrict__ pl,
@@ -241,12 +242,17 @@ __global__ void __launch_bounds__(128) lanes_init_kernel(const uint8_t* __restri
   __shared__ uint64_t ws[33];
   const uint32_t len = *len_p;
   const int t = threadIdx.x;
-  const uint32_t hdr = 8u + 4u * static_cast<uint32_t>(L);
-  if (len < hdr || rd32(pl) != static_cast<uint32_t>(L) || rd32(pl + 4) != expect) {
+  // header: L, symbol count, length-entry width w (2 or 4), then L lengths
+  const uint32_t w = len >= 12 ? rd32(pl + 8) : 0u;
+  const uint64_t hdr = 12u + static_cast<uint64_t>(w) * static_cast<uint32_t>(L);
+  if (len < 12 || (w != 2 && w != 4) || len < hdr || rd32(pl) != static_cast<uint32_t>(L) ||
+      rd32(pl + 4) != expect) {
     if (t == 0) atomicOr(status, 1);
     return;
   }
-  const uint32_t* lens = reinterpret_cast<const uint32_t*>(pl + 8);  // 256 B-aligned payload
+  const uint16_t* lens16 = reinterpret_cast<const uint16_t*>(pl + 12);  // 256 B-aligned payload
+  const uint32_t* lens32 = reinterpret_cast<const uint32_t*>(pl + 12);
+  auto lens = [&](int i) -> uint32_t { return w == 2 ? lens16[i] : lens32[i]; };
   const int l0 = blockIdx.x * blockDim.x;
   uint64_t before = 0;
   {
@@ -254,17 +260,17 @@ __global__ void __launch_bounds__(128) lanes_init_kernel(const uint8_t* __restri
     for (; i + 7 * 128 < l0; i += 8 * 128) {
       uint32_t v[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = lens[i + j * 128];
+      for (int j = 0; j < 8; ++j) v[j] = lens(i + j * 128);
 #pragma unroll
       for (int j = 0; j < 8; ++j) before += v[j];
     }
-    for (; i < l0; i += 128) before += lens[i];
+    for (; i < l0; i += 128) before += lens(i);
   }
   block_excl_scan(before, ws);
   before = ws[32];
   __syncthreads();  // ws is reused below
   const int l = l0 + t;
-  const uint32_t ln = l < L ? lens[l] : 0u;
+  const uint32_t ln = l < L ? lens(l) : 0u;
   const uint64_t off = hdr + before + block_excl_scan(ln, ws);
   if (l >= L) return;
   if (off + ln > len || ln < 4) {  // past the payload / shorter than the flush
@@ -904,32 +910,42 @@ __global__ void pack_offsets_kernel(const uint32_t* __restrict__ lens, int L, ui
   pdl_wait();
   pdl_trigger();
   __shared__ uint64_t ws[33];
+  __shared__ uint32_t longest;
   const int t = threadIdx.x;
   const int per = (L + blockDim.x - 1) / blockDim.x;
   const int l0 = t * per, l1 = min(L, l0 + per);
+  if (t == 0) longest = 0;
+  __syncthreads();
   uint64_t acc = 0;
-  for (int l = l0; l < l1; ++l) acc += lens[l];
-  const uint64_t excl = block_excl_scan(acc, ws);
+  uint32_t mx = 0;
+  for (int l = l0; l < l1; ++l) {
+    acc += lens[l];
+    mx = max(mx, lens[l]);
+  }
+  if (mx) atomicMax(&longest, mx);
+  const uint64_t excl = block_excl_scan(acc, ws);  // (its barriers publish `longest`)
+  // length entries of 2 bytes when every lane is shorter than 64 KiB
+  const uint32_t w = longest < 65536u ? 2u : 4u;
+  const uint64_t hdr = 12 + static_cast<uint64_t>(w) * L;
   if (t == 0) {
-    const uint64_t hdr = 8 + 4ull * L;
     *total = hdr + ws[32];
     if (hdr + ws[32] > cap) atomicOr(status, 8);
   }
-  const uint64_t hdr = 8 + 4ull * L;
   uint64_t off = hdr + excl;
   for (int l = l0; l < l1; ++l) {
     offs[l] = off;
     off += lens[l];
   }
-  auto wr32 = [&](uint64_t at, uint32_t v) {
-    if (at + 4 <= cap)
-      for (int b = 0; b < 4; ++b) payload[at + b] = static_cast<uint8_t>(v >> (8 * b));
+  auto wr = [&](uint64_t at, uint32_t v, uint32_t nb) {
+    if (at + nb <= cap)
+      for (uint32_t b = 0; b < nb; ++b) payload[at + b] = static_cast<uint8_t>(v >> (8 * b));
   };
   if (t == 0) {
-    wr32(0, static_cast<uint32_t>(L));
-    wr32(4, count);
+    wr(0, static_cast<uint32_t>(L), 4);
+    wr(4, count, 4);
+    wr(8, w, 4);
   }
-  for (int l = l0; l < l1; ++l) wr32(8 + 4ull * l, lens[l]);
+  for (int l = l0; l < l1; ++l) wr(12 + static_cast<uint64_t>(w) * l, lens[l], w);
 }
 
 __global__ void pack_copy_kernel(const uint8_t* __restrict__ enc, uint32_t cap_lane,

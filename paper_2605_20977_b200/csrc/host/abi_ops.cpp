@@ -92,7 +92,7 @@ extern "C" int pswa_gpu_op_encode_symbols(const int32_t* v, const int32_t* idx, 
     PSWA_CUDA(cudaMemcpyAsync(dv.p, v, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
     PSWA_CUDA(cudaMemcpyAsync(di.p, idx8.data(), n, cudaMemcpyHostToDevice, st));
     const uint32_t lane_cap = static_cast<uint32_t>(16 * ((n + lanes - 1) / lanes) + 16);
-    const uint64_t pcap = 8 + 4ull * lanes + static_cast<uint64_t>(lane_cap) * lanes;
+    const uint64_t pcap = 12 + 4ull * lanes + static_cast<uint64_t>(lane_cap) * lanes;
     DevBuf enc(static_cast<size_t>(lane_cap) * lanes), lens(sizeof(uint32_t) * lanes),
         lbits(sizeof(double) * lanes), payload(pcap), total(2 * sizeof(unsigned long long)),
         offs(sizeof(uint64_t) * lanes), status(sizeof(int)), bits(sizeof(double));
@@ -124,11 +124,11 @@ extern "C" int pswa_gpu_op_encode_symbols(const int32_t* v, const int32_t* idx, 
 extern "C" int pswa_gpu_op_decode_symbols(const uint8_t* payload, size_t len, const int32_t* idx,
                                           size_t n, int laplace, int32_t* v_out, double* bits_out) {
   return pswa_abi::guard([&] {
-    if (len < 8) throw pswa_abi::TruncatedError("payload shorter than its header");
+    if (len < 12) throw pswa_abi::TruncatedError("payload shorter than its header");
     check_idx(idx, n);
     uint32_t L = 0;
     std::memcpy(&L, payload, 4);
-    if (L < 1 || 8 + 4ull * L > len) throw pswa_abi::TruncatedError("bad lane count");
+    if (L < 1 || 12 + 2ull * L > len) throw pswa_abi::TruncatedError("bad lane count");
     cudaStream_t st = nullptr;
     PSWA_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     struct StreamGuard {

@@ -441,8 +441,8 @@ void Engine::alloc_all() {
   musig_ = dalloc<float>(nb * ms);
 
   const size_t nsym = static_cast<size_t>(HWo) * C, nz = static_cast<size_t>(D.hc) * D.zh * D.zw;
-  main_cap_ = 8 + 4ull * L + 6 * static_cast<size_t>(L) + 16 * nsym;
-  hyper_cap_ = 8 + 4ull * Lz + 6 * static_cast<size_t>(Lz) + 16 * nz;
+  main_cap_ = 12 + 4ull * L + 6 * static_cast<size_t>(L) + 16 * nsym;
+  hyper_cap_ = 12 + 4ull * Lz + 6 * static_cast<size_t>(Lz) + 16 * nz;
   // + 64 B: the decoder's byte reservoirs read up to 32 B past a lane's end
   d_main_ = dalloc<uint8_t>(main_cap_ + 64);
   d_hyper_ = dalloc<uint8_t>(hyper_cap_ + 64);
@@ -1372,7 +1372,7 @@ Program& Engine::program(const std::string& key) {
     add(P, [=, this](cudaStream_t s) {
       pswa_dev::lanes_init(d_main_, d_lens_ + 1, L, static_cast<uint32_t>(HW) * C, lanes_, status_, s);
     });
-    tag(P, "lanes_init", 0.0, L * (4.0 + 6.0 + sizeof(pswa_dev::LaneState)));
+    tag(P, "lanes_init", 0.0, L * (2.0 + 6.0 + sizeof(pswa_dev::LaneState)));
     for (int t = 0; t < D.c.s; ++t) {
       if (t > 0) build_s1(P, batch_of(t - 1), false);
       build_step(P, batch_of(t), 0);

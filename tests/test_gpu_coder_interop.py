@@ -70,7 +70,7 @@ def test_gpu_and_oracle_lane_streams_interoperate(lanes, n):
 
 
 @pytest.mark.parametrize("lanes", [1, 64, 8192])
-def test_empty_stream(lanes):
+def test_empty_stream(lanes):  # a flush-only stream per lane
     v = np.zeros(0, np.int32)
     g, gb = gpu_encode(v, v, lanes)
     assert g == encode_lanes(v, v, lanes) and gb == 0.0
@@ -90,8 +90,9 @@ def test_truncated_and_corrupt_payloads_are_rejected():
         gpu_decode(bytes(bad), idx)
     # flipping a lane byte (not in its 4-byte flush, whose low bits are free)
     # either changes symbols or is detected
-    lens = np.frombuffer(g[8:8 + 4 * 64], np.uint32)
-    starts = 8 + 4 * 64 + np.concatenate([[0], np.cumsum(lens)[:-1]])
+    assert np.frombuffer(g[8:12], np.uint32)[0] == 2  # 16-bit length entries
+    lens = np.frombuffer(g[12:12 + 2 * 64], np.uint16).astype(np.int64)
+    starts = 12 + 2 * 64 + np.concatenate([[0], np.cumsum(lens)[:-1]])
     rng = np.random.default_rng(0)
     silent = 0
     for lane in rng.choice(64, 16, replace=False):
@@ -115,7 +116,24 @@ def test_laplace_family_roundtrip():
 
 
 def test_single_stream_bound():
-    """L = 1: coded size <= estimate + 32 bits plus the 12 B header."""
+    """L = 1: coded size <= estimate + 32 bits plus the 12 B
+    header and the lane's length entry (4 B once the lane passes 64 KiB)."""
     v, idx = symbols(100000, 5, escapes=False)
     g, gb = gpu_encode(v, idx, 1)
-    assert 8 * (len(g) - 12) <= gb + 32
+    w = int(np.frombuffer(g[8:12], np.uint32)[0])
+    assert (w == 4) == (len(g) - 14 >= 65536)
+    assert 8 * (len(g) - 12 - w) <= gb + 32
+
+
+@pytest.mark.parametrize("lanes,n", [(1, 120000), (2, 240000)])
+def test_wide_length_entries(lanes, n):
+    """Lanes longer than 64 KiB switch the length table to 4-byte entries on
+    both sides; the streams stay byte-identical and interchangeable."""
+    rng = np.random.default_rng(lanes)
+    idx = np.full(n, 63, np.int32)  # the widest table: ~9.6 bits per symbol
+    v = np.rint(rng.laplace(0, 40.0, n)).astype(np.int32)
+    g, _ = gpu_encode(v, idx, lanes)
+    assert np.frombuffer(g[8:12], np.uint32)[0] == 4
+    assert g == encode_lanes(v, idx, lanes)
+    assert np.array_equal(decode_lanes(g, idx), v)
+    assert np.array_equal(gpu_decode(g, idx)[0], v)

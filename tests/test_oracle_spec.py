@@ -151,7 +151,7 @@ def test_cdf_kats():
 
 def test_coder_empty_stream():
     data = encode_lanes(np.zeros(0), np.zeros(0), 1)
-    assert len(data) == 4 + 4 + 4 + 4  # header(lanes, count) + 1 length + 4-byte flush
+    assert len(data) == 4 + 4 + 4 + 2 + 4  # header(lanes, count, width) + 1 u16 length + 4-byte flush
     assert decode_lanes(data, np.zeros(0, np.int32)).size == 0
 
 
@@ -177,8 +177,8 @@ def test_coder_random_roundtrip_and_bound(lanes):
         v[esc] = rng.integers(-5000, 5000, esc.sum())
         data = encode_lanes(v, idx, lanes)
         assert np.array_equal(decode_lanes(data, idx), v)
-        if lanes == 1:
-            payload_bits = 8 * (len(data) - 12)
+        if lanes == 1:  # header: lanes, count, width + one 2-byte length entry
+            payload_bits = 8 * (len(data) - 14)
             worst = max(worst, payload_bits - bits(v, idx))
     if lanes == 1:
         assert worst <= 32.0 + 1e-9, worst
