@@ -1096,6 +1096,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // the peer must have started before its shared memory is written: arrive
+  // now, wait right before the partial-sum exchange
+  cluster_arrive_relaxed();
   const uint32_t tmem = *tmem_slot;
   // weights (B) of the first stages requested before the PDL wait
   int npre = 0;
@@ -1163,11 +1166,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_ld_32x32(acc + c_exp * 32, xp);
     tmem_ld_32x32(acc + c_own * 32, own);
     tc_wait_ld();
+    cluster_wait();  // (the peer has started)
     const uint32_t rbase = mapa_shared(smem_u32(recv), peer);
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       st_cluster_v4(rbase + recv_off(row, hsel, j), make_uint4(xp[4 * j], xp[4 * j + 1], xp[4 * j + 2], xp[4 * j + 3]));
   }
+  if (warp < 2) cluster_wait();  // (producer / MMA warps: the start barrier)
   // the peer's partials of this CTA's columns have landed (release / acquire)
   cluster_sync();
   if (warp >= 2) {

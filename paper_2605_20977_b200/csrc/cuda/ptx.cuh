@@ -117,6 +117,16 @@ __device__ __forceinline__ void cluster_sync() {
                    : "memory");
 }
 
+// Split cluster barrier: arrive early (no memory ordering), wait later --
+// e.g. to know every CTA of the cluster has started before the first
+// distributed-shared-memory access without stalling in between.
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
 // Address of the same-offset shared variable in CTA `rank` of the cluster.
 __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   uint32_t r;
