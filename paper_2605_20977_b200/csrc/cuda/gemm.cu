@@ -13,10 +13,12 @@
 //               drains one 32-lane quarter x one column half; lane = output
 //               row, written with 16 B stores straight from registers.
 // The epilogue kind is a template parameter (no per-element mode branches).
-// K is walked in ascending 64-wide blocks and never split: every output
-// element has one fixed reduction order, so results are bitwise identical run
-// to run and independent of M and of the tile schedule (the encoder/decoder
-// symmetry contract).
+// K is walked in ascending 64-wide blocks: every output element has one
+// fixed reduction order, so results are bitwise identical run to run and
+// independent of M and of the tile schedule (the encoder/decoder symmetry
+// contract). The one exception is opt-in per layer
+// (GemmEpi::split_k, gemm_splitk_kernel below): two fixed K halves summed as
+// fl(P0 + P1), again independent of M and schedule.
 #include <cuda.h>
 
 #include <algorithm>
