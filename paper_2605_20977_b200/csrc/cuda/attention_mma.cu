@@ -100,15 +100,22 @@ struct AttnArgs {
   int hpc;     // heads per CTA (pipelined)
 };
 
-// NP passes of up to kPassChunks 16-key chunks per (head, slot) stage; the
-// online softmax carries across passes like across slots, so the register
+// NP passes of up to PC 16-key chunks per (head, slot) stage; the online
+// softmax carries across passes like across slots, so the register
 // footprint is that of one pass. NP = 2 keeps 2 CTAs per SM: forcing 3
 // (80 registers, 68 B of spills) measured slower (15.7 -> 18.5 us).
-constexpr int kPassChunks = 5;
-template <int NP>
-__global__ void __launch_bounds__(256, NP == 1 ? 3 : 2)
+// QW = queries per warp: 8 (one MMA N tile) or 16 (two N tiles sharing every
+// K / V fragment: a 4x4 query block scans a 10x10 key band, 6.25 keys per
+// query against 10 for the 2x4 block of QW = 8).
+template <int QW>
+constexpr int pass_chunks() { return QW == 16 ? 4 : 5; }
+template <int NP, int QW>
+__global__ void __launch_bounds__(256, (NP == 1 && QW == 8) ? 3 : 2)
     window_attn_t8_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap kvmap) {
-  constexpr int NCH = NP * kPassChunks;  // chunk slots held in registers (row keys)
+  constexpr int PC = pass_chunks<QW>();
+  constexpr int NT = QW / 8;       // MMA N tiles (8 queries each)
+  constexpr int WI = 2 + QW;       // tile ints per warp
+  constexpr int NCH = NP * PC;     // chunk slots held in registers (row keys)
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // grid x = head group (fastest in dispatch order), y = tile: a tile's head
@@ -123,13 +130,13 @@ __global__ void __launch_bounds__(256, NP == 1 ? 3 : 2)
   const uint32_t sraw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
   const uint32_t sbase = (sraw + 1023u) & ~1023u;  // swizzled TMA boxes: 1024 B aligned
   uint8_t* smem = smem_raw + (sbase - sraw);
-  // [2][kAttnMaxBandKeys][8] fp16 score offsets (128 B aligned), then barriers, band keys
+  // [2][kAttnMaxBandKeys][QW] fp16 score offsets (128 B aligned), then barriers, band keys
   __half* stbl0 = reinterpret_cast<__half*>(smem + nbuf * 2 * a.kbuf);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stbl0 + 2 * kAttnMaxBandKeys * 8);  // [2] stage-full
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stbl0 + 2 * kAttnMaxBandKeys * QW);  // [2] stage-full
   int16_t* sbk = reinterpret_cast<int16_t*>(bars + 2);  // band key: row<<8 | col
   const int nbk = a.shape.nbk;
   const uint32_t box_bytes = static_cast<uint32_t>(HR * a.hw * 64);
-  const uint32_t tbl_bytes = static_cast<uint32_t>(nbk * 8 * 2);
+  const uint32_t tbl_bytes = static_cast<uint32_t>(nbk * QW * 2);
   const CUtensorMap* kvm = &kvmap;  // param-space address (never copied to local memory)
 
   if (threadIdx.x == 0) {
@@ -155,8 +162,8 @@ __global__ void __launch_bounds__(256, NP == 1 ? 3 : 2)
       tma_load_4d(kb + a.kbuf, kvm, &bars[buf], a.d + h * kHD, hx0, hy0, j);
       const int so = a.wt > 0 ? j - sl + a.wt - 1 : 0;
       if (tbl_bytes)
-        bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(stbl0 + buf * kAttnMaxBandKeys * 8)),
-                  a.tables + (static_cast<size_t>(h) * a.nsl + so) * nbk * 8, tbl_bytes, &bars[buf]);
+        bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(stbl0 + buf * kAttnMaxBandKeys * QW)),
+                  a.tables + (static_cast<size_t>(h) * a.nsl + so) * nbk * QW, tbl_bytes, &bars[buf]);
     }
   };
   uint32_t phase = 0;  // bit b: parity of the next completion of bars[b]
@@ -166,10 +173,15 @@ __global__ void __launch_bounds__(256, NP == 1 ? 3 : 2)
   };
   stage(h0, j0, 0);
 
-  const int32_t* Wd = T + 8 + warp * 10;
+  const int32_t* Wd = T + 8 + warp * WI;
   const int br = warp < nw ? Wd[0] : 0, bc = warp < nw ? Wd[1] : 0;  // band origin in the halo
-  const int qrow = warp < nw ? Wd[2 + (lane >> 2)] : -1;  // query n = lane/4 (B-operand column)
-  const bool live = __any_sync(0xffffffffu, qrow >= 0);
+  int qrow[NT];  // query 8n + lane/4 of N tile n (B-operand column)
+#pragma unroll
+  for (int n = 0; n < NT; ++n) qrow[n] = warp < nw ? Wd[2 + 8 * n + (lane >> 2)] : -1;
+  bool any_q = false;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) any_q = any_q || qrow[n] >= 0;
+  const bool live = __any_sync(0xffffffffu, any_q);
 
   // per-lane ldmatrix row keys (K: non-transposed A operand; V: transposed,
   // read per chunk) and the in-grid bits of the two score rows per chunk
@@ -196,9 +208,9 @@ __global__ void __launch_bounds__(256, NP == 1 ? 3 : 2)
   }
   const int qc = (lane & 3) * 2;                         // my two query columns in C fragments
   const float qscale = 0.17677669529663687f * kLog2e;    // log2(e) / sqrt(32)
-  uint32_t qb[2][2];
-  float o[2][4];
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
+  uint32_t qb[NT][2][2];
+  float o[NT][2][4];
+  float m0[NT], m1[NT], l0[NT], l1[NT];
 
   int hi = 0, js = 0;  // stage st = (head h0 + hi, slot j0 + js)
   for (int st = 0; st < nstages; ++st) {
@@ -210,111 +222,142 @@ __global__ void __launch_bounds__(256, NP == 1 ? 3 : 2)
       stage(wrap ? h + 1 : h, wrap ? j0 : j + 1, buf ^ 1);
     }
     if (js == 0) {  // new head: my queries' fragments, fresh softmax state
-      const __half* qp = a.q + static_cast<size_t>(qrow < 0 ? 0 : qrow) * a.ldq + h * kHD + qc;
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        qb[ks][0] = qrow >= 0 ? *reinterpret_cast<const uint32_t*>(qp + ks * 16) : 0u;
-        qb[ks][1] = qrow >= 0 ? *reinterpret_cast<const uint32_t*>(qp + ks * 16 + 8) : 0u;
+      for (int n = 0; n < NT; ++n) {
+        const __half* qp = a.q + static_cast<size_t>(qrow[n] < 0 ? 0 : qrow[n]) * a.ldq + h * kHD + qc;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          qb[n][ks][0] = qrow[n] >= 0 ? *reinterpret_cast<const uint32_t*>(qp + ks * 16) : 0u;
+          qb[n][ks][1] = qrow[n] >= 0 ? *reinterpret_cast<const uint32_t*>(qp + ks * 16 + 8) : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[n][i][e] = 0.0f;
+        m0[n] = m1[n] = -INFINITY;
+        l0[n] = l1[n] = 0.0f;
       }
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) o[i][e] = 0.0f;
-      m0 = m1 = -INFINITY;
-      l0 = l1 = 0.0f;
     }
     wait_buf(buf);  // halo and score-offset table of this stage landed
     const uint32_t sK = sbase + buf * 2 * a.kbuf, sV = sK + a.kbuf;
-    const __half* stbl = stbl0 + buf * kAttnMaxBandKeys * 8;
+    const __half* stbl = stbl0 + buf * kAttnMaxBandKeys * QW;
     if (live) {
 #pragma unroll
       for (int ps = 0; ps < NP; ++ps) {
-        if (ps * kPassChunks >= nch) break;
-        // pass 1: scores and their per-query max over these chunks
-        float s[kPassChunks][4];
-        float mx0 = -INFINITY, mx1 = -INFINITY;
+        if (ps * PC >= nch) break;
+        // pass 1: scores and their per-query max over these chunks; each K
+        // fragment feeds the NT query tiles
+        float s[PC][NT][4];
+        float mx0[NT], mx1[NT];
 #pragma unroll
-        for (int ci = 0; ci < kPassChunks; ++ci) {
-          const int c = ps * kPassChunks + ci;
+        for (int n = 0; n < NT; ++n) mx0[n] = mx1[n] = -INFINITY;
+#pragma unroll
+        for (int ci = 0; ci < PC; ++ci) {
+          const int c = ps * PC + ci;
           if (c < nch) {
-            float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            float acc[NT][4];
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) acc[n][e] = 0.0f;
             uint32_t fa[4];
             ldsm_x4(sK + swz(hk[c], lane >> 4), fa);
-            mma16816(acc, fa, qb[0][0], qb[0][1]);
+#pragma unroll
+            for (int n = 0; n < NT; ++n) mma16816(acc[n], fa, qb[n][0][0], qb[n][0][1]);
             ldsm_x4(sK + swz(hk[c], (lane >> 4) + 2), fa);
-            mma16816(acc, fa, qb[1][0], qb[1][1]);
+#pragma unroll
+            for (int n = 0; n < NT; ++n) mma16816(acc[n], fa, qb[n][1][0], qb[n][1][1]);
             const int r0 = c * 16 + (lane >> 2);
-            const float2 t0 = __half22float2(*reinterpret_cast<const __half2*>(stbl + r0 * 8 + qc));
-            const float2 t1 = __half22float2(*reinterpret_cast<const __half2*>(stbl + (r0 + 8) * 8 + qc));
             const bool k0 = (inb >> (2 * c)) & 1u, k1 = (inb >> (2 * c + 1)) & 1u;
-            s[ci][0] = k0 ? fmaf(acc[0], qscale, t0.x) : -INFINITY;
-            s[ci][1] = k0 ? fmaf(acc[1], qscale, t0.y) : -INFINITY;
-            s[ci][2] = k1 ? fmaf(acc[2], qscale, t1.x) : -INFINITY;
-            s[ci][3] = k1 ? fmaf(acc[3], qscale, t1.y) : -INFINITY;
-            mx0 = fmaxf(mx0, fmaxf(s[ci][0], s[ci][2]));
-            mx1 = fmaxf(mx1, fmaxf(s[ci][1], s[ci][3]));
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+              const float2 t0 = __half22float2(*reinterpret_cast<const __half2*>(stbl + r0 * QW + 8 * n + qc));
+              const float2 t1 =
+                  __half22float2(*reinterpret_cast<const __half2*>(stbl + (r0 + 8) * QW + 8 * n + qc));
+              s[ci][n][0] = k0 ? fmaf(acc[n][0], qscale, t0.x) : -INFINITY;
+              s[ci][n][1] = k0 ? fmaf(acc[n][1], qscale, t0.y) : -INFINITY;
+              s[ci][n][2] = k1 ? fmaf(acc[n][2], qscale, t1.x) : -INFINITY;
+              s[ci][n][3] = k1 ? fmaf(acc[n][3], qscale, t1.y) : -INFINITY;
+              mx0[n] = fmaxf(mx0[n], fmaxf(s[ci][n][0], s[ci][n][2]));
+              mx1[n] = fmaxf(mx1[n], fmaxf(s[ci][n][1], s[ci][n][3]));
+            }
           }
         }
+        float ms0[NT], ms1[NT];
 #pragma unroll
-        for (int off = 4; off < 32; off <<= 1) {
-          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        for (int n = 0; n < NT; ++n) {
+#pragma unroll
+          for (int off = 4; off < 32; off <<= 1) {
+            mx0[n] = fmaxf(mx0[n], __shfl_xor_sync(0xffffffffu, mx0[n], off));
+            mx1[n] = fmaxf(mx1[n], __shfl_xor_sync(0xffffffffu, mx1[n], off));
+          }
+          const float mn0 = fmaxf(m0[n], mx0[n]), mn1 = fmaxf(m1[n], mx1[n]);
+          const float al0 = mn0 == -INFINITY ? 1.0f : ex2(m0[n] - mn0);  // ex2(-inf) = 0
+          const float al1 = mn1 == -INFINITY ? 1.0f : ex2(m1[n] - mn1);
+          m0[n] = mn0;
+          m1[n] = mn1;
+          // exp offsets: a query with no allowed key yet keeps m = -inf; use
+          // 0 so that ex2(-inf - 0) = 0 instead of NaN
+          ms0[n] = mn0 == -INFINITY ? 0.0f : mn0;
+          ms1[n] = mn1 == -INFINITY ? 0.0f : mn1;
+          l0[n] *= al0;
+          l1[n] *= al1;
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            o[n][mt][0] *= al0;
+            o[n][mt][1] *= al1;
+            o[n][mt][2] *= al0;
+            o[n][mt][3] *= al1;
+          }
         }
-        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-        const float al0 = mn0 == -INFINITY ? 1.0f : ex2(m0 - mn0);  // ex2(-inf) = 0
-        const float al1 = mn1 == -INFINITY ? 1.0f : ex2(m1 - mn1);
-        m0 = mn0;
-        m1 = mn1;
-        // exp offsets: a query with no allowed key yet keeps m = -inf; use 0
-        // so that ex2(-inf - 0) = 0 instead of NaN
-        const float ms0 = mn0 == -INFINITY ? 0.0f : mn0, ms1 = mn1 == -INFINITY ? 0.0f : mn1;
-        l0 *= al0;
-        l1 *= al1;
+        // pass 2: probabilities (fp16) and O^T += V^T P^T; each V fragment
+        // feeds the NT query tiles
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          o[mt][0] *= al0;
-          o[mt][1] *= al1;
-          o[mt][2] *= al0;
-          o[mt][3] *= al1;
-        }
-        // pass 2: probabilities (fp16) and O^T += V^T P^T
-#pragma unroll
-        for (int ci = 0; ci < kPassChunks; ++ci) {
-          const int c = ps * kPassChunks + ci;
+        for (int ci = 0; ci < PC; ++ci) {
+          const int c = ps * PC + ci;
           if (c < nch) {
-            const float p0 = ex2(s[ci][0] - ms0), p1 = ex2(s[ci][1] - ms1);
-            const float p2 = ex2(s[ci][2] - ms0), p3 = ex2(s[ci][3] - ms1);
-            l0 += p0 + p2;
-            l1 += p1 + p3;
-            const uint32_t b0 = movtrans(pack_h2(p0, p1)), b1 = movtrans(pack_h2(p2, p3));
+            uint32_t b0[NT], b1[NT];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+              const float p0 = ex2(s[ci][n][0] - ms0[n]), p1 = ex2(s[ci][n][1] - ms1[n]);
+              const float p2 = ex2(s[ci][n][2] - ms0[n]), p3 = ex2(s[ci][n][3] - ms1[n]);
+              l0[n] += p0 + p2;
+              l1[n] += p1 + p3;
+              b0[n] = movtrans(pack_h2(p0, p1));
+              b1[n] = movtrans(pack_h2(p2, p3));
+            }
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
               uint32_t fv[4];
               ldsm_x4_t(sV + swz(hv[c], ((lane >> 3) & 1) + 2 * mt), fv);
-              mma16816(o[mt], fv, b0, b1);
+#pragma unroll
+              for (int n = 0; n < NT; ++n) mma16816(o[n][mt], fv, b0[n], b1[n]);
             }
           }
         }
       }
       if (js == nslots - 1) {  // head done: normalise and store
-        float t0 = l0, t1 = l1;
 #pragma unroll
-        for (int off = 4; off < 32; off <<= 1) {
-          t0 += __shfl_xor_sync(0xffffffffu, t0, off);
-          t1 += __shfl_xor_sync(0xffffffffu, t1, off);
-        }
-        const float inv0 = t0 > 0.0f ? 1.0f / t0 : 0.0f;
-        const float inv1 = t1 > 0.0f ? 1.0f / t1 : 0.0f;
-        // O^T blocks (8 dims x 8 queries) -> row-major O rows via movmatrix
+        for (int n = 0; n < NT; ++n) {
+          float t0 = l0[n], t1 = l1[n];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int hb = 0; hb < 2; ++hb) {
-            const uint32_t v = movtrans(pack_h2(o[mt][2 * hb] * inv0, o[mt][2 * hb + 1] * inv1));
-            if (qrow >= 0)
-              *reinterpret_cast<uint32_t*>(a.out + static_cast<size_t>(qrow) * a.ldo + h * kHD +
-                                           mt * 16 + hb * 8 + (lane & 3) * 2) = v;
+          for (int off = 4; off < 32; off <<= 1) {
+            t0 += __shfl_xor_sync(0xffffffffu, t0, off);
+            t1 += __shfl_xor_sync(0xffffffffu, t1, off);
           }
+          const float inv0 = t0 > 0.0f ? 1.0f / t0 : 0.0f;
+          const float inv1 = t1 > 0.0f ? 1.0f / t1 : 0.0f;
+          // O^T blocks (8 dims x 8 queries) -> row-major O rows via movmatrix
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int hb = 0; hb < 2; ++hb) {
+              const uint32_t v = movtrans(pack_h2(o[n][mt][2 * hb] * inv0, o[n][mt][2 * hb + 1] * inv1));
+              if (qrow[n] >= 0)
+                *reinterpret_cast<uint32_t*>(a.out + static_cast<size_t>(qrow[n]) * a.ldo + h * kHD +
+                                             mt * 16 + hb * 8 + (lane & 3) * 2) = v;
+            }
+        }
       }
     }
     __syncthreads();  // buffer `buf` (halo + table) is rewritten by a later stage
@@ -339,7 +382,7 @@ int box_buf_bytes(int halo_keys) { return (halo_keys * 64 + 1023) / 1024 * 1024;
 
 int smem_bytes(int halo_keys, int dbuf) {
   // alignment slack + K/V buffers + 2 fp16 score-offset tables + barriers + band keys
-  return 1024 + (dbuf ? 4 : 2) * box_buf_bytes(halo_keys) + 2 * kAttnMaxBandKeys * 8 * 2 + 16 +
+  return 1024 + (dbuf ? 4 : 2) * box_buf_bytes(halo_keys) + 2 * kAttnMaxBandKeys * 16 * 2 + 16 +
          kAttnMaxBandKeys * 2;
 }
 
@@ -354,10 +397,10 @@ __global__ void score_table_kernel(const float* __restrict__ bias, int taps_tota
   }
 }
 
-template <int NP>
+template <int NP, int QW>
 void launch_t8(const AttnArgs& a, const CUtensorMap& map, int halo_keys, int ntiles, int heads,
                int warps, cudaStream_t st) {
-  launch_k(window_attn_t8_kernel<NP>, dim3(heads / a.hpc, ntiles), dim3(warps * 32),
+  launch_k(window_attn_t8_kernel<NP, QW>, dim3(heads / a.hpc, ntiles), dim3(warps * 32),
            smem_bytes(halo_keys, a.dbuf), st, a, map);
 }
 
@@ -371,7 +414,7 @@ int window_attention_tiles_smem(int halo_keys, bool) { return smem_bytes(halo_ke
 
 void build_score_tables(const float* bias, int heads, int wt, AttnShape shape, __half* out,
                         cudaStream_t st) {
-  const int nsl = wt > 0 ? wt : 1, n = shape.nbk * 8;
+  const int nsl = wt > 0 ? wt : 1, n = shape.nbk * shape.qw;
   if (n == 0) return;
   score_table_kernel<<<dim3((n + 255) / 256, heads, nsl), 256, 0, st>>>(bias, nsl * 49, shape.taps, n,
                                                                        nsl, out);
@@ -379,9 +422,11 @@ void build_score_tables(const float* bias, int heads, int wt, AttnShape shape, _
 }
 
 void window_attention_tiles_init(int max_smem_bytes) {
-  PSWA_CUDA(cudaFuncSetAttribute(window_attn_t8_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PSWA_CUDA(cudaFuncSetAttribute(window_attn_t8_kernel<1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  max_smem_bytes));
-  PSWA_CUDA(cudaFuncSetAttribute(window_attn_t8_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PSWA_CUDA(cudaFuncSetAttribute(window_attn_t8_kernel<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 max_smem_bytes));
+  PSWA_CUDA(cudaFuncSetAttribute(window_attn_t8_kernel<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  max_smem_bytes));
 }
 
@@ -398,8 +443,14 @@ void window_attention_tiles(const __half* q, int ldq, const int32_t* tiles, int 
   const int hk = halo_rows * halo_width;
   AttnArgs a{q, ldq, tiles, heads * kHD, wt, tables, wt > 0 ? wt : 1, out, ldo, shape, halo_width,
              box_buf_bytes(hk), wt > 0 ? dbuf3 : dbuf2, hpc};
-  if (shape.nbk <= 16 * kPassChunks) launch_t8<1>(a, kv_map, hk, ntiles, heads, warps_per_tile, st);
-  else launch_t8<2>(a, kv_map, hk, ntiles, heads, warps_per_tile, st);
+  if (shape.qw == 16) {
+    if (shape.nbk > 2 * 16 * pass_chunks<16>()) throw std::invalid_argument("attention shape (16 queries)");
+    launch_t8<2, 16>(a, kv_map, hk, ntiles, heads, warps_per_tile, st);
+  } else if (shape.nbk <= 16 * pass_chunks<8>()) {
+    launch_t8<1, 8>(a, kv_map, hk, ntiles, heads, warps_per_tile, st);
+  } else {
+    launch_t8<2, 8>(a, kv_map, hk, ntiles, heads, warps_per_tile, st);
+  }
   PSWA_LAUNCH_CHECK();
 }
 

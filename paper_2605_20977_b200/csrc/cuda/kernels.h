@@ -72,15 +72,16 @@ void window_attention(const __half* q, int ldq, const int32_t* qinfo, int Mq, co
 // warps of 8 queries, keys on the MMA's M side. Work is a list of CTA tiles,
 // kAttnTileInts ints each: [0] halo top row, [1] halo left col, [2] halo
 // rows, [3] query slot, [4] warps with queries, then per warp w at
-// [8 + 10w]: band origin (row, col) inside the halo and 8 query rows of q /
-// out (-1 = none). All warps of a launch share one band shape:
+// [8 + (2 + qw) w]: band origin (row, col) inside the halo and qw query rows
+// of q / out (-1 = none). All warps of a launch share one band shape:
 constexpr int kAttnTileInts = 8 + 10 * 16;
 constexpr int kAttnMaxBandKeys = 144;
 struct AttnShape {
-  const int8_t* taps;   // [nbk][8]: window tap (dy+3)*7+(dx+3) of (band key, query), -1 = excluded
+  const int8_t* taps;   // [nbk][qw]: window tap (dy+3)*7+(dx+3) of (band key, query), -1 = excluded
   const int16_t* bkey;  // [nbk]: band key -> row << 8 | col relative to the band origin
   int nbk;              // band keys scanned (multiple of 16, <= kAttnMaxBandKeys; 0 = none)
   int H, W;             // key grid bounds (keys outside are masked)
+  int qw = 8;           // queries per warp: 8, or 16 (two MMA N tiles; tiles hold 2 + 16 ints per warp)
 };
 bool window_attention_tiles_supported(int hd, int win_h, int win_w);
 int window_attention_tiles_smem(int halo_keys, bool three_d);

@@ -44,7 +44,16 @@ void put_linear(std::vector<__half>& dst, int ldk, const float* src, int in, int
 // step batches 16 x 16 positions; +3 rows / columns of window margin
 // halo widths 22 + pad columns: spread the ldmatrix rows over the banks
 // under the TMA 64 B swizzle (see attention_mma.cu)
-constexpr int kCtxHaloRows = 10, kCtxHaloW = 23;
+constexpr int kCtxHaloRows = 10, kCtxHaloW = 23;  // 2x4-query warps (default)
+constexpr int kCtx16HaloRows = 14;                 // 4x4-query warps (PSWA_ATTN_Q16=1)
+// 16 queries per context warp: correct (same tests), but 149 vs 118 us per
+// context layer (127 registers, 2 CTAs per SM, 1.4x the scanned keys per
+// query), 7.11 vs 6.90 ms per frame -- opt-in
+bool ctx_q16() {
+  static const bool on = std::getenv("PSWA_ATTN_Q16") != nullptr;
+  return on;
+}
+int ctx_halo_rows() { return ctx_q16() ? kCtx16HaloRows : kCtxHaloRows; }
 constexpr int kStepHaloRows = 22, kStepHaloW = 24;
 
 // Step-t positions of the own rows of a band, as local raster indices, in
@@ -207,29 +216,32 @@ void Engine::alloc_all() {
     mma_attn_ = pswa_dev::window_attention_tiles_supported(D.hd, D.c.win_h, D.c.win_w) && D.c.s == 4;
     if (mma_attn_) {
       constexpr int TI = pswa_dev::kAttnTileInts;
-      // context: CTA = 8 warps as 2 x 4 blocks of 2x4 queries (a 4 x 16 query
-      // rectangle of one slot), halo 10 rows x 23 columns
-      auto ctx_tiles = [&](int slot_from, int row_base, int S) {
+      // context: CTA = 8 warps as 2 x 4 blocks of 2x4 queries (a 4 x 16
+      // query rectangle of one slot), halo 10 rows x 23 columns; or
+      // (PSWA_ATTN_Q16) 2 x 4 blocks of 4x4 queries (8 x 16), halo 14 x 23
+      const bool q16 = ctx_q16();
+      const int qh = q16 ? 4 : 2, qw = 2 * qh * 2;  // warp block qh x 4: 16 or 8 queries
+      auto ctx_tiles = [&, q16, qh, qw](int slot_from, int row_base, int S) {
         std::vector<int> v;
         const int yend = own0 + B_.nown;
         // newest slot first: a slot-j tile walks min(j + 1, wt) key slots, so
         // the heaviest tiles are dispatched first and the launch tail is light
         for (int j = S - 1; j >= slot_from; --j)
-          for (int y0 = own0; y0 < yend; y0 += 4)
+          for (int y0 = own0; y0 < yend; y0 += 2 * qh)
             for (int x0 = 0; x0 < D.W; x0 += 16) {
               std::vector<int> t(TI, -1);
               t[0] = y0 - 3;
               t[1] = x0 - 3;
-              t[2] = kCtxHaloRows;
+              t[2] = q16 ? kCtx16HaloRows : kCtxHaloRows;
               t[3] = j;
               t[4] = 8;
               for (int w = 0; w < 8; ++w) {
                 const int wy = w / 4, wx = w % 4;
-                int* W8 = &t[8 + 10 * w];
-                W8[0] = 2 * wy;
+                int* W8 = &t[8 + (2 + qw) * w];
+                W8[0] = qh * wy;
                 W8[1] = 4 * wx;
-                for (int i = 0; i < 8; ++i) {
-                  const int y = y0 + 2 * wy + i / 4, x = x0 + 4 * wx + i % 4;
+                for (int i = 0; i < qw; ++i) {
+                  const int y = y0 + qh * wy + i / 4, x = x0 + 4 * wx + i % 4;
                   W8[2 + i] = (y < yend && x < D.W) ? j * HWo + (y - own0) * D.W + x - row_base : -1;
                 }
               }
@@ -290,15 +302,15 @@ void Engine::alloc_all() {
       {
         std::vector<int8_t> all_taps;
         std::vector<int16_t> all_keys;
-        struct Pending { size_t tap_off, key_off; int nbk; };
+        struct Pending { size_t tap_off, key_off; int nbk, qw; };
         auto add_shape = [&](std::vector<std::pair<int, int>> keys /* (row, col) in band */,
-                             auto query_pos, int t, int mk) {
+                             auto query_pos, int t, int mk, int nq) {
           std::vector<std::pair<int, int>> used;
           std::vector<int8_t> taps;
           for (auto [kr, kc] : keys) {
-            int8_t row[8];
+            int8_t row[16];
             bool any = false;
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < nq; ++i) {
               const auto [qr, qc] = query_pos(i);
               const int dy = kr - qr, dx = kc - qc;
               row[i] = -1;
@@ -314,23 +326,25 @@ void Engine::alloc_all() {
             }
             if (!any) continue;
             used.push_back({kr, kc});
-            taps.insert(taps.end(), row, row + 8);
+            taps.insert(taps.end(), row, row + nq);
           }
           while (used.size() % 16) {  // pad to whole 16-key chunks (all taps -1)
             used.push_back({0, 0});
-            taps.insert(taps.end(), 8, int8_t(-1));
+            taps.insert(taps.end(), nq, int8_t(-1));
           }
-          Pending p{all_taps.size(), all_keys.size(), static_cast<int>(used.size())};
+          Pending p{all_taps.size(), all_keys.size(), static_cast<int>(used.size()), nq};
           all_taps.insert(all_taps.end(), taps.begin(), taps.end());
           for (auto [kr, kc] : used) all_keys.push_back(static_cast<int16_t>(kr << 8 | kc));
           return p;
         };
-        // context: 8 x 10 band, column-major (conflict-free ldmatrix with a
-        // 23-wide halo and the TMA 64 B swizzle); query i at (3 + i/4, 3 + i%4)
+        // context: (qh + 6) x 10 band, column-major (conflict-free ldmatrix
+        // with a 23-wide halo and the TMA 64 B swizzle); query i at
+        // (3 + i/4, 3 + i%4)
         std::vector<std::pair<int, int>> ck;
         for (int c = 0; c < 10; ++c)
-          for (int r = 0; r < 8; ++r) ck.push_back({r, c});
-        const Pending pc = add_shape(ck, [](int i) { return std::make_pair(3 + i / 4, 3 + i % 4); }, -1, 0);
+          for (int r = 0; r < qh + 6; ++r) ck.push_back({r, c});
+        const Pending pc =
+            add_shape(ck, [](int i) { return std::make_pair(3 + i / 4, 3 + i % 4); }, -1, 0, qw);
         // steps: 10 x 14 band sorted by step class, then row, column
         Pending ps[4][3];
         for (int t = 0; t < 4; ++t)
@@ -344,21 +358,21 @@ void Engine::alloc_all() {
             ps[t][mk] = add_shape(keys, [t](int i) {
               const int ry = i / 2, jj = i % 2;
               return std::make_pair(3 + ry, 3 + 4 * jj + ((t - ry) % 4 + 4) % 4);
-            }, t, mk);
+            }, t, mk, 8);
           }
         int8_t* dt = dalloc<int8_t>(all_taps.size());
         int16_t* dk = dalloc<int16_t>(all_keys.size());
         PSWA_CUDA(cudaMemcpyAsync(dt, all_taps.data(), all_taps.size(), cudaMemcpyHostToDevice, st_));
         PSWA_CUDA(cudaMemcpyAsync(dk, all_keys.data(), all_keys.size() * 2, cudaMemcpyHostToDevice, st_));
         auto shape = [&](const Pending& p) {
-          return pswa_dev::AttnShape{dt + p.tap_off, dk + p.key_off, p.nbk, B_.Hl, D.W};
+          return pswa_dev::AttnShape{dt + p.tap_off, dk + p.key_off, p.nbk, B_.Hl, D.W, p.qw};
         };
         shape_ctx_ = shape(pc);
         for (int t = 0; t < 4; ++t)
           for (int mk = 0; mk < 3; ++mk) shape_step_[t][mk] = shape(ps[t][mk]);
       }
       pswa_dev::window_attention_tiles_init(
-          std::max(pswa_dev::window_attention_tiles_smem(kCtxHaloRows * kCtxHaloW, true),
+          std::max(pswa_dev::window_attention_tiles_smem(ctx_halo_rows() * kCtxHaloW, true),
                    pswa_dev::window_attention_tiles_smem(kStepHaloRows * kStepHaloW, false)));
     }
     std::vector<int> crop(HWp);
@@ -852,7 +866,7 @@ void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq
     }, 0);
   } else if (mma_attn_) {
     const pswa_dev::AttnShape sh = *shape;
-    const int hr = wt > 0 ? kCtxHaloRows : kStepHaloRows, hw = wt > 0 ? kCtxHaloW : kStepHaloW;
+    const int hr = wt > 0 ? ctx_halo_rows() : kStepHaloRows, hw = wt > 0 ? kCtxHaloW : kStepHaloW;
     CUtensorMap map;  // halo boxes of this K/V buffer: 32 channels x hw x hr x 1 slot
     pswa_dev::make_kv_tmap(&map, kv, 2 * d, D.W, Hl, wt > 0 ? (kv_slots > 0 ? kv_slots : D.T) : 1,
                            slot_stride > 0 ? slot_stride : HWl_,
@@ -861,7 +875,7 @@ void Engine::attention(Program& P, const __half* q, const int32_t* qinfo, int Mq
     // every program that launches this layer on this shape
     __half*& tab = score_tables_[{bias, shape}];
     if (!tab && sh.nbk > 0) {
-      tab = dalloc<__half>(static_cast<size_t>(D.heads) * std::max(wt, 1) * sh.nbk * 8);
+      tab = dalloc<__half>(static_cast<size_t>(D.heads) * std::max(wt, 1) * sh.nbk * sh.qw);
       pswa_dev::build_score_tables(bias, D.heads, wt, sh, tab, st_);
     }
     const __half* tables = tab;

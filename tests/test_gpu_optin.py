@@ -1,5 +1,6 @@
 """The opt-in experimental paths stay correct: the persistent
-GEMM chains (PSWA_CHAIN, PSWA_CH_CHAIN), each in a fresh process (the switches are read
+GEMM chains (PSWA_CHAIN, PSWA_CH_CHAIN) and the 16-query context attention
+(PSWA_ATTN_Q16), each in a fresh process (the switches are read
 once): a paper-scale P-frame encodes and decodes bit-exactly, the decoder's
 mu/sigma equal the encoder program's bitwise, and on a common z_hat stay
 within the stated parity tolerance of the default path's (the chains never
@@ -54,7 +55,7 @@ def run(env_extra, out, zfile):
     return np.load(out)
 
 
-@pytest.mark.parametrize("switch", ["PSWA_CHAIN", "PSWA_CH_CHAIN"])
+@pytest.mark.parametrize("switch", ["PSWA_CHAIN", "PSWA_CH_CHAIN", "PSWA_ATTN_Q16"])
 def test_optin_path_matches_default(switch, tmp_path):
     import numpy as np
     zfile = str(tmp_path / "zhat.npy")
