@@ -184,6 +184,23 @@ def test_coder_random_roundtrip_and_bound(lanes):
         assert worst <= 32.0 + 1e-9, worst
 
 
+def test_lane_length_entry_width():
+    """FORMAT.md §2: 2-byte lane lengths while every lane is under 64 KiB,
+    4-byte ones beyond; both decode."""
+    rng = np.random.default_rng(11)
+    for n, lanes, w in ((2000, 4, 2), (120000, 1, 4)):
+        idx = np.full(n, 63, np.int32)
+        v = np.rint(rng.laplace(0, 40.0, n)).astype(np.int32)
+        data = encode_lanes(v, idx, lanes)
+        assert np.frombuffer(data[8:12], np.uint32)[0] == w
+        lens = np.frombuffer(data[12:12 + w * lanes], np.uint16 if w == 2 else np.uint32)
+        assert 12 + w * lanes + int(lens.astype(np.int64).sum()) == len(data)
+        assert np.array_equal(decode_lanes(data, idx), v)
+    bad = bytearray(encode_lanes(np.zeros(4, np.int32), np.zeros(4, np.int32), 2))
+    bad[8] = 3  # a width other than 2 or 4
+    assert decode_lanes(bytes(bad), np.zeros(4, np.int32)) is None
+
+
 def test_coder_truncation_detected():  # SPEC.md:461
     rng = np.random.default_rng(9)
     idx = rng.integers(0, 30, 500).astype(np.int32)
