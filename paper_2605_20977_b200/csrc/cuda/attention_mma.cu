@@ -109,6 +109,8 @@ struct AttnArgs {
 // query against 10 for the 2x4 block of QW = 8).
 template <int QW>
 constexpr int pass_chunks() { return QW == 16 ? 4 : 5; }
+// (Step tiles recomputing their ldmatrix row keys per chunk to fit 3 CTAs
+// per SM at 76 registers measured 15.9 vs 15.6 us per launch: reverted.)
 template <int NP, int QW>
 __global__ void __launch_bounds__(256, (NP == 1 && QW == 8) ? 3 : 2)
     window_attn_t8_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap kvmap) {
@@ -380,9 +382,10 @@ int env_int(const char* n, int dflt) {
 
 int box_buf_bytes(int halo_keys) { return (halo_keys * 64 + 1023) / 1024 * 1024; }
 
-int smem_bytes(int halo_keys, int dbuf) {
+int smem_bytes(int halo_keys, int dbuf, int qw) {
   // alignment slack + K/V buffers + 2 fp16 score-offset tables + barriers + band keys
-  return 1024 + (dbuf ? 4 : 2) * box_buf_bytes(halo_keys) + 2 * kAttnMaxBandKeys * 16 * 2 + 16 +
+  // (75.5 KB for a single-buffered 8-query step tile: 3 CTAs per SM)
+  return 1024 + (dbuf ? 4 : 2) * box_buf_bytes(halo_keys) + 2 * kAttnMaxBandKeys * qw * 2 + 16 +
          kAttnMaxBandKeys * 2;
 }
 
@@ -401,7 +404,7 @@ template <int NP, int QW>
 void launch_t8(const AttnArgs& a, const CUtensorMap& map, int halo_keys, int ntiles, int heads,
                int warps, cudaStream_t st) {
   launch_k(window_attn_t8_kernel<NP, QW>, dim3(heads / a.hpc, ntiles), dim3(warps * 32),
-           smem_bytes(halo_keys, a.dbuf), st, a, map);
+           smem_bytes(halo_keys, a.dbuf, QW), st, a, map);
 }
 
 }  // namespace
@@ -410,7 +413,7 @@ bool window_attention_tiles_supported(int hd, int win_h, int win_w) {
   return hd == kHD && win_h == 7 && win_w == 7;
 }
 
-int window_attention_tiles_smem(int halo_keys, bool) { return smem_bytes(halo_keys, 1); }
+int window_attention_tiles_smem(int halo_keys, bool) { return smem_bytes(halo_keys, 1, 16); }
 
 void build_score_tables(const float* bias, int heads, int wt, AttnShape shape, __half* out,
                         cudaStream_t st) {
