@@ -205,7 +205,7 @@ PROBE_DESC = {  # the probes the bench names; every other probe is listed by nam
     "step_wq": "gemm_tc_kernel S2 block 0 fused Q|K|V projection, step 3 batch, M=2040 N=1536 K=512",
     "step_wo": "gemm_tc_kernel S2 block 0 out projection + residual + norm outputs, M=2040 N=K=512",
     "step_gu": "gemm_tc_kernel S2 block 0 FFN gate|up (SwiGLU), M=2040 N=2736 K=512",
-    "step_wd": "gemm_tc_kernel S2 block 0 FFN down + residual, M=2040 N=512 K=1368",
+    "step_wd": "gemm_splitk_kernel (K halves on a CTA pair, DSMEM reduction) S2 block 0 FFN down + residual, M=2040 N=512 K=1368",
     "rms_prep": "rms_prep_kernel, context block 0 norm inputs (fp32 -> fp16 + sums of squares), 32640 x 512",
     "rmsnorm": "rmsnorm_kernel, final context norm, 8160 x 512",
     "fill_slots": "fill_slots_kernel, 4 context slots from the ring (fp32), 32640 x 512",
