@@ -198,10 +198,10 @@ def run_reference(args, rank, world):
 
 # ---------------------------------------------------------------- ours ------
 PROBE_DESC = {  # the probes the bench names; every other probe is listed by name
-    "ctx_attn": "window_attn_mma_kernel, context block 0: 3D 4-slot 7x7 window, 32640 queries x 16 heads",
+    "ctx_attn": "window_attn_t8_kernel<1,8> (8 queries per warp), context block 0: 3D 4-slot 7x7 window, 32640 queries x 16 heads",
     "ctx_ffn_gu": "gemm_tc_kernel<256> context FFN gate|up (SwiGLU epilogue), M=32640 N=2736 K=512",
     "ctx_wqkv": "gemm_tc_kernel context block 0 fused Q|K|V, M=32640 N=1536 K=512",
-    "step_attn": "window_attn_mma_kernel, S2 block 0 self attention, step 3 batch (2040 queries)",
+    "step_attn": "window_attn_t8_kernel<2,8>, S2 block 0 self attention, step 3 batch (2040 queries)",
     "step_wq": "gemm_tc_kernel S2 block 0 fused Q|K|V projection, step 3 batch, M=2040 N=1536 K=512",
     "step_wo": "gemm_tc_kernel S2 block 0 out projection + residual + norm outputs, M=2040 N=K=512",
     "step_gu": "gemm_tc_kernel S2 block 0 FFN gate|up (SwiGLU), M=2040 N=2736 K=512",
@@ -209,7 +209,7 @@ PROBE_DESC = {  # the probes the bench names; every other probe is listed by nam
     "rms_prep": "rms_prep_kernel, context block 0 norm inputs (fp32 -> fp16 + sums of squares), 32640 x 512",
     "rmsnorm": "rmsnorm_kernel, final context norm, 8160 x 512",
     "fill_slots": "fill_slots_kernel, 4 context slots from the ring (fp32), 32640 x 512",
-    "im2col": "im2col3x3_kernel, hyper decoder RB 2, 68x120 x (9 x 128)",
+    "im2col": "im2col3x3_v8_kernel, hyper decoder RB 2, 68x120 x (9 x 128)",
     "lanes_init": "lanes_init_kernel, 8192 main-payload lanes",
     "decode_hyper": "hyper lanes: lanes_init + decode_hyper_kernel (1024 lanes, 261k symbols)",
     "cdf_build": "build_cdf_kernel, 64 fp64 tables + costs + search index",
