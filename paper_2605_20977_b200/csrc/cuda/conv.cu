@@ -70,7 +70,7 @@ __global__ void im2col3x3_v8_kernel(const float* __restrict__ x, int h, int w, i
 }
 
 __global__ void resample_kernel(const float* __restrict__ x, int h, int w, int c, int up,
-                                float* __restrict__ out) {
+                                float* __restrict__ out, __half* __restrict__ out16) {
   pdl_wait();
   pdl_trigger();
   const int oh = up ? 2 * h : h / 2, ow = up ? 2 * w : w / 2;
@@ -81,7 +81,9 @@ __global__ void resample_kernel(const float* __restrict__ x, int h, int w, int c
     const size_t pix = idx / c;
     const int oy = static_cast<int>(pix / ow), ox = static_cast<int>(pix % ow);
     const int sy = up ? oy >> 1 : 2 * oy, sx = up ? ox >> 1 : 2 * ox;
-    out[idx] = x[(static_cast<size_t>(sy) * w + sx) * c + ci];
+    const float v = x[(static_cast<size_t>(sy) * w + sx) * c + ci];
+    out[idx] = v;
+    if (out16) out16[idx] = __float2half_rn(v);  // the implicit-GEMM conv's operand
   }
 }
 
@@ -132,14 +134,15 @@ void im2col3x3(const float* x, int h, int w, int c, int stride, int up2, __half*
   PSWA_LAUNCH_CHECK();
 }
 
-void upsample2_nhwc(const float* x, int h, int w, int c, float* out, cudaStream_t st) {
-  launch_k(resample_kernel, dim3(grid_for(static_cast<size_t>(4) * h * w * c)), dim3(256), 0, st, x, h, w, c, 1, out);
+void upsample2_nhwc(const float* x, int h, int w, int c, float* out, cudaStream_t st, __half* out16) {
+  launch_k(resample_kernel, dim3(grid_for(static_cast<size_t>(4) * h * w * c)), dim3(256), 0, st, x, h, w, c, 1, out,
+           out16);
   PSWA_LAUNCH_CHECK();
 }
 
 void subsample2_nhwc(const float* x, int h, int w, int c, float* out, cudaStream_t st) {
   launch_k(resample_kernel, dim3(grid_for(static_cast<size_t>(h) * w * c / 4 + 1)), dim3(256), 0, st, x, h, w, c, 0,
-                                                                                     out);
+           out, static_cast<__half*>(nullptr));
   PSWA_LAUNCH_CHECK();
 }
 

@@ -475,13 +475,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      // A operand: a 2D box of the row-major activation, or (conv_w > 0)
+      // the 128 output pixels' patches of one 3x3 tap and 64 channels,
+      // gathered from the NHWC image by TMA in im2col mode
+      auto load_a = [&](uint8_t* dst, uint64_t* bar, int kb, int m0) {
+        if (ep.conv_w > 0) {
+          // coordinates live in the map's bounding box, which starts at its
+          // lower corner (-1, -1): output pixel (x, y) -> (x - 1, y - 1)
+          const int tap = kb / ep.conv_cb;
+          tma_load_im2col_4d(dst, &tma, bar, (kb - tap * ep.conv_cb) * kBK, m0 % ep.conv_w - 1, m0 / ep.conv_w - 1,
+                             0, static_cast<uint16_t>(tap % 3), static_cast<uint16_t>(tap / 3));
+        } else {
+          tma_load_2d(dst, &tma, bar, kb * kBK, m0);
+        }
+      };
       int g = 0;  // global k-block counter across tiles
       for (int u = unit0; u < n_units; u += unit_step) {
         const int m0 = ((u / tiles_n) * CL + rank) * kBM, n0 = (u % tiles_n) * BN;
         for (int kb = 0; kb < kblocks; ++kb, ++g) {
           const int s = g % S, round = g / S;
           if (g < npre) {  // B already requested (and the stage's bytes expected)
-            tma_load_2d(sa + s * Cfg::kABytes, &tma, &full[s], kb * kBK, m0);
+            load_a(sa + s * Cfg::kABytes, &full[s], kb, m0);
             continue;
           }
           if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
@@ -490,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           mbar_expect_tx(&full[s], Cfg::kStageBytes);
-          tma_load_2d(sa + s * Cfg::kABytes, &tma, &full[s], kb * kBK, m0);
+          load_a(sa + s * Cfg::kABytes, &full[s], kb, m0);
           if (CL > 1)
             tma_load_2d_mc(sb + s * Cfg::kBBytes + rank * (Cfg::kBBytes / CL), &tmb, &full[s],
                            kb * kBK, n0 + rank * (BN / CL), static_cast<uint16_t>((1u << CL) - 1));
@@ -1234,6 +1248,25 @@ void make_tmap(CUtensorMap* m, const __half* base, int ld, int rows, int cols, i
     throw CudaError("cuTensorMapEncodeTiled failed (code " + std::to_string(int(r)) + ")");
 }
 
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PSWA_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p)
+      throw CudaError("cuTensorMapEncodeIm2col entry point unavailable");
+    fn = reinterpret_cast<EncodeIm2colFn>(p);
+  });
+  return fn;
+}
+
 int sm_count() {
   static int n = [] {
     int dev = 0, v = 0;
@@ -1452,6 +1485,33 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   if (bn == 64) prep<64>(kind);
   if (bn == 128) prep<128>(kind);
   if (bn == 256) prep<256>(kind);
+}
+
+void gemm_plan_conv3x3(GemmPlan* p, const __half* x, int h, int w, int c, const __half* B, int ldb, int N,
+                       const GemmEpi& epi) {
+  if (c % kBK != 0 || h < 1 || w < 1 || reinterpret_cast<uintptr_t>(x) % 16 != 0)
+    throw std::invalid_argument("gemm_plan_conv3x3: channels % 64, 16 B aligned NHWC input");
+  // plan as a GEMM over [h*w][9c] (tile width, epilogue, B map), then swap
+  // A's map for the im2col one over the image itself
+  GemmEpi e = epi;
+  e.conv_w = w;
+  e.conv_cb = c / kBK;
+  gemm_plan(p, x, 9 * c, h * w, B, ldb, N, 9 * c, e);  // (A's 2D map is replaced below)
+  if (p->pair || p->splitk || p->cluster != 1)
+    throw std::invalid_argument("gemm_plan_conv3x3: single-CTA tiles only");
+  // dims (c, w, h, n = 1); 3x3 taps at offsets 0..2 from the lower corner
+  // (-1, -1): padding 1 on every side, output grid = input grid
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h), 1};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2, static_cast<cuuint64_t>(w) * c * 2,
+                                 static_cast<cuuint64_t>(h) * w * c * 2};
+  const int lower[2] = {-1, -1}, upper[2] = {-1, -1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_im2col_fn()(&p->ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half*>(x), dims, strides,
+                                  lower, upper, static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(kBM), estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw CudaError("cuTensorMapEncodeIm2col failed (code " + std::to_string(int(r)) + ")");
 }
 
 int gemm_chain_counter_words(int M) { return kChainMaxJobs * ((M + kBM - 1) / kBM) + 2; }

@@ -52,6 +52,10 @@ struct GemmEpi {
   // every output is fl(P0 + P1) of the two halves' ascending sums, the same
   // for any M -- a layer must request it in every program that runs it
   int split_k = 0;
+  // set by gemm_plan_conv3x3: A is the implicit im2col of an NHWC fp16 image
+  // of this width (K block kb = tap kb / cb, channels 64 (kb % cb) ...),
+  // loaded by TMA in im2col mode
+  int conv_w = 0, conv_cb = 0;
   // Second fp16 output (fused projections sharing A, e.g. Q | K V): output
   // columns >= split_n go to out2[row_map2[m]][n - split_n] (split_n % BN == 0).
   void* out2 = nullptr;
@@ -85,6 +89,13 @@ struct GemmPlan {
 void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, int ldb, int N,
                int K, const GemmEpi& epi, int force_bn = 0);
 void gemm_run(const GemmPlan& p, cudaStream_t stream);
+// 3x3 convolution, zero padding 1, stride 1, as an implicit GEMM: A = the
+// im2col patches of x (NHWC fp16 [h][w][c], c % 64 == 0) gathered by TMA in
+// im2col mode -- never materialised -- in K order (ky, kx, c); B = the
+// packed weights [N][9c]. Bitwise equal to gemm_plan over im2col3x3's
+// patches of the same fp16 values.
+void gemm_plan_conv3x3(GemmPlan* p, const __half* x, int h, int w, int c, const __half* B, int ldb, int N,
+                       const GemmEpi& epi);
 
 // A chain of dependent GEMMs in ONE persistent launch (the S1/S2 block
 // tail: out-projection + residual -> SwiGLU gate|up -> down + residual -> the

@@ -105,8 +105,9 @@ void window_attention_tiles(const __half* q, int ldq, const int32_t* tiles, int 
 // half-resolution grid (nearest x2 folded into the addressing).
 void im2col3x3(const float* x, int h, int w, int c, int stride, int up2, __half* out, int kcols,
                cudaStream_t st);
-// out[y][x][:] = x[y/2][x/2][:] (fp32, NHWC) or subsample x[2y][2x]
-void upsample2_nhwc(const float* x, int h, int w, int c, float* out, cudaStream_t st);
+// out[y][x][:] = x[y/2][x/2][:] (fp32, NHWC; plus an fp16 copy when out16
+// is given: the operand of the implicit-GEMM conv) or subsample x[2y][2x]
+void upsample2_nhwc(const float* x, int h, int w, int c, float* out, cudaStream_t st, __half* out16 = nullptr);
 void subsample2_nhwc(const float* x, int h, int w, int c, float* out, cudaStream_t st);
 // z_hat [c][h][w] int32 -> NHWC fp32
 void zhat_to_nhwc(const int32_t* z, int c, int hw, float* out, cudaStream_t st);

@@ -83,6 +83,18 @@ __device__ __forceinline__ void tma_load_4d(uint32_t smem_dst, const CUtensorMap
       "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
+// 4D TMA load in im2col mode (NHWC tensor, cuTensorMapEncodeIm2col map):
+// the map's pixelsPerColumn output pixels starting at (w, h, n), each
+// reading channels [c, c + channelsPerPixel) of input pixel (w, h) + the
+// map's lower corner + (off_w, off_h); zero fill outside the image.
+__device__ __forceinline__ void tma_load_im2col_4d(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int c,
+                                                   int w, int h, int n, uint16_t off_w, uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(smem_u32(smem_dst)),
+      "l"(m), "r"(c), "r"(w), "r"(h), "r"(n), "r"(smem_u32(bar)), "h"(off_w), "h"(off_h)
+      : "memory");
+}
 // 1D bulk copy global -> shared (bytes % 16 == 0), completing on an mbarrier.
 __device__ __forceinline__ void bulk_load(uint32_t smem_dst, const void* src, uint32_t bytes,
                                           uint64_t* bar) {

@@ -427,6 +427,8 @@ void Engine::alloc_all() {
   hu_ = dalloc<float>(HWp * D.hc);
   hh_ = dalloc<float>(HWp * D.hc);
   hcol_ = dalloc<__half>(HWp * D.kconv);
+  hu16_ = dalloc<__half>(HWp * D.hc);  // implicit-GEMM conv operands (fp16 NHWC)
+  hyh16_ = dalloc<__half>(HWp * D.hc);
   hcast_ = dalloc<__half>(HWp * D.hcp);
   s1full_ = dalloc<__half>(HWp * d);
 
@@ -1074,6 +1076,25 @@ void Engine::build_lrp(Program& P) {
   });
 }
 
+// The hyper decoder's 3x3 convolutions run as implicit GEMMs (TMA im2col)
+// when the channel count allows 64-channel tap blocks (paper scale: 128);
+// PSWA_CONV_IM2COL_MATERIALISE=1 keeps the patch-matrix path.
+bool Engine::implicit_conv() const {
+  static const bool off = std::getenv("PSWA_CONV_IM2COL_MATERIALISE") != nullptr;
+  return !off && D_.hc % 64 == 0 && D_.kconv == 9 * D_.hc;
+}
+
+void Engine::conv(Program& P, const __half* x, int h, int w, const PW& B, const pswa_dev::GemmEpi& ep) {
+  pswa_dev::GemmPlan plan;
+  pswa_dev::gemm_plan_conv3x3(&plan, x, h, w, D_.hc, B.p, B.K, B.N, ep);
+  auto op = [plan](cudaStream_t s) { pswa_dev::gemm_run(plan, s); };
+  add(P, op);
+  if (log_gemms_) {
+    gemm_log_.push_back(op);
+    gemm_log_flops_ += 2.0 * h * w * B.N * 9.0 * D_.hc;
+  }
+}
+
 void Engine::build_hyper_decode(Program& P) {
   const Dims& D = D_;
   const int hc = D.hc;
@@ -1085,25 +1106,37 @@ void Engine::build_hyper_decode(Program& P) {
     const int ih = h, iw = w;
     float* in = src;
     float* out = dst;
-    add(P, [=](cudaStream_t s) { pswa_dev::upsample2_nhwc(in, ih, iw, hc, out, s); });
     h *= 2;
     w *= 2;
     const int oh = h, ow = w;
-    add(P, [=, this](cudaStream_t s) { pswa_dev::im2col3x3(out, oh, ow, hc, 1, 0, hcol_, D.kconv, s); });
-    if (j == 1) tag(P, "im2col", 0.0, static_cast<double>(oh) * ow * (hc * 4.0 + D.kconv * 2.0));
     GemmEpi e1;
-    e1.out = hh_;
-    e1.ld_out = hc;
-    e1.out_f32 = 1;
     e1.bias = hd_b_[j][0];
     e1.act = kActSilu;
     e1.n_store = hc;
-    gemm(P, hcol_, D.kconv, oh * ow, hd_c_[j][0], D.kconv, e1);
-    if (j == 1) tag(P, "hd_conv", 2.0 * oh * ow * hc * 9.0 * hc);
-    add(P, [=, this](cudaStream_t s) { pswa_dev::im2col3x3(hh_, oh, ow, hc, 1, 0, hcol_, D.kconv, s); });
     GemmEpi e2 = f32_acc(out, hc, hc);  // RB-up: out = up2(x) + conv(silu(conv(up2(x))))
     e2.bias = hd_b_[j][1];
-    gemm(P, hcol_, D.kconv, oh * ow, hd_c_[j][1], D.kconv, e2);
+    if (implicit_conv()) {
+      // implicit-GEMM convolutions: the tcgen05 GEMM gathers its A tiles
+      // from the fp16 NHWC image by TMA in im2col mode (no patch matrix);
+      // same fp16 operands and K order as the materialised path below
+      add(P, [=, this](cudaStream_t s) { pswa_dev::upsample2_nhwc(in, ih, iw, hc, out, s, hu16_); });
+      e1.out = hyh16_;
+      e1.ld_out = hc;
+      conv(P, hu16_, oh, ow, hd_c_[j][0], e1);
+      if (j == 1) tag(P, "hd_conv", 2.0 * oh * ow * hc * 9.0 * hc);
+      conv(P, hyh16_, oh, ow, hd_c_[j][1], e2);
+    } else {
+      add(P, [=](cudaStream_t s) { pswa_dev::upsample2_nhwc(in, ih, iw, hc, out, s); });
+      add(P, [=, this](cudaStream_t s) { pswa_dev::im2col3x3(out, oh, ow, hc, 1, 0, hcol_, D.kconv, s); });
+      if (j == 1) tag(P, "im2col", 0.0, static_cast<double>(oh) * ow * (hc * 4.0 + D.kconv * 2.0));
+      e1.out = hh_;
+      e1.ld_out = hc;
+      e1.out_f32 = 1;
+      gemm(P, hcol_, D.kconv, oh * ow, hd_c_[j][0], D.kconv, e1);
+      if (j == 1) tag(P, "hd_conv", 2.0 * oh * ow * hc * 9.0 * hc);
+      add(P, [=, this](cudaStream_t s) { pswa_dev::im2col3x3(hh_, oh, ow, hc, 1, 0, hcol_, D.kconv, s); });
+      gemm(P, hcol_, D.kconv, oh * ow, hd_c_[j][1], D.kconv, e2);
+    }
     std::swap(src, dst);
   }
   const float* fin = src;

@@ -219,6 +219,9 @@ class Engine {
   static bool chain_enabled();
   // alg_flops: the layer's algorithmic FLOPs when the packed operands are
   // padded (default 2 M N K of the padded GEMM)
+  // 3x3 conv (padding 1) of an fp16 NHWC image as an implicit GEMM
+  void conv(Program& P, const __half* x, int h, int w, const PW& B, const pswa_dev::GemmEpi& ep);
+  bool implicit_conv() const;
   void gemm(Program& P, const __half* A, int lda, int M, const PW& B, int K,
             const pswa_dev::GemmEpi& ep, double alg_flops = -1.0);
   // every GEMM launch of the decode program being built, for the whole-class
@@ -385,6 +388,7 @@ class Engine {
   // hyper
   float *hx_ = nullptr, *hu_ = nullptr, *hh_ = nullptr;
   __half *hcol_ = nullptr, *hcast_ = nullptr, *s1full_ = nullptr;
+  __half *hu16_ = nullptr, *hyh16_ = nullptr;  // hyper decoder conv operands (fp16 NHWC)
   // batch buffers
   int nmax_ = 0;
   float *bx_ = nullptr, *chx_ = nullptr, *musig_ = nullptr;
