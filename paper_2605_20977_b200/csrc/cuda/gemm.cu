@@ -45,7 +45,15 @@ template <int BN>
 struct GemmCfg {
   // as deep as shared memory allows (<= 227 KB with the epilogue staging):
   // the small-M step GEMMs are latency bound, so all K blocks in flight helps
-  static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int kStages = BN == 352 ? 3 : BN >= 192 ? 4 : (BN == 128 ? 6 : 8);
+  // BN = 352 (the 2040-row gate|up GEMMs in one wave of 128 tiles instead of
+  // 176 tiles over 148 SMs): two N = 176 MMAs per K step (UMMA N <= 256),
+  // two 176-row B boxes per stage (TMA box <= 256 rows), one accumulator
+  // (2 x 352 columns exceed the 512 of TMEM)
+  static constexpr int kBSplit = BN > 256 ? 2 : 1;
+  static constexpr int kSubN = BN / kBSplit;
+  static constexpr int kAccBufs = 2 * BN <= 512 ? 2 : 1;
+  static constexpr int kTmemCols = kAccBufs * BN <= 128 ? 128 : kAccBufs * BN <= 256 ? 256 : 512;
   static_assert(kStages * (kBM * kBK * 2 + BN * kBK * 2) + 1280 + kEpiWarps * 4096 <= 227 * 1024, "smem");
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
@@ -447,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
   tc_fence_before();
   if (CL > 1)
     cluster_sync();  // peer barriers initialised before any multicast
@@ -465,7 +473,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     npre = min(S, kblocks);
     for (int kb = 0; kb < npre; ++kb) {
       mbar_expect_tx(&full[kb], Cfg::kStageBytes);
-      tma_load_2d(sb + kb * Cfg::kBBytes, &tmb, &full[kb], kb * kBK, n0);
+#pragma unroll
+      for (int h = 0; h < Cfg::kBSplit; ++h)
+        tma_load_2d(sb + kb * Cfg::kBBytes + h * Cfg::kSubN * 128, &tmb, &full[kb], kb * kBK, n0 + h * Cfg::kSubN);
     }
   }
   // everything above overlaps the previous kernel (PDL); inputs are read below
@@ -509,17 +519,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d_mc(sb + s * Cfg::kBBytes + rank * (Cfg::kBBytes / CL), &tmb, &full[s],
                            kb * kBK, n0 + rank * (BN / CL), static_cast<uint16_t>((1u << CL) - 1));
           else
-            tma_load_2d(sb + s * Cfg::kBBytes, &tmb, &full[s], kb * kBK, n0);
+#pragma unroll
+            for (int h = 0; h < Cfg::kBSplit; ++h)
+              tma_load_2d(sb + s * Cfg::kBBytes + h * Cfg::kSubN * 128, &tmb, &full[s], kb * kBK, n0 + h * Cfg::kSubN);
         }
       }
       stamp(10);
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_f16_f32(kBM, BN);
+      constexpr uint32_t idesc = umma_idesc_f16_f32(kBM, Cfg::kSubN);
       int g = 0, it = 0;
       for (int u = unit0; u < n_units; u += unit_step, ++it) {
-        const int buf = it & 1, use = it >> 1;
+        const int buf = it % Cfg::kAccBufs, use = it / Cfg::kAccBufs;
         if (use > 0) mbar_wait(&tempty[buf], (use - 1) & 1);  // epilogue drained it
         tc_fence_after();
         const uint32_t acc = tmem + buf * BN;
@@ -533,8 +545,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!exp_no_mma) {
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk)
-              tc_mma_f16(acc, umma_desc_k_sw128(a_base + kk * 32), umma_desc_k_sw128(b_base + kk * 32),
-                         idesc, (kb | kk) != 0 ? 1u : 0u);
+#pragma unroll
+              for (int h = 0; h < Cfg::kBSplit; ++h)
+                tc_mma_f16(acc + h * Cfg::kSubN, umma_desc_k_sw128(a_base + kk * 32),
+                           umma_desc_k_sw128(b_base + h * Cfg::kSubN * 128 + kk * 32), idesc,
+                           (kb | kk) != 0 ? 1u : 0u);
           }
           if (CL > 1)
             tc_commit_mc(&empty[s], static_cast<uint16_t>((1u << CL) - 1));
@@ -552,13 +567,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = ew >> 2;              // column half of the tile
     int it = 0;
     for (int u = unit0; u < n_units; u += unit_step, ++it) {
-      const int buf = it & 1, use = it >> 1;
+      const int buf = it % Cfg::kAccBufs, use = it / Cfg::kAccBufs;
       const int m0 = ((u / tiles_n) * CL + rank) * kBM, n0 = (u % tiles_n) * BN;
-      const int c0 = half * (BN / 64), c1 = (half + 1) * (BN / 64);
+      // 32-column chunks split between the two column halves (6 + 5 at BN 352)
+      constexpr int kCh = BN / 32, kCh0 = (kCh + 1) / 2;
+      const int c0 = half ? kCh0 : 0, c1 = half ? kCh : kCh0;
       const int m = m0 + q * 32 + lane;
-      const bool side2 = ep.out2 != nullptr && n0 >= ep.split_n;  // fused second output
+      // fused second output (columns >= split_n, own row map): decided per
+      // 32-column chunk, so a tile may straddle split_n (BN 192 over the
+      // 512 + 1024 Q|K|V columns); the residual kinds never split
+      const bool side2_any = ep.out2 != nullptr && n0 + BN > ep.split_n;
+      const bool side2 = ep.out2 != nullptr && n0 >= ep.split_n;
       const int* rmap = side2 ? ep.row_map2 : ep.row_map;
       const int orow = m < M ? (rmap ? rmap[m] : m) : -1;
+      const int orow2 = side2_any && m < M ? (ep.row_map2 ? ep.row_map2[m] : m) : -1;
       // residual segments prefetched two chunks ahead (two register
       // buffers): the row-per-lane residual read is the epilogue's HBM
       // latency chain in the 32640-row context GEMMs
@@ -605,7 +627,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);
         }
-        epi_chunk<EPI>(ep, orow, n0 + c * 32, raw, res, row_scale, side2,
+        const bool s2 = side2_any && n0 + c * 32 >= ep.split_n;
+        epi_chunk<EPI>(ep, s2 ? orow2 : orow, n0 + c * 32, raw, res, row_scale, s2,
                        (no_coalesce || !stg_base) ? 0u : smem_u32(stg_base + ew * 4096),
                        head_pre ? resA : nullptr, head_pre ? resB : nullptr);
         if (ew == 0 && lane == 0 && it == 0 && c == c0) stamp(12);
@@ -626,7 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_free(tmem, 2 * BN);
+    tmem_free(tmem, Cfg::kTmemCols);
   }
   if (tr && threadIdx.x == 0) {
     stamp(7);
@@ -1283,8 +1306,9 @@ void set_attr() {
   std::call_once(once, [] {
     PSWA_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, 1>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::smem_for(EPI)));
-    PSWA_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, 2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::smem_for(EPI)));
+    if constexpr (GemmCfg<BN>::kBSplit == 1)
+      PSWA_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, 2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::smem_for(EPI)));
   });
 }
 
@@ -1310,10 +1334,14 @@ void launch_epi(const GemmPlan& p, cudaStream_t st) {
   const int tiles = tiles_m * (p.N / BN);
   const int smem = GemmCfg<BN>::smem_for(EPI);
   if (p.cluster == 2) {
-    const int units = (tiles_m + 1) / 2 * (p.N / BN);
-    const int clusters = units < sm_count() / 2 ? units : sm_count() / 2;
-    launch_kc(gemm_tc_kernel<BN, EPI, 2>, dim3(2 * clusters), dim3(kThreads), smem, st, 2u, p.ta,
-              p.tb, p.M, p.K, tiles_m, tiles, p.epi);
+    if constexpr (GemmCfg<BN>::kBSplit == 1) {
+      const int units = (tiles_m + 1) / 2 * (p.N / BN);
+      const int clusters = units < sm_count() / 2 ? units : sm_count() / 2;
+      launch_kc(gemm_tc_kernel<BN, EPI, 2>, dim3(2 * clusters), dim3(kThreads), smem, st, 2u, p.ta,
+                p.tb, p.M, p.K, tiles_m, tiles, p.epi);
+    } else {
+      throw std::invalid_argument("gemm: BN 352 has no cluster variant");
+    }
   } else {
     const int grid = tiles < sm_count() ? tiles : sm_count();
     launch_k(gemm_tc_kernel<BN, EPI, 1>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.M,
@@ -1399,16 +1427,27 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
     // BN=128 when its tiles fill the SMs, else BN=64 (the N = 512 step
     // GEMMs: BN=128 there measured 7.47+ ms)
     const int mt = (M + kBM - 1) / kBM, sms = sm_count();
-    if (N % 256 == 0 && mt * (N / 256) >= sms / 2)
+    // one wave of wider / narrower tiles where 128 x 256 would not fill
+    // the SMs in whole waves (tools/gemm_bn_probe.py, M = 2040): gate|up
+    // N = 2816 as 128 tiles of 352 (176 tiles of 256 take 1.2 waves;
+    // 8.70 vs 8.88 us), Q|K|V N = 1536 as 128 tiles of 192 (96 tiles of
+    // 256 leave 52 SMs idle; 6.66 vs 7.22 us). PSWA_GEMM_NO_WIDE=1: off.
+    static const bool no_wide = std::getenv("PSWA_GEMM_NO_WIDE") != nullptr;
+    if (!no_wide && N % 352 == 0 && mt * (N / 256) > sms && mt * (N / 352) <= sms)
+      bn = 352;
+    else if (!no_wide && N % 192 == 0 && N % 256 == 0 && mt * (N / 256) < sms && mt * (N / 192) <= sms &&
+             mt * (N / 256) >= sms / 2)
+      bn = 192;
+    else if (N % 256 == 0 && mt * (N / 256) >= sms / 2)
       bn = 256;
     else if (N % 128 == 0 && mt * (N / 128) >= sms)
       bn = 128;
     else
       bn = 64;
   }
-  if (N % bn != 0 || (bn != 64 && bn != 128 && bn != 256))
+  if (N % bn != 0 || (bn != 64 && bn != 128 && bn != 192 && bn != 256 && bn != 352))
     throw std::invalid_argument("gemm_plan: bad BN");
-  if (epi.out2 && (epi.out_f32 || epi.act != kActNone || epi.split_n % bn != 0))
+  if (epi.out2 && (epi.out_f32 || epi.act != kActNone || epi.split_n % (bn == 192 ? 32 : bn) != 0))
     throw std::invalid_argument("gemm_plan: split output needs fp16 out and split_n % BN == 0");
   p->M = M;
   p->N = N;
@@ -1435,14 +1474,19 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   // 7.80 vs 7.59 ms / frame), so opt-in via PSWA_GEMM_CLUSTER=1.
   static const bool use_cluster = std::getenv("PSWA_GEMM_CLUSTER") != nullptr;
   if (std::getenv("PSWA_GEMM_TRACE")) p->epi.trace = trace_buffer();
-  p->cluster = (use_cluster && M > kBM) ? 2 : 1;
+  p->cluster = (use_cluster && M > kBM && bn <= 256) ? 2 : 1;
   // CTA-pair tiles (cta_group::2) for the large context GEMMs: correct and
   // bitwise equal to the single-SM kernel (test_pair_gemm_bitwise_equals_
   // single_sm) but measured no faster on B200 -- the context SwiGLU GEMM took
   // 90 vs 84.5 us and the frame 7.38 vs 7.25 ms: these tiles are paced by the
   // epilogue (TMEM reads, SiLU, stores), not the per-SM operand stream the
   // pair halves. Opt-in: PSWA_GEMM_PAIR=1, or force_bn = -1 per call.
-  static const bool use_pair = std::getenv("PSWA_GEMM_PAIR") != nullptr;
+  // PSWA_GEMM_PAIR_KINDS=<mask>: pairs for the epilogue kinds in the mask
+  // only (1 fp16 out, 2 fp32 residual, 4 SwiGLU, 8 head)
+  static const int pair_kinds = std::getenv("PSWA_GEMM_PAIR")         ? 15
+                                : std::getenv("PSWA_GEMM_PAIR_KINDS") ? std::atoi(std::getenv("PSWA_GEMM_PAIR_KINDS"))
+                                                                      : 0;
+  const bool use_pair = (pair_kinds >> epi_kind(epi)) & 1;
   const int pair_units = ((M + 2 * kBM - 1) / (2 * kBM)) * (N / kPBN);
   p->pair = N % kPBN == 0 &&
             (force_pair || (use_pair && force_bn == 0 && M >= 16384 && pair_units >= sm_count()));
@@ -1462,7 +1506,7 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
     p->cluster = 1;
   }
   make_tmap(&p->ta, A, lda, M, K, kBM);
-  make_tmap(&p->tb, B, ldb, N, K, p->pair ? kPBN / 2 : bn / p->cluster);
+  make_tmap(&p->tb, B, ldb, N, K, p->pair ? kPBN / 2 : bn > 256 ? bn / 2 : bn / p->cluster);
   if (p->splitk) {
     static std::once_flag once_sk;
     std::call_once(once_sk, [] {
@@ -1484,7 +1528,9 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   const int kind = epi_kind(epi);
   if (bn == 64) prep<64>(kind);
   if (bn == 128) prep<128>(kind);
+  if (bn == 192) prep<192>(kind);
   if (bn == 256) prep<256>(kind);
+  if (bn == 352) prep<352>(kind);
 }
 
 void gemm_plan_conv3x3(GemmPlan* p, const __half* x, int h, int w, int c, const __half* B, int ldb, int N,
@@ -1584,7 +1630,9 @@ void gemm_run(const GemmPlan& p, cudaStream_t stream) {
   switch (p.BN) {
     case 64: launch<64>(p, kind, stream); break;
     case 128: launch<128>(p, kind, stream); break;
+    case 192: launch<192>(p, kind, stream); break;
     case 256: launch<256>(p, kind, stream); break;
+    case 352: launch<352>(p, kind, stream); break;
     default: throw std::invalid_argument("gemm_run: bad BN");
   }
   PSWA_LAUNCH_CHECK();

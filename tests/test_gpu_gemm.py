@@ -133,3 +133,40 @@ def test_splitk_rows_independent_of_m():
         outs.append(c)
     torch.cuda.synchronize()
     assert torch.equal(outs[0][:2040], outs[1])
+
+
+@pytest.mark.parametrize("M,N,K,kind,bn", [(2040, 2816, 512, "swiglu", 352), (2040, 2816, 512, "f16", 352),
+                                           (2040, 1408, 512, "f32acc", 352), (8160, 2816, 512, "swiglu", 352),
+                                           (300, 704, 128, "f16", 352), (2040, 1536, 512, "f16", 192),
+                                           (8160, 1536, 512, "f32acc", 192)])
+def test_wide_tiles_bitwise_equal_bn256(M, N, K, kind, bn):
+    """128 x 352 tiles (two N = 176 MMAs per K step, one TMEM accumulator;
+    chosen for the 2040-row gate|up GEMMs, which fit one wave of 128 tiles)
+    give bitwise the 128 x 256 / 128 x 64 kernels' results: the K order per
+    element is the same, so the encoder (8160 rows, BN 256) and the decoder
+    (2040 rows, BN 352) stay bitwise symmetric. 8160 rows also runs BN 352
+    with several tiles per CTA (single-buffered accumulator). 128 x 192
+    tiles (one wave of 128 for the 2040-row Q|K|V GEMMs) likewise."""
+    torch.manual_seed(M + N + K)
+    a = (torch.randn(M, K, device="cuda") * 0.5).half()
+    b = (torch.randn(N, K, device="cuda") * 0.05).half()
+    act = 2 if kind == "swiglu" else 0
+    f32 = 1 if kind == "f32acc" else 0
+    ncol = N // 2 if kind == "swiglu" else N
+    base = torch.randn(M, ncol, device="cuda")
+    outs = []
+    for bn in (bn, 256 if N % 256 == 0 else 64):
+        c = base.clone() if f32 else torch.zeros(M, ncol, device="cuda", dtype=torch.float16)
+        check(lib().pswa_gpu_op_gemm_f16(a.data_ptr(), K, M, b.data_ptr(), K, N, K, c.data_ptr(), ncol,
+                                         f32, f32, None, None, act, bn, None))
+        torch.cuda.synchronize()
+        outs.append(c)
+    assert torch.equal(outs[0], outs[1])
+    acc = a.float() @ b.float().t()
+    if kind == "swiglu":
+        ref = torch.nn.functional.silu(acc[:, 0::2]) * acc[:, 1::2]
+    elif kind == "f32acc":
+        ref = acc + base
+    else:
+        ref = acc
+    assert torch.allclose(outs[0].float(), ref, atol=3e-2, rtol=2e-2)
