@@ -201,6 +201,8 @@ PROBE_DESC = {  # the probes the bench names; every other probe is listed by nam
     "ctx_attn": "window_attn_t8_kernel<1,8> (8 queries per warp), context block 0: 3D 4-slot 7x7 window, 32640 queries x 16 heads",
     "ctx_ffn_gu": "gemm_tc_kernel<256> context FFN gate|up (SwiGLU epilogue), M=32640 N=2736 K=512",
     "ctx_wqkv": "gemm_tc_kernel context block 0 fused Q|K|V, M=32640 N=1536 K=512",
+    "ctx_wo": "gemm_tc_kernel<256> context block 0 out-projection + fp32 residual (fp16 row copy, sums of squares), M=32640 N=512 K=512; HBM-bound on the residual stream",
+    "ctx_wd": "gemm_tc_kernel<256> context block 0 FFN down + fp32 residual (fp16 row copy, sums of squares), M=32640 N=512 K=1408; HBM-bound on the residual stream",
     "step_attn": "window_attn_t8_kernel<2,8>, S2 block 0 self attention, step 3 batch (2040 queries)",
     "step_wq": "gemm_tc_kernel S2 block 0 fused Q|K|V projection, step 3 batch, M=2040 N=1536 K=512",
     "step_wo": "gemm_tc_kernel S2 block 0 out projection + residual + norm outputs, M=2040 N=K=512",

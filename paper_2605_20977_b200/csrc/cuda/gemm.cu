@@ -1433,7 +1433,10 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
     // 8.70 vs 8.88 us), Q|K|V N = 1536 as 128 tiles of 192 (96 tiles of
     // 256 leave 52 SMs idle; 6.66 vs 7.22 us). PSWA_GEMM_NO_WIDE=1: off.
     static const bool no_wide = std::getenv("PSWA_GEMM_NO_WIDE") != nullptr;
-    if (!no_wide && N % 352 == 0 && mt * (N / 256) > sms && mt * (N / 352) <= sms)
+    static const int big_f32_bn = std::getenv("PSWA_GEMM_BIG_F32_BN") ? std::atoi(std::getenv("PSWA_GEMM_BIG_F32_BN")) : 0;
+    if (big_f32_bn && epi.out_f32 && epi.act == kActNone && M >= 16384 && N % big_f32_bn == 0)
+      bn = big_f32_bn;  // (experiment: residual GEMMs of the context stack)
+    else if (!no_wide && N % 352 == 0 && mt * (N / 256) > sms && mt * (N / 352) <= sms)
       bn = 352;
     else if (!no_wide && N % 192 == 0 && N % 256 == 0 && mt * (N / 256) < sms && mt * (N / 192) <= sms &&
              mt * (N / 256) >= sms / 2)

@@ -1002,10 +1002,16 @@ void Engine::run_stack3d(Program& P, const Block* blocks, int nblocks, int S, co
     if (b == 0 && probe) tag(P, std::string(probe) + "_attn", attn_flops(-1, 0, S));
     float* xq = ctx_x_ + static_cast<size_t>(q0) * d;
     __half* xnq = ctx_xn_ + static_cast<size_t>(q0) * d;
+    // the residual GEMMs are HBM-bound on the fp32 residual stream: their
+    // probes carry algorithmic bytes (A, weights, residual in, fp32 + fp16
+    // rows and sums of squares out)
+    const double res_bytes = static_cast<double>(nq) * d * (4.0 + 4.0 + 2.0) + nq * (d / 32) * 4.0;
     gemm(P, ctx_att_, d, nq, B.wo, d, rms_out(f32_acc(xq, d), xnq, ssq_q));
+    if (b == 0 && probe) tag(P, std::string(probe) + "_wo", 0.0, res_bytes + nq * d * 2.0 + d * d * 2.0);
     gemm(P, xnq, d, nq, B.wgu, d, rms_in(swiglu_out(ctx_h_, D.fp), ssq_q), 2.0 * nq * 2.0 * D.f * d);
     if (b == 0 && probe) tag(P, std::string(probe) + "_ffn_gu", 2.0 * nq * (2.0 * D.f) * d);
     gemm(P, ctx_h_, D.fp, nq, B.wd, D.fp, rms_out(f32_acc(xq, d), xnq, ssq_q), 2.0 * nq * d * D.f);
+    if (b == 0 && probe) tag(P, std::string(probe) + "_wd", 0.0, res_bytes + nq * D.fp * 2.0 + d * D.fp * 2.0);
   }
 }
 
