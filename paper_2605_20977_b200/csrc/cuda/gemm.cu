@@ -249,7 +249,8 @@ template <int EPI>
 __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
                                           const uint32_t (&raw)[32], const float4 (&res)[8],
                                           float row_scale, bool side2, uint32_t stg = 0,
-                                          const float4* hb = nullptr, const float4* hs = nullptr) {
+                                          const float4* hb = nullptr, const float4* hs = nullptr,
+                                          const CUtensorMap* tmo = nullptr, int box_row = 0) {
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]) * row_scale;
@@ -282,11 +283,34 @@ __device__ __forceinline__ void epi_chunk(const GemmEpi& ep, int orow, int n0,
         (q & 1 ? hp[q >> 1].z : hp[q >> 1].x) = *reinterpret_cast<uint32_t*>(&h0);
         (q & 1 ? hp[q >> 1].w : hp[q >> 1].y) = *reinterpret_cast<uint32_t*>(&h1);
       }
-      warp_store_rows<8>(stg, ov, orow >= 0 ? static_cast<float*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0 : nullptr,
-                         threadIdx.x & 31);
-      if (EPI == kEpiF32 && ep.x16_out)
-        warp_store_rows<4>(stg, hp, orow >= 0 ? ep.x16_out + static_cast<size_t>(orow) * ep.ld_x16 + oc0 : nullptr,
+      if (EPI == kEpiF32 && tmo) {
+        // fp16 row copy through the stage first, then the fp32 rows leave it
+        // by one TMA store (32 x 32 fp32 box at (oc0, box_row); rows past M
+        // are clipped), so the lanes issue no shared loads / global stores
+        // for them; the stage is reusable once the TMA has read it
+        const int ln = threadIdx.x & 31;
+        if (ep.x16_out)
+          warp_store_rows<4>(stg, hp, orow >= 0 ? ep.x16_out + static_cast<size_t>(orow) * ep.ld_x16 + oc0 : nullptr, ln);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + ln * 128 + ((c ^ (ln & 7)) << 4)),
+                       "r"(ov[c].x), "r"(ov[c].y), "r"(ov[c].z), "r"(ov[c].w)
+                       : "memory");
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (ln == 0) {
+          tma_store_2d(tmo, stg, oc0, box_row);
+          bulk_commit();
+          bulk_wait_read0();
+        }
+        __syncwarp();
+      } else {
+        warp_store_rows<8>(stg, ov, orow >= 0 ? static_cast<float*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + oc0 : nullptr,
                            threadIdx.x & 31);
+        if (EPI == kEpiF32 && ep.x16_out)
+          warp_store_rows<4>(stg, hp, orow >= 0 ? ep.x16_out + static_cast<size_t>(orow) * ep.ld_x16 + oc0 : nullptr,
+                             threadIdx.x & 31);
+      }
       if (EPI == kEpiF32 && ep.ssq_out && orow >= 0) ep.ssq_out[static_cast<size_t>(orow) * ep.ld_ssq + (oc0 >> 5)] = ss;
     } else {
       constexpr int NCH = EPI == kEpiSwiGLU ? 2 : 4;  // 16 / 32 fp16 per row
@@ -388,7 +412,8 @@ __device__ int g_gemm_exp = 0;
 template <int BN, int EPI, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
-                   int M, int K, int tiles_m, int num_tiles, const __grid_constant__ GemmEpi ep) {
+                   const __grid_constant__ CUtensorMap tmo, int M, int K, int tiles_m, int num_tiles,
+                   const __grid_constant__ GemmEpi ep) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -563,6 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     const int ew = warp - 2;
     const bool no_coalesce = !ep.coalesce;
+    const bool use_tmo = EPI == kEpiF32 && ep.tma_store && stg_base != nullptr && !no_coalesce;
     const int q = warp & 3;                // TMEM lane quarter this warp may access
     const int half = ew >> 2;              // column half of the tile
     int it = 0;
@@ -630,7 +656,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool s2 = side2_any && n0 + c * 32 >= ep.split_n;
         epi_chunk<EPI>(ep, s2 ? orow2 : orow, n0 + c * 32, raw, res, row_scale, s2,
                        (no_coalesce || !stg_base) ? 0u : smem_u32(stg_base + ew * 4096),
-                       head_pre ? resA : nullptr, head_pre ? resB : nullptr);
+                       head_pre ? resA : nullptr, head_pre ? resB : nullptr,
+                       use_tmo ? &tmo : nullptr, m0 + q * 32);
         if (ew == 0 && lane == 0 && it == 0 && c == c0) stamp(12);
         if (acc_res && c + 2 < c1) prefetch_residual(ep, orow, n0 + (c + 2) * 32, res);
       };
@@ -640,6 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c + 1 < c1) chunk(c + 1, resB);
       }
     }
+    if (use_tmo && lane == 0) bulk_wait0();  // this warp's TMA stores complete
     if (ew == 0 && lane == 0) stamp(6);
   }
   tc_fence_before();
@@ -1271,6 +1299,19 @@ void make_tmap(CUtensorMap* m, const __half* base, int ld, int rows, int cols, i
     throw CudaError("cuTensorMapEncodeTiled failed (code " + std::to_string(int(r)) + ")");
 }
 
+// fp32 output map for the TMA-stored epilogue: 32 x 32 boxes, 128 B rows
+void make_tmap_f32_out(CUtensorMap* m, const float* base, int ld, int rows, int cols) {
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw CudaError("cuTensorMapEncodeTiled (fp32 out) failed (code " + std::to_string(int(r)) + ")");
+}
+
 using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -1338,13 +1379,13 @@ void launch_epi(const GemmPlan& p, cudaStream_t st) {
       const int units = (tiles_m + 1) / 2 * (p.N / BN);
       const int clusters = units < sm_count() / 2 ? units : sm_count() / 2;
       launch_kc(gemm_tc_kernel<BN, EPI, 2>, dim3(2 * clusters), dim3(kThreads), smem, st, 2u, p.ta,
-                p.tb, p.M, p.K, tiles_m, tiles, p.epi);
+                p.tb, p.to, p.M, p.K, tiles_m, tiles, p.epi);
     } else {
       throw std::invalid_argument("gemm: BN 352 has no cluster variant");
     }
   } else {
     const int grid = tiles < sm_count() ? tiles : sm_count();
-    launch_k(gemm_tc_kernel<BN, EPI, 1>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.M,
+    launch_k(gemm_tc_kernel<BN, EPI, 1>, dim3(grid), dim3(kThreads), smem, st, p.ta, p.tb, p.to, p.M,
              p.K, tiles_m, tiles, p.epi);
   }
 }
@@ -1529,6 +1570,18 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
     return;
   }
   const int kind = epi_kind(epi);
+  // fp32 outputs with contiguous rows leave the epilogue stage by TMA, on
+  // request (PSWA_GEMM_TMA_STORE=1): measured neutral on B200 (context
+  // out-projection 53.0 -> 50.4 us, context down 66.4 -> 68.1 us, frame
+  // 6.89 vs 6.92 ms); the epilogue is latency-bound, not store-issue-bound
+  static const bool tma_store = std::getenv("PSWA_GEMM_TMA_STORE") != nullptr;
+  p->tma_store = tma_store && kind == kEpiF32 && p->epi.coalesce && epi.row_map == nullptr &&
+                 epi.out != nullptr && reinterpret_cast<uintptr_t>(epi.out) % 16 == 0 && (epi.ld_out * 4) % 16 == 0;
+  p->epi.tma_store = p->tma_store ? 1 : 0;
+  if (p->tma_store)
+    make_tmap_f32_out(&p->to, static_cast<const float*>(epi.out), epi.ld_out, M, std::min(N, epi.n_store));
+  else
+    p->to = p->ta;  // (unused)
   if (bn == 64) prep<64>(kind);
   if (bn == 128) prep<128>(kind);
   if (bn == 192) prep<192>(kind);

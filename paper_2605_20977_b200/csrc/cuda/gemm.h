@@ -48,6 +48,7 @@ struct GemmEpi {
   float rms_inv_d = 0.0f;
   int v8 = 0;  // set by gemm_plan: every output row segment is 32 B aligned (256-bit ld/st)
   int coalesce = 0;  // set by gemm_plan: stores go through the per-warp smem stage
+  int tma_store = 0;  // set by gemm_plan: fp32 rows leave the stage by TMA (GemmPlan::to)
   // request: split K over a CTA pair (fp32 / fp16 outputs, N % 128 == 0):
   // every output is fl(P0 + P1) of the two halves' ascending sums, the same
   // for any M -- a layer must request it in every program that runs it
@@ -81,6 +82,11 @@ struct GemmPlan {
   int cluster = 1;  // 2: CTA pairs multicasting the shared B tile
   bool pair = false;  // cta_group::2 256 x 256 tiles (large M, N % 256 == 0)
   bool splitk = false;  // split-K CTA pairs, 128 x 128 tiles (GemmEpi::split_k)
+  // fp32-output tiles of the persistent kernel stored by TMA from the
+  // per-warp smem stage (rows contiguous: no row map); to = the output map,
+  // 32 x 32 fp32 boxes, SWIZZLE_128B
+  bool tma_store = false;
+  CUtensorMap to;
   GemmEpi epi;
 };
 
