@@ -204,9 +204,9 @@ PROBE_DESC = {  # the probes the bench names; every other probe is listed by nam
     "ctx_wo": "gemm_tc_kernel<256> context block 0 out-projection + fp32 residual (fp16 row copy, sums of squares), M=32640 N=512 K=512; HBM-bound on the residual stream",
     "ctx_wd": "gemm_tc_kernel<256> context block 0 FFN down + fp32 residual (fp16 row copy, sums of squares), M=32640 N=512 K=1408; HBM-bound on the residual stream",
     "step_attn": "window_attn_t8_kernel<2,8>, S2 block 0 self attention, step 3 batch (2040 queries)",
-    "step_wq": "gemm_tc_kernel S2 block 0 fused Q|K|V projection, step 3 batch, M=2040 N=1536 K=512",
+    "step_wq": "gemm_tc_kernel<192> (one wave of 128 tiles) S2 block 0 fused Q|K|V projection, step 3 batch, M=2040 N=1536 K=512",
     "step_wo": "gemm_tc_kernel S2 block 0 out projection + residual + norm outputs, M=2040 N=K=512",
-    "step_gu": "gemm_tc_kernel S2 block 0 FFN gate|up (SwiGLU), M=2040 N=2736 K=512",
+    "step_gu": "gemm_tc_kernel<352> (one wave of 128 tiles, two N=176 MMAs per K step) S2 block 0 FFN gate|up (SwiGLU), M=2040 N=2816 (2736 used) K=512",
     "step_wd": "gemm_splitk_kernel (K halves on a CTA pair, DSMEM reduction) S2 block 0 FFN down + residual, M=2040 N=512 K=1368",
     "rms_prep": "rms_prep_kernel, context block 0 norm inputs (fp32 -> fp16 + sums of squares), 32640 x 512",
     "rmsnorm": "rmsnorm_kernel, final context norm, 8160 x 512",
