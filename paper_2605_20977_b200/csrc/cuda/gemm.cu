@@ -1,14 +1,15 @@
 // tcgen05 / TMA GEMM for sm_100a. See gemm.h for the contract.
 //
 // Persistent kernel, one CTA per SM, 128 x BN output tiles (cta_group::1,
-// UMMA M=128, N=BN, K=16 per instruction), tiles walked N-fastest: the
+// UMMA M=128, N=BN, K=16 per instruction; BN 64 / 128 / 192 / 256, and 352
+// as two N=176 MMAs per K step), tiles walked N-fastest: the
 // weights (<= 3 MB) stay L2-resident and the CTAs in flight share each
 // activation row panel, which is then read from HBM once (M-fastest order
 // re-streamed the whole activation matrix from HBM for every N tile of the
 // 32640-row context GEMMs). Warp roles:
 //   warp 0    : TMA producer (one elected lane), STAGES-deep smem ring
 //   warp 1    : TMEM allocator + MMA issuer (one elected lane)
-//   warps 2-9 : epilogue. Two TMEM accumulators (2 x BN columns) let the
+//   warps 2-9 : epilogue. Two TMEM accumulators (2 x BN columns; one at BN 352) let the
 //               epilogue of tile i overlap the MMAs of tile i+1. Each warp
 //               drains one 32-lane quarter x one column half; lane = output
 //               row, written with 16 B stores straight from registers.
@@ -615,6 +616,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (acc_res) {
         prefetch_residual(ep, orow, n0 + c0 * 32, resA);
         if (c0 + 1 < c1) prefetch_residual(ep, orow, n0 + (c0 + 1) * 32, resB);
+        // the rest of this lane's residual segment is pulled into L2 by one
+        // bulk prefetch while the tile's MMAs run, so the in-loop loads two
+        // chunks ahead hit L2 instead of waiting out HBM latency (the
+        // 32640-row residual GEMMs are epilogue-latency-bound)
+        if (ep.l2_prefetch && orow >= 0 && c0 + 2 < c1) {
+          const int col0 = n0 + (c0 + 2) * 32, col1 = min(n0 + c1 * 32, ep.n_store);
+          if (col1 > col0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                             static_cast<const float*>(ep.out) + static_cast<size_t>(orow) * ep.ld_out + col0),
+                         "r"(static_cast<uint32_t>(col1 - col0) * 4u)
+                         : "memory");
+        }
       }
       // head with one chunk per warp: its bias / rate scales (resA / resB)
       // are loaded ahead of the accumulator wait as well
@@ -1578,6 +1591,13 @@ void gemm_plan(GemmPlan* p, const __half* A, int lda, int M, const __half* B, in
   p->tma_store = tma_store && kind == kEpiF32 && p->epi.coalesce && epi.row_map == nullptr &&
                  epi.out != nullptr && reinterpret_cast<uintptr_t>(epi.out) % 16 == 0 && (epi.ld_out * 4) % 16 == 0;
   p->epi.tma_store = p->tma_store ? 1 : 0;
+  // residual rows bulk-prefetched into L2 at tile start (16 B aligned
+  // segments), on request (PSWA_GEMM_L2_PREFETCH=1): measured neutral
+  // (context out-projection 53.3 -> 52.0 us, down 70.9 -> 71.7 us)
+  static const bool l2_prefetch = std::getenv("PSWA_GEMM_L2_PREFETCH") != nullptr;
+  p->epi.l2_prefetch = l2_prefetch && kind == kEpiF32 && epi.accumulate && epi.out != nullptr &&
+                       reinterpret_cast<uintptr_t>(epi.out) % 16 == 0 && (epi.ld_out * 4) % 16 == 0 &&
+                       (std::min(N, epi.n_store) % 4) == 0;
   if (p->tma_store)
     make_tmap_f32_out(&p->to, static_cast<const float*>(epi.out), epi.ld_out, M, std::min(N, epi.n_store));
   else

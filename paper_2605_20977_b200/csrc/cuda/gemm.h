@@ -49,6 +49,7 @@ struct GemmEpi {
   int v8 = 0;  // set by gemm_plan: every output row segment is 32 B aligned (256-bit ld/st)
   int coalesce = 0;  // set by gemm_plan: stores go through the per-warp smem stage
   int tma_store = 0;  // set by gemm_plan: fp32 rows leave the stage by TMA (GemmPlan::to)
+  int l2_prefetch = 0;  // set by gemm_plan: residual segments bulk-prefetched into L2 per tile
   // request: split K over a CTA pair (fp32 / fp16 outputs, N % 128 == 0):
   // every output is fl(P0 + P1) of the two halves' ascending sums, the same
   // for any M -- a layer must request it in every program that runs it
